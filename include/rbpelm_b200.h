@@ -1,0 +1,153 @@
+/*
+ * rbpelm_b200.h -- C ABI of the B200-native RBP-ELM training hot path.
+ *
+ * This is the drop-in boundary: plain C types, host or device pointers with
+ * explicit sizes, an error record instead of C++ exceptions.  The host C++
+ * API in rbpelm_b200.hpp (namespace rbpelm, same signatures as the reference's
+ * proj/include/rbpelm/{matrix,linalg,elm}.hpp) is implemented on top of these
+ * entry points and rethrows the reference's exception types from the record.
+ *
+ * All matrices are row-major fp64.  "ld" arguments are leading dimensions in
+ * elements.  Host-pointer entry points copy in/out around the device work;
+ * *_device entry points take device pointers and run on the context's stream.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/proj).
+ */
+#ifndef RBPELM_B200_H
+#define RBPELM_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes; the C++ layer maps them onto the reference's exceptions */
+enum {
+  RBPG_OK = 0,
+  RBPG_SHAPE_ERROR = 1,       /* rbpelm::ShapeError            (matrix.hpp:11-14)  */
+  RBPG_INVALID_ARGUMENT = 2,  /* std::invalid_argument                              */
+  RBPG_SINGULAR_MATRIX = 3,   /* rbpelm::SingularMatrix{pivot}  (linalg.hpp:15-20) */
+  RBPG_SINGULAR_SPLIT = 4,    /* rbpelm::SingularSplit{block}   (elm.hpp:67-72)    */
+  RBPG_RUNTIME_ERROR = 5,     /* std::runtime_error (e.g. non-finite beta)          */
+  RBPG_CUDA_ERROR = 6,        /* device failure                                     */
+  RBPG_NOT_SUPPORTED = 7      /* path not implemented on device (SVD fallback)      */
+};
+
+/* strategy kinds (elm.hpp:36-48) */
+enum { RBPG_DIRECT = 0, RBPG_DF_SPLIT = 1, RBPG_RANK_BASED = 2 };
+
+typedef struct rbpg_status {
+  int code;
+  size_t pivot_index;   /* SingularMatrix::pivot_index */
+  double pivot_value;   /* SingularMatrix::pivot_value */
+  int block;            /* SingularSplit::which: 0 = A, 1 = D */
+  char message[256];
+} rbpg_status;
+
+typedef struct rbpg_strategy {  /* SolverStrategy (elm.hpp:36-48) */
+  int kind;
+  size_t split_index;
+  double rank_tol;
+} rbpg_strategy;
+
+typedef struct rbpg_diagnostics {  /* SolveDiagnostics (elm.hpp:51-63) */
+  size_t rank;
+  int rank_known;
+  size_t split_lo, split_hi;
+  int ridge_applied;
+  int fallback_to_direct;
+  int used_svd_path;
+  double solve_seconds;
+  double hidden_seconds;
+  double training_accuracy;
+} rbpg_diagnostics;
+
+typedef struct rbpg_context rbpg_context;
+
+/* ---- context (one per device; per-call stream-safe when not shared across threads) */
+int rbpg_context_create(int device, rbpg_context** out, rbpg_status* st);
+void rbpg_context_destroy(rbpg_context* ctx);
+/* stream the device entry points run on (cudaStream_t); NULL = context's own stream */
+int rbpg_context_set_stream(rbpg_context* ctx, void* stream, rbpg_status* st);
+int rbpg_context_synchronize(rbpg_context* ctx, rbpg_status* st);
+/* number of kernels this context has launched (evidence counter for bench.py) */
+uint64_t rbpg_context_launch_count(const rbpg_context* ctx);
+const char* rbpg_version(void);
+
+/* ---- host utilities (no device work) */
+/* init_hidden (elm.cpp:74-91): W (inputs x hidden), b (hidden) from mt19937_64(seed) */
+int rbpg_init_hidden(size_t inputs, size_t hidden, size_t outputs, uint64_t seed, double* w, double* b,
+                     rbpg_status* st);
+/* accuracy (elm.cpp:286-300): fraction of rows with argmax(pred) == argmax(y) */
+int rbpg_accuracy(const double* pred, size_t rows, size_t cols, const double* y, size_t yrows, size_t ycols,
+                  double* out, rbpg_status* st);
+/* Synthetic classification data: X iid U[0,1] (N x d), one-hot T (N x m) from
+ * argmax(X V + eps), V ~ N(0,1) (d x m) from teacher_seed, eps ~ N(0, noise_sigma).  Rows are
+ * generated in 65536-row blocks seeded from (seed, block), so any row range [row0, row0+N)
+ * of the global matrix can be generated independently (row sharding). */
+int rbpg_synth_classification(size_t row0, size_t n, size_t d, size_t m, uint64_t seed, uint64_t teacher_seed,
+                              double noise_sigma, double* x, double* t, rbpg_status* st);
+
+/* Config-3 inputs: X = [B, B C] (n x 2*base), B iid U[0,1], C iid U[-1,1] (mix_seed); one-hot T. */
+int rbpg_synth_rank_deficient(size_t n, size_t base, size_t m, uint64_t seed, uint64_t mix_seed,
+                              uint64_t teacher_seed, double noise_sigma, double* x, double* t, rbpg_status* st);
+/* Overwrite ndup hidden nodes (W column + bias) with copies of distinct other nodes (seeded). */
+int rbpg_duplicate_nodes(double* w, double* b, size_t d, size_t l, size_t ndup, uint64_t seed, size_t* target_out,
+                         size_t* source_out, rbpg_status* st);
+
+/* ---- host-buffer entry points (reference-facing; copy in, compute on device, copy out) */
+
+/* hidden_matrix (elm.cpp:93-106): H (n x L) = sigmoid(X W + b) */
+int rbpg_hidden_matrix(rbpg_context* ctx, const double* w, const double* b, size_t d, size_t l, const double* x,
+                       size_t n, size_t xcols, double* h, rbpg_status* st);
+/* gram (matrix.cpp:152-161): G (cols x cols) = A^T A, exactly symmetric */
+int rbpg_gram(rbpg_context* ctx, const double* a, size_t rows, size_t cols, double* g, rbpg_status* st);
+/* rank_revealing_factor (linalg.cpp:157-248); factor may be NULL (= rank_revealing_permutation) */
+int rbpg_rank_revealing_factor(rbpg_context* ctx, const double* a, size_t rows, size_t cols, double tol,
+                               size_t* order, size_t* rank, double* tolerance, double* factor, rbpg_status* st);
+/* solve_factored_gram (linalg.cpp:254-270): out (n x m) = (F F^T)^{-1} rhs in permuted coordinates */
+int rbpg_solve_factored_gram(rbpg_context* ctx, const double* factor, const size_t* order, size_t n, size_t rank,
+                             const double* rhs, size_t rrows, size_t m, double* out, rbpg_status* st);
+/* solve_spd (linalg.cpp:99-155): out = m^{-1} rhs through a blocked Cholesky */
+int rbpg_solve_spd(rbpg_context* ctx, const double* m, size_t mrows, size_t mcols, const double* rhs, size_t rrows,
+                   size_t rcols, double* out, rbpg_status* st);
+/* solve_beta (elm.cpp:158-229) on a host H (n x L), Y (n x m) */
+int rbpg_solve_beta(rbpg_context* ctx, const double* h, size_t n, size_t l, const double* y, size_t yrows, size_t m,
+                    const rbpg_strategy* strategy, double* beta, rbpg_diagnostics* diag, rbpg_status* st);
+/* train (elm.cpp:231-280): outputs W (inputs x L), b (L), beta (L x m); order (L) optional */
+int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, uint64_t seed, const double* x,
+               size_t n, size_t xcols, const double* y, size_t yrows, size_t ycols, const rbpg_strategy* strategy,
+               double* w, double* b, double* beta, size_t* order, rbpg_diagnostics* diag, rbpg_status* st);
+/* predict (elm.cpp:282-284): scores (n x m) = sigmoid(X W + b) beta */
+int rbpg_predict(rbpg_context* ctx, const double* w, const double* b, size_t d, size_t l, const double* beta,
+                 size_t m, const double* x, size_t n, size_t xcols, double* scores, rbpg_status* st);
+
+/* ---- device-pointer stage API (torch plumbing, row-sharded multi-GPU)
+ * Stage 1 (per shard): G (L x L, ld ldg) and HtT (L x m, ld ldt) of the local rows.  If keep_h,
+ * H stays resident in the context for stage 3.  accumulate != 0 adds into G/HtT. */
+int rbpg_gram_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in,
+                           size_t n, size_t d, size_t l, size_t m, const double* dw, size_t ldw, const double* db,
+                           double* dg, size_t ldg, double* dhtt, size_t ldt, int accumulate, int keep_h,
+                           rbpg_status* st);
+/* Stage 2 (replicated): beta (L x m, ld ldb) from the (all-reduced) G, HtT.  n_total is the global
+ * row count (default tolerance, linalg.cpp:171).  order_out (host, L) optional. */
+int rbpg_solve_stage_device(rbpg_context* ctx, const double* dg, size_t ldg, const double* dhtt, size_t ldt,
+                            size_t l, size_t m, size_t n_total, const rbpg_strategy* strategy, double* dbeta,
+                            size_t ldb, size_t* order_out, rbpg_diagnostics* diag, rbpg_status* st);
+/* Stage 3 (per shard): number of local rows whose argmax(H beta) equals argmax(T).  Uses the H kept
+ * by stage 1 when available, otherwise rebuilds it from X. */
+int rbpg_accuracy_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in,
+                               size_t n, size_t d, size_t l, size_t m, const double* dw, size_t ldw,
+                               const double* db, const double* dbeta, size_t ldb, uint64_t* hits, rbpg_status* st);
+/* Whole train() on device-resident X, T (W, b host arrays from init_hidden). */
+int rbpg_train_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in, size_t n,
+                      size_t d, size_t l, size_t m, const double* w, const double* b, const rbpg_strategy* strategy,
+                      double* dbeta, size_t ldb, size_t* order_out, rbpg_diagnostics* diag, rbpg_status* st);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBPELM_B200_H */

@@ -1,0 +1,924 @@
+// Host engine of the B200 RBP-ELM hot path: workspace, TMA descriptors, the
+// solve dispatch of the reference's solve_beta (elm.cpp:158-229) and train()
+// (elm.cpp:231-280), and the C ABI declared in include/rbpelm_b200.h.
+//
+// Pipeline of train() with the rank strategy, all on one stream:
+//   K1 hidden_kernel   H = sigmoid(X W + b)               (elm.cpp:93-106)
+//   K2 syrk_kernel     G = H^T H, HtT = H^T T              (linalg.cpp:179-184, elm.cpp:207)
+//   K3 panel_kernel +  diagonal-pivoted blocked Cholesky  (linalg.cpp:186-247)
+//      syrk_kernel(trailing)
+//   K4 trsm_pair       beta = P F^-T F^-1 P^T HtT          (elm.cpp:202-214, linalg.cpp:254-270)
+//   accuracy           argmax(H beta) vs argmax(T)         (elm.cpp:278, 286-300)
+// If rank < L the Schur block solve (elm.cpp:124-156) runs on sub-blocks of the
+// original Gram and HtT (no N-sized passes): H1^T(T - H2 B) = HtT[P1] - G[P1,P2] B.
+#include "../../include/rbpelm_b200.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace rbpg {
+cudaError_t launch_hidden(const CUtensorMap&, const CUtensorMap&, const HiddenParams&, cudaStream_t);
+cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams&, int, cudaStream_t);
+cudaError_t launch_syrk_finish(const SyrkParams&, int, int, int, cudaStream_t);
+cudaError_t launch_gemm(const GemmParams&, cudaStream_t);
+cudaError_t launch_factor_setup(const double*, long long, int, long long, double, int, double*, int*, FactorState*,
+                                cudaStream_t);
+cudaError_t launch_panel(const PanelParams&, int, cudaStream_t);
+int panel_max_ctas(int, int, int);
+cudaError_t launch_gather_factor(const double*, long long, const int*, int, double*, long long, int, cudaStream_t);
+cudaError_t launch_gather_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
+cudaError_t launch_scatter_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
+cudaError_t launch_trsm_pair(const double*, long long, double*, long long, int, int, int, int, int, cudaStream_t);
+cudaError_t launch_accuracy(const double*, long long, const double*, long long, long long, int, unsigned long long*,
+                            int, cudaStream_t);
+cudaError_t launch_add_diag(double*, long long, int, double, cudaStream_t);
+cudaError_t launch_gather_block(const double*, long long, const int*, int, const int*, int, double*, long long,
+                                cudaStream_t);
+cudaError_t launch_symmetrize(double*, long long, int, cudaStream_t);
+cudaError_t launch_trace(const double*, long long, int, double*, cudaStream_t);
+cudaError_t launch_nonfinite(const double*, long long, int, int, int*, cudaStream_t);
+cudaError_t launch_axpy_rows(const double*, long long, const double*, long long, int, int, double*, long long,
+                             cudaStream_t);
+}  // namespace rbpg
+
+using namespace rbpg;
+
+// ============================================================================
+// errors
+// ============================================================================
+namespace {
+struct Fail {
+  int code;
+  std::string msg;
+  size_t pivot_index = 0;
+  double pivot_value = 0.0;
+  int block = 0;
+};
+[[noreturn]] void fail(int code, const std::string& m) { throw Fail{code, m}; }
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(RBPG_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
+}
+std::string shp(size_t r, size_t c) { return std::to_string(r) + "x" + std::to_string(c); }
+inline size_t even(size_t v) { return (v + 1) & ~size_t(1); }
+inline size_t round_up(size_t v, size_t m) { return (v + m - 1) / m * m; }
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+}  // namespace
+
+struct rbpg_context {
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::map<std::string, std::pair<void*, size_t>> bufs;
+  uint64_t launches = 0;
+  EncodeTiledFn encode = nullptr;
+  cudaEvent_t ev[8] = {};
+  // H kept resident by the gram stage for the accuracy stage
+  const double* kept_h = nullptr;
+  size_t kept_n = 0, kept_l = 0, kept_ldh = 0;
+  size_t h_budget_bytes = size_t(48) << 30;
+  std::mutex mu;
+
+  void* buf(const std::string& name, size_t bytes) {
+    auto it = bufs.find(name);
+    if (it != bufs.end() && it->second.second >= bytes) return it->second.first;
+    if (it != bufs.end()) {
+      cudaStreamSynchronize(stream);
+      cudaFree(it->second.first);
+      bufs.erase(it);
+      if (kept_h && name == "H") kept_h = nullptr;
+    }
+    void* p = nullptr;
+    ck(cudaMalloc(&p, bytes < 256 ? 256 : bytes), ("cudaMalloc " + name).c_str());
+    bufs[name] = {p, bytes};
+    return p;
+  }
+  double* dbuf(const std::string& name, size_t elems) { return static_cast<double*>(buf(name, elems * 8)); }
+  void chk(cudaError_t e, const char* what) {
+    ck(e, what);
+    ++launches;
+  }
+};
+
+namespace {
+
+CUtensorMap make_map(rbpg_context* ctx, const double* base, uint64_t cols, uint64_t rows, uint64_t ld,
+                     uint32_t box_cols, uint32_t box_rows, bool swizzle128) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * sizeof(double)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = ctx->encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    fail(RBPG_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ") dims " +
+                              std::to_string(cols) + "x" + std::to_string(rows) + " ld " + std::to_string(ld));
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// device building blocks
+// ---------------------------------------------------------------------------
+void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_t d, const double* dW, size_t ldw,
+                const double* db, size_t L, double* dH, size_t ldh) {
+  if (N == 0) return;
+  CUtensorMap tmX = make_map(ctx, dX, d, N, ldx, 16, kTile, true);
+  CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, kTile, kBK, false);
+  HiddenParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), db, dH, static_cast<long long>(ldh)};
+  ctx->chk(launch_hidden(tmX, tmW, p, ctx->stream), "hidden_kernel");
+}
+
+// G (+)= A^T A over rows [0, N) of A (N x L, ld lda); HtT (+)= A^T T when m > 0.
+void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t L, const double* dT, size_t ldt_in,
+              size_t m, double* dG, size_t ldg, double* dHtT, size_t ldt, bool accumulate) {
+  SyrkParams p{};
+  p.M = static_cast<int>(L);
+  p.mB = static_cast<int>(m);
+  p.nbI = static_cast<int>((L + kTile - 1) / kTile);
+  p.nGram = p.nbI * (p.nbI + 1) / 2;
+  p.nbT = m > 0 ? static_cast<int>((m + kTile - 1) / kTile) : 0;
+  const int tiles = p.nGram + p.nbI * p.nbT;
+  int splits = 1;
+  if (tiles < 2 * ctx->num_sms) splits = std::max(1, (2 * ctx->num_sms + tiles - 1) / tiles);
+  splits = std::min<int>(splits, 32);
+  splits = std::max<int>(1, std::min<int>(splits, static_cast<int>(N / 1024)));
+  long long per = static_cast<long long>(round_up((N + splits - 1) / splits, kBK));
+  if (per == 0) per = kBK;
+  splits = static_cast<int>((N + per - 1) / per);
+  if (splits < 1) splits = 1;
+  p.kRows = static_cast<long long>(N);
+  p.kPerSplit = per;
+  p.G = dG;
+  p.ldg = static_cast<long long>(ldg);
+  p.HtT = dHtT;
+  p.ldt = static_cast<long long>(ldt);
+  const bool direct = splits == 1 && !accumulate;
+  p.mode = direct ? kSyrkDirect : kSyrkPartial;
+  if (!direct) {
+    p.ws = ctx->dbuf("syrk_ws", size_t(splits) * L * ldg);
+    p.wsStride = static_cast<long long>(L * ldg);
+    if (m > 0) {
+      p.wsT = ctx->dbuf("syrk_wsT", size_t(splits) * L * ldt);
+      p.wsTStride = static_cast<long long>(L * ldt);
+    }
+  }
+  if (N == 0) {
+    if (!accumulate) {
+      ck(cudaMemsetAsync(dG, 0, sizeof(double) * L * ldg, ctx->stream), "memset G");
+      if (m > 0) ck(cudaMemsetAsync(dHtT, 0, sizeof(double) * L * ldt, ctx->stream), "memset HtT");
+    }
+    return;
+  }
+  CUtensorMap tmA = make_map(ctx, dA, L, N, lda, kTile, kBK, false);
+  CUtensorMap tmB = m > 0 ? make_map(ctx, dT, m, N, ldt_in, kTile, kBK, false) : tmA;
+  ctx->chk(launch_syrk(tmA, tmB, p, splits, ctx->stream), "syrk_kernel");
+  if (!direct) ctx->chk(launch_syrk_finish(p, splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream), "syrk_finish");
+}
+
+void gemm_dev(rbpg_context* ctx, int M, int N, int K, const double* A, size_t lda, bool tA, const double* B,
+              size_t ldb, bool tB, double* C, size_t ldc, double alpha, double beta) {
+  GemmParams p{M, N, K, A, static_cast<long long>(lda), tA ? 1 : 0, B, static_cast<long long>(ldb), tB ? 1 : 0,
+               C, static_cast<long long>(ldc), alpha, beta};
+  ctx->chk(launch_gemm(p, ctx->stream), "gemm_kernel");
+}
+
+// X (n x m, ld ldx) <- (F F^T)^{-1} X, column chunks of <= 128 right-hand sides
+void trsm_pair_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X, size_t ldx, size_t n, size_t m) {
+  for (size_t c0 = 0; c0 < m; c0 += 128) {
+    const int mc = static_cast<int>(std::min<size_t>(128, m - c0));
+    ctx->chk(launch_trsm_pair(F, static_cast<long long>(ldf), X + c0, static_cast<long long>(ldx),
+                              static_cast<int>(n), mc, 1, 1, ctx->num_sms, ctx->stream),
+             "trsm_pair_kernel");
+  }
+}
+
+struct FactorResult {
+  const double* F = nullptr;  // factor rows by final position (n x n, ld ldF)
+  size_t ldF = 0;
+  const int* ord = nullptr;   // device: position -> original column
+  FactorState st{};
+};
+
+// Diagonal-pivoted (pivoting = 1, linalg.cpp:157-248) or unpivoted SpdFactor (pivoting = 0,
+// linalg.cpp:99-139) blocked Cholesky of the symmetric dG (n x n, ld ldg).  dG is not modified.
+FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t n, size_t rows_for_tol, double tol,
+                        int pivoting, const std::string& tag) {
+  cudaStream_t s = ctx->stream;
+  const size_t ldn = round_up(n, 8);
+  double* Ga = ctx->dbuf(tag + ".Ga", n * ldn);
+  double* Gb = ctx->dbuf(tag + ".Gb", n * ldn);
+  double* Fo = ctx->dbuf(tag + ".Fo", n * ldn);
+  double* F = ctx->dbuf(tag + ".F", n * ldn);
+  double* dv[2] = {ctx->dbuf(tag + ".d0", n), ctx->dbuf(tag + ".d1", n)};
+  int* ov[2] = {static_cast<int*>(ctx->buf(tag + ".o0", n * 4)), static_cast<int*>(ctx->buf(tag + ".o1", n * 4))};
+  int* lab = static_cast<int*>(ctx->buf(tag + ".lab", n * 4));
+  double* Pg = ctx->dbuf(tag + ".Pg", n * 64);
+  const size_t ldp = even(n);
+  double* PcT = ctx->dbuf(tag + ".PcT", 64 * ldp);
+  const int max_ctas = ctx->num_sms;
+  PivotSlot* slots = static_cast<PivotSlot*>(ctx->buf(tag + ".slots", sizeof(PivotSlot) * 2 * (max_ctas + 32)));
+  FactorState* st = static_cast<FactorState*>(ctx->buf(tag + ".state", sizeof(FactorState)));
+
+  ck(cudaMemsetAsync(Fo, 0, sizeof(double) * n * ldn, s), "memset Fo");
+  ck(cudaMemsetAsync(Pg, 0, sizeof(double) * n * 64, s), "memset Pg");
+  ck(cudaMemsetAsync(slots, 0, sizeof(PivotSlot) * 2 * (max_ctas + 32), s), "memset slots");
+  ck(cudaMemcpy2DAsync(Ga, ldn * 8, dG, ldg * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "copy G");
+  ctx->chk(launch_factor_setup(Ga, static_cast<long long>(ldn), static_cast<int>(n),
+                               static_cast<long long>(rows_for_tol), tol, pivoting, dv[0], ov[0], st, s),
+           "factor_setup");
+  double* gcur = Ga;
+  double* gnext = Gb;
+  int cur = 0;
+  for (size_t k = 0; k < n; k += 64) {
+    const int kb = static_cast<int>(std::min<size_t>(64, n - k));
+    const int nl = static_cast<int>(n - k);
+    int R = std::max(32, (nl + ctx->num_sms - 1) / ctx->num_sms);
+    int C = (nl + R - 1) / R;
+    const int cap = panel_max_ctas(nl, R, ctx->num_sms);
+    if (cap < 1) fail(RBPG_CUDA_ERROR, "panel kernel cannot be resident (shared memory)");
+    while (C > std::min(cap, max_ctas)) {
+      R *= 2;
+      C = (nl + R - 1) / R;
+    }
+    PanelParams pp{};
+    pp.G = gcur;
+    pp.ldg = static_cast<long long>(ldn);
+    pp.d_in = dv[cur];
+    pp.d_out = dv[1 - cur];
+    pp.ord_in = ov[cur];
+    pp.ord_out = ov[1 - cur];
+    pp.k = static_cast<int>(k);
+    pp.kb = kb;
+    pp.n = static_cast<int>(n);
+    pp.st = st;
+    pp.Pg = Pg;
+    pp.PcT = PcT;
+    pp.ldp = static_cast<long long>(ldp);
+    pp.lab_out = lab;
+    pp.slots = slots;
+    pp.Fo = Fo;
+    pp.ldf = static_cast<long long>(ldn);
+    pp.pivoting = pivoting;
+    pp.rows_per_cta = R;
+    ctx->chk(launch_panel(pp, C, s), "panel_kernel");
+    const size_t t0 = k + kb;
+    if (t0 < n) {
+      const size_t nrem = n - t0;
+      CUtensorMap tm = make_map(ctx, PcT, nrem, static_cast<uint64_t>(kb), ldp, kTile, kBK, false);
+      SyrkParams sp{};
+      sp.M = static_cast<int>(nrem);
+      sp.nbI = static_cast<int>((nrem + kTile - 1) / kTile);
+      sp.nGram = sp.nbI * (sp.nbI + 1) / 2;
+      sp.nbT = 0;
+      sp.kRows = kb;
+      sp.kPerSplit = static_cast<long long>(round_up(kb, kBK));
+      sp.mode = kSyrkTrailing;
+      sp.G = gnext;
+      sp.ldg = static_cast<long long>(ldn);
+      sp.Gold = gcur;
+      sp.lab = lab;
+      sp.off = static_cast<int>(t0);
+      ctx->chk(launch_syrk(tm, tm, sp, 1, s), "syrk_trailing");
+      std::swap(gcur, gnext);
+    }
+    cur = 1 - cur;
+  }
+  ctx->chk(launch_gather_factor(Fo, static_cast<long long>(ldn), ov[cur], static_cast<int>(n), F,
+                                static_cast<long long>(ldn), ctx->num_sms, s),
+           "gather_factor");
+  FactorResult r;
+  ck(cudaMemcpyAsync(&r.st, st, sizeof(FactorState), cudaMemcpyDeviceToHost, s), "read factor state");
+  ck(cudaStreamSynchronize(s), "factor sync");
+  r.F = F;
+  r.ldF = ldn;
+  r.ord = ov[cur];
+  return r;
+}
+
+// SpdFactor with the one-shot ridge rescue (elm.cpp:30-49).  Returns the factor; throws
+// SingularSplit(block) if the ridge retry also fails.
+FactorResult spd_with_ridge(rbpg_context* ctx, const double* dA, size_t lda, size_t n, double ridge, bool& applied,
+                            int block, const std::string& tag) {
+  FactorResult f = factor_dev(ctx, dA, lda, n, n, 0.0, 0, tag);
+  if (!f.st.fail) return f;
+  double* tr = ctx->dbuf(tag + ".trace", 1);
+  ctx->chk(launch_trace(dA, static_cast<long long>(lda), static_cast<int>(n), tr, ctx->stream), "trace");
+  double htr = 0.0;
+  ck(cudaMemcpyAsync(&htr, tr, 8, cudaMemcpyDeviceToHost, ctx->stream), "read trace");
+  ck(cudaStreamSynchronize(ctx->stream), "trace sync");
+  double eps = ridge * htr / static_cast<double>(n);
+  if (eps <= 0.0) eps = ridge;
+  double* R = ctx->dbuf(tag + ".ridge", n * lda);
+  ck(cudaMemcpyAsync(R, dA, sizeof(double) * n * lda, cudaMemcpyDeviceToDevice, ctx->stream), "copy ridge");
+  ctx->chk(launch_add_diag(R, static_cast<long long>(lda), static_cast<int>(n), eps, ctx->stream), "add_diag");
+  f = factor_dev(ctx, R, lda, n, n, 0.0, 0, tag);
+  if (f.st.fail) {
+    Fail e{RBPG_SINGULAR_SPLIT, std::string("singular ") + (block == 0 ? "A" : "D") + " block after ridge retry"};
+    e.block = block;
+    throw e;
+  }
+  applied = true;
+  return f;
+}
+
+// solve_direct (elm.cpp:108-122) on the Gram: SpdFactor(G) then two triangular solves; the SVD
+// pseudoinverse fallback exists on device only for H == 0 (pinv(0) = 0).
+void direct_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dHtT, size_t ldt, size_t L, size_t m,
+                size_t rows, double* dBeta, size_t ldb, rbpg_diagnostics* diag) {
+  if (rows >= L) {
+    FactorResult f = factor_dev(ctx, dG, ldg, L, L, 0.0, 0, "direct");
+    if (!f.st.fail) {
+      ck(cudaMemcpy2DAsync(dBeta, ldb * 8, dHtT, ldt * 8, m * 8, L, cudaMemcpyDeviceToDevice, ctx->stream),
+         "copy rhs");
+      trsm_pair_dev(ctx, f.F, f.ldF, dBeta, ldb, L, m);
+      return;
+    }
+    if (diag) diag->used_svd_path = 1;
+    if (f.st.dmax0 == 0.0) {  // every column of H is zero: pinv(H) = 0
+      ck(cudaMemset2DAsync(dBeta, ldb * 8, 0, m * 8, L, ctx->stream), "zero beta");
+      return;
+    }
+  } else {
+    if (diag) diag->used_svd_path = 1;
+  }
+  fail(RBPG_NOT_SUPPORTED, "solve_direct: SVD pseudoinverse fallback is not implemented on the device path");
+}
+
+// Schur block solve (elm.cpp:124-156) on Gram sub-blocks.  ord: device position -> original
+// column; the first `split` positions form H1, the rest H2.  Writes beta in ORIGINAL order.
+void block_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dHtT, size_t ldt, size_t L, size_t m,
+               size_t rows, const int* ord, size_t split, double* dBeta, size_t ldb, rbpg_diagnostics* diag) {
+  const size_t n1 = split, n2 = L - split;
+  if (rows < L) fail(RBPG_SHAPE_ERROR, "solve_block_split: needs at least as many samples as columns");
+  cudaStream_t s = ctx->stream;
+  const int* P1 = ord;
+  const int* P2 = ord + n1;
+  const size_t l1 = even(n1), l2 = even(n2), lm = even(m);
+  double* A = ctx->dbuf("blk.A", n2 * l2);
+  double* G21 = ctx->dbuf("blk.G21", n2 * l1);
+  double* D = ctx->dbuf("blk.D", n1 * l1);
+  double* X = ctx->dbuf("blk.X", n2 * l1);
+  double* Bm = ctx->dbuf("blk.B", n2 * lm);
+  double* R1 = ctx->dbuf("blk.R1", n1 * lm);
+  double* T2 = ctx->dbuf("blk.T2", n2 * lm);
+  double* Bp = ctx->dbuf("blk.beta", L * lm);
+  ctx->chk(launch_gather_block(dG, ldg, P2, n2, P2, n2, A, l2, s), "gather A");
+  ctx->chk(launch_gather_block(dG, ldg, P2, n2, P1, n1, G21, l1, s), "gather G21");
+  ctx->chk(launch_gather_block(dG, ldg, P1, n1, P1, n1, D, l1, s), "gather G11");
+  ctx->chk(launch_gather_rows(dHtT, ldt, P2, n2, m, Bm, lm, s), "gather H2tT");
+  ctx->chk(launch_gather_rows(dHtT, ldt, P1, n1, m, R1, lm, s), "gather H1tT");
+  bool ridge = false;
+  FactorResult fa = spd_with_ridge(ctx, A, l2, n2, 1e-8, ridge, 0, "fa");
+  trsm_pair_dev(ctx, fa.F, fa.ldF, Bm, lm, n2, m);                                  // B = A^-1 H2^T T
+  ck(cudaMemcpy2DAsync(X, l1 * 8, G21, l1 * 8, n1 * 8, n2, cudaMemcpyDeviceToDevice, s), "copy G21");
+  trsm_pair_dev(ctx, fa.F, fa.ldF, X, l1, n2, n1);                                  // A^-1 G21
+  gemm_dev(ctx, n1, n1, n2, G21, l1, true, X, l1, false, D, l1, -1.0, 1.0);         // D = G11 - G21^T A^-1 G21
+  ctx->chk(launch_symmetrize(D, l1, n1, s), "symmetrize");                          // (D + D^T)/2
+  FactorResult fd = spd_with_ridge(ctx, D, l1, n1, 1e-8, ridge, 1, "fd");
+  gemm_dev(ctx, n1, m, n2, G21, l1, true, Bm, lm, false, R1, lm, -1.0, 1.0);        // H1^T(T - H2 B)
+  trsm_pair_dev(ctx, fd.F, fd.ldF, R1, lm, n1, m);                                  // beta1
+  gemm_dev(ctx, n2, m, n1, G21, l1, false, R1, lm, false, T2, lm, 1.0, 0.0);        // G21 beta1
+  trsm_pair_dev(ctx, fa.F, fa.ldF, T2, lm, n2, m);                                  // A^-1 G21 beta1
+  ck(cudaMemcpy2DAsync(Bp, lm * 8, R1, lm * 8, m * 8, n1, cudaMemcpyDeviceToDevice, s), "stack beta1");
+  ctx->chk(launch_axpy_rows(Bm, lm, T2, lm, n2, m, Bp + n1 * lm, lm, s), "beta2");  // beta2 = B - ...
+  ctx->chk(launch_scatter_rows(Bp, lm, ord, L, m, dBeta, ldb, s), "unpermute beta");
+  if (ridge && diag) diag->ridge_applied = 1;
+}
+
+// solve_beta dispatch (elm.cpp:158-229) on device G (original coordinates) and HtT.
+void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dHtT, size_t ldt, size_t L, size_t m,
+               size_t rows, const rbpg_strategy& sg, double* dBeta, size_t ldb, size_t* order_out,
+               rbpg_diagnostics* diag) {
+  if (sg.kind == RBPG_DIRECT) {
+    diag->split_lo = L;
+    diag->split_hi = 0;
+    direct_dev(ctx, dG, ldg, dHtT, ldt, L, m, rows, dBeta, ldb, diag);
+    return;
+  }
+  if (sg.kind == RBPG_DF_SPLIT) {
+    const size_t sidx = sg.split_index;
+    if (sidx < 1 || sidx >= L)
+      fail(RBPG_INVALID_ARGUMENT, "solve_beta: df split index must be in (0, " + std::to_string(L) + "), got " +
+                                      std::to_string(sidx));
+    diag->split_lo = sidx;
+    diag->split_hi = L - sidx;
+    std::vector<int> id(L);
+    for (size_t i = 0; i < L; ++i) id[i] = static_cast<int>(i);
+    int* dord = static_cast<int*>(ctx->buf("df.ord", L * 4));
+    ck(cudaMemcpyAsync(dord, id.data(), L * 4, cudaMemcpyHostToDevice, ctx->stream), "upload identity");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    try {
+      block_dev(ctx, dG, ldg, dHtT, ldt, L, m, rows, dord, sidx, dBeta, ldb, diag);
+    } catch (const Fail& e) {
+      if (e.code != RBPG_SINGULAR_SPLIT) throw;
+      diag->fallback_to_direct = 1;
+      direct_dev(ctx, dG, ldg, dHtT, ldt, L, m, rows, dBeta, ldb, diag);
+    }
+    return;
+  }
+  if (sg.kind != RBPG_RANK_BASED) fail(RBPG_RUNTIME_ERROR, "solve_beta: unknown strategy");
+  if (sg.rank_tol < 0.0 || !std::isfinite(sg.rank_tol))
+    fail(RBPG_INVALID_ARGUMENT, "rank_revealing_permutation: tolerance must be >= 0");
+  FactorResult f = factor_dev(ctx, dG, ldg, L, rows, sg.rank_tol, 1, "rrf");
+  const size_t rank = static_cast<size_t>(f.st.rank);
+  diag->rank = rank;
+  diag->rank_known = 1;
+  if (order_out) {
+    std::vector<int> o(L);
+    ck(cudaMemcpy(o.data(), f.ord, L * 4, cudaMemcpyDeviceToHost), "read order");
+    for (size_t i = 0; i < L; ++i) order_out[i] = static_cast<size_t>(o[i]);
+  }
+  if (rank == 0 || L < 2) {
+    diag->fallback_to_direct = 1;
+    diag->split_lo = L;
+    diag->split_hi = 0;
+    direct_dev(ctx, dG, ldg, dHtT, ldt, L, m, rows, dBeta, ldb, diag);
+    return;
+  }
+  const size_t split = (rank == L) ? (L + 1) / 2 : rank;
+  diag->split_lo = split;
+  diag->split_hi = L - split;
+  if (rank == L) {
+    const size_t lm = even(m);
+    double* rhs = ctx->dbuf("rank.rhs", L * lm);
+    ctx->chk(launch_gather_rows(dHtT, ldt, f.ord, L, m, rhs, lm, ctx->stream), "gather rhs");
+    trsm_pair_dev(ctx, f.F, f.ldF, rhs, lm, L, m);
+    ctx->chk(launch_scatter_rows(rhs, lm, f.ord, L, m, dBeta, ldb, ctx->stream), "unpermute beta");
+    return;
+  }
+  try {
+    block_dev(ctx, dG, ldg, dHtT, ldt, L, m, rows, f.ord, split, dBeta, ldb, diag);
+  } catch (const Fail& e) {
+    if (e.code != RBPG_SINGULAR_SPLIT) throw;
+    diag->fallback_to_direct = 1;
+    direct_dev(ctx, dG, ldg, dHtT, ldt, L, m, rows, dBeta, ldb, diag);
+  }
+}
+
+void check_finite(rbpg_context* ctx, const double* dBeta, size_t ldb, size_t L, size_t m) {
+  int* flag = static_cast<int*>(ctx->buf("nonfinite", 4));
+  ck(cudaMemsetAsync(flag, 0, 4, ctx->stream), "memset flag");
+  ctx->chk(launch_nonfinite(dBeta, static_cast<long long>(ldb), static_cast<int>(L), static_cast<int>(m), flag,
+                            ctx->stream),
+           "nonfinite");
+  int h = 0;
+  ck(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, ctx->stream), "read flag");
+  ck(cudaStreamSynchronize(ctx->stream), "sync");
+  if (h) fail(RBPG_RUNTIME_ERROR, "train: solver produced non-finite output weights");
+}
+
+struct Padded {
+  const double* p;
+  size_t ld;
+};
+// device matrix with an even leading dimension and 16-byte aligned base (TMA rules)
+Padded pad_device(rbpg_context* ctx, const std::string& name, const double* d, size_t ld, size_t rows, size_t cols) {
+  if (ld % 2 == 0 && (reinterpret_cast<uintptr_t>(d) & 15) == 0) return {d, ld};
+  const size_t nld = even(cols);
+  double* q = ctx->dbuf(name, rows * nld);
+  ck(cudaMemcpy2DAsync(q, nld * 8, d, ld * 8, cols * 8, rows, cudaMemcpyDeviceToDevice, ctx->stream), "pad copy");
+  return {q, nld};
+}
+Padded upload(rbpg_context* ctx, const std::string& name, const double* h, size_t rows, size_t cols) {
+  const size_t ld = even(cols);
+  double* q = ctx->dbuf(name, std::max<size_t>(1, rows) * ld);
+  if (rows && cols)
+    ck(cudaMemcpy2DAsync(q, ld * 8, h, cols * 8, cols * 8, rows, cudaMemcpyHostToDevice, ctx->stream), "upload");
+  return {q, ld};
+}
+void download(rbpg_context* ctx, double* h, const double* d, size_t ld, size_t rows, size_t cols) {
+  if (rows && cols)
+    ck(cudaMemcpy2DAsync(h, cols * 8, d, ld * 8, cols * 8, rows, cudaMemcpyDeviceToHost, ctx->stream), "download");
+  ck(cudaStreamSynchronize(ctx->stream), "sync");
+}
+
+size_t h_chunk_rows(rbpg_context* ctx, size_t N, size_t ldh) {
+  size_t rows = ctx->h_budget_bytes / (ldh * 8);
+  rows = std::max<size_t>(rows / kTile * kTile, kTile);
+  return std::min(rows, N);
+}
+
+// Stage 1: H build + Gram/HtT over the local rows (chunked when H exceeds the budget).
+// Returns the summed K1 time (ms) when timing events are requested.
+float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* dT, size_t ldt_in, size_t N,
+                 size_t d, size_t L, size_t m, const double* dW, size_t ldw, const double* db, double* dG, size_t ldg,
+                 double* dHtT, size_t ldt, bool accumulate, bool keep_h, bool timed) {
+  const size_t ldh = even(L);
+  const size_t chunk = std::max<size_t>(1, h_chunk_rows(ctx, std::max<size_t>(N, 1), ldh));
+  double* dH = ctx->dbuf("H", chunk * ldh);
+  float hidden_ms = 0.f;
+  if (N == 0) {
+    gram_dev(ctx, dH, ldh, 0, L, dT, ldt_in, m, dG, ldg, dHtT, ldt, accumulate);
+    return 0.f;
+  }
+  for (size_t r0 = 0; r0 < N; r0 += chunk) {
+    const size_t nr = std::min(chunk, N - r0);
+    if (timed) cudaEventRecord(ctx->ev[0], ctx->stream);
+    hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh);
+    if (timed) {
+      cudaEventRecord(ctx->ev[1], ctx->stream);
+      cudaEventSynchronize(ctx->ev[1]);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+      hidden_ms += ms;
+    }
+    gram_dev(ctx, dH, ldh, nr, L, dT + r0 * ldt_in, ldt_in, m, dG, ldg, dHtT, ldt, accumulate || r0 > 0);
+  }
+  if (keep_h && chunk >= N) {
+    ctx->kept_h = dH;
+    ctx->kept_n = N;
+    ctx->kept_l = L;
+    ctx->kept_ldh = ldh;
+  } else {
+    ctx->kept_h = nullptr;
+  }
+  return hidden_ms;
+}
+
+// Stage 3: hits = #rows with argmax(H beta) == argmax(T)
+uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* dT, size_t ldt_in, size_t N,
+                        size_t d, size_t L, size_t m, const double* dW, size_t ldw, const double* db,
+                        const double* dBeta, size_t ldb) {
+  unsigned long long* hits = static_cast<unsigned long long*>(ctx->buf("hits", 8));
+  ck(cudaMemsetAsync(hits, 0, 8, ctx->stream), "memset hits");
+  if (N > 0) {
+    const size_t ldh = even(L);
+    const bool kept = ctx->kept_h && ctx->kept_n == N && ctx->kept_l == L;
+    const size_t chunk = kept ? N : h_chunk_rows(ctx, N, ldh);
+    const size_t lm = even(m);
+    double* S = ctx->dbuf("scores", chunk * lm);
+    for (size_t r0 = 0; r0 < N; r0 += chunk) {
+      const size_t nr = std::min(chunk, N - r0);
+      const double* H = ctx->kept_h;
+      size_t hld = ctx->kept_ldh;
+      if (!kept) {
+        double* dH = ctx->dbuf("H", chunk * ldh);
+        hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh);
+        H = dH;
+        hld = ldh;
+      }
+      gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(L), H, hld, false, dBeta, ldb, false,
+               S, lm, 1.0, 0.0);
+      ctx->chk(launch_accuracy(S, static_cast<long long>(lm), dT + r0 * ldt_in, static_cast<long long>(ldt_in),
+                               static_cast<long long>(nr), static_cast<int>(m), hits, ctx->num_sms, ctx->stream),
+               "accuracy");
+    }
+  }
+  unsigned long long h = 0;
+  ck(cudaMemcpyAsync(&h, hits, 8, cudaMemcpyDeviceToHost, ctx->stream), "read hits");
+  ck(cudaStreamSynchronize(ctx->stream), "sync");
+  return h;
+}
+
+// train() body on device-resident X, T (elm.cpp:231-280 after validation and init_hidden)
+void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* dT, size_t ldt_in, size_t N, size_t d,
+                size_t L, size_t m, const double* w, const double* b, const rbpg_strategy& sg, double* dBeta,
+                size_t ldb, size_t* order_out, rbpg_diagnostics* diag) {
+  Padded X = pad_device(ctx, "X.pad", dX, ldx, N, d);
+  Padded T = pad_device(ctx, "T.pad", dT, ldt_in, N, m);
+  Padded W = upload(ctx, "W", w, d, L);
+  double* db = ctx->dbuf("b", L);
+  ck(cudaMemcpyAsync(db, b, L * 8, cudaMemcpyHostToDevice, ctx->stream), "upload b");
+  const size_t ldg = round_up(L, 8), ldt = even(m);
+  double* G = ctx->dbuf("G0", L * ldg);
+  double* HtT = ctx->dbuf("HtT", L * ldt);
+
+  const auto wall0 = std::chrono::steady_clock::now();
+  cudaEventRecord(ctx->ev[2], ctx->stream);
+  float hidden_ms = gram_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, G, ldg, HtT, ldt, false, true,
+                               true);
+  solve_dev(ctx, G, ldg, HtT, ldt, L, m, N, sg, dBeta, ldb, order_out, diag);
+  cudaEventRecord(ctx->ev[3], ctx->stream);
+  cudaEventSynchronize(ctx->ev[3]);
+  float total_ms = 0.f;
+  cudaEventElapsedTime(&total_ms, ctx->ev[2], ctx->ev[3]);
+  (void)wall0;
+  diag->hidden_seconds = hidden_ms * 1e-3;
+  diag->solve_seconds = std::max(0.f, total_ms - hidden_ms) * 1e-3;
+  check_finite(ctx, dBeta, ldb, L, m);
+  const uint64_t hits = accuracy_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, dBeta, ldb);
+  diag->training_accuracy = N ? static_cast<double>(hits) / static_cast<double>(N) : 0.0;
+}
+
+template <typename F>
+int guarded(rbpg_context* ctx, rbpg_status* st, F&& body) {
+  if (st) std::memset(st, 0, sizeof(*st));
+  try {
+    if (ctx) {
+      std::lock_guard<std::mutex> lk(ctx->mu);
+      ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+      body();
+    } else {
+      body();
+    }
+    return RBPG_OK;
+  } catch (const Fail& e) {
+    if (st) {
+      st->code = e.code;
+      st->pivot_index = e.pivot_index;
+      st->pivot_value = e.pivot_value;
+      st->block = e.block;
+      std::snprintf(st->message, sizeof st->message, "%s", e.msg.c_str());
+    }
+    return e.code;
+  } catch (const std::exception& e) {
+    if (st) {
+      st->code = RBPG_RUNTIME_ERROR;
+      std::snprintf(st->message, sizeof st->message, "%s", e.what());
+    }
+    return RBPG_RUNTIME_ERROR;
+  }
+}
+
+void zero_diag(rbpg_diagnostics* d) { std::memset(d, 0, sizeof(*d)); d->training_accuracy = -1.0; }
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+int rbpg_context_create(int device, rbpg_context** out, rbpg_status* st) {
+  return guarded(nullptr, st, [&] {
+    int count = 0;
+    ck(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count) fail(RBPG_CUDA_ERROR, "no such CUDA device " + std::to_string(device));
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop;
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major != 10)
+      fail(RBPG_CUDA_ERROR, std::string("rbpelm-b200 is built for sm_100a (B200); device is ") + prop.name);
+    auto* c = new rbpg_context();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "stream");
+    c->stream = c->own;
+    for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    ck(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q), "driver entry point");
+    if (!fn || q != cudaDriverEntryPointSuccess) fail(RBPG_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    c->encode = reinterpret_cast<EncodeTiledFn>(fn);
+    if (const char* e = std::getenv("RBPG_H_BUDGET_GB")) c->h_budget_bytes = size_t(std::atof(e) * (1ull << 30));
+    *out = c;
+  });
+}
+
+void rbpg_context_destroy(rbpg_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
+  for (auto& e : ctx->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+int rbpg_context_set_stream(rbpg_context* ctx, void* stream, rbpg_status* st) {
+  return guarded(ctx, st, [&] { ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own; });
+}
+int rbpg_context_synchronize(rbpg_context* ctx, rbpg_status* st) {
+  return guarded(ctx, st, [&] { ck(cudaStreamSynchronize(ctx->stream), "sync"); });
+}
+uint64_t rbpg_context_launch_count(const rbpg_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int rbpg_hidden_matrix(rbpg_context* ctx, const double* w, const double* b, size_t d, size_t l, const double* x,
+                       size_t n, size_t xcols, double* h, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (xcols != d)
+      fail(RBPG_SHAPE_ERROR, "hidden_matrix: sample has " + std::to_string(xcols) +
+                                 " features but the layer expects " + std::to_string(d));
+    Padded X = upload(ctx, "X.in", x, n, d);
+    Padded W = upload(ctx, "W", w, d, l);
+    double* db = ctx->dbuf("b", l);
+    ck(cudaMemcpyAsync(db, b, l * 8, cudaMemcpyHostToDevice, ctx->stream), "upload b");
+    const size_t ldh = even(l);
+    double* H = ctx->dbuf("H", n * ldh);
+    ctx->kept_h = nullptr;
+    hidden_dev(ctx, X.p, X.ld, n, d, W.p, W.ld, db, l, H, ldh);
+    download(ctx, h, H, ldh, n, l);
+  });
+}
+
+int rbpg_gram(rbpg_context* ctx, const double* a, size_t rows, size_t cols, double* g, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    Padded A = upload(ctx, "A.in", a, rows, cols);
+    const size_t ldg = round_up(cols, 8);
+    double* G = ctx->dbuf("G0", cols * ldg);
+    gram_dev(ctx, A.p, A.ld, rows, cols, nullptr, 0, 0, G, ldg, nullptr, 0, false);
+    download(ctx, g, G, ldg, cols, cols);
+  });
+}
+
+int rbpg_rank_revealing_factor(rbpg_context* ctx, const double* a, size_t rows, size_t cols, double tol,
+                               size_t* order, size_t* rank, double* tolerance, double* factor, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (rows == 0 || cols == 0) fail(RBPG_SHAPE_ERROR, "rank_revealing_permutation: empty matrix");
+    if (tol < 0.0 || !std::isfinite(tol))
+      fail(RBPG_INVALID_ARGUMENT, "rank_revealing_permutation: tolerance must be >= 0");
+    Padded A = upload(ctx, "A.in", a, rows, cols);
+    const size_t ldg = round_up(cols, 8);
+    double* G = ctx->dbuf("G0", cols * ldg);
+    gram_dev(ctx, A.p, A.ld, rows, cols, nullptr, 0, 0, G, ldg, nullptr, 0, false);
+    FactorResult f = factor_dev(ctx, G, ldg, cols, rows, tol, 1, "rrf");
+    std::vector<int> o(cols);
+    ck(cudaMemcpy(o.data(), f.ord, cols * 4, cudaMemcpyDeviceToHost), "read order");
+    for (size_t i = 0; i < cols; ++i) order[i] = static_cast<size_t>(o[i]);
+    *rank = static_cast<size_t>(f.st.rank);
+    *tolerance = f.st.tolerance;
+    if (factor) download(ctx, factor, f.F, f.ldF, cols, cols);
+  });
+}
+
+int rbpg_solve_factored_gram(rbpg_context* ctx, const double* factor, const size_t* order, size_t n, size_t rank,
+                             const double* rhs, size_t rrows, size_t m, double* out, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    (void)order;
+    if (rank != n)
+      fail(RBPG_INVALID_ARGUMENT, "solve_factored_gram: factor is rank-deficient (" + std::to_string(rank) + " of " +
+                                      std::to_string(n) + ")");
+    if (rrows != n)
+      fail(RBPG_SHAPE_ERROR,
+           "solve_factored_gram: rhs has " + std::to_string(rrows) + " rows, expected " + std::to_string(n));
+    Padded F = upload(ctx, "F.in", factor, n, n);
+    Padded X = upload(ctx, "rhs.in", rhs, n, m);
+    trsm_pair_dev(ctx, F.p, F.ld, const_cast<double*>(X.p), X.ld, n, m);
+    download(ctx, out, X.p, X.ld, n, m);
+  });
+}
+
+int rbpg_solve_spd(rbpg_context* ctx, const double* mat, size_t mrows, size_t mcols, const double* rhs, size_t rrows,
+                   size_t rcols, double* out, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (mrows != mcols) fail(RBPG_SHAPE_ERROR, "solve_spd: matrix is not square, " + shp(mrows, mcols));
+    const size_t n = mrows;
+    double scale = 0.0, asym = 0.0;  // linalg.cpp:104-107 (host validation)
+    for (size_t i = 0; i < n * n; ++i) scale = std::max(scale, std::fabs(mat[i]));
+    for (size_t i = 0; i < n; ++i)
+      for (size_t j = 0; j < n; ++j) asym = std::max(asym, std::fabs(mat[i * n + j] - mat[j * n + i]));
+    if (asym > 1e-12 * std::max(scale, 1.0))
+      fail(RBPG_INVALID_ARGUMENT, "solve_spd: matrix is not symmetric within 1e-12 relative");
+    Padded M = upload(ctx, "M.in", mat, n, n);
+    FactorResult f = factor_dev(ctx, M.p, M.ld, n, n, 0.0, 0, "spd");
+    if (f.st.fail) {
+      Fail e{RBPG_SINGULAR_MATRIX, "non-positive pivot " + std::to_string(f.st.fail_value) + " at index " +
+                                       std::to_string(f.st.fail_index) + " in symmetric factorization"};
+      e.pivot_index = static_cast<size_t>(f.st.fail_index);
+      e.pivot_value = f.st.fail_value;
+      throw e;
+    }
+    if (rrows != n)
+      fail(RBPG_SHAPE_ERROR, "solve_spd: rhs has " + std::to_string(rrows) + " rows, expected " + std::to_string(n));
+    Padded X = upload(ctx, "rhs.in", rhs, n, rcols);
+    trsm_pair_dev(ctx, f.F, f.ldF, const_cast<double*>(X.p), X.ld, n, rcols);
+    download(ctx, out, X.p, X.ld, n, rcols);
+  });
+}
+
+int rbpg_solve_beta(rbpg_context* ctx, const double* h, size_t n, size_t l, const double* y, size_t yrows, size_t m,
+                    const rbpg_strategy* strategy, double* beta, rbpg_diagnostics* diag, rbpg_status* st) {
+  rbpg_diagnostics local;
+  if (!diag) diag = &local;
+  zero_diag(diag);
+  return guarded(ctx, st, [&] {
+    if (n == 0 || l == 0) fail(RBPG_SHAPE_ERROR, "solve_beta: empty hidden matrix");
+    if (yrows != n) fail(RBPG_SHAPE_ERROR, "solve_beta: H is " + shp(n, l) + " but Y is " + shp(yrows, m));
+    Padded H = upload(ctx, "H.in", h, n, l);
+    Padded Y = upload(ctx, "Y.in", y, n, m);
+    const size_t ldg = round_up(l, 8), ldt = even(m), lb = even(m);
+    double* G = ctx->dbuf("G0", l * ldg);
+    double* HtT = ctx->dbuf("HtT", l * ldt);
+    double* B = ctx->dbuf("beta", l * lb);
+    gram_dev(ctx, H.p, H.ld, n, l, Y.p, Y.ld, m, G, ldg, HtT, ldt, false);
+    solve_dev(ctx, G, ldg, HtT, ldt, l, m, n, *strategy, B, lb, nullptr, diag);
+    download(ctx, beta, B, lb, l, m);
+  });
+}
+
+int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, uint64_t seed, const double* x,
+               size_t n, size_t xcols, const double* y, size_t yrows, size_t ycols, const rbpg_strategy* strategy,
+               double* w, double* b, double* beta, size_t* order, rbpg_diagnostics* diag, rbpg_status* st) {
+  rbpg_diagnostics local;
+  if (!diag) diag = &local;
+  zero_diag(diag);
+  return guarded(ctx, st, [&] {
+    // validation order of elm.cpp:234-258
+    if (n != yrows) fail(RBPG_SHAPE_ERROR, "train: X is " + shp(n, xcols) + " but Y is " + shp(yrows, ycols));
+    if (xcols != inputs)
+      fail(RBPG_SHAPE_ERROR, "train: X has " + std::to_string(xcols) + " features but params.inputs is " +
+                                 std::to_string(inputs));
+    if (ycols != outputs)
+      fail(RBPG_SHAPE_ERROR, "train: Y has " + std::to_string(ycols) + " columns but params.outputs is " +
+                                 std::to_string(outputs));
+    if (strategy->kind != RBPG_DIRECT && n < hidden)
+      fail(RBPG_INVALID_ARGUMENT, "train: block strategies need at least as many samples as hidden nodes (" +
+                                      std::to_string(n) + " < " + std::to_string(hidden) + "); use the direct strategy");
+    if (strategy->kind == RBPG_DF_SPLIT && (strategy->split_index < 1 || strategy->split_index >= hidden))
+      fail(RBPG_INVALID_ARGUMENT, "train: df split index must be in (0, " + std::to_string(hidden) + "), got " +
+                                      std::to_string(strategy->split_index));
+    rbpg_status s2;
+    if (rbpg_init_hidden(inputs, hidden, outputs, seed, w, b, &s2)) fail(s2.code, s2.message);
+    Padded X = upload(ctx, "X.in", x, n, xcols);
+    Padded T = upload(ctx, "T.in", y, n, ycols);
+    const size_t lb = even(outputs);
+    double* B = ctx->dbuf("beta", hidden * lb);
+    train_core(ctx, X.p, X.ld, T.p, T.ld, n, inputs, hidden, outputs, w, b, *strategy, B, lb, order, diag);
+    download(ctx, beta, B, lb, hidden, outputs);
+  });
+}
+
+int rbpg_predict(rbpg_context* ctx, const double* w, const double* b, size_t d, size_t l, const double* beta,
+                 size_t m, const double* x, size_t n, size_t xcols, double* scores, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (xcols != d)
+      fail(RBPG_SHAPE_ERROR, "hidden_matrix: sample has " + std::to_string(xcols) +
+                                 " features but the layer expects " + std::to_string(d));
+    Padded X = upload(ctx, "X.in", x, n, d);
+    Padded W = upload(ctx, "W", w, d, l);
+    Padded Bt = upload(ctx, "beta.in", beta, l, m);
+    double* db = ctx->dbuf("b", l);
+    ck(cudaMemcpyAsync(db, b, l * 8, cudaMemcpyHostToDevice, ctx->stream), "upload b");
+    const size_t ldh = even(l), lm = even(m);
+    const size_t chunk = h_chunk_rows(ctx, std::max<size_t>(n, 1), ldh);
+    double* H = ctx->dbuf("H", chunk * ldh);
+    ctx->kept_h = nullptr;
+    double* S = ctx->dbuf("scores", std::max<size_t>(n, 1) * lm);
+    for (size_t r0 = 0; r0 < n; r0 += chunk) {
+      const size_t nr = std::min(chunk, n - r0);
+      hidden_dev(ctx, X.p + r0 * X.ld, X.ld, nr, d, W.p, W.ld, db, l, H, ldh);
+      gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(l), H, ldh, false, Bt.p, Bt.ld,
+               false, S + r0 * lm, lm, 1.0, 0.0);
+    }
+    download(ctx, scores, S, lm, n, m);
+  });
+}
+
+int rbpg_gram_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in,
+                           size_t n, size_t d, size_t l, size_t m, const double* dw, size_t ldw, const double* db,
+                           double* dg, size_t ldg, double* dhtt, size_t ldt, int accumulate, int keep_h,
+                           rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    Padded X = pad_device(ctx, "X.pad", dx, ldx, n, d);
+    Padded T = pad_device(ctx, "T.pad", dt, ldt_in, n, m);
+    Padded W = pad_device(ctx, "W.pad", dw, ldw, d, l);
+    gram_stage(ctx, X.p, X.ld, T.p, T.ld, n, d, l, m, W.p, W.ld, db, dg, ldg, dhtt, ldt, accumulate != 0,
+               keep_h != 0, false);
+  });
+}
+
+int rbpg_solve_stage_device(rbpg_context* ctx, const double* dg, size_t ldg, const double* dhtt, size_t ldt,
+                            size_t l, size_t m, size_t n_total, const rbpg_strategy* strategy, double* dbeta,
+                            size_t ldb, size_t* order_out, rbpg_diagnostics* diag, rbpg_status* st) {
+  rbpg_diagnostics local;
+  if (!diag) diag = &local;
+  zero_diag(diag);
+  return guarded(ctx, st, [&] {
+    solve_dev(ctx, dg, ldg, dhtt, ldt, l, m, n_total, *strategy, dbeta, ldb, order_out, diag);
+    check_finite(ctx, dbeta, ldb, l, m);
+  });
+}
+
+int rbpg_accuracy_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in,
+                               size_t n, size_t d, size_t l, size_t m, const double* dw, size_t ldw,
+                               const double* db, const double* dbeta, size_t ldb, uint64_t* hits, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    Padded X = pad_device(ctx, "X.pad", dx, ldx, n, d);
+    Padded T = pad_device(ctx, "T.pad", dt, ldt_in, n, m);
+    Padded W = pad_device(ctx, "W.pad", dw, ldw, d, l);
+    *hits = accuracy_stage(ctx, X.p, X.ld, T.p, T.ld, n, d, l, m, W.p, W.ld, db, dbeta, ldb);
+  });
+}
+
+int rbpg_train_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in, size_t n,
+                      size_t d, size_t l, size_t m, const double* w, const double* b, const rbpg_strategy* strategy,
+                      double* dbeta, size_t ldb, size_t* order_out, rbpg_diagnostics* diag, rbpg_status* st) {
+  rbpg_diagnostics local;
+  if (!diag) diag = &local;
+  zero_diag(diag);
+  return guarded(ctx, st, [&] {
+    if (strategy->kind != RBPG_DIRECT && n < l)
+      fail(RBPG_INVALID_ARGUMENT, "train: block strategies need at least as many samples as hidden nodes (" +
+                                      std::to_string(n) + " < " + std::to_string(l) + "); use the direct strategy");
+    train_core(ctx, dx, ldx, dt, ldt_in, n, d, l, m, w, b, *strategy, dbeta, ldb, order_out, diag);
+  });
+}
+
+}  // extern "C"

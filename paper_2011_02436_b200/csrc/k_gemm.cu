@@ -1,0 +1,467 @@
+// FP64 tensor-core (DMMA) kernels fed by TMA:
+//   K1 hidden_kernel : H = sigmoid(X W + b)      -- reference elm.cpp:93-106 (matmul at
+//                      matrix.cpp:69-77, bias added after the dot at elm.cpp:102, sigmoid elm.cpp:27)
+//   K2 syrk_kernel   : lower-tile G = H^T H (+ H^T T tiles), split-K with a fixed-order
+//                      reduction; also the rank-kb trailing update of the pivoted Cholesky
+//                      -- reference linalg.cpp:179-184 (Gram), 237-244 (trailing update),
+//                      matrix.cpp:79-87 (matmul_at for H^T T)
+//   gemm_kernel      : generic C = alpha op(A) op(B) + beta C for the small solve-side products
+//
+// Data layout: every matrix is row-major fp64 with an even leading dimension
+// (16-byte TMA stride rule).  Output tiles are 128x128 per CTA, 8 warps each
+// owning a 64x32 sub-tile as 4x4 m16n8k4 DMMA fragments (64 fp64 accumulators
+// per thread).  Shared-memory operand tiles are stored "MN-major" ([k][mn], mn
+// contiguous) and read as 16-byte pairs: MMA row g / g+8 (or n-tile pair)
+// are mapped onto adjacent columns so each quarter-warp reads one 128-byte
+// row, which is bank-conflict free without padding.
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <cstdio>
+
+namespace rbpg {
+
+namespace {
+
+// 128B-swizzled [row][16] fp64 tile written by TMA (CU_TENSOR_MAP_SWIZZLE_128B):
+// the 16-byte chunk index inside each 128-byte row is XORed with (row & 7).
+__device__ __forceinline__ int swz16(int row, int col) {
+  return row * 16 + ((((col >> 1) ^ (row & 7)) << 1) | (col & 1));
+}
+
+__device__ __forceinline__ unsigned char* align1024(unsigned char* p) {
+  return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+}  // namespace
+
+// ============================================================================
+// K1: hidden-layer build
+// ============================================================================
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    hidden_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, HiddenParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = align1024(smem_raw);
+  double* Xs = reinterpret_cast<double*>(smem);        // [stage][128 rows][16] swizzled
+  double* Ws = Xs + kStages * kTile * kBK;             // [stage][16][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Ws + kStages * kBK * kTile);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int l0 = blockIdx.x * kTile, n0 = blockIdx.y * kTile;
+  const int ktiles = (p.d + kBK - 1) / kBK;
+  constexpr uint32_t kStageBytes = 2u * kTile * kBK * sizeof(double);
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmW);
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kStages && s < ktiles; ++s) {
+      mbar_arrive_expect_tx(&full[s], kStageBytes);
+      tma_load_2d(Xs + s * kTile * kBK, &tmX, &full[s], s * kBK, n0);
+      tma_load_2d(Ws + s * kBK * kTile, &tmW, &full[s], l0, s * kBK);
+    }
+  }
+
+  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+  double acc[4][4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int s = kt % kStages;
+    mbar_wait(&full[s], (kt / kStages) & 1);
+    const double* xs = Xs + s * kTile * kBK;
+    const double* ws = Ws + s * kBK * kTile;
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const int kc = ks * 4 + t;
+      double a[4][2], b[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const int r = wm + mt * 16 + g;
+        a[mt][0] = xs[swz16(r, kc)];
+        a[mt][1] = xs[swz16(r + 8, kc)];
+      }
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const double2 w = *reinterpret_cast<const double2*>(ws + kc * kTile + wn + pp * 16 + 2 * g);
+        b[2 * pp] = w.x;
+        b[2 * pp + 1] = w.y;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
+    }
+    __syncthreads();
+    if (tid == 0 && kt + kStages < ktiles) {
+      const int kn = kt + kStages;
+      mbar_arrive_expect_tx(&full[s], kStageBytes);
+      tma_load_2d(Xs + s * kTile * kBK, &tmX, &full[s], kn * kBK, n0);
+      tma_load_2d(Ws + s * kBK * kTile, &tmW, &full[s], l0, kn * kBK);
+    }
+  }
+
+  // epilogue: bias after the full dot product, then sigmoid (elm.cpp:102, :27)
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const int cb = l0 + wn + pp * 16 + 4 * t;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int r = n0 + wm + mt * 16 + g + half * 8;
+        if (r >= p.N) continue;
+        double v[4] = {acc[mt][2 * pp][2 * half], acc[mt][2 * pp + 1][2 * half], acc[mt][2 * pp][2 * half + 1],
+                       acc[mt][2 * pp + 1][2 * half + 1]};
+        double h[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = cb + q;
+          const double z = add_rn(v[q], c < p.L ? p.bias[c] : 0.0);
+          h[q] = 1.0 / (1.0 + exp(-z));
+        }
+        double* dst = p.H + (long long)r * p.ldh + cb;
+        if (cb + 3 < p.L) {
+          reinterpret_cast<double2*>(dst)[0] = make_double2(h[0], h[1]);
+          reinterpret_cast<double2*>(dst)[1] = make_double2(h[2], h[3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (cb + q < p.L) dst[q] = h[q];
+        }
+      }
+    }
+  }
+}
+
+// ============================================================================
+// K2: SYRK-TN family.  A (kRows x M) row-major via tmA; B = A for Gram tiles,
+// B = T (kRows x mB) via tmB for the H^T T tiles.
+// ============================================================================
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    syrk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SyrkParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = align1024(smem_raw);
+  double* As = reinterpret_cast<double*>(smem);   // [stage][16][128]
+  double* Bs = As + kStages * kBK * kTile;        // [stage][16][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBK * kTile);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+
+  // ---- tile decode: lower-triangular Gram tiles first, then H^T T tiles
+  const int bx = blockIdx.x;
+  int I, J;
+  bool isT;
+  if (bx < p.nGram) {
+    int i = static_cast<int>((sqrt(8.0 * bx + 1.0) - 1.0) * 0.5);
+    while (i * (i + 1) / 2 > bx) --i;
+    while ((i + 1) * (i + 2) / 2 <= bx) ++i;
+    I = i;
+    J = bx - i * (i + 1) / 2;
+    isT = false;
+  } else {
+    const int tt = bx - p.nGram;
+    I = tt / p.nbT;
+    J = tt % p.nbT;
+    isT = true;
+  }
+  const CUtensorMap* mapB = isT ? &tmB : &tmA;
+  const int i0 = I * kTile, j0 = J * kTile;
+
+  const long long kbeg = (long long)blockIdx.y * p.kPerSplit;
+  long long kend = kbeg + p.kPerSplit;
+  if (kend > p.kRows) kend = p.kRows;
+  const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kBK - 1) / kBK) : 0;
+  constexpr uint32_t kStageBytes = 2u * kTile * kBK * sizeof(double);
+
+  if (tid == 0) {
+    tma_prefetch_desc(&tmA);
+    if (isT) tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kStages && s < ktiles; ++s) {
+      const int kr = static_cast<int>(kbeg + s * kBK);
+      mbar_arrive_expect_tx(&full[s], kStageBytes);
+      tma_load_2d(As + s * kBK * kTile, &tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * kTile, mapB, &full[s], j0, kr);
+    }
+  }
+
+  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
+  double acc[4][4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
+
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int s = kt % kStages;
+    mbar_wait(&full[s], (kt / kStages) & 1);
+    const double* as = As + s * kBK * kTile;
+    const double* bs = Bs + s * kBK * kTile;
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const int kc = ks * 4 + t;
+      double a[4][2], b[4];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const double2 v = *reinterpret_cast<const double2*>(as + kc * kTile + wm + mt * 16 + 2 * g);
+        a[mt][0] = v.x;   // MMA row g   <-> tile row 2g
+        a[mt][1] = v.y;   // MMA row g+8 <-> tile row 2g+1
+      }
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const double2 w = *reinterpret_cast<const double2*>(bs + kc * kTile + wn + pp * 16 + 2 * g);
+        b[2 * pp] = w.x;       // n-tile 2pp   col g <-> tile col 16pp + 2g
+        b[2 * pp + 1] = w.y;   // n-tile 2pp+1 col g <-> tile col 16pp + 2g + 1
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
+    }
+    __syncthreads();
+    if (tid == 0 && kt + kStages < ktiles) {
+      const int kr = static_cast<int>(kbeg + (long long)(kt + kStages) * kBK);
+      mbar_arrive_expect_tx(&full[s], kStageBytes);
+      tma_load_2d(As + s * kBK * kTile, &tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * kTile, mapB, &full[s], j0, kr);
+    }
+  }
+
+  // ---- epilogue.  Thread holds rows r, r+1 (r even) x cols c..c+3 per (mt, pp).
+  const int split = blockIdx.y;
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt) {
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const int r0 = i0 + wm + mt * 16 + 2 * g;
+      const int c0 = j0 + wn + pp * 16 + 4 * t;
+      double v[2][4];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        v[h][0] = acc[mt][2 * pp][2 * h];
+        v[h][1] = acc[mt][2 * pp + 1][2 * h];
+        v[h][2] = acc[mt][2 * pp][2 * h + 1];
+        v[h][3] = acc[mt][2 * pp + 1][2 * h + 1];
+      }
+      if (isT) {
+        double* out = (p.mode == kSyrkPartial) ? p.wsT + split * p.wsTStride : p.HtT;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + h;
+          if (r >= p.M) continue;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c0 + q < p.mB) out[(long long)r * p.ldt + c0 + q] = v[h][q];
+        }
+        continue;
+      }
+      if (p.mode == kSyrkPartial) {
+        double* out = p.ws + split * p.wsStride;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + h;
+          if (r >= p.M) continue;
+          double* dst = out + (long long)r * p.ldg + c0;
+          if (c0 + 3 < p.M) {
+            reinterpret_cast<double2*>(dst)[0] = make_double2(v[h][0], v[h][1]);
+            reinterpret_cast<double2*>(dst)[1] = make_double2(v[h][2], v[h][3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (c0 + q < p.M) dst[q] = v[h][q];
+          }
+        }
+        continue;
+      }
+      // direct / trailing: lower element (r >= c) written at (r, c) and mirrored to (c, r)
+      const int off = (p.mode == kSyrkTrailing) ? p.off : 0;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = r0 + h;
+        if (r >= p.M) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + q;
+          if (c >= p.M || c > r) continue;
+          double val = v[h][q];
+          if (p.mode == kSyrkTrailing) {
+            const int sr = p.lab[off + r], sc = p.lab[off + c];
+            val = sub_rn(p.Gold[(long long)sr * p.ldg + sc], val);
+          }
+          p.G[(long long)(off + r) * p.ldg + off + c] = val;
+          p.G[(long long)(off + c) * p.ldg + off + r] = val;
+        }
+      }
+    }
+  }
+}
+
+// Fixed-order split reduction: G[i][j] = G[j][i] = (acc ? G[i][j] : 0) + sum_s ws[s][i][j]
+// over the lower triangle (i >= j), plus the H^T T partials.
+__global__ void syrk_finish_kernel(SyrkParams p, int splits, int accumulate) {
+  const long long Mg = p.M;
+  const long long total = Mg * Mg;
+  const long long totalT = (long long)p.M * p.mB;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total + totalT;
+       e += (long long)gridDim.x * blockDim.x) {
+    if (e < total) {
+      const long long i = e / Mg, j = e % Mg;
+      if (j > i) continue;
+      double v = p.ws[i * p.ldg + j];
+      for (int s = 1; s < splits; ++s) v = add_rn(v, p.ws[s * p.wsStride + i * p.ldg + j]);
+      if (accumulate) v = add_rn(p.G[i * p.ldg + j], v);
+      p.G[i * p.ldg + j] = v;
+      p.G[j * p.ldg + i] = v;
+    } else {
+      const long long f = e - total;
+      const long long i = f / p.mB, j = f % p.mB;
+      double v = p.wsT[i * p.ldt + j];
+      for (int s = 1; s < splits; ++s) v = add_rn(v, p.wsT[s * p.wsTStride + i * p.ldt + j]);
+      if (accumulate) v = add_rn(p.HtT[i * p.ldt + j], v);
+      p.HtT[i * p.ldt + j] = v;
+    }
+  }
+}
+
+// ============================================================================
+// Generic DMMA GEMM (64x64 tiles, 4 warps of 32x32), plain staged loads.
+// Used for the small solve-side products (block path, scores).
+// ============================================================================
+constexpr int kGT = 64, kGK = 16, kGPad = 66;
+
+__global__ void __launch_bounds__(128) gemm_kernel(GemmParams p) {
+  __shared__ __align__(16) double As[kGK][kGPad];
+  __shared__ __align__(16) double Bs[kGK][kGPad];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int m0 = blockIdx.y * kGT, n0 = blockIdx.x * kGT;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
+
+  for (int k0 = 0; k0 < p.K; k0 += kGK) {
+    // A tile: op(A)(m, k) -> As[k][m]
+    for (int e = tid; e < kGK * kGT; e += 128) {
+      int kk, mm;
+      if (!p.transA) { kk = e % kGK; mm = e / kGK; } else { mm = e % kGT; kk = e / kGT; }
+      const int gm = m0 + mm, gk = k0 + kk;
+      double v = 0.0;
+      if (gm < p.M && gk < p.K) v = p.transA ? p.A[(long long)gk * p.lda + gm] : p.A[(long long)gm * p.lda + gk];
+      As[kk][mm] = v;
+    }
+    // B tile: op(B)(k, n) -> Bs[k][n]
+    for (int e = tid; e < kGK * kGT; e += 128) {
+      int kk, nn;
+      if (!p.transB) { nn = e % kGT; kk = e / kGT; } else { kk = e % kGK; nn = e / kGK; }
+      const int gn = n0 + nn, gk = k0 + kk;
+      double v = 0.0;
+      if (gn < p.N && gk < p.K) v = p.transB ? p.B[(long long)gn * p.ldb + gk] : p.B[(long long)gk * p.ldb + gn];
+      Bs[kk][nn] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < kGK / 4; ++ks) {
+      const int kc = ks * 4 + t;
+      double a[2][2], b[4];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const double2 v = *reinterpret_cast<const double2*>(&As[kc][wm + mt * 16 + 2 * g]);
+        a[mt][0] = v.x;
+        a[mt][1] = v.y;
+      }
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const double2 w = *reinterpret_cast<const double2*>(&Bs[kc][wn + pp * 16 + 2 * g]);
+        b[2 * pp] = w.x;
+        b[2 * pp + 1] = w.y;
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp) {
+      const int r0 = m0 + wm + mt * 16 + 2 * g;
+      const int c0 = n0 + wn + pp * 16 + 4 * t;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = r0 + h;
+        if (r >= p.M) continue;
+        const double v[4] = {acc[mt][2 * pp][2 * h], acc[mt][2 * pp + 1][2 * h], acc[mt][2 * pp][2 * h + 1],
+                             acc[mt][2 * pp + 1][2 * h + 1]};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int c = c0 + q;
+          if (c >= p.N) continue;
+          double* dst = p.C + (long long)r * p.ldc + c;
+          const double prod = p.alpha == 1.0 ? v[q] : p.alpha * v[q];
+          *dst = p.beta == 0.0 ? prod : add_rn(p.beta == 1.0 ? *dst : p.beta * *dst, prod);
+        }
+      }
+    }
+}
+
+// ============================================================================
+// launchers
+// ============================================================================
+cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const HiddenParams& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+    attr = true;
+  }
+  dim3 grid((p.L + kTile - 1) / kTile, (p.N + kTile - 1) / kTile);
+  hidden_kernel<<<grid, kGemmThreads, kTmaSmemBytes, s>>>(tmX, tmW, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const SyrkParams& p, int splits,
+                        cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+    attr = true;
+  }
+  dim3 grid(p.nGram + p.nbI * p.nbT, splits);
+  syrk_kernel<<<grid, kGemmThreads, kTmaSmemBytes, s>>>(tmA, tmB, p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_syrk_finish(const SyrkParams& p, int splits, int accumulate, int num_sms, cudaStream_t s) {
+  syrk_finish_kernel<<<num_sms * 4, 256, 0, s>>>(p, splits, accumulate);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(const GemmParams& p, cudaStream_t s) {
+  if (p.M <= 0 || p.N <= 0) return cudaSuccess;
+  dim3 grid((p.N + kGT - 1) / kGT, (p.M + kGT - 1) / kGT);
+  gemm_kernel<<<grid, 128, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace rbpg

@@ -1,0 +1,100 @@
+// Kernel parameter blocks and host-side launcher declarations shared by the
+// kernel translation units and the engine.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rbpg {
+
+// CTA tile for the TMA-fed DMMA kernels (K1 hidden build, K2 Gram/trailing SYRK)
+constexpr int kTile = 128;   // rows x cols of the output tile
+constexpr int kBK = 16;      // reduction rows per pipeline stage
+constexpr int kStages = 4;   // TMA pipeline depth
+constexpr int kGemmThreads = 256;
+constexpr size_t kTmaSmemBytes = size_t(kStages) * 2 * kTile * kBK * sizeof(double) + 1024 + 256;
+
+// ---- K1: H = sigmoid(X W + b)   (reference elm.cpp:93-106)
+struct HiddenParams {
+  int N, d, L;
+  const double* bias;
+  double* H;
+  long long ldh;
+};
+
+// ---- K2: lower-tile SYRK C = A^T A (+ A^T B tiles), TN layout (A is K x M row-major)
+enum SyrkMode : int {
+  kSyrkDirect = 0,   // write lower tile + mirror into G, HtT tiles into HtT
+  kSyrkPartial = 1,  // raw tiles into per-split workspaces (reduced by finish kernel)
+  kSyrkTrailing = 2  // G_new[off+a][off+b] = G_old[lab[a]][lab[b]] - acc, lower + mirror
+};
+struct SyrkParams {
+  int M;                 // columns of A (= L, or trailing size)
+  int mB;                // columns of B (T) for A^T B tiles
+  int nbI;               // ceil(M / kTile)
+  int nGram;             // nbI*(nbI+1)/2 lower tiles
+  int nbT;               // ceil(mB / kTile) (0: no A^T B tiles)
+  long long kRows;       // reduction length (rows of A)
+  long long kPerSplit;   // multiple of kBK
+  int mode;
+  double* G;
+  long long ldg;
+  double* HtT;
+  long long ldt;
+  double* ws;            // partial: split s writes ws + s*wsStride (ld = ldg)
+  long long wsStride;
+  double* wsT;           // partial HtT: wsT + s*wsTStride (ld = ldt)
+  long long wsTStride;
+  const double* Gold;    // trailing: source Gram (panel-start coordinates)
+  const int* lab;        // trailing: lab[p] = source index of position p (absolute)
+  int off;               // trailing: first trailing position
+};
+
+// ---- generic DMMA GEMM: C = alpha * op(A) op(B) + beta * C (row-major)
+struct GemmParams {
+  int M, N, K;
+  const double* A; long long lda; int transA;
+  const double* B; long long ldb; int transB;
+  double* C; long long ldc;
+  double alpha, beta;
+};
+
+// ---- K3: pivoted-Cholesky panel (reference linalg.cpp:186-247)
+struct FactorState {
+  int rank;          // L until the stop rule fires
+  int stopped;       // factorisation finished early (rank < L) or failed (spd)
+  int fail;          // spd mode: SingularMatrix raised
+  int fail_index;
+  double fail_value;
+  double dmax0;      // max diag of the initial Gram
+  double cut;        // tolerance * sqrt(dmax0)   (pivoted mode)
+  double thresh;     // n * eps * maxdiag         (spd mode, linalg.cpp:109)
+  double tolerance;
+  double min_margin; // not used on device (diagnostic placeholder)
+};
+
+struct __align__(16) PivotSlot {
+  double val;
+  int pos;
+  int label;
+  unsigned int epoch;
+  int pad[3];
+};
+
+struct PanelParams {
+  const double* G;  long long ldg;     // Gram in panel-start position coordinates
+  const double* d_in; double* d_out;   // running diagonal by position
+  const int* ord_in; int* ord_out;     // position -> original column
+  int k, kb, n;
+  FactorState* st;
+  double* Pg;                           // [n][64] panel columns by label (global mirror)
+  double* PcT; long long ldp;           // [64][ldp] remaining rows, by new position - (k+kb)
+  int* lab_out;                         // [n] position -> panel-start label (for trailing gather)
+  PivotSlot* slots;                     // [2][gridDim.x]
+  double* Fo; long long ldf;            // factor rows by original column
+  int pivoting;                         // 1 = rank-revealing (diag pivot), 0 = SpdFactor (no pivot)
+  int rows_per_cta;
+};
+
+}  // namespace rbpg
