@@ -76,6 +76,12 @@ int rbpg_context_synchronize(rbpg_context* ctx, rbpg_status* st);
 /* number of kernels this context has launched (evidence counter for bench.py) */
 uint64_t rbpg_context_launch_count(const rbpg_context* ctx);
 const char* rbpg_version(void);
+/* per-kernel-class device timing with CUDA events on the context stream (off by default);
+ * enabling/disabling resets the counters.  Names: "hidden_kernel", "syrk_kernel", "syrk_trailing",
+ * "panel_kernel", "trsm_pair_kernel", "gemm_kernel", ... */
+int rbpg_context_set_profiling(rbpg_context* ctx, int enable, rbpg_status* st);
+int rbpg_context_profile_get(rbpg_context* ctx, const char* name, double* total_ms, uint64_t* count,
+                             rbpg_status* st);
 
 /* ---- host utilities (no device work) */
 /* init_hidden (elm.cpp:74-91): W (inputs x hidden), b (hidden) from mt19937_64(seed) */

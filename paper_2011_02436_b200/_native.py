@@ -54,6 +54,8 @@ SIGNATURES = {
     "rbpg_context_set_stream": (c_int, [P, P, ST]),
     "rbpg_context_synchronize": (c_int, [P, ST]),
     "rbpg_context_launch_count": (c_uint64, [P]),
+    "rbpg_context_set_profiling": (c_int, [P, c_int, ST]),
+    "rbpg_context_profile_get": (c_int, [P, ctypes.c_char_p, POINTER(c_double), POINTER(c_uint64), ST]),
     "rbpg_init_hidden": (c_int, [c_size_t, c_size_t, c_size_t, c_uint64, P, P, ST]),
     "rbpg_accuracy": (c_int, [P, c_size_t, c_size_t, P, c_size_t, c_size_t, POINTER(c_double), ST]),
     "rbpg_synth_classification": (c_int, [c_size_t, c_size_t, c_size_t, c_size_t, c_uint64, c_uint64, c_double, P, P, ST]),

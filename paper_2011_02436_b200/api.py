@@ -210,6 +210,22 @@ class Context:
         self.lib.rbpg_context_synchronize(self.handle, ctypes.byref(st))
         _raise(st)
 
+    def set_profiling(self, enable: bool) -> None:
+        """Per-kernel-class CUDA-event timing on the context stream (resets counters)."""
+        st = rbpg_status()
+        self.lib.rbpg_context_set_profiling(self.handle, int(enable), ctypes.byref(st))
+        _raise(st)
+
+    def profile(self, name: str):
+        """(total_ms, launches) recorded for kernel class `name` since profiling was enabled."""
+        ms = ctypes.c_double()
+        cnt = ctypes.c_uint64()
+        st = rbpg_status()
+        self.lib.rbpg_context_profile_get(self.handle, name.encode(), ctypes.byref(ms), ctypes.byref(cnt),
+                                          ctypes.byref(st))
+        _raise(st)
+        return float(ms.value), int(cnt.value)
+
     @property
     def launch_count(self) -> int:
         return int(self.lib.rbpg_context_launch_count(self.handle))

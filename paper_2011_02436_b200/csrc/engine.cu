@@ -34,12 +34,12 @@ cudaError_t launch_syrk_finish(const SyrkParams&, int, int, int, cudaStream_t);
 cudaError_t launch_gemm(const GemmParams&, cudaStream_t);
 cudaError_t launch_factor_setup(const double*, long long, int, long long, double, int, double*, int*, FactorState*,
                                 cudaStream_t);
-cudaError_t launch_panel(const PanelParams&, int, cudaStream_t);
-int panel_max_ctas(int, int, int);
+cudaError_t launch_panel(const PanelParams&, int, int*, cudaStream_t);
 cudaError_t launch_gather_factor(const double*, long long, const int*, int, double*, long long, int, cudaStream_t);
 cudaError_t launch_gather_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
 cudaError_t launch_scatter_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
-cudaError_t launch_trsm_pair(const double*, long long, double*, long long, int, int, int, int, int, cudaStream_t);
+cudaError_t launch_trsm_pair(const double*, long long, double*, long long, int, int, int, int, int, double*,
+                             cudaStream_t);
 cudaError_t launch_accuracy(const double*, long long, const double*, long long, long long, int, unsigned long long*,
                             int, cudaStream_t);
 cudaError_t launch_add_diag(double*, long long, int, double, cudaStream_t);
@@ -108,9 +108,53 @@ struct rbpg_context {
     return p;
   }
   double* dbuf(const std::string& name, size_t elems) { return static_cast<double*>(buf(name, elems * 8)); }
-  void chk(cudaError_t e, const char* what) {
-    ck(e, what);
+  // per-kernel-class device timing (bench.py roofline evidence), off by default
+  bool profile = false;
+  struct Prof {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    double ms = 0.0;
+    uint64_t count = 0;
+  };
+  std::map<std::string, Prof> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t take_event() {
+    if (!ev_pool.empty()) {
+      cudaEvent_t e = ev_pool.back();
+      ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+  }
+  template <typename F>
+  void run(const char* name, F&& launch) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (profile) {
+      a = take_event();
+      b = take_event();
+      cudaEventRecord(a, stream);
+    }
+    ck(launch(), name);
     ++launches;
+    if (profile) {
+      cudaEventRecord(b, stream);
+      prof[name].pending.emplace_back(a, b);
+    }
+  }
+  void collect() {
+    cudaStreamSynchronize(stream);
+    for (auto& kv : prof) {
+      for (auto& pr : kv.second.pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pr.first, pr.second);
+        kv.second.ms += ms;
+        kv.second.count += 1;
+        ev_pool.push_back(pr.first);
+        ev_pool.push_back(pr.second);
+      }
+      kv.second.pending.clear();
+    }
   }
 };
 
@@ -142,7 +186,7 @@ void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_
   CUtensorMap tmX = make_map(ctx, dX, d, N, ldx, 16, kTile, true);
   CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, kTile, kBK, false);
   HiddenParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), db, dH, static_cast<long long>(ldh)};
-  ctx->chk(launch_hidden(tmX, tmW, p, ctx->stream), "hidden_kernel");
+  ctx->run("hidden_kernel", [&] { return launch_hidden(tmX, tmW, p, ctx->stream); });
 }
 
 // G (+)= A^T A over rows [0, N) of A (N x L, ld lda); HtT (+)= A^T T when m > 0.
@@ -155,10 +199,22 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
   p.nGram = p.nbI * (p.nbI + 1) / 2;
   p.nbT = m > 0 ? static_cast<int>((m + kTile - 1) / kTile) : 0;
   const int tiles = p.nGram + p.nbI * p.nbT;
+  // split-K count: fill whole waves of one CTA per SM (wave quantisation), each split >= 1024 rows
   int splits = 1;
-  if (tiles < 2 * ctx->num_sms) splits = std::max(1, (2 * ctx->num_sms + tiles - 1) / tiles);
-  splits = std::min<int>(splits, 32);
-  splits = std::max<int>(1, std::min<int>(splits, static_cast<int>(N / 1024)));
+  if (tiles < 4 * ctx->num_sms) {
+    double best = -1.0;
+    for (int s = 1; s <= 32; ++s) {
+      if (s > 1 && N / static_cast<size_t>(s) < 1024) break;
+      const long long ctas = static_cast<long long>(tiles) * s;
+      const long long waves = (ctas + ctx->num_sms - 1) / ctx->num_sms;
+      const double eff = static_cast<double>(ctas) / static_cast<double>(waves * ctx->num_sms);
+      const double score = eff - 0.004 * s;
+      if (score > best + 1e-12) {
+        best = score;
+        splits = s;
+      }
+    }
+  }
   long long per = static_cast<long long>(round_up((N + splits - 1) / splits, kBK));
   if (per == 0) per = kBK;
   splits = static_cast<int>((N + per - 1) / per);
@@ -188,24 +244,26 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
   }
   CUtensorMap tmA = make_map(ctx, dA, L, N, lda, kTile, kBK, false);
   CUtensorMap tmB = m > 0 ? make_map(ctx, dT, m, N, ldt_in, kTile, kBK, false) : tmA;
-  ctx->chk(launch_syrk(tmA, tmB, p, splits, ctx->stream), "syrk_kernel");
-  if (!direct) ctx->chk(launch_syrk_finish(p, splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream), "syrk_finish");
+  ctx->run("syrk_kernel", [&] { return launch_syrk(tmA, tmB, p, splits, ctx->stream); });
+  if (!direct) ctx->run("syrk_finish", [&] { return launch_syrk_finish(p, splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
 }
 
 void gemm_dev(rbpg_context* ctx, int M, int N, int K, const double* A, size_t lda, bool tA, const double* B,
               size_t ldb, bool tB, double* C, size_t ldc, double alpha, double beta) {
   GemmParams p{M, N, K, A, static_cast<long long>(lda), tA ? 1 : 0, B, static_cast<long long>(ldb), tB ? 1 : 0,
                C, static_cast<long long>(ldc), alpha, beta};
-  ctx->chk(launch_gemm(p, ctx->stream), "gemm_kernel");
+  ctx->run("gemm_kernel", [&] { return launch_gemm(p, ctx->stream); });
 }
 
 // X (n x m, ld ldx) <- (F F^T)^{-1} X, column chunks of <= 128 right-hand sides
 void trsm_pair_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X, size_t ldx, size_t n, size_t m) {
   for (size_t c0 = 0; c0 < m; c0 += 128) {
     const int mc = static_cast<int>(std::min<size_t>(128, m - c0));
-    ctx->chk(launch_trsm_pair(F, static_cast<long long>(ldf), X + c0, static_cast<long long>(ldx),
-                              static_cast<int>(n), mc, 1, 1, ctx->num_sms, ctx->stream),
-             "trsm_pair_kernel");
+    double* dinv = ctx->dbuf("trsm.dinv", ((n + 63) / 64) * 64 * 64);
+    ctx->run("trsm_pair_kernel", [&] {
+      return launch_trsm_pair(F, static_cast<long long>(ldf), X + c0, static_cast<long long>(ldx), static_cast<int>(n),
+                              mc, 1, 1, ctx->num_sms, dinv, ctx->stream);
+    });
   }
 }
 
@@ -237,26 +295,21 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
   FactorState* st = static_cast<FactorState*>(ctx->buf(tag + ".state", sizeof(FactorState)));
 
   ck(cudaMemsetAsync(Fo, 0, sizeof(double) * n * ldn, s), "memset Fo");
+  unsigned long long* trace = nullptr;
+  if (std::getenv("RBPG_PANEL_TRACE")) {
+    trace = static_cast<unsigned long long*>(ctx->buf(tag + ".ptrace", 48));
+    ck(cudaMemsetAsync(trace, 0, 48, s), "memset trace");
+  }
   ck(cudaMemsetAsync(Pg, 0, sizeof(double) * n * 64, s), "memset Pg");
   ck(cudaMemsetAsync(slots, 0, sizeof(PivotSlot) * 2 * (max_ctas + 32), s), "memset slots");
   ck(cudaMemcpy2DAsync(Ga, ldn * 8, dG, ldg * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "copy G");
-  ctx->chk(launch_factor_setup(Ga, static_cast<long long>(ldn), static_cast<int>(n),
-                               static_cast<long long>(rows_for_tol), tol, pivoting, dv[0], ov[0], st, s),
-           "factor_setup");
+  ctx->run("factor_setup", [&] { return launch_factor_setup(Ga, static_cast<long long>(ldn), static_cast<int>(n),
+                               static_cast<long long>(rows_for_tol), tol, pivoting, dv[0], ov[0], st, s); });
   double* gcur = Ga;
   double* gnext = Gb;
   int cur = 0;
   for (size_t k = 0; k < n; k += 64) {
     const int kb = static_cast<int>(std::min<size_t>(64, n - k));
-    const int nl = static_cast<int>(n - k);
-    int R = std::max(32, (nl + ctx->num_sms - 1) / ctx->num_sms);
-    int C = (nl + R - 1) / R;
-    const int cap = panel_max_ctas(nl, R, ctx->num_sms);
-    if (cap < 1) fail(RBPG_CUDA_ERROR, "panel kernel cannot be resident (shared memory)");
-    while (C > std::min(cap, max_ctas)) {
-      R *= 2;
-      C = (nl + R - 1) / R;
-    }
     PanelParams pp{};
     pp.G = gcur;
     pp.ldg = static_cast<long long>(ldn);
@@ -276,8 +329,9 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     pp.Fo = Fo;
     pp.ldf = static_cast<long long>(ldn);
     pp.pivoting = pivoting;
-    pp.rows_per_cta = R;
-    ctx->chk(launch_panel(pp, C, s), "panel_kernel");
+    pp.rows_per_cta = 0;  // chosen by launch_panel
+    pp.trace = trace;
+    ctx->run("panel_kernel", [&] { return launch_panel(pp, ctx->num_sms, nullptr, s); });
     const size_t t0 = k + kb;
     if (t0 < n) {
       const size_t nrem = n - t0;
@@ -295,17 +349,23 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
       sp.Gold = gcur;
       sp.lab = lab;
       sp.off = static_cast<int>(t0);
-      ctx->chk(launch_syrk(tm, tm, sp, 1, s), "syrk_trailing");
+      ctx->run("syrk_trailing", [&] { return launch_syrk(tm, tm, sp, 1, s); });
       std::swap(gcur, gnext);
     }
     cur = 1 - cur;
   }
-  ctx->chk(launch_gather_factor(Fo, static_cast<long long>(ldn), ov[cur], static_cast<int>(n), F,
-                                static_cast<long long>(ldn), ctx->num_sms, s),
-           "gather_factor");
+  ctx->run("gather_factor", [&] { return launch_gather_factor(Fo, static_cast<long long>(ldn), ov[cur], static_cast<int>(n), F,
+                                static_cast<long long>(ldn), ctx->num_sms, s); });
   FactorResult r;
   ck(cudaMemcpyAsync(&r.st, st, sizeof(FactorState), cudaMemcpyDeviceToHost, s), "read factor state");
   ck(cudaStreamSynchronize(s), "factor sync");
+  if (trace) {
+    unsigned long long h[6];
+    cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
+    const double st = double(h[5] ? h[5] : 1);
+    std::fprintf(stderr, "[panel trace %s n=%zu] steps %llu cycles/step: barrier %.0f winner+row %.0f update %.0f reduce+sync %.0f publish %.0f\n",
+                 tag.c_str(), n, h[5], h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st);
+  }
   r.F = F;
   r.ldF = ldn;
   r.ord = ov[cur];
@@ -319,7 +379,7 @@ FactorResult spd_with_ridge(rbpg_context* ctx, const double* dA, size_t lda, siz
   FactorResult f = factor_dev(ctx, dA, lda, n, n, 0.0, 0, tag);
   if (!f.st.fail) return f;
   double* tr = ctx->dbuf(tag + ".trace", 1);
-  ctx->chk(launch_trace(dA, static_cast<long long>(lda), static_cast<int>(n), tr, ctx->stream), "trace");
+  ctx->run("trace", [&] { return launch_trace(dA, static_cast<long long>(lda), static_cast<int>(n), tr, ctx->stream); });
   double htr = 0.0;
   ck(cudaMemcpyAsync(&htr, tr, 8, cudaMemcpyDeviceToHost, ctx->stream), "read trace");
   ck(cudaStreamSynchronize(ctx->stream), "trace sync");
@@ -327,7 +387,7 @@ FactorResult spd_with_ridge(rbpg_context* ctx, const double* dA, size_t lda, siz
   if (eps <= 0.0) eps = ridge;
   double* R = ctx->dbuf(tag + ".ridge", n * lda);
   ck(cudaMemcpyAsync(R, dA, sizeof(double) * n * lda, cudaMemcpyDeviceToDevice, ctx->stream), "copy ridge");
-  ctx->chk(launch_add_diag(R, static_cast<long long>(lda), static_cast<int>(n), eps, ctx->stream), "add_diag");
+  ctx->run("add_diag", [&] { return launch_add_diag(R, static_cast<long long>(lda), static_cast<int>(n), eps, ctx->stream); });
   f = factor_dev(ctx, R, lda, n, n, 0.0, 0, tag);
   if (f.st.fail) {
     Fail e{RBPG_SINGULAR_SPLIT, std::string("singular ") + (block == 0 ? "A" : "D") + " block after ridge retry"};
@@ -379,26 +439,26 @@ void block_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   double* R1 = ctx->dbuf("blk.R1", n1 * lm);
   double* T2 = ctx->dbuf("blk.T2", n2 * lm);
   double* Bp = ctx->dbuf("blk.beta", L * lm);
-  ctx->chk(launch_gather_block(dG, ldg, P2, n2, P2, n2, A, l2, s), "gather A");
-  ctx->chk(launch_gather_block(dG, ldg, P2, n2, P1, n1, G21, l1, s), "gather G21");
-  ctx->chk(launch_gather_block(dG, ldg, P1, n1, P1, n1, D, l1, s), "gather G11");
-  ctx->chk(launch_gather_rows(dHtT, ldt, P2, n2, m, Bm, lm, s), "gather H2tT");
-  ctx->chk(launch_gather_rows(dHtT, ldt, P1, n1, m, R1, lm, s), "gather H1tT");
+  ctx->run("gather A", [&] { return launch_gather_block(dG, ldg, P2, n2, P2, n2, A, l2, s); });
+  ctx->run("gather G21", [&] { return launch_gather_block(dG, ldg, P2, n2, P1, n1, G21, l1, s); });
+  ctx->run("gather G11", [&] { return launch_gather_block(dG, ldg, P1, n1, P1, n1, D, l1, s); });
+  ctx->run("gather H2tT", [&] { return launch_gather_rows(dHtT, ldt, P2, n2, m, Bm, lm, s); });
+  ctx->run("gather H1tT", [&] { return launch_gather_rows(dHtT, ldt, P1, n1, m, R1, lm, s); });
   bool ridge = false;
   FactorResult fa = spd_with_ridge(ctx, A, l2, n2, 1e-8, ridge, 0, "fa");
   trsm_pair_dev(ctx, fa.F, fa.ldF, Bm, lm, n2, m);                                  // B = A^-1 H2^T T
   ck(cudaMemcpy2DAsync(X, l1 * 8, G21, l1 * 8, n1 * 8, n2, cudaMemcpyDeviceToDevice, s), "copy G21");
   trsm_pair_dev(ctx, fa.F, fa.ldF, X, l1, n2, n1);                                  // A^-1 G21
   gemm_dev(ctx, n1, n1, n2, G21, l1, true, X, l1, false, D, l1, -1.0, 1.0);         // D = G11 - G21^T A^-1 G21
-  ctx->chk(launch_symmetrize(D, l1, n1, s), "symmetrize");                          // (D + D^T)/2
+  ctx->run("symmetrize", [&] { return launch_symmetrize(D, l1, n1, s); });                          // (D + D^T)/2
   FactorResult fd = spd_with_ridge(ctx, D, l1, n1, 1e-8, ridge, 1, "fd");
   gemm_dev(ctx, n1, m, n2, G21, l1, true, Bm, lm, false, R1, lm, -1.0, 1.0);        // H1^T(T - H2 B)
   trsm_pair_dev(ctx, fd.F, fd.ldF, R1, lm, n1, m);                                  // beta1
   gemm_dev(ctx, n2, m, n1, G21, l1, false, R1, lm, false, T2, lm, 1.0, 0.0);        // G21 beta1
   trsm_pair_dev(ctx, fa.F, fa.ldF, T2, lm, n2, m);                                  // A^-1 G21 beta1
   ck(cudaMemcpy2DAsync(Bp, lm * 8, R1, lm * 8, m * 8, n1, cudaMemcpyDeviceToDevice, s), "stack beta1");
-  ctx->chk(launch_axpy_rows(Bm, lm, T2, lm, n2, m, Bp + n1 * lm, lm, s), "beta2");  // beta2 = B - ...
-  ctx->chk(launch_scatter_rows(Bp, lm, ord, L, m, dBeta, ldb, s), "unpermute beta");
+  ctx->run("beta2", [&] { return launch_axpy_rows(Bm, lm, T2, lm, n2, m, Bp + n1 * lm, lm, s); });  // beta2 = B - ...
+  ctx->run("unpermute beta", [&] { return launch_scatter_rows(Bp, lm, ord, L, m, dBeta, ldb, s); });
   if (ridge && diag) diag->ridge_applied = 1;
 }
 
@@ -458,9 +518,9 @@ void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   if (rank == L) {
     const size_t lm = even(m);
     double* rhs = ctx->dbuf("rank.rhs", L * lm);
-    ctx->chk(launch_gather_rows(dHtT, ldt, f.ord, L, m, rhs, lm, ctx->stream), "gather rhs");
+    ctx->run("gather rhs", [&] { return launch_gather_rows(dHtT, ldt, f.ord, L, m, rhs, lm, ctx->stream); });
     trsm_pair_dev(ctx, f.F, f.ldF, rhs, lm, L, m);
-    ctx->chk(launch_scatter_rows(rhs, lm, f.ord, L, m, dBeta, ldb, ctx->stream), "unpermute beta");
+    ctx->run("unpermute beta", [&] { return launch_scatter_rows(rhs, lm, f.ord, L, m, dBeta, ldb, ctx->stream); });
     return;
   }
   try {
@@ -475,9 +535,8 @@ void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
 void check_finite(rbpg_context* ctx, const double* dBeta, size_t ldb, size_t L, size_t m) {
   int* flag = static_cast<int*>(ctx->buf("nonfinite", 4));
   ck(cudaMemsetAsync(flag, 0, 4, ctx->stream), "memset flag");
-  ctx->chk(launch_nonfinite(dBeta, static_cast<long long>(ldb), static_cast<int>(L), static_cast<int>(m), flag,
-                            ctx->stream),
-           "nonfinite");
+  ctx->run("nonfinite", [&] { return launch_nonfinite(dBeta, static_cast<long long>(ldb), static_cast<int>(L), static_cast<int>(m), flag,
+                            ctx->stream); });
   int h = 0;
   ck(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, ctx->stream), "read flag");
   ck(cudaStreamSynchronize(ctx->stream), "sync");
@@ -576,9 +635,8 @@ uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const d
       }
       gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(L), H, hld, false, dBeta, ldb, false,
                S, lm, 1.0, 0.0);
-      ctx->chk(launch_accuracy(S, static_cast<long long>(lm), dT + r0 * ldt_in, static_cast<long long>(ldt_in),
-                               static_cast<long long>(nr), static_cast<int>(m), hits, ctx->num_sms, ctx->stream),
-               "accuracy");
+      ctx->run("accuracy", [&] { return launch_accuracy(S, static_cast<long long>(lm), dT + r0 * ldt_in, static_cast<long long>(ldt_in),
+                               static_cast<long long>(nr), static_cast<int>(m), hits, ctx->num_sms, ctx->stream); });
     }
   }
   unsigned long long h = 0;
@@ -699,6 +757,24 @@ int rbpg_context_synchronize(rbpg_context* ctx, rbpg_status* st) {
   return guarded(ctx, st, [&] { ck(cudaStreamSynchronize(ctx->stream), "sync"); });
 }
 uint64_t rbpg_context_launch_count(const rbpg_context* ctx) { return ctx ? ctx->launches : 0; }
+
+int rbpg_context_set_profiling(rbpg_context* ctx, int enable, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    ctx->collect();
+    ctx->prof.clear();
+    ctx->profile = enable != 0;
+  });
+}
+
+int rbpg_context_profile_get(rbpg_context* ctx, const char* name, double* total_ms, uint64_t* count,
+                             rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    ctx->collect();
+    auto it = ctx->prof.find(name);
+    *total_ms = it == ctx->prof.end() ? 0.0 : it->second.ms;
+    *count = it == ctx->prof.end() ? 0 : it->second.count;
+  });
+}
 
 int rbpg_hidden_matrix(rbpg_context* ctx, const double* w, const double* b, size_t d, size_t l, const double* x,
                        size_t n, size_t xcols, double* h, rbpg_status* st) {

@@ -29,8 +29,11 @@ __device__ __forceinline__ int swz16(int row, int col) {
   return row * 16 + ((((col >> 1) ^ (row & 7)) << 1) | (col & 1));
 }
 
+// Round a dynamic-shared-memory pointer up to 1024 B (128B-swizzle atom) by pointer
+// arithmetic on the shared base, so the compiler keeps shared-window addressing (LDS,
+// not generic LD) for every derived pointer.
 __device__ __forceinline__ unsigned char* align1024(unsigned char* p) {
-  return reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
 }  // namespace

@@ -1,0 +1,474 @@
+// K3: one panel (<= 64 columns) of the diagonal-pivoted blocked Cholesky of the Gram
+// matrix -- reference linalg.cpp:197-236: pivot = first maximum of the running diagonal d
+// over positions >= j (strict '>', :207-210), swaps (:211-218), stop rule rjj <= cut
+// (:219-223), column update col = (G[:,j] - F[:,k:j] F[j,k:j]^T) / rjj and d -= col^2
+// (:225-235).  With pivoting = 0 the same kernel is the unpivoted SpdFactor panel with the
+// reference's singular-pivot rule (linalg.cpp:116-129).
+//
+// Labels instead of swaps: every CTA owns a contiguous range of labels (a label is the
+// column's position at panel start) and keeps, in shared memory, its labels' running
+// diagonal and panel columns (stored transposed, PsT[c][label]).  Positions are tracked by
+// two replicated maps (lab_at, pos_of) that every CTA updates identically, so a swap is O(1).
+// The arg-max key is (d, -position): an order-preserving 64-bit image of d reduced with three
+// warp REDUX ops (max hi word, max lo word, min position), which is exactly the reference's
+// first-maximum scan.
+//
+// Latency structure of one column step (the loop is strictly sequential over L columns):
+//   exchange -> every warp reads all CTAs' candidates and resolves the winner itself
+//   fetch    -> every warp loads the pivot's panel row and the G entries of its own labels
+//   update   -> quad (4 lanes) per label, fused local arg-max, ONE __syncthreads, warp 0
+//               combines the 8 warp candidates, applies the swap, publishes.
+// Exchange variants:
+//   * cluster (nl <= 16 * 256): the panel runs in ONE thread-block cluster; candidates sit in
+//     each CTA's shared memory, one barrier.cluster per column, the pivot's panel row is read
+//     from its owner through distributed shared memory;
+//   * grid (larger panels): cooperative grid, candidates in global slots with release/acquire
+//     epochs, the panel row mirrored to global memory.
+#include "common.cuh"
+#include "kernels.cuh"
+
+#include <cooperative_groups.h>
+#include <cfloat>
+#include <climits>
+
+namespace cg = cooperative_groups;
+
+namespace rbpg {
+
+constexpr int kPanelW = 64;
+constexpr int kPThreads = 256;
+constexpr int kPWarps = kPThreads / 32;
+constexpr int kMaxCluster = 16;
+constexpr int kMaxLabelsPerCta = 256;
+
+// order-preserving image of a double (larger value <=> larger unsigned key)
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  const unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(v));
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dkey_inv(unsigned long long k) {
+  const unsigned long long u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double(static_cast<long long>(u));
+}
+
+// warp arg-max: largest key, ties -> smallest position.  All lanes get the result.
+__device__ __forceinline__ void warp_argmax(unsigned long long& key, int& pos) {
+  const unsigned hi = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(key >> 32));
+  const unsigned lo =
+      __reduce_max_sync(0xffffffffu, static_cast<unsigned>(key >> 32) == hi ? static_cast<unsigned>(key) : 0u);
+  const unsigned long long best = (static_cast<unsigned long long>(hi) << 32) | lo;
+  pos = static_cast<int>(__reduce_min_sync(0xffffffffu, key == best ? static_cast<unsigned>(pos) : 0x7fffffffu));
+  key = best;
+}
+
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+
+struct __align__(16) Cand {
+  unsigned long long key;
+  int pos;
+  int pad;
+};
+
+template <bool kCluster>
+__global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = p.n, k = p.k, kb = p.kb, nl = n - k;
+  const int R = p.rows_per_cta;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  int C, cta;
+  if constexpr (kCluster) {
+    cg::cluster_group cl = cg::this_cluster();
+    C = static_cast<int>(cl.num_blocks());
+    cta = static_cast<int>(cl.block_rank());
+  } else {
+    C = gridDim.x;
+    cta = blockIdx.x;
+  }
+
+  double* PsT = reinterpret_cast<double*>(smem_raw);  // [64][R]
+  double* dl = PsT + kPanelW * R;                      // [R]
+  int* lab_at = reinterpret_cast<int*>(dl + R);       // [nl]  position-k -> label
+  int* pos_of = lab_at + nl;                          // [nl]  label-k -> position
+  // cluster: every CTA's candidate and its panel row, pushed by the owner before the barrier
+  __shared__ Cand cand_all[2][kMaxCluster];
+  __shared__ __align__(16) double rows_all[2][kMaxCluster][kPanelW];
+  __shared__ Cand wbest[kPWarps];
+  __shared__ int s_stop;
+
+  FactorState* st = p.st;
+  if (st->stopped) {  // an earlier panel ended the factorisation: carry the order through
+    if (cta == 0)
+      for (int i = tid; i < n; i += blockDim.x) p.ord_out[i] = p.ord_in[i];
+    return;
+  }
+  const int lbeg = k + cta * R;
+  const int lend = min(n, lbeg + R);
+  const int nown = max(0, lend - lbeg);
+
+  for (int i = tid; i < nl; i += blockDim.x) {
+    lab_at[i] = k + i;
+    pos_of[i] = k + i;
+  }
+  for (int i = tid; i < kPanelW * R; i += blockDim.x) PsT[i] = 0.0;
+  for (int i = tid; i < R; i += blockDim.x) dl[i] = (i < nown) ? p.d_in[lbeg + i] : -DBL_MAX;
+  if (tid == 0) s_stop = 0;
+  __syncthreads();
+  const double cut = st->cut;
+  const double thresh = st->thresh;
+
+  // warp 0: combine the per-warp candidates and publish this CTA's candidate for step j.
+  // Cluster: push (key, pos) and the candidate's panel row (columns 0..j-k-1) into every CTA's
+  // shared memory; the next barrier.cluster (release/acquire) makes them visible.
+  auto combine_publish = [&](int j) {
+    if (warp != 0) return;
+    unsigned long long key = 0;
+    int pos = INT_MAX;
+    if (lane < kPWarps) {
+      key = wbest[lane].key;
+      pos = wbest[lane].pos;
+    }
+    warp_argmax(key, pos);
+    if constexpr (kCluster) {
+      __syncwarp();
+      const int cvalid = j - k;  // panel columns already computed
+      double2 rv = make_double2(0.0, 0.0);
+      if (pos != INT_MAX) {
+        const int lib = lab_at[pos - k] - lbeg;
+        if (2 * lane < cvalid) rv.x = PsT[(2 * lane) * R + lib];
+        if (2 * lane + 1 < cvalid) rv.y = PsT[(2 * lane + 1) * R + lib];
+      }
+      cg::cluster_group cl = cg::this_cluster();
+      const int par = j & 1;
+      for (int d = 0; d < C; ++d) {
+        double2* dst = reinterpret_cast<double2*>(cl.map_shared_rank(&rows_all[par][cta][0], d));
+        dst[lane] = rv;
+      }
+      if (lane < C) {
+        Cand* dc = cl.map_shared_rank(&cand_all[par][cta], lane);
+        *reinterpret_cast<ulonglong2*>(dc) = make_ulonglong2(key, static_cast<unsigned long long>(pos));
+      }
+    } else if (lane == 0) {
+      PivotSlot* sl = p.slots + (j & 1) * C + cta;
+      *reinterpret_cast<unsigned long long*>(&sl->val) = key;
+      sl->pos = pos;
+      st_release_u32(&sl->epoch, static_cast<unsigned int>(j + 1));
+    }
+  };
+
+  // ---- initial candidates for step k
+  {
+    unsigned long long key = 0;
+    int pos = INT_MAX;
+    if (p.pivoting) {
+      for (int i = tid; i < nown; i += kPThreads) {
+        const unsigned long long kk = dkey(dl[i]);
+        if (kk > key || (kk == key && lbeg + i < pos)) {
+          key = kk;
+          pos = lbeg + i;
+        }
+      }
+    } else if (k >= lbeg && k < lend && tid == 0) {
+      key = dkey(dl[k - lbeg]);
+      pos = k;
+    }
+    warp_argmax(key, pos);
+    if (lane == 0) {
+      wbest[warp].key = key;
+      wbest[warp].pos = pos;
+    }
+    __syncthreads();
+    combine_publish(k);
+  }
+
+  unsigned long long* trace = p.trace;
+  long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  __shared__ unsigned long long s_wkey;
+  __shared__ int s_piv, s_xp, s_y;
+  __shared__ double prow[kPanelW];
+  for (int c = 0; c < kb; ++c) {
+    const int j = k + c;
+    long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    if (trace) t0 = clock64();
+    // ---------------- exchange: warp 0 resolves the winner and fetches its panel row
+    if constexpr (kCluster) cg::this_cluster().sync();
+    if (trace) t1 = clock64();
+    if (warp == 0) {
+      unsigned long long wkey = 0;
+      int wpos = INT_MAX;
+      if constexpr (kCluster) {
+        if (lane < C) {
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&cand_all[j & 1][lane]);
+          wkey = v.x;
+          wpos = static_cast<int>(v.y & 0xffffffffull);
+        }
+      } else {
+        const PivotSlot* base = p.slots + (j & 1) * C;
+        for (int i = lane; i < C; i += 32) {
+          while (ld_acquire_u32(&base[i].epoch) != static_cast<unsigned int>(j + 1)) {
+          }
+          const unsigned long long kk = __ldcg(reinterpret_cast<const unsigned long long*>(&base[i].val));
+          const int ps = __ldcg(&base[i].pos);
+          if (kk > wkey || (kk == wkey && ps < wpos)) {
+            wkey = kk;
+            wpos = ps;
+          }
+        }
+      }
+      warp_argmax(wkey, wpos);
+      const int xpw = lab_at[wpos - k];
+      if (lane == 0) {
+        s_wkey = wkey;
+        s_piv = wpos;
+        s_xp = xpw;
+        s_y = lab_at[j - k];
+      }
+      named_bar_arrive(1, kPThreads);  // winner known to the CTA
+      // pivot panel row
+      double v0 = 0.0, v1 = 0.0;
+      if constexpr (kCluster) {
+        // the row was pushed with the candidate: slot of the CTA whose candidate won
+        const unsigned m = __ballot_sync(0xffffffffu, lane < C && cand_all[j & 1][lane].key == wkey &&
+                                                          cand_all[j & 1][lane].pos == wpos);
+        const double* rp = rows_all[j & 1][__ffs(m) - 1];
+        v0 = rp[lane];
+        v1 = rp[lane + 32];
+      } else {
+        const double* rp = p.Pg + (long long)(xpw - k) * kPanelW;
+        if (lane < c) v0 = __ldcg(rp + lane);
+        if (lane + 32 < c) v1 = __ldcg(rp + lane + 32);
+      }
+      prow[lane] = v0;
+      prow[lane + 32] = v1;
+      named_bar_arrive(2, kPThreads);  // panel row staged
+    } else {
+      named_bar_sync(1, kPThreads);
+    }
+    const int piv = s_piv, xp = s_xp, y = s_y;
+    const double dj = dkey_inv(s_wkey);
+    // this warp's first-pass G entries, issued before the FP64 math and the panel-row wait
+    const double* grow = p.G + (long long)xp * p.ldg;
+    double gpre = 0.0;
+    {
+      const int li0 = warp * 8 + (lane >> 2);
+      if ((lane & 3) == 0 && li0 < nown) gpre = grow[lbeg + li0];
+    }
+    bool stop;
+    if (p.pivoting) {
+      stop = (dj > 0.0 ? sqrt(dj) : 0.0) <= cut;                 // linalg.cpp:219-223
+    } else {
+      stop = !isfinite(dj) || dj <= thresh || dj <= 0.0;        // linalg.cpp:118-119
+    }
+    if (warp != 0) named_bar_sync(2, kPThreads);
+    if (stop) {
+      __syncthreads();  // every warp has read the maps for this step
+      if (tid == 0) {
+        // the swap at step j happens before the stop test in the reference
+        if (piv != j) {
+          lab_at[j - k] = xp;
+          lab_at[piv - k] = y;
+          pos_of[xp - k] = j;
+          pos_of[y - k] = piv;
+        }
+        s_stop = p.pivoting ? 1 : 2;
+        if (cta == 0) {
+          st->stopped = 1;
+          st->rank = j;
+          if (!p.pivoting) {
+            st->fail = 1;
+            st->fail_index = j;
+            st->fail_value = dj;
+          }
+        }
+      }
+      __syncthreads();
+      break;
+    }
+    const double rjj = sqrt(dj);
+    const double inv_rjj = 1.0 / rjj;
+    if (tid == 0 && (xp - k) / R == cta) {
+      const int oli = (xp - k) % R;
+      PsT[c * R + oli] = rjj;  // F(j, j) = rjj
+      if constexpr (!kCluster) p.Pg[(long long)(xp - k) * kPanelW + c] = rjj;
+    }
+    __syncwarp();
+    if (trace) t2 = clock64();
+
+    // ---------------- update: quad (4 lanes) per label; warp w owns labels w*8 + 64*pass + lane/4
+    unsigned long long bkey = 0;
+    int bpos = INT_MAX;
+    for (int base = warp * 8; base < nown; base += kPThreads / 4) {
+      const int li = base + (lane >> 2);
+      const int q = lane & 3;
+      const int x = lbeg + li;
+      // position after this step's swap, without touching the shared maps
+      int pos = -1;
+      if (li < nown) pos = (x == y) ? piv : (x == xp ? j : pos_of[x - k]);
+      const bool alive = pos > j;
+      const double gv = (alive && q == 0) ? (base == warp * 8 ? gpre : grow[x]) : 0.0;
+      double s = 0.0;
+      if (alive) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int cc = q;
+        for (; cc + 12 < c; cc += 16) {
+          a0 = fma(PsT[cc * R + li], prow[cc], a0);
+          a1 = fma(PsT[(cc + 4) * R + li], prow[cc + 4], a1);
+          a2 = fma(PsT[(cc + 8) * R + li], prow[cc + 8], a2);
+          a3 = fma(PsT[(cc + 12) * R + li], prow[cc + 12], a3);
+        }
+        for (; cc < c; cc += 4) a0 = fma(PsT[cc * R + li], prow[cc], a0);
+        s = (a0 + a1) + (a2 + a3);
+      }
+      const double s1 = __shfl_down_sync(0xffffffffu, s, 1, 4);
+      const double s2 = __shfl_down_sync(0xffffffffu, s, 2, 4);
+      const double s3 = __shfl_down_sync(0xffffffffu, s, 3, 4);
+      if (alive && q == 0) {
+        const double tot = (s + s1) + (s2 + s3);
+        const double col = (gv - tot) * inv_rjj;
+        PsT[c * R + li] = col;
+        if constexpr (!kCluster) p.Pg[(long long)(x - k) * kPanelW + c] = col;
+        const double dn = fma(-col, col, dl[li]);
+        dl[li] = dn;
+        const unsigned long long kk = dkey(dn);
+        if (p.pivoting) {
+          if (kk > bkey || (kk == bkey && pos < bpos)) {
+            bkey = kk;
+            bpos = pos;
+          }
+        } else if (pos == j + 1) {
+          bkey = kk;
+          bpos = pos;
+        }
+      }
+    }
+    if (trace) t3 = clock64();
+    warp_argmax(bkey, bpos);
+    if (lane == 0) {
+      wbest[warp].key = bkey;
+      wbest[warp].pos = bpos;
+    }
+    __syncthreads();
+    if (trace) t4 = clock64();
+    if (tid == 0 && piv != j) {  // apply the swap (linalg.cpp:211-218) to the replicated maps
+      lab_at[j - k] = xp;
+      lab_at[piv - k] = y;
+      pos_of[xp - k] = j;
+      pos_of[y - k] = piv;
+    }
+    if (c + 1 < kb) combine_publish(j + 1);
+    if (trace) {
+      const long long t5 = clock64();
+      tacc[0] += t1 - t0;
+      tacc[1] += t2 - t1;
+      tacc[2] += t3 - t2;
+      tacc[3] += t4 - t3;
+      tacc[4] += t5 - t4;
+      tacc[5] += 1;
+    }
+    __syncthreads();  // maps settled before the next step reads them
+  }
+  if (trace && cta == 0 && tid == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd(&trace[i], static_cast<unsigned long long>(tacc[i]));
+  if constexpr (kCluster) cg::this_cluster().sync();  // no CTA leaves while its smem may be read
+  __syncthreads();
+
+  // ---- write back: factor rows by original column, compacted trailing panel, d, order
+  for (int e = tid; e < nown * kPanelW; e += blockDim.x) {
+    const int li = e / kPanelW, cc = e % kPanelW;
+    if (cc >= kb) continue;
+    const int x = lbeg + li;
+    p.Fo[(long long)p.ord_in[x] * p.ldf + k + cc] = PsT[cc * R + li];
+  }
+  if (!s_stop) {
+    const int t0 = k + kb;
+    for (int e = tid; e < nown * kPanelW; e += blockDim.x) {
+      const int li = e / kPanelW, cc = e % kPanelW;
+      if (cc >= kb) continue;
+      const int pos = pos_of[lbeg + li - k];
+      if (pos >= t0) p.PcT[(long long)cc * p.ldp + (pos - t0)] = PsT[cc * R + li];
+    }
+    for (int li = tid; li < nown; li += blockDim.x) {
+      const int pos = pos_of[lbeg + li - k];
+      if (pos >= t0) p.d_out[pos] = dl[li];
+    }
+  }
+  for (int pos = cta * blockDim.x + tid; pos < n; pos += C * blockDim.x) {
+    if (pos < k) {
+      p.ord_out[pos] = p.ord_in[pos];
+    } else {
+      const int lb = lab_at[pos - k];
+      p.ord_out[pos] = p.ord_in[lb];
+      p.lab_out[pos] = lb;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+size_t panel_smem_bytes(int nl, int R) {
+  return size_t(kPanelW) * R * sizeof(double) + size_t(R) * sizeof(double) + size_t(2) * nl * sizeof(int);
+}
+
+// Cluster size for a panel of nl labels (0 = use the grid variant).
+int panel_cluster_size(int nl) {
+  if (nl <= 256) return nl <= 64 ? 1 : (nl <= 128 ? 2 : 4);
+  if (nl <= 512) return 8;
+  if (nl <= kMaxCluster * kMaxLabelsPerCta) return kMaxCluster;
+  return 0;
+}
+
+cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cudaStream_t s) {
+  const int nl = p.n - p.k;
+  PanelParams pp = p;
+  const int CL = panel_cluster_size(nl);
+  if (CL > 0) {
+    pp.rows_per_cta = (nl + CL - 1) / CL;
+    const size_t smem = panel_smem_bytes(nl, pp.rows_per_cta);
+    static size_t attr = 0;
+    if (smem > attr) {
+      cudaError_t e = cudaFuncSetAttribute(panel_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(panel_kernel_t<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      attr = smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(kPThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (ctas_used) *ctas_used = CL;
+    return cudaLaunchKernelEx(&cfg, panel_kernel_t<true>, pp);
+  }
+  // grid variant: ~ceil(nl / num_sms) labels per CTA, every CTA co-resident (cooperative launch)
+  int R = (nl + num_sms - 1) / num_sms;
+  if (R < 32) R = 32;
+  if (R > kMaxLabelsPerCta) return cudaErrorInvalidValue;  // n > 256 * num_sms unsupported
+  const int C = (nl + R - 1) / R;
+  pp.rows_per_cta = R;
+  const size_t smem = panel_smem_bytes(nl, R);
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(panel_kernel_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  if (ctas_used) *ctas_used = C;
+  void* args[] = {&pp};
+  return cudaLaunchCooperativeKernel((void*)panel_kernel_t<false>, dim3(C), dim3(kPThreads), args, smem, s);
+}
+
+}  // namespace rbpg

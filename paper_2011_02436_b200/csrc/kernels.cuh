@@ -95,6 +95,7 @@ struct PanelParams {
   double* Fo; long long ldf;            // factor rows by original column
   int pivoting;                         // 1 = rank-revealing (diag pivot), 0 = SpdFactor (no pivot)
   int rows_per_cta;
+  unsigned long long* trace;                   // optional per-phase cycle counters (CTA 0, thread 0)
 };
 
 }  // namespace rbpg
