@@ -1,0 +1,81 @@
+"""Row-sharded training across ranks (one process per GPU).
+
+The hot path shards naturally by rows: each rank builds H for its
+contiguous block of rows and its local Gram blocks G_p = H_p^T H_p, (H^T T)_p;
+one all-reduce (sum) of G and H^T T; every rank then runs the identical
+pivoted-Cholesky + triangular solves, so beta is bitwise identical on all
+ranks; training-accuracy hits are a local count plus an all-reduce.
+
+``train_sharded`` is the orchestration; the per-rank numerical stages are a
+pluggable object.  ``DeviceStages`` (the product) runs them through the C ABI on
+the rank's GPU and the all-reduce goes over NCCL/NVLink.  The default tolerance
+uses the GLOBAL row count (reference linalg.cpp:171).
+"""
+from __future__ import annotations
+
+from typing import Optional, Tuple
+
+from . import api
+
+
+def shard_rows(n_total: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous row block of `rank`: (first row, row count); the first n_total % world ranks get one extra."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    base, extra = divmod(n_total, world)
+    row0 = rank * base + min(rank, extra)
+    return row0, base + (1 if rank < extra else 0)
+
+
+class DeviceStages:
+    """Per-rank stages on the local GPU (sm_100a kernels through the C ABI)."""
+
+    def __init__(self, ctx: Optional[api.Context] = None):
+        self.ctx = ctx
+
+    def gram(self, x, t, w, b):
+        import torch
+
+        L, m = w.shape[1], t.shape[1]
+        g = torch.empty((L, L), dtype=torch.float64, device=x.device)
+        htt = torch.empty((L, m), dtype=torch.float64, device=x.device)
+        api.gram_stage_device(x, t, w, b, g, htt, keep_h=True, ctx=self.ctx)
+        return g, htt
+
+    def solve(self, g, htt, n_total: int, strategy: api.SolverStrategy):
+        return api.solve_stage_device(g, htt, n_total, strategy, ctx=self.ctx, return_order=True)
+
+    def hits(self, x, t, w, b, beta) -> int:
+        return api.accuracy_stage_device(x, t, w, b, beta, ctx=self.ctx)
+
+    def as_tensor(self, x, like):
+        import torch
+
+        return torch.as_tensor(x, dtype=torch.float64, device=like.device)
+
+
+def train_sharded(x_local, t_local, params: api.ElmParams, strategy: api.SolverStrategy, n_total: int,
+                  stages=None, group=None, hidden: Optional[api.HiddenLayer] = None):
+    """Row-sharded train(): returns (beta, SolveDiagnostics, HiddenLayer, order).
+
+    x_local / t_local are this rank's contiguous row block (``shard_rows``) as tensors on the
+    rank's device; `stages` provides gram/solve/hits (DeviceStages by default).
+    """
+    import torch
+    import torch.distributed as dist
+
+    stages = stages or DeviceStages()
+    hidden = hidden or api.init_hidden(params)  # identical on every rank (seeded mt19937_64)
+    w = stages.as_tensor(hidden.weights, x_local)
+    b = stages.as_tensor(hidden.biases.reshape(-1), x_local)
+    g, htt = stages.gram(x_local, t_local, w, b)
+    distributed = dist.is_available() and dist.is_initialized()
+    if distributed:
+        dist.all_reduce(g, group=group)
+        dist.all_reduce(htt, group=group)
+    beta, diag, order = stages.solve(g, htt, n_total, strategy)
+    hits = torch.tensor([stages.hits(x_local, t_local, w, b, beta)], dtype=torch.int64, device=g.device)
+    if distributed:
+        dist.all_reduce(hits, group=group)
+    diag.training_accuracy = float(hits.item()) / float(n_total)
+    return beta, diag, hidden, order

@@ -1,0 +1,267 @@
+"""GPU parity on BASELINE.json's configs: the B200 path (C ABI -> sm_100a kernels)
+against the CPU oracle on identical seeded inputs.
+
+Bars (BASELINE.json north_star):
+  * rank, pivot order and predicted labels bit-exact (C3: pivots modulo exact-twin classes);
+  * beta within relative Frobenius max(1e-9, 4 * oracle self-floor), the floor being the
+    oracle's own 1-vs-8-row-shard Gram summation difference;
+  * H within 1e-12 elementwise (reference test_elm.cpp:75);
+  * configs beyond the oracle's reach are checked through size-independent properties
+    (pivots of the oracle factorisation applied to the GPU's own Gram, FF^T = P^T G P,
+    normal-equation backward error, accuracy re-derived from predictions).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2011_02436_b200 as rb
+
+pytestmark = pytest.mark.gpu
+
+SEED_X, SEED_T, SEED_W = 1001, 2001, 3001
+
+
+def rel_fro(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+def self_floor(h, t, tol=0.0):
+    b1, _, _ = oracle.solve_beta(h, t, "rank", 0, tol, 1)
+    b8, _, _ = oracle.solve_beta(h, t, "rank", 0, tol, 8)
+    return rel_fro(b8, b1)
+
+
+def train_both(n, d, L, m, seeds=(SEED_X, SEED_T, SEED_W), tol=0.0):
+    x, t = rb.synth_classification(n, d, m, seeds[0], seeds[1])
+    params = rb.ElmParams(d, L, m, seeds[2])
+    model, diag, order = rb.train(params, x, t, rb.SolverStrategy.rank_based(tol), return_order=True)
+    ref = oracle.train(d, L, m, seeds[2], x, t, "rank", 0, tol)
+    return x, t, model, diag, order, ref
+
+
+@pytest.mark.parametrize("cfg", [
+    pytest.param((2000, 16, 200, 2), id="C1"),
+    pytest.param((50000, 64, 1000, 10), id="C2"),
+])
+def test_train_parity_baseline_configs(cfg):
+    n, d, L, m = cfg
+    x, t, model, diag, order, ref = train_both(n, d, L, m)
+    assert diag.rank == ref["diag"]["rank"] == L
+    assert order == ref["order"], "pivot order differs from the oracle"
+    assert np.array_equal(model.hidden.weights, ref["w"]) and np.array_equal(model.hidden.biases, ref["b"])
+    h_o = oracle.hidden_matrix(ref["w"], ref["b"], x)
+    floor = self_floor(h_o, t)
+    tol = max(1e-9, 4 * floor)
+    err = rel_fro(model.beta, ref["beta"])
+    print(f"{cfg}: beta rel {err:.3e} (floor {floor:.3e}, gate {tol:.1e}), margin {ref['diag']['min_pivot_margin']:.2e}")
+    assert err <= tol
+    assert diag.training_accuracy == ref["diag"]["training_accuracy"]
+    assert diag.split_lo == (L + 1) // 2 and diag.split_hi == L // 2 and not diag.fallback_to_direct
+    # predicted labels on the training rows and on 1000 seeded test rows
+    xt, _ = rb.synth_classification(1000, d, m, SEED_X + 100, SEED_T)
+    for xx in (x, xt):
+        s = rb.predict(model, xx)
+        so = oracle.predict(ref["w"], ref["b"], ref["beta"], xx)
+        assert (s.argmax(1) == so.argmax(1)).all()
+        assert rel_fro(s, so) < 1e-8
+
+
+def test_hidden_matrix_parity_c1():
+    x, _ = rb.synth_classification(2000, 16, 2, SEED_X, SEED_T)
+    hid = rb.init_hidden(rb.ElmParams(16, 200, 2, SEED_W))
+    h = rb.hidden_matrix(hid, x)
+    ho = oracle.hidden_matrix(hid.weights, hid.biases, x)
+    assert np.abs(h - ho).max() < 1e-12
+
+
+@pytest.mark.parametrize("shape", [(5, 3, 1, 1), (40, 5, 10, 3), (129, 7, 65, 3), (300, 33, 129, 5),
+                                   (1000, 17, 257, 7), (4097, 130, 300, 1), (700, 3, 64, 2)])
+def test_train_parity_ragged_shapes(shape):
+    n, d, L, m = shape
+    x, t, model, diag, order, ref = train_both(n, d, L, m, seeds=(n, d + 1, L + 2))
+    assert diag.rank == ref["diag"]["rank"]
+    assert diag.fallback_to_direct == bool(ref["diag"]["fallback_to_direct"])
+    if L >= 2:
+        assert order == ref["order"]
+    if diag.rank == L:
+        assert rel_fro(model.beta, ref["beta"]) < 1e-8
+    else:  # beta is non-unique when rank < L: compare fitted values
+        h = oracle.hidden_matrix(ref["w"], ref["b"], x)
+        assert rel_fro(h @ model.beta, h @ ref["beta"]) < 1e-8
+    assert diag.training_accuracy == ref["diag"]["training_accuracy"]
+
+
+@pytest.mark.xfail(raises=rb.NotSupportedError, strict=True,
+                   reason="SVD pseudoinverse fallback (solve_direct after SingularSplit) not yet on device")
+def test_svd_fallback_branch():
+    # d=2 inputs, L=640: H is numerically rank-deficient, the Schur block stays singular after the
+    # ridge retry (SingularSplit) and the reference falls back to solve_direct -> pinv_svd.
+    train_both(700, 2, 640, 2, seeds=(700, 3, 642))
+
+
+def test_determinism_bitwise():
+    x, t = rb.synth_classification(3000, 20, 4, 5, 6)
+    p = rb.ElmParams(20, 300, 4, 7)
+    b1 = rb.train(p, x, t, rb.SolverStrategy.rank_based())[0].beta
+    b2 = rb.train(p, x, t, rb.SolverStrategy.rank_based())[0].beta
+    assert np.array_equal(b1, b2)
+
+
+def twin_classes(L, tgt, src):
+    cls = np.arange(L)
+    for a, b in zip(tgt, src):
+        cls[a] = b
+    return cls
+
+
+def test_c3_rank_deficient_twins():
+    """C3: N=20000, d=32 (16 base + 16 linear combinations), L=2000 with 500 exact duplicate nodes,
+    m=5; hidden_matrix + solve_beta(rank_based(1e-6)) as SURVEY §8(b) prescribes."""
+    n, base, L, m = 20000, 16, 2000, 5
+    x, t = rb.synth_rank_deficient(n, base, m, SEED_X, 4001, SEED_T)
+    hid0 = rb.init_hidden(rb.ElmParams(2 * base, L, m, SEED_W))
+    hid, tgt, src = rb.duplicate_nodes(hid0, 500, 5001)
+    cls = twin_classes(L, tgt, src)
+    h = rb.hidden_matrix(hid, x)
+    ho = oracle.hidden_matrix(hid.weights, hid.biases, x)
+    assert np.array_equal(h[:, tgt], h[:, src]) and np.array_equal(ho[:, tgt], ho[:, src])  # exact twins
+    diag = rb.SolveDiagnostics()
+    beta = rb.solve_beta(h, t, rb.SolverStrategy.rank_based(1e-6), diag)
+    beta_o, diag_o, order_o = oracle.solve_beta(ho, t, "rank", 0, 1e-6)
+    assert diag.rank == diag_o["rank"] == 1500
+    assert diag.ridge_applied == bool(diag_o["ridge_applied"])
+    assert diag.fallback_to_direct == bool(diag_o["fallback_to_direct"])
+    f = rb.rank_revealing_factor(h, 1e-6)
+    assert f.permutation.rank == 1500
+    order = f.permutation.order
+    r = 1500
+    assert [cls[i] for i in order[:r]] == [cls[i] for i in order_o[:r]], "pivots differ beyond twin classes"
+    print("raw pivot order identical:", order[:r] == order_o[:r])
+    fit, fit_o = h @ beta, ho @ beta_o
+    err = rel_fro(fit, fit_o)
+    print(f"C3 fitted rel {err:.3e}, beta rel {rel_fro(beta, beta_o):.3e} (beta is non-unique)")
+    assert err < 1e-8
+    assert (fit.argmax(1) == fit_o.argmax(1)).all()
+
+
+def test_c3_small_duplicates():
+    n, d, L, m = 3000, 12, 200, 3
+    x, t = rb.synth_classification(n, d, m, 31, 32)
+    hid, tgt, src = rb.duplicate_nodes(rb.init_hidden(rb.ElmParams(d, L, m, 33)), 40, 34)
+    cls = twin_classes(L, tgt, src)
+    h = rb.hidden_matrix(hid, x)
+    ho = oracle.hidden_matrix(hid.weights, hid.biases, x)
+    diag = rb.SolveDiagnostics()
+    beta = rb.solve_beta(h, t, rb.SolverStrategy.rank_based(1e-6), diag)
+    beta_o, diag_o, order_o = oracle.solve_beta(ho, t, "rank", 0, 1e-6)
+    assert diag.rank == diag_o["rank"] == L - 40
+    order = rb.rank_revealing_factor(h, 1e-6).permutation.order
+    assert [cls[i] for i in order[:L - 40]] == [cls[i] for i in order_o[:L - 40]]
+    assert rel_fro(h @ beta, ho @ beta_o) < 1e-8
+
+
+def _device_stages(n, d, L, m, seeds):
+    import torch
+
+    x, t = rb.synth_classification(n, d, m, seeds[0], seeds[1])
+    hid = rb.init_hidden(rb.ElmParams(d, L, m, seeds[2]))
+    X, T = torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda()
+    W = torch.from_numpy(hid.weights).cuda()
+    B = torch.from_numpy(hid.biases.reshape(-1)).cuda()
+    G = torch.empty((L, L), dtype=torch.float64, device="cuda")
+    HtT = torch.empty((L, m), dtype=torch.float64, device="cuda")
+    rb.gram_stage_device(X, T, W, B, G, HtT)
+    beta, diag, order = rb.solve_stage_device(G, HtT, n, rb.SolverStrategy.rank_based(), return_order=True)
+    hits = rb.accuracy_stage_device(X, T, W, B, beta)
+    return x, t, hid, G.cpu().numpy(), HtT.cpu().numpy(), beta.cpu().numpy(), diag, order, hits
+
+
+@pytest.mark.parametrize("L", [250, 500, 1000])
+def test_c4_sweep_vs_oracle(L):
+    n, d, m = 100000, 128, 10
+    x, t, model, diag, order, ref = train_both(n, d, L, m, seeds=(SEED_X + 4, SEED_T + 4, SEED_W + L))
+    assert diag.rank == ref["diag"]["rank"] == L
+    assert order == ref["order"]
+    err = rel_fro(model.beta, ref["beta"])
+    print(f"C4 L={L}: beta rel {err:.3e}")
+    assert err < 1e-8
+    assert diag.training_accuracy == ref["diag"]["training_accuracy"]
+
+
+@pytest.mark.parametrize("L", [2000, 4000, pytest.param(8000, marks=pytest.mark.slow)])
+def test_c4_sweep_properties(L):
+    """Full C4 sizes: pivots/rank equal to the oracle factorisation applied to the GPU's own Gram,
+    FF^T = P^T G P, normal-equation backward error, accuracy re-derived on the host."""
+    n, d, m = 100000, 128, 10
+    x, t, hid, G, HtT, beta, diag, order, hits = _device_stages(n, d, L, m, (SEED_X + 4, SEED_T + 4, SEED_W + L))
+    assert diag.rank == L
+    assert np.array_equal(G, G.T)
+    if L <= 4000:
+        o_ord, o_rank, _, o_f, margin = oracle.factor_gram(G, n)
+        assert o_rank == L and list(order) == o_ord, "pivots differ from the oracle on the same Gram"
+        bo = oracle.solve_factored_gram(o_f, o_ord, L, HtT[o_ord])
+        beta_o = np.empty_like(bo)
+        beta_o[o_ord] = bo
+        print(f"C4 L={L}: beta vs oracle-on-same-Gram {rel_fro(beta, beta_o):.3e}, margin {margin:.2e}")
+        assert rel_fro(beta, beta_o) < 1e-7
+    bwd = np.linalg.norm(G @ beta - HtT) / (np.linalg.norm(G) * np.linalg.norm(beta))
+    print(f"C4 L={L}: normal-equation backward error {bwd:.3e}")
+    assert bwd < 1e-12
+    model = rb.ElmModel(rb.ElmParams(d, L, m, 0), hid, beta)
+    s = rb.predict(model, x[:20000])
+    local_hits = int((s.argmax(1) == t[:20000].argmax(1)).sum())
+    assert 0 < local_hits <= hits
+
+
+def test_sharded_stages_equal_single_pass():
+    """Two row shards on one GPU (the per-rank stages + a summed Gram, as the NCCL all-reduce does)."""
+    import torch
+
+    n, d, L, m = 30000, 32, 600, 6
+    x, t = rb.synth_classification(n, d, m, 41, 42)
+    params = rb.ElmParams(d, L, m, 43)
+    hid = rb.init_hidden(params)
+    W = torch.from_numpy(hid.weights).cuda()
+    B = torch.from_numpy(hid.biases.reshape(-1)).cuda()
+    parts = []
+    for r0, r1 in [(0, 17001), (17001, n)]:
+        X, T = torch.from_numpy(x[r0:r1]).cuda(), torch.from_numpy(t[r0:r1]).cuda()
+        G = torch.empty((L, L), dtype=torch.float64, device="cuda")
+        HtT = torch.empty((L, m), dtype=torch.float64, device="cuda")
+        rb.gram_stage_device(X, T, W, B, G, HtT, keep_h=False)
+        parts.append((G, HtT, X, T))
+    G = parts[0][0] + parts[1][0]
+    HtT = parts[0][1] + parts[1][1]
+    beta, diag, order = rb.solve_stage_device(G, HtT, n, rb.SolverStrategy.rank_based(), return_order=True)
+    hits = sum(rb.accuracy_stage_device(X, T, W, B, beta) for _, _, X, T in parts)
+    model, d1, order1 = rb.train(params, x, t, rb.SolverStrategy.rank_based(), return_order=True)
+    assert order == order1 and diag.rank == d1.rank == L
+    assert rel_fro(beta.cpu().numpy(), model.beta) < 1e-9
+    assert hits / n == d1.training_accuracy
+
+
+def test_c5_standin_properties():
+    """C5 stand-in on one GPU (N reduced to 120k, d=256, L=8192, m=100)."""
+    n, d, L, m = 120000, 256, 8192, 100
+    x, t, hid, G, HtT, beta, diag, order, hits = _device_stages(n, d, L, m, (SEED_X + 5, SEED_T + 5, SEED_W + 5))
+    assert diag.rank == L
+    assert np.array_equal(G, G.T)
+    assert sorted(order) == list(range(L))
+    bwd = np.linalg.norm(G @ beta - HtT) / (np.linalg.norm(G) * np.linalg.norm(beta))
+    print(f"C5 stand-in: backward error {bwd:.3e}, accuracy {hits / n:.4f}")
+    assert bwd < 1e-12
+    # pivot 0 is the largest Gram diagonal (first max), as the reference's first step
+    dg = np.diag(G)
+    assert order[0] == int(np.flatnonzero(dg == dg.max())[0])
+
+
+def test_errors_from_device_path():
+    with pytest.raises(rb.SingularMatrix) as e:
+        rb.solve_spd(np.diag([1.0, 0.0, 2.0]), np.ones((3, 1)))
+    assert e.value.pivot_index == 1
+    with pytest.raises(ValueError, match="direct"):
+        rb.train(rb.ElmParams(3, 50, 2, 1), np.zeros((10, 3)), np.zeros((10, 2)), rb.SolverStrategy.rank_based())
+    with pytest.raises(ValueError):
+        rb.rank_revealing_factor(np.ones((4, 2)), -1.0)
+    with pytest.raises(rb.ShapeError):
+        rb.hidden_matrix(rb.init_hidden(rb.ElmParams(3, 4, 1, 1)), np.zeros((2, 5)))
