@@ -69,6 +69,29 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
 }
 
 // ---------------------------------------------------------------------------
+// distributed shared memory: cluster address of a local smem address in CTA `rank`, and
+// asynchronous remote stores that complete their bytes on the receiver's mbarrier
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t smem_addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_async_v2f64(uint32_t cluster_addr, double a, double b, uint32_t cluster_mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];\n" ::"r"(
+                   cluster_addr),
+               "d"(a), "d"(b), "r"(cluster_mbar)
+               : "memory");
+}
+__device__ __forceinline__ void st_async_v2b64(uint32_t cluster_addr, unsigned long long a, unsigned long long b,
+                                               uint32_t cluster_mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.b64 [%0], {%1, %2}, [%3];\n" ::"r"(
+                   cluster_addr),
+               "l"(a), "l"(b), "r"(cluster_mbar)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
 // gpu-scope release/acquire helpers for inter-CTA flag exchange
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {

@@ -32,6 +32,7 @@ cudaError_t launch_hidden(const CUtensorMap&, const CUtensorMap&, const HiddenPa
 cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams&, int, cudaStream_t);
 cudaError_t launch_syrk_finish(const SyrkParams&, int, int, int, cudaStream_t);
 cudaError_t launch_gemm(const GemmParams&, cudaStream_t);
+cudaError_t launch_scores(const CUtensorMap&, const CUtensorMap&, const ScoresParams&, cudaStream_t);
 cudaError_t launch_factor_setup(const double*, long long, int, long long, double, int, double*, int*, FactorState*,
                                 cudaStream_t);
 cudaError_t launch_panel(const PanelParams&, int, int*, cudaStream_t);
@@ -612,6 +613,19 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
 }
 
 // Stage 3: hits = #rows with argmax(H beta) == argmax(T)
+// K6: S (optional) = H beta and/or hits += #rows with argmax(H beta) == argmax(T); m <= 128.
+void scores_dev(rbpg_context* ctx, const double* H, size_t ldh, size_t N, size_t L, const double* dBeta, size_t ldb,
+                size_t m, double* S, size_t lds, const double* T, size_t ldt, unsigned long long* hits) {
+  if (N == 0) return;
+  Padded B = pad_device(ctx, "beta.pad", dBeta, ldb, L, m);
+  const uint32_t bn = m <= 16 ? 16 : m <= 32 ? 32 : m <= 64 ? 64 : 128;
+  CUtensorMap tmH = make_map(ctx, H, L, N, ldh, 16, kTile, true);
+  CUtensorMap tmB = make_map(ctx, B.p, m, L, B.ld, bn, kBK, false);
+  ScoresParams p{static_cast<int>(N), static_cast<int>(L), static_cast<int>(m), S, static_cast<long long>(lds), T,
+                 static_cast<long long>(ldt), hits};
+  ctx->run("scores_kernel", [&] { return launch_scores(tmH, tmB, p, ctx->stream); });
+}
+
 uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* dT, size_t ldt_in, size_t N,
                         size_t d, size_t L, size_t m, const double* dW, size_t ldw, const double* db,
                         const double* dBeta, size_t ldb) {
@@ -633,10 +647,16 @@ uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const d
         H = dH;
         hld = ldh;
       }
-      gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(L), H, hld, false, dBeta, ldb, false,
-               S, lm, 1.0, 0.0);
-      ctx->run("accuracy", [&] { return launch_accuracy(S, static_cast<long long>(lm), dT + r0 * ldt_in, static_cast<long long>(ldt_in),
-                               static_cast<long long>(nr), static_cast<int>(m), hits, ctx->num_sms, ctx->stream); });
+      if (m <= 128) {  // K6: skinny DMMA GEMM with the fused arg-max / hit count, scores never stored
+        scores_dev(ctx, H, hld, nr, L, dBeta, ldb, m, nullptr, 0, dT + r0 * ldt_in, ldt_in, hits);
+      } else {
+        gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(L), H, hld, false, dBeta, ldb,
+                 false, S, lm, 1.0, 0.0);
+        ctx->run("accuracy", [&] {
+          return launch_accuracy(S, static_cast<long long>(lm), dT + r0 * ldt_in, static_cast<long long>(ldt_in),
+                                 static_cast<long long>(nr), static_cast<int>(m), hits, ctx->num_sms, ctx->stream);
+        });
+      }
     }
   }
   unsigned long long h = 0;
@@ -940,8 +960,11 @@ int rbpg_predict(rbpg_context* ctx, const double* w, const double* b, size_t d, 
     for (size_t r0 = 0; r0 < n; r0 += chunk) {
       const size_t nr = std::min(chunk, n - r0);
       hidden_dev(ctx, X.p + r0 * X.ld, X.ld, nr, d, W.p, W.ld, db, l, H, ldh);
-      gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(l), H, ldh, false, Bt.p, Bt.ld,
-               false, S + r0 * lm, lm, 1.0, 0.0);
+      if (m <= 128)
+        scores_dev(ctx, H, ldh, nr, l, Bt.p, Bt.ld, m, S + r0 * lm, lm, nullptr, 0, nullptr);
+      else
+        gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(l), H, ldh, false, Bt.p, Bt.ld,
+                 false, S + r0 * lm, lm, 1.0, 0.0);
     }
     download(ctx, scores, S, lm, n, m);
   });

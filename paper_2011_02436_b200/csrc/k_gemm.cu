@@ -460,6 +460,127 @@ cudaError_t launch_syrk_finish(const SyrkParams& p, int splits, int accumulate, 
   return cudaGetLastError();
 }
 
+// ============================================================================
+// K6: scores = H beta with a fused arg-max epilogue (training accuracy, predict).
+// Skinny DMMA GEMM: CTA = 128 rows of H x all m (<= BN) columns, K = L streamed by TMA
+// (H tile [128][16] 128B-swizzled, beta tile [16][BN]); 8 warps x 16 rows each.
+// Epilogue: optional score store, per-row arg-max (strict '>', lowest index on ties,
+// elm.cpp:291-296) compared with arg-max(T), hits accumulated per CTA.
+// ============================================================================
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads)
+    scores_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmB, ScoresParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = align1024(smem_raw);
+  constexpr int kS = 4;
+  double* Hs = reinterpret_cast<double*>(smem);        // [stage][128][16] swizzled
+  double* Bs = Hs + kS * kTile * kBK;                  // [stage][16][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kS * kBK * BN);
+  double* sc = reinterpret_cast<double*>(smem);  // [128][BN+1], aliases the drained pipeline
+  constexpr int SCL = BN + 1;
+  __shared__ unsigned long long blk_hits;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int r0 = blockIdx.x * kTile;
+  const int ktiles = (p.L + kBK - 1) / kBK;
+  constexpr uint32_t kStageBytes = (kTile * kBK + kBK * BN) * sizeof(double);
+  if (tid == 0) {
+    tma_prefetch_desc(&tmH);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < kS; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+    blk_hits = 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kS && s < ktiles; ++s) {
+      mbar_arrive_expect_tx(&full[s], kStageBytes);
+      tma_load_2d(Hs + s * kTile * kBK, &tmH, &full[s], s * kBK, r0);
+      tma_load_2d(Bs + s * kBK * BN, &tmB, &full[s], 0, s * kBK);
+    }
+  }
+  constexpr int NT = BN / 8;
+  double acc[NT][4];
+#pragma unroll
+  for (int i = 0; i < NT; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
+  const int wm = warp * 16;
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int s = kt % kS;
+    mbar_wait(&full[s], (kt / kS) & 1);
+    const double* hs = Hs + s * kTile * kBK;
+    const double* bs = Bs + s * kBK * BN;
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const int kc = ks * 4 + t;
+      const double a0 = hs[swz16(wm + g, kc)];
+      const double a1 = hs[swz16(wm + g + 8, kc)];
+#pragma unroll
+      for (int pp = 0; pp < NT / 2; ++pp) {
+        const double2 w = *reinterpret_cast<const double2*>(bs + kc * BN + pp * 16 + 2 * g);
+        dmma_16x8x4(acc[2 * pp], a0, a1, w.x);
+        dmma_16x8x4(acc[2 * pp + 1], a0, a1, w.y);
+      }
+    }
+    __syncthreads();
+    if (tid == 0 && kt + kS < ktiles) {
+      const int kn = kt + kS;
+      mbar_arrive_expect_tx(&full[s], kStageBytes);
+      tma_load_2d(Hs + s * kTile * kBK, &tmH, &full[s], kn * kBK, r0);
+      tma_load_2d(Bs + s * kBK * BN, &tmB, &full[s], 0, kn * kBK);
+    }
+  }
+  // scatter the accumulators to smem in natural column order
+#pragma unroll
+  for (int pp = 0; pp < NT / 2; ++pp) {
+    const int cb = pp * 16 + 4 * t;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = wm + g + 8 * h;
+      sc[r * SCL + cb + 0] = acc[2 * pp][2 * h];
+      sc[r * SCL + cb + 1] = acc[2 * pp + 1][2 * h];
+      sc[r * SCL + cb + 2] = acc[2 * pp][2 * h + 1];
+      sc[r * SCL + cb + 3] = acc[2 * pp + 1][2 * h + 1];
+    }
+  }
+  __syncthreads();
+  if (p.S)
+    for (int e = tid; e < kTile * p.m; e += kGemmThreads) {
+      const int r = e / p.m, c = e % p.m;
+      if (r0 + r < p.N) p.S[(long long)(r0 + r) * p.lds + c] = sc[r * SCL + c];
+    }
+  if (p.T && tid < kTile && r0 + tid < p.N) {
+    const double* tr = p.T + (long long)(r0 + tid) * p.ldt;
+    int ap = 0, ay = 0;
+    for (int j = 1; j < p.m; ++j) {
+      if (sc[tid * SCL + j] > sc[tid * SCL + ap]) ap = j;
+      if (tr[j] > tr[ay]) ay = j;
+    }
+    if (ap == ay) atomicAdd(&blk_hits, 1ull);
+  }
+  __syncthreads();
+  if (tid == 0 && p.hits && blk_hits) atomicAdd(p.hits, blk_hits);
+}
+
+cudaError_t launch_scores(const CUtensorMap& tmH, const CUtensorMap& tmB, const ScoresParams& p, cudaStream_t s) {
+  const int grid = (p.N + kTile - 1) / kTile;
+  auto go = [&](auto kern, int bn) -> cudaError_t {
+    const size_t pipe = size_t(4) * (kTile * kBK + kBK * bn) * sizeof(double) + 64;
+    const size_t scb = size_t(kTile) * (bn + 1) * sizeof(double);
+    const size_t smem = (pipe > scb ? pipe : scb) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<grid, kGemmThreads, smem, s>>>(tmH, tmB, p);
+    return cudaGetLastError();
+  };
+  if (p.m <= 16) return go(scores_kernel<16>, 16);
+  if (p.m <= 32) return go(scores_kernel<32>, 32);
+  if (p.m <= 64) return go(scores_kernel<64>, 64);
+  if (p.m <= 128) return go(scores_kernel<128>, 128);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_gemm(const GemmParams& p, cudaStream_t s) {
   if (p.M <= 0 || p.N <= 0) return cudaSuccess;
   dim3 grid((p.N + kGT - 1) / kGT, (p.M + kGT - 1) / kGT);

@@ -98,6 +98,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
   // cluster: every CTA's candidate and its panel row, pushed by the owner before the barrier
   __shared__ Cand cand_all[2][kMaxCluster];
   __shared__ __align__(16) double rows_all[2][kMaxCluster][kPanelW];
+  __shared__ __align__(8) uint64_t cand_full[2];  // tx-count barriers of the two candidate buffers
   __shared__ Cand wbest[kPWarps];
   __shared__ int s_stop;
 
@@ -118,15 +119,26 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
   for (int i = tid; i < kPanelW * R; i += blockDim.x) PsT[i] = 0.0;
   for (int i = tid; i < R; i += blockDim.x) dl[i] = (i < nown) ? p.d_in[lbeg + i] : -DBL_MAX;
   if (tid == 0) s_stop = 0;
+  if constexpr (kCluster) {
+    if (tid == 0) {
+      mbar_init(&cand_full[0], 1);
+      mbar_init(&cand_full[1], 1);
+      fence_mbar_init();
+    }
+    cg::this_cluster().sync();  // every CTA's barriers exist before any remote st.async
+  }
   __syncthreads();
+  // bytes one step's exchange delivers into each CTA: C candidates + C panel rows
+  const uint32_t kStepBytes = static_cast<uint32_t>(C) * (sizeof(Cand) + kPanelW * sizeof(double));
   const double cut = st->cut;
   const double thresh = st->thresh;
 
-  // warp 0: combine the per-warp candidates and publish this CTA's candidate for step j.
-  // Cluster: push (key, pos) and the candidate's panel row (columns 0..j-k-1) into every CTA's
-  // shared memory; the next barrier.cluster (release/acquire) makes them visible.
-  auto combine_publish = [&](int j) {
-    if (warp != 0) return;
+  // Combine the per-warp candidates and publish this CTA's candidate for step j.  (piv, y)
+  // describe the swap of the step just finished, still pending in the maps (tid 0 applies it).
+  // Cluster: every warp combines redundantly and pushes to destinations d = warp (mod 8):
+  // (key, pos) and the candidate's panel row (columns 0..j-k-1) by st.async, which completes
+  // on the receiver's mbarrier.  Grid: warp 0 writes the global slot with a release epoch.
+  auto combine_publish = [&](int j, int piv, int y) {
     unsigned long long key = 0;
     int pos = INT_MAX;
     if (lane < kPWarps) {
@@ -135,25 +147,24 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
     }
     warp_argmax(key, pos);
     if constexpr (kCluster) {
-      __syncwarp();
       const int cvalid = j - k;  // panel columns already computed
       double2 rv = make_double2(0.0, 0.0);
       if (pos != INT_MAX) {
-        const int lib = lab_at[pos - k] - lbeg;
+        const int lab = (pos == piv) ? y : lab_at[pos - k];
+        const int lib = lab - lbeg;
         if (2 * lane < cvalid) rv.x = PsT[(2 * lane) * R + lib];
         if (2 * lane + 1 < cvalid) rv.y = PsT[(2 * lane + 1) * R + lib];
       }
-      cg::cluster_group cl = cg::this_cluster();
-      const int par = j & 1;
-      for (int d = 0; d < C; ++d) {
-        double2* dst = reinterpret_cast<double2*>(cl.map_shared_rank(&rows_all[par][cta][0], d));
-        dst[lane] = rv;
+      const int par = (j - k) & 1;
+      const uint32_t row_l = smem_u32(&rows_all[par][cta][2 * lane]);
+      const uint32_t cand_l = smem_u32(&cand_all[par][cta]);
+      const uint32_t bar_l = smem_u32(&cand_full[par]);
+      for (int d = warp; d < C; d += kPWarps) {
+        const uint32_t rbar = mapa_u32(bar_l, d);
+        st_async_v2f64(mapa_u32(row_l, d), rv.x, rv.y, rbar);
+        if (lane == 0) st_async_v2b64(mapa_u32(cand_l, d), key, static_cast<unsigned long long>(pos), rbar);
       }
-      if (lane < C) {
-        Cand* dc = cl.map_shared_rank(&cand_all[par][cta], lane);
-        *reinterpret_cast<ulonglong2*>(dc) = make_ulonglong2(key, static_cast<unsigned long long>(pos));
-      }
-    } else if (lane == 0) {
+    } else if (warp == 0 && lane == 0) {
       PivotSlot* sl = p.slots + (j & 1) * C + cta;
       *reinterpret_cast<unsigned long long*>(&sl->val) = key;
       sl->pos = pos;
@@ -183,30 +194,43 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
       wbest[warp].pos = pos;
     }
     __syncthreads();
-    combine_publish(k);
+    combine_publish(k, -1, -1);
   }
 
   unsigned long long* trace = p.trace;
   long long tacc[6] = {0, 0, 0, 0, 0, 0};
   __shared__ unsigned long long s_wkey;
-  __shared__ int s_piv, s_xp, s_y;
-  __shared__ double prow[kPanelW];
+  __shared__ int s_piv, s_xp, s_y, s_src;
+  __shared__ double prow_g[kPanelW];  // grid variant: pivot panel row staged from global
+  // sqrt(d) <= cut  <=>  d <= cut^2 up to rounding: values above cut^2 (1 + 2^-30) never stop
+  const double cut_sq_hi = cut * cut * (1.0 + 0x1.0p-30);
   for (int c = 0; c < kb; ++c) {
     const int j = k + c;
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
     if (trace) t0 = clock64();
-    // ---------------- exchange: warp 0 resolves the winner and fetches its panel row
-    if constexpr (kCluster) cg::this_cluster().sync();
+    // ---------------- exchange: warp 0 resolves the winner
+    if constexpr (kCluster) {
+      if (warp == 0) {
+        // arm this step's buffer (remote bytes may already have landed: the tx-count may be
+        // transiently negative within the phase), then wait for all C candidates + rows
+        if (lane == 0) mbar_arrive_expect_tx(&cand_full[c & 1], kStepBytes);
+        mbar_wait(&cand_full[c & 1], (c >> 1) & 1);
+      }
+    }
     if (trace) t1 = clock64();
     if (warp == 0) {
       unsigned long long wkey = 0;
       int wpos = INT_MAX;
+      unsigned long long ck = 0;
+      int cp = INT_MAX;
       if constexpr (kCluster) {
         if (lane < C) {
-          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&cand_all[j & 1][lane]);
-          wkey = v.x;
-          wpos = static_cast<int>(v.y & 0xffffffffull);
+          const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(&cand_all[c & 1][lane]);
+          ck = v.x;
+          cp = static_cast<int>(v.y & 0xffffffffull);
         }
+        wkey = ck;
+        wpos = cp;
       } else {
         const PivotSlot* base = p.slots + (j & 1) * C;
         for (int i = lane; i < C; i += 32) {
@@ -222,36 +246,35 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
       }
       warp_argmax(wkey, wpos);
       const int xpw = lab_at[wpos - k];
+      int src = 0;
+      if constexpr (kCluster) {
+        const unsigned msk = __ballot_sync(0xffffffffu, lane < C && ck == wkey && cp == wpos);
+        src = __ffs(msk) - 1;
+      } else {
+        const double* rp = p.Pg + (long long)(xpw - k) * kPanelW;
+        prow_g[lane] = lane < c ? __ldcg(rp + lane) : 0.0;
+        prow_g[lane + 32] = lane + 32 < c ? __ldcg(rp + lane + 32) : 0.0;
+      }
       if (lane == 0) {
         s_wkey = wkey;
         s_piv = wpos;
         s_xp = xpw;
         s_y = lab_at[j - k];
+        s_src = src;
       }
       named_bar_arrive(1, kPThreads);  // winner known to the CTA
-      // pivot panel row
-      double v0 = 0.0, v1 = 0.0;
-      if constexpr (kCluster) {
-        // the row was pushed with the candidate: slot of the CTA whose candidate won
-        const unsigned m = __ballot_sync(0xffffffffu, lane < C && cand_all[j & 1][lane].key == wkey &&
-                                                          cand_all[j & 1][lane].pos == wpos);
-        const double* rp = rows_all[j & 1][__ffs(m) - 1];
-        v0 = rp[lane];
-        v1 = rp[lane + 32];
-      } else {
-        const double* rp = p.Pg + (long long)(xpw - k) * kPanelW;
-        if (lane < c) v0 = __ldcg(rp + lane);
-        if (lane + 32 < c) v1 = __ldcg(rp + lane + 32);
-      }
-      prow[lane] = v0;
-      prow[lane + 32] = v1;
-      named_bar_arrive(2, kPThreads);  // panel row staged
     } else {
       named_bar_sync(1, kPThreads);
     }
     const int piv = s_piv, xp = s_xp, y = s_y;
     const double dj = dkey_inv(s_wkey);
-    // this warp's first-pass G entries, issued before the FP64 math and the panel-row wait
+    const double* prow;
+    if constexpr (kCluster) {
+      prow = rows_all[c & 1][s_src];
+    } else {
+      prow = prow_g;
+    }
+    // this warp's first-pass G entries, issued before the FP64 math
     const double* grow = p.G + (long long)xp * p.ldg;
     double gpre = 0.0;
     {
@@ -260,11 +283,10 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
     }
     bool stop;
     if (p.pivoting) {
-      stop = (dj > 0.0 ? sqrt(dj) : 0.0) <= cut;                 // linalg.cpp:219-223
+      stop = !(dj > cut_sq_hi) && (dj > 0.0 ? sqrt(dj) : 0.0) <= cut;  // linalg.cpp:219-223
     } else {
-      stop = !isfinite(dj) || dj <= thresh || dj <= 0.0;        // linalg.cpp:118-119
+      stop = !isfinite(dj) || dj <= thresh || dj <= 0.0;               // linalg.cpp:118-119
     }
-    if (warp != 0) named_bar_sync(2, kPThreads);
     if (stop) {
       __syncthreads();  // every warp has read the maps for this step
       if (tid == 0) {
@@ -296,7 +318,6 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
       PsT[c * R + oli] = rjj;  // F(j, j) = rjj
       if constexpr (!kCluster) p.Pg[(long long)(xp - k) * kPanelW + c] = rjj;
     }
-    __syncwarp();
     if (trace) t2 = clock64();
 
     // ---------------- update: quad (4 lanes) per label; warp w owns labels w*8 + 64*pass + lane/4
@@ -354,13 +375,14 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
     }
     __syncthreads();
     if (trace) t4 = clock64();
+    if (c + 1 < kb) combine_publish(j + 1, piv, y);
     if (tid == 0 && piv != j) {  // apply the swap (linalg.cpp:211-218) to the replicated maps
       lab_at[j - k] = xp;
       lab_at[piv - k] = y;
       pos_of[xp - k] = j;
       pos_of[y - k] = piv;
     }
-    if (c + 1 < kb) combine_publish(j + 1);
+    __syncwarp();
     if (trace) {
       const long long t5 = clock64();
       tacc[0] += t1 - t0;
@@ -370,8 +392,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
       tacc[4] += t5 - t4;
       tacc[5] += 1;
     }
-    __syncthreads();  // maps settled before the next step reads them
   }
+  __syncthreads();
   if (trace && cta == 0 && tid == 0)
     for (int i = 0; i < 6; ++i) atomicAdd(&trace[i], static_cast<unsigned long long>(tacc[i]));
   if constexpr (kCluster) cg::this_cluster().sync();  // no CTA leaves while its smem may be read

@@ -53,67 +53,89 @@ __global__ void __launch_bounds__(64) tri_inv_kernel(const double* F, long long 
 __global__ void __launch_bounds__(256) trsm_sweep_kernel(const double* F, long long ldf, const double* Dinv, double* X,
                                                          long long ldx, int n, int m, int backward) {
   extern __shared__ __align__(16) double sm[];
-  double* Rb = sm;                 // [64][m]   right-hand side block
-  double* Yb = Rb + kTB * m;       // [64][m]   block solution
-  double* Ft = Yb + kTB * m;       // [64][kTB+1] F tile (forward: [32][65] rows x q; backward: [64][33])
+  double* Rb = sm;                      // [64][m]      right-hand side block
+  double* Yb = Rb + kTB * m;            // [64][m]      block solution
+  double* Ds = Yb + kTB * m;            // [64][65]     diagonal-block inverse
+  double* Ft = Ds + kTB * (kTB + 1);    // [32][65]     F tile of the row update
   cg::grid_group grid = cg::this_grid();
   const int tid = threadIdx.x, nt = blockDim.x;
   const int nblk = (n + kTB - 1) / kTB;
 
+  auto load_tile = [&](int i0, int nb, int r0, int nr) {
+    if (!backward) {
+      for (int e = tid; e < kTR * kTB; e += nt) {
+        const int rr = e / kTB, q = e % kTB;
+        Ft[rr * (kTB + 1) + q] = (rr < nr && q < nb) ? __ldg(F + (long long)(r0 + rr) * ldf + i0 + q) : 0.0;
+      }
+    } else {
+      for (int e = tid; e < kTR * kTB; e += nt) {
+        const int q = e / kTR, rr = e % kTR;
+        Ft[rr * (kTB + 1) + q] = (rr < nr && q < nb) ? __ldg(F + (long long)(i0 + q) * ldf + r0 + rr) : 0.0;
+      }
+    }
+  };
+
+  // The owner stores block b's solution only after the step's grid barrier (deferred to the
+  // start of step s+1): every CTA reads block b's right-hand side from X during step s.
+  auto store_solution = [&](int bb) {
+    const int j0 = bb * kTB, jb = min(kTB, n - j0);
+    for (int e = tid; e < jb * m; e += nt) X[(long long)(j0 + e / m) * ldx + e % m] = Yb[e];
+  };
   for (int s = 0; s < nblk; ++s) {
     const int b = backward ? nblk - 1 - s : s;
+    if (s > 0) {
+      const int bp = backward ? b + 1 : b - 1;
+      if (blockIdx.x == bp % gridDim.x) store_solution(bp);
+    }
     const int i0 = b * kTB, nb = min(kTB, n - i0);
+    const int rlo = backward ? 0 : i0 + nb;  // rows updated by this block: forward [i0+nb, n), backward [0, i0)
+    const int rhi = backward ? i0 : n;
+    const int ntiles = (rhi - rlo + kTR - 1) / kTR;
+    // all loads of the step issued together: D_b, R_b and the first F tile
+    const double* D = Dinv + (long long)b * kTB * kTB;
+    for (int e = tid; e < kTB * kTB; e += nt) Ds[(e / kTB) * (kTB + 1) + e % kTB] = __ldg(D + e);
     for (int e = tid; e < kTB * m; e += nt) {
-      const int q = e / m, c = e - (e / m) * m;
+      const int q = e / m, c = e - q * m;
       Rb[e] = q < nb ? __ldcg(X + (long long)(i0 + q) * ldx + c) : 0.0;
     }
+    if (blockIdx.x < ntiles) load_tile(i0, nb, rlo + blockIdx.x * kTR, min(kTR, rhi - (rlo + blockIdx.x * kTR)));
     __syncthreads();
-    const double* D = Dinv + (long long)b * kTB * kTB;
     for (int e = tid; e < nb * m; e += nt) {
-      const int i = e / m, c = e - (e / m) * m;
+      const int i = e / m, c = e - i * m;
       double acc = 0.0;
       if (!backward) {
-        for (int q = 0; q <= i; ++q) acc = fma(__ldg(D + i * kTB + q), Rb[q * m + c], acc);
+        for (int q = 0; q <= i; ++q) acc = fma(Ds[i * (kTB + 1) + q], Rb[q * m + c], acc);
       } else {
-        for (int q = i; q < nb; ++q) acc = fma(__ldg(D + q * kTB + i), Rb[q * m + c], acc);
+        for (int q = i; q < nb; ++q) acc = fma(Ds[q * (kTB + 1) + i], Rb[q * m + c], acc);
       }
       Yb[e] = acc;
     }
     __syncthreads();
-    if (blockIdx.x == b % gridDim.x)
-      for (int e = tid; e < nb * m; e += nt) X[(long long)(i0 + e / m) * ldx + e % m] = Yb[e];
 
-    // remaining rows: forward [i0+nb, n), backward [0, i0)
-    const int rlo = backward ? 0 : i0 + nb;
-    const int rhi = backward ? i0 : n;
-    const int ntiles = (rhi - rlo + kTR - 1) / kTR;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int r0 = rlo + t * kTR, nr = min(kTR, rhi - r0);
-      if (!backward) {
-        for (int e = tid; e < kTR * kTB; e += nt) {
-          const int rr = e / kTB, q = e % kTB;
-          Ft[rr * (kTB + 1) + q] = (rr < nr && q < nb) ? __ldg(F + (long long)(r0 + rr) * ldf + i0 + q) : 0.0;
-        }
-      } else {
-        for (int e = tid; e < kTR * kTB; e += nt) {
-          const int q = e / kTR, rr = e % kTR;
-          Ft[rr * (kTB + 1) + q] = (rr < nr && q < nb) ? __ldg(F + (long long)(i0 + q) * ldf + r0 + rr) : 0.0;
-        }
+      if (t != blockIdx.x) {
+        __syncthreads();
+        load_tile(i0, nb, r0, nr);
+        __syncthreads();
       }
-      __syncthreads();
       for (int e = tid; e < nr * m; e += nt) {
-        const int rr = e / m, c = e - (e / m) * m;
+        const int rr = e / m, c = e - rr * m;
         const double* fr = Ft + rr * (kTB + 1);
-        double acc = 0.0;
+        double a0 = 0.0, a1 = 0.0;
 #pragma unroll 8
-        for (int q = 0; q < kTB; ++q) acc = fma(fr[q], Yb[q * m + c], acc);
+        for (int q = 0; q < kTB; q += 2) {
+          a0 = fma(fr[q], Yb[q * m + c], a0);
+          a1 = fma(fr[q + 1], Yb[(q + 1) * m + c], a1);
+        }
         double* xp = X + (long long)(r0 + rr) * ldx + c;
-        *xp = __ldcg(xp) - acc;
+        *xp = __ldcg(xp) - (a0 + a1);
       }
-      __syncthreads();
     }
     grid.sync();
   }
+  const int blast = backward ? 0 : nblk - 1;
+  if (nblk > 0 && blockIdx.x == blast % gridDim.x) store_solution(blast);
 }
 
 // ---------------------------------------------------------------------------
@@ -130,7 +152,7 @@ cudaError_t launch_trsm_pair(const double* F, long long ldf, double* X, long lon
   tri_inv_kernel<<<nblk, kTB, kInvSmem, s>>>(F, ldf, n, dinv_ws);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const size_t smem = (size_t(2) * kTB * m + size_t(kTB) * (kTB + 1)) * sizeof(double);
+  const size_t smem = (size_t(2) * kTB * m + size_t(kTB + kTR) * (kTB + 1)) * sizeof(double);
   static size_t attr_smem = 0;
   if (smem > attr_smem) {
     e = cudaFuncSetAttribute(trsm_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

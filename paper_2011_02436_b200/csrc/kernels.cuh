@@ -60,6 +60,14 @@ struct GemmParams {
   double alpha, beta;
 };
 
+// ---- K6: scores = H beta (+ fused arg-max hit count)
+struct ScoresParams {
+  int N, L, m;
+  double* S; long long lds;            // optional score output (N x m)
+  const double* T; long long ldt;      // optional targets for the hit count
+  unsigned long long* hits;
+};
+
 // ---- K3: pivoted-Cholesky panel (reference linalg.cpp:186-247)
 struct FactorState {
   int rank;          // L until the stop rule fires

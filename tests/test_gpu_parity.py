@@ -83,10 +83,10 @@ def test_train_parity_ragged_shapes(shape):
     assert diag.fallback_to_direct == bool(ref["diag"]["fallback_to_direct"])
     if L >= 2:
         assert order == ref["order"]
-    if diag.rank == L:
-        assert rel_fro(model.beta, ref["beta"]) < 1e-8
+    h = oracle.hidden_matrix(ref["w"], ref["b"], x)
+    if diag.rank == L:  # gate on the oracle's own reduction-order floor (ill-conditioned small-d cases)
+        assert rel_fro(model.beta, ref["beta"]) <= max(1e-8, 4 * self_floor(h, t))
     else:  # beta is non-unique when rank < L: compare fitted values
-        h = oracle.hidden_matrix(ref["w"], ref["b"], x)
         assert rel_fro(h @ model.beta, h @ ref["beta"]) < 1e-8
     assert diag.training_accuracy == ref["diag"]["training_accuracy"]
 
@@ -265,3 +265,14 @@ def test_errors_from_device_path():
         rb.rank_revealing_factor(np.ones((4, 2)), -1.0)
     with pytest.raises(rb.ShapeError):
         rb.hidden_matrix(rb.init_hidden(rb.ElmParams(3, 4, 1, 1)), np.zeros((2, 5)))
+
+
+@pytest.mark.parametrize("n,m", [(200, 2), (256, 1), (257, 3), (1000, 10), (2047, 130), (4100, 100)])
+def test_triangular_solve_pair_sizes(n, m):
+    """K4 on its own: (F F^T)^-1 rhs for many block counts / CTA counts / RHS chunks."""
+    rng = np.random.default_rng(n + m)
+    f = np.tril(rng.uniform(-0.1, 0.1, (n, n))) + np.eye(n) * 2.0
+    rhs = rng.uniform(-1, 1, (n, m))
+    perm = rb.ColumnPermutation(list(range(n)), n, 0.0)
+    x = rb.solve_factored_gram(rb.RankRevealingFactor(perm, f), rhs)
+    assert rel_fro(x, np.linalg.solve(f @ f.T, rhs)) < 1e-13
