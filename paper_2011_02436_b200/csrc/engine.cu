@@ -29,7 +29,7 @@
 
 namespace rbpg {
 cudaError_t launch_hidden(const CUtensorMap&, const CUtensorMap&, const HiddenParams&, cudaStream_t);
-cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams&, int, cudaStream_t);
+cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams&, int, int, cudaStream_t);
 cudaError_t launch_syrk_finish(const SyrkParams&, int, int, int, cudaStream_t);
 cudaError_t launch_gemm(const GemmParams&, cudaStream_t);
 cudaError_t launch_scores(const CUtensorMap&, const CUtensorMap&, const ScoresParams&, cudaStream_t);
@@ -49,6 +49,7 @@ cudaError_t launch_gather_block(const double*, long long, const int*, int, const
 cudaError_t launch_symmetrize(double*, long long, int, cudaStream_t);
 cudaError_t launch_trace(const double*, long long, int, double*, cudaStream_t);
 cudaError_t launch_nonfinite(const double*, long long, int, int, int*, cudaStream_t);
+cudaError_t launch_add_block(double*, long long, const double*, long long, long long, long long, cudaStream_t);
 cudaError_t launch_axpy_rows(const double*, long long, const double*, long long, int, int, double*, long long,
                              cudaStream_t);
 }  // namespace rbpg
@@ -245,7 +246,7 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
   }
   CUtensorMap tmA = make_map(ctx, dA, L, N, lda, kTile, kBK, false);
   CUtensorMap tmB = m > 0 ? make_map(ctx, dT, m, N, ldt_in, kTile, kBK, false) : tmA;
-  ctx->run("syrk_kernel", [&] { return launch_syrk(tmA, tmB, p, splits, ctx->stream); });
+  ctx->run("syrk_kernel", [&] { return launch_syrk(tmA, tmB, p, splits, kTile, ctx->stream); });
   if (!direct) ctx->run("syrk_finish", [&] { return launch_syrk_finish(p, splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
 }
 
@@ -336,10 +337,13 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     const size_t t0 = k + kb;
     if (t0 < n) {
       const size_t nrem = n - t0;
-      CUtensorMap tm = make_map(ctx, PcT, nrem, static_cast<uint64_t>(kb), ldp, kTile, kBK, false);
+      // 64-wide tiles while 128-wide ones would not fill two waves of SMs
+      const size_t nb128 = (nrem + kTile - 1) / kTile;
+      const int ttile = (nb128 * (nb128 + 1) / 2 < size_t(2 * ctx->num_sms)) ? 64 : kTile;
+      CUtensorMap tm = make_map(ctx, PcT, nrem, static_cast<uint64_t>(kb), ldp, ttile, kBK, false);
       SyrkParams sp{};
       sp.M = static_cast<int>(nrem);
-      sp.nbI = static_cast<int>((nrem + kTile - 1) / kTile);
+      sp.nbI = static_cast<int>((nrem + ttile - 1) / ttile);
       sp.nGram = sp.nbI * (sp.nbI + 1) / 2;
       sp.nbT = 0;
       sp.kRows = kb;
@@ -350,7 +354,7 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
       sp.Gold = gcur;
       sp.lab = lab;
       sp.off = static_cast<int>(t0);
-      ctx->run("syrk_trailing", [&] { return launch_syrk(tm, tm, sp, 1, s); });
+      ctx->run("syrk_trailing", [&] { return launch_syrk(tm, tm, sp, 1, ttile, s); });
       std::swap(gcur, gnext);
     }
     cur = 1 - cur;
@@ -577,15 +581,19 @@ size_t h_chunk_rows(rbpg_context* ctx, size_t N, size_t ldh) {
 
 // Stage 1: H build + Gram/HtT over the local rows (chunked when H exceeds the budget).
 // Returns the summed K1 time (ms) when timing events are requested.
+// The Gram is taken of the augmented rows [H | T] (N x (L+m)): its lower triangle holds H^T H and,
+// mirrored, H^T T = Gaug[0:L, L:L+m], so the H^T T product rides in the SYRK's last tile row
+// instead of 128-wide tiles that would carry only m useful columns.
 float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* dT, size_t ldt_in, size_t N,
-                 size_t d, size_t L, size_t m, const double* dW, size_t ldw, const double* db, double* dG, size_t ldg,
-                 double* dHtT, size_t ldt, bool accumulate, bool keep_h, bool timed) {
-  const size_t ldh = even(L);
+                 size_t d, size_t L, size_t m, const double* dW, size_t ldw, const double* db, double* dGaug,
+                 size_t ldga, bool accumulate, bool keep_h, bool timed) {
+  const size_t M = L + m;
+  const size_t ldh = even(M);
   const size_t chunk = std::max<size_t>(1, h_chunk_rows(ctx, std::max<size_t>(N, 1), ldh));
   double* dH = ctx->dbuf("H", chunk * ldh);
   float hidden_ms = 0.f;
   if (N == 0) {
-    gram_dev(ctx, dH, ldh, 0, L, dT, ldt_in, m, dG, ldg, dHtT, ldt, accumulate);
+    gram_dev(ctx, dH, ldh, 0, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate);
     return 0.f;
   }
   for (size_t r0 = 0; r0 < N; r0 += chunk) {
@@ -599,7 +607,11 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
       cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
       hidden_ms += ms;
     }
-    gram_dev(ctx, dH, ldh, nr, L, dT + r0 * ldt_in, ldt_in, m, dG, ldg, dHtT, ldt, accumulate || r0 > 0);
+    if (m > 0)
+      ck(cudaMemcpy2DAsync(dH + L, ldh * 8, dT + r0 * ldt_in, ldt_in * 8, m * 8, nr, cudaMemcpyDeviceToDevice,
+                           ctx->stream),
+         "append T");
+    gram_dev(ctx, dH, ldh, nr, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate || r0 > 0);
   }
   if (keep_h && chunk >= N) {
     ctx->kept_h = dH;
@@ -674,14 +686,14 @@ void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* d
   Padded W = upload(ctx, "W", w, d, L);
   double* db = ctx->dbuf("b", L);
   ck(cudaMemcpyAsync(db, b, L * 8, cudaMemcpyHostToDevice, ctx->stream), "upload b");
-  const size_t ldg = round_up(L, 8), ldt = even(m);
-  double* G = ctx->dbuf("G0", L * ldg);
-  double* HtT = ctx->dbuf("HtT", L * ldt);
+  // augmented Gram [H T]^T [H T]: G = Gaug[0:L, 0:L], H^T T = Gaug[0:L, L:L+m] (same ld)
+  const size_t ldg = round_up(L + m, 8), ldt = ldg;
+  double* G = ctx->dbuf("G0", (L + m) * ldg);
+  double* HtT = G + L;
 
   const auto wall0 = std::chrono::steady_clock::now();
   cudaEventRecord(ctx->ev[2], ctx->stream);
-  float hidden_ms = gram_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, G, ldg, HtT, ldt, false, true,
-                               true);
+  float hidden_ms = gram_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, G, ldg, false, true, true);
   solve_dev(ctx, G, ldg, HtT, ldt, L, m, N, sg, dBeta, ldb, order_out, diag);
   cudaEventRecord(ctx->ev[3], ctx->stream);
   cudaEventSynchronize(ctx->ev[3]);
@@ -897,13 +909,16 @@ int rbpg_solve_beta(rbpg_context* ctx, const double* h, size_t n, size_t l, cons
   return guarded(ctx, st, [&] {
     if (n == 0 || l == 0) fail(RBPG_SHAPE_ERROR, "solve_beta: empty hidden matrix");
     if (yrows != n) fail(RBPG_SHAPE_ERROR, "solve_beta: H is " + shp(n, l) + " but Y is " + shp(yrows, m));
-    Padded H = upload(ctx, "H.in", h, n, l);
-    Padded Y = upload(ctx, "Y.in", y, n, m);
-    const size_t ldg = round_up(l, 8), ldt = even(m), lb = even(m);
-    double* G = ctx->dbuf("G0", l * ldg);
-    double* HtT = ctx->dbuf("HtT", l * ldt);
+    // [H | Y] in one buffer: one SYRK gives H^T H and H^T Y (see gram_stage)
+    const size_t lda = even(l + m);
+    double* A = ctx->dbuf("A.in", n * lda);
+    ck(cudaMemcpy2DAsync(A, lda * 8, h, l * 8, l * 8, n, cudaMemcpyHostToDevice, ctx->stream), "upload H");
+    ck(cudaMemcpy2DAsync(A + l, lda * 8, y, m * 8, m * 8, n, cudaMemcpyHostToDevice, ctx->stream), "upload Y");
+    const size_t ldg = round_up(l + m, 8), ldt = ldg, lb = even(m);
+    double* G = ctx->dbuf("G0", (l + m) * ldg);
+    double* HtT = G + l;
     double* B = ctx->dbuf("beta", l * lb);
-    gram_dev(ctx, H.p, H.ld, n, l, Y.p, Y.ld, m, G, ldg, HtT, ldt, false);
+    gram_dev(ctx, A, lda, n, l + m, nullptr, 0, 0, G, ldg, nullptr, 0, false);
     solve_dev(ctx, G, ldg, HtT, ldt, l, m, n, *strategy, B, lb, nullptr, diag);
     download(ctx, beta, B, lb, l, m);
   });
@@ -978,8 +993,18 @@ int rbpg_gram_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, cons
     Padded X = pad_device(ctx, "X.pad", dx, ldx, n, d);
     Padded T = pad_device(ctx, "T.pad", dt, ldt_in, n, m);
     Padded W = pad_device(ctx, "W.pad", dw, ldw, d, l);
-    gram_stage(ctx, X.p, X.ld, T.p, T.ld, n, d, l, m, W.p, W.ld, db, dg, ldg, dhtt, ldt, accumulate != 0,
-               keep_h != 0, false);
+    const size_t lda = round_up(l + m, 8);
+    double* ga = ctx->dbuf("Gaug", (l + m) * lda);
+    gram_stage(ctx, X.p, X.ld, T.p, T.ld, n, d, l, m, W.p, W.ld, db, ga, lda, false, keep_h != 0, false);
+    if (accumulate) {  // add this block's partial sums to the caller's
+      ctx->run("add_block", [&] { return launch_add_block(dg, ldg, ga, lda, l, l, ctx->stream); });
+      if (m) ctx->run("add_block", [&] { return launch_add_block(dhtt, ldt, ga + l, lda, l, m, ctx->stream); });
+    } else {
+      ck(cudaMemcpy2DAsync(dg, ldg * 8, ga, lda * 8, l * 8, l, cudaMemcpyDeviceToDevice, ctx->stream), "store G");
+      if (m)
+        ck(cudaMemcpy2DAsync(dhtt, ldt * 8, ga + l, lda * 8, m * 8, l, cudaMemcpyDeviceToDevice, ctx->stream),
+           "store HtT");
+    }
   });
 }
 

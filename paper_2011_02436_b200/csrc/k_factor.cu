@@ -236,3 +236,20 @@ cudaError_t launch_trace(const double* A, long long lda, int n, double* out, cud
 }
 
 }  // namespace rbpg
+
+namespace rbpg {
+// out += in (rows x cols), fixed element-wise order
+__global__ void add_block_kernel(double* out, long long ldo, const double* in, long long ldi, long long rows,
+                                 long long cols) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < rows * cols;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long i = e / cols, j = e % cols;
+    out[i * ldo + j] = add_rn(out[i * ldo + j], in[i * ldi + j]);
+  }
+}
+cudaError_t launch_add_block(double* out, long long ldo, const double* in, long long ldi, long long rows,
+                             long long cols, cudaStream_t s) {
+  add_block_kernel<<<512, 256, 0, s>>>(out, ldo, in, ldi, rows, cols);
+  return cudaGetLastError();
+}
+}  // namespace rbpg

@@ -150,13 +150,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // K2: SYRK-TN family.  A (kRows x M) row-major via tmA; B = A for Gram tiles,
 // B = T (kRows x mB) via tmB for the H^T T tiles.
 // ============================================================================
-__global__ void __launch_bounds__(kGemmThreads, 1)
+template <int TILE>
+__global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
     syrk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SyrkParams p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = align1024(smem_raw);
   double* As = reinterpret_cast<double*>(smem);   // [stage][16][128]
-  double* Bs = As + kStages * kBK * kTile;        // [stage][16][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBK * kTile);
+  double* Bs = As + kStages * kBK * TILE;        // [stage][16][128]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBK * TILE);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
 
@@ -178,13 +179,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     isT = true;
   }
   const CUtensorMap* mapB = isT ? &tmB : &tmA;
-  const int i0 = I * kTile, j0 = J * kTile;
+  const int i0 = I * TILE, j0 = J * TILE;
 
   const long long kbeg = (long long)blockIdx.y * p.kPerSplit;
   long long kend = kbeg + p.kPerSplit;
   if (kend > p.kRows) kend = p.kRows;
   const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kBK - 1) / kBK) : 0;
-  constexpr uint32_t kStageBytes = 2u * kTile * kBK * sizeof(double);
+  constexpr uint32_t kStageBytes = 2u * TILE * kBK * sizeof(double);
 
   if (tid == 0) {
     tma_prefetch_desc(&tmA);
@@ -197,15 +198,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int s = 0; s < kStages && s < ktiles; ++s) {
       const int kr = static_cast<int>(kbeg + s * kBK);
       mbar_arrive_expect_tx(&full[s], kStageBytes);
-      tma_load_2d(As + s * kBK * kTile, &tmA, &full[s], i0, kr);
-      tma_load_2d(Bs + s * kBK * kTile, mapB, &full[s], j0, kr);
+      tma_load_2d(As + s * kBK * TILE, &tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * TILE, mapB, &full[s], j0, kr);
     }
   }
 
-  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
-  double acc[4][4][4];
+  constexpr int WM = TILE / 2, WARPS_N = TILE / 32, MT = WM / 16;
+  const int wm = (warp / WARPS_N) * WM, wn = (warp % WARPS_N) * 32;
+  double acc[MT][4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -214,26 +216,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   for (int kt = 0; kt < ktiles; ++kt) {
     const int s = kt % kStages;
     mbar_wait(&full[s], (kt / kStages) & 1);
-    const double* as = As + s * kBK * kTile;
-    const double* bs = Bs + s * kBK * kTile;
+    const double* as = As + s * kBK * TILE;
+    const double* bs = Bs + s * kBK * TILE;
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
       const int kc = ks * 4 + t;
-      double a[4][2], b[4];
+      double a[MT][2], b[4];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
-        const double2 v = *reinterpret_cast<const double2*>(as + kc * kTile + wm + mt * 16 + 2 * g);
+      for (int mt = 0; mt < MT; ++mt) {
+        const double2 v = *reinterpret_cast<const double2*>(as + kc * TILE + wm + mt * 16 + 2 * g);
         a[mt][0] = v.x;   // MMA row g   <-> tile row 2g
         a[mt][1] = v.y;   // MMA row g+8 <-> tile row 2g+1
       }
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp) {
-        const double2 w = *reinterpret_cast<const double2*>(bs + kc * kTile + wn + pp * 16 + 2 * g);
+        const double2 w = *reinterpret_cast<const double2*>(bs + kc * TILE + wn + pp * 16 + 2 * g);
         b[2 * pp] = w.x;       // n-tile 2pp   col g <-> tile col 16pp + 2g
         b[2 * pp + 1] = w.y;   // n-tile 2pp+1 col g <-> tile col 16pp + 2g + 1
       }
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
     }
@@ -241,15 +243,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (tid == 0 && kt + kStages < ktiles) {
       const int kr = static_cast<int>(kbeg + (long long)(kt + kStages) * kBK);
       mbar_arrive_expect_tx(&full[s], kStageBytes);
-      tma_load_2d(As + s * kBK * kTile, &tmA, &full[s], i0, kr);
-      tma_load_2d(Bs + s * kBK * kTile, mapB, &full[s], j0, kr);
+      tma_load_2d(As + s * kBK * TILE, &tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * TILE, mapB, &full[s], j0, kr);
     }
   }
 
   // ---- epilogue.  Thread holds rows r, r+1 (r even) x cols c..c+3 per (mt, pp).
   const int split = blockIdx.y;
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
+  for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
       const int r0 = i0 + wm + mt * 16 + 2 * g;
@@ -443,15 +445,30 @@ cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const SyrkParams& p, int splits,
+// tile = 128 (256 threads, 1 CTA/SM: the Gram) or 64 (128 threads, several CTAs/SM: small
+// trailing updates, where 128-wide tiles would leave most SMs idle).  The tensor maps' boxes
+// must be {tile, kBK}.
+cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const SyrkParams& p, int splits, int tile,
                         cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
-    attr = true;
-  }
   dim3 grid(p.nGram + p.nbI * p.nbT, splits);
-  syrk_kernel<<<grid, kGemmThreads, kTmaSmemBytes, s>>>(tmA, tmB, p);
+  if (tile == 128) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(syrk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+      attr = true;
+    }
+    syrk_kernel<128><<<grid, 256, kTmaSmemBytes, s>>>(tmA, tmB, p);
+  } else if (tile == 64) {
+    constexpr size_t smem = size_t(kStages) * 2 * 64 * kBK * sizeof(double) + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(syrk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    syrk_kernel<64><<<grid, 128, smem, s>>>(tmA, tmB, p);
+  } else {
+    return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
