@@ -28,6 +28,7 @@
 #include <vector>
 
 namespace rbpg {
+void trsm_trace_dump();
 cudaError_t launch_hidden(const CUtensorMap&, const CUtensorMap&, const HiddenParams&, cudaStream_t);
 cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams&, int, int, cudaStream_t);
 cudaError_t launch_syrk_finish(const SyrkParams&, int, int, int, cudaStream_t);
@@ -259,6 +260,9 @@ void gemm_dev(rbpg_context* ctx, int M, int N, int K, const double* A, size_t ld
 
 // X (n x m, ld ldx) <- (F F^T)^{-1} X, column chunks of <= 128 right-hand sides
 void trsm_pair_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X, size_t ldx, size_t n, size_t m) {
+  static const bool tr = std::getenv("RBPG_TRSM_TRACE") != nullptr;
+  if (tr) { cudaStreamSynchronize(ctx->stream); trsm_trace_dump(); }
+  struct Dump { bool on; cudaStream_t s; ~Dump() { if (on) { cudaStreamSynchronize(s); trsm_trace_dump(); } } } dump{tr, ctx->stream};
   for (size_t c0 = 0; c0 < m; c0 += 128) {
     const int mc = static_cast<int>(std::min<size_t>(128, m - c0));
     double* dinv = ctx->dbuf("trsm.dinv", ((n + 63) / 64) * 64 * 64);

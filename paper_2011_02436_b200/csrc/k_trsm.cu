@@ -17,6 +17,8 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 
 namespace cg = cooperative_groups;
 
@@ -139,6 +141,223 @@ __global__ void __launch_bounds__(256) trsm_sweep_kernel(const double* F, long l
 }
 
 // ---------------------------------------------------------------------------
+// Cluster variant for small right-hand sides (m <= 32, all owned rows fit in shared memory):
+// one thread-block cluster; 64-row block b is owned by CTA b % CL, which alone updates and
+// solves it.  The only exchange is the block solution Y_b, pushed by its owner into every
+// CTA's ring buffer with st.async (bytes complete on the receiver's mbarrier) -- no grid
+// barrier.  A cluster barrier every kSyncEvery steps bounds the skew below the ring depth.
+// ---------------------------------------------------------------------------
+constexpr int kRing = 8;
+constexpr int kSyncEvery = 4;
+constexpr int kClusterMaxM = 32;
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+constexpr int kPadT = kTB + 2;  // 16-byte aligned padded tile rows
+
+// 64 x 64 block of F starting at (row0, col0) into T[64][kPadT] by cp.async; rows >= nrows and
+// columns >= ncols are zero-filled (F beyond n is never read: ld padding holds garbage).
+__device__ __forceinline__ void load_tile_async(double* T, const double* F, long long ldf, int row0, int nrows,
+                                                int col0, int ncols, int tid, int nt) {
+  for (int e = tid; e < kTB * (kTB / 2); e += nt) {
+    const int r = e / (kTB / 2), ch = e % (kTB / 2);
+    const int c = 2 * ch;
+    uint32_t bytes = 0;
+    if (r < nrows && c < ncols) bytes = (c + 1 < ncols) ? 16u : 8u;
+    const double* src = bytes ? F + (long long)(row0 + r) * ldf + col0 + c : F;
+    cp_async16(T + r * kPadT + c, src, bytes);
+  }
+}
+
+__device__ long long* g_trsm_trace = nullptr;
+// C[64][m] = A * B  (or C -= A * B), A 64x64 with A(r, k) = aT ? A[k*lda + r] : A[r*lda + k],
+// B 64 x m row-major (ld m), on FP64 tensor cores: one (m16, n8) output tile per warp pass,
+// two interleaved accumulator chains over K = 64.
+__device__ __forceinline__ void mma64(const double* A, int lda, bool aT, const double* B, int m, double* Cm,
+                                      bool subtract, int tid) {
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int nt8 = (m + 7) / 8;
+  for (int tile = warp; tile < 4 * nt8; tile += 8) {
+    const int m0 = (tile / nt8) * 16, n0 = (tile % nt8) * 8;
+    double c0[4] = {0.0, 0.0, 0.0, 0.0}, c1[4] = {0.0, 0.0, 0.0, 0.0};
+    const int col = n0 + g;
+#pragma unroll 4
+    for (int k0 = 0; k0 < kTB; k0 += 8) {
+      const int ka = k0 + t, kb = k0 + 4 + t;
+      const double a0 = aT ? A[ka * lda + m0 + g] : A[(m0 + g) * lda + ka];
+      const double a1 = aT ? A[ka * lda + m0 + g + 8] : A[(m0 + g + 8) * lda + ka];
+      const double b0 = col < m ? B[ka * m + col] : 0.0;
+      const double a2 = aT ? A[kb * lda + m0 + g] : A[(m0 + g) * lda + kb];
+      const double a3 = aT ? A[kb * lda + m0 + g + 8] : A[(m0 + g + 8) * lda + kb];
+      const double b1 = col < m ? B[kb * m + col] : 0.0;
+      dmma_16x8x4(c0, a0, a1, b0);
+      dmma_16x8x4(c1, a2, a3, b1);
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = m0 + g + 8 * h;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int cc = n0 + 2 * t + q;
+        if (cc >= m) continue;
+        const double v = c0[2 * h + q] + c1[2 * h + q];
+        if (subtract)
+          Cm[r * m + cc] -= v;
+        else
+          Cm[r * m + cc] = v;
+      }
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, long long ldf, const double* Dinv,
+                                                              double* X, long long ldx, int n, int m) {
+  extern __shared__ __align__(16) double csm[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), cta = static_cast<int>(cl.block_rank());
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int nblk = (n + kTB - 1) / kTB;
+  const int nown = (nblk - cta + C - 1) / C;  // owned blocks: cta, cta + C, ...
+  const int nown_max = (nblk + C - 1) / C;   // identical layout in every CTA (remote addresses)
+  double* Rown = csm;                                 // [nown_max][64][m]  rhs -> solutions
+  double* Ring = Rown + (size_t)nown_max * kTB * m;   // [kRing][64][m] block solutions
+  double* Ds = Ring + kRing * kTB * m;                // [2][64][kPadT] diagonal-block inverses
+  double* Tc = Ds + 2 * kTB * kPadT;                  // [64][kPadT] critical F tile (prefetched)
+  double* To = Tc + kTB * kPadT;                      // [64][kPadT] other F tiles
+  __shared__ __align__(8) uint64_t rbar[kRing];
+  if (tid < kRing) mbar_init(&rbar[tid], 1);
+  if (tid == 0) fence_mbar_init();
+  for (int e = tid; e < nown * kTB * m; e += nt) {
+    const int ob = e / (kTB * m), rem = e % (kTB * m), q = rem / m, c = rem % m;
+    const int row = (cta + ob * C) * kTB + q;
+    Rown[e] = row < n ? X[(long long)row * ldx + c] : 0.0;
+  }
+  cl.sync();
+  const uint32_t ybytes = static_cast<uint32_t>(kTB * m * sizeof(double));
+  auto block_of = [&](int s) { return s < nblk ? s : 2 * nblk - 1 - s; };
+  auto owns = [&](int b) { return b % C == cta; };
+
+  // Y_s = D_b^{-1} R_b (forward steps) or D_b^{-T} R_b (backward), pushed to every CTA's ring slot
+  auto solve_and_push = [&](int s, const double* D) {
+    const bool bwd = s >= nblk;
+    const int b = block_of(s);
+    double* Rb = Rown + (size_t)(b / C) * kTB * m;
+    const int slot = s % kRing;
+    double* Y = Ring + slot * kTB * m;
+    mma64(D, kPadT, bwd, Rb, m, Y, false, tid);
+    __syncthreads();
+    for (int e = tid; e < kTB * m; e += nt) Rb[e] = Y[e];  // the block's solution
+    const uint32_t yl = smem_u32(Y), bl = smem_u32(&rbar[slot]);
+    for (int d = 0; d < C; ++d) {
+      if (d == cta) continue;
+      const uint32_t ry = mapa_u32(yl, d), rb = mapa_u32(bl, d);
+      for (int e = tid; e < kTB * m / 2; e += nt) st_async_v2f64(ry + 16 * e, Y[2 * e], Y[2 * e + 1], rb);
+    }
+    if (tid == 0)  // the own copy was written in place
+      asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;\n" ::"r"(bl), "r"(ybytes) : "memory");
+  };
+  // R_bp -= F-tile * Y (forward: tile = F[bp rows][b cols]; backward: tile = F[b rows][bp cols]^T)
+  auto update = [&](int bp, const double* T, bool bwd, const double* Yb) {
+    double* Rp = Rown + (size_t)(bp / C) * kTB * m;
+    mma64(T, kPadT, bwd, Yb, m, Rp, true, tid);
+  };
+  auto issue_tile = [&](double* T, int b, int bp, bool bwd) {
+    if (!bwd) load_tile_async(T, F, ldf, bp * kTB, min(kTB, n - bp * kTB), b * kTB, min(kTB, n - b * kTB), tid, nt);
+    else load_tile_async(T, F, ldf, b * kTB, min(kTB, n - b * kTB), bp * kTB, min(kTB, n - bp * kTB), tid, nt);
+  };
+  auto issue_dinv = [&](double* D, int b) {
+    const double* src = Dinv + (long long)b * kTB * kTB;
+    for (int e = tid; e < kTB * (kTB / 2); e += nt) {
+      const int r = e / (kTB / 2), c = 2 * (e % (kTB / 2));
+      cp_async16(D + r * kPadT + c, src + r * kTB + c, 16u);
+    }
+  };
+
+  // step 0's solution needs no update
+  if (owns(block_of(0))) {
+    issue_dinv(Ds, block_of(0));
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+  }
+  if (tid < kRing && tid == 0) mbar_arrive_expect_tx(&rbar[0], ybytes);
+  __syncthreads();
+  if (owns(block_of(0))) solve_and_push(0, Ds);
+
+  long long tw = 0, tc = 0, to = 0;
+  for (int s = 0; s < 2 * nblk; ++s) {
+    const bool bwd = s >= nblk;
+    const int b = block_of(s);
+    const int slot = s % kRing;
+    const bool last = s + 1 == 2 * nblk;
+    const int bn = last ? -1 : block_of(s + 1);
+    const bool bwd_n = s + 1 >= nblk;
+    // does the next step's block need this step's Y? (not at the forward -> backward turn)
+    const bool crit = !last && owns(bn) && (bwd ? bn < b : bn > b) && bwd_n == bwd;
+    // prefetch (independent of Y_s): the critical tile, the first non-critical tile and the
+    // next diagonal inverse
+    if (crit) issue_tile(Tc, b, bn, bwd);
+    int first_other = -1;
+    for (int ob = 0; ob < nown; ++ob) {
+      const int bp = cta + ob * C;
+      if ((bwd ? bp >= b : bp <= b) || (crit && bp == bn)) continue;
+      first_other = bp;
+      break;
+    }
+    if (first_other >= 0) issue_tile(To, b, first_other, bwd);
+    if (!last && owns(bn)) issue_dinv(Ds + ((s + 1) & 1) * kTB * kPadT, bn);
+    cp_async_commit();
+    if (!last && tid == 0) mbar_arrive_expect_tx(&rbar[(s + 1) % kRing], ybytes);
+    if ((s + 1) % kSyncEvery == 0) cl.sync();  // skew < kRing steps
+    long long t1 = clock64();
+    mbar_wait(&rbar[slot], (s / kRing) & 1);
+    const double* Yb = Ring + slot * kTB * m;
+    cp_async_wait_all();
+    __syncthreads();
+    long long t2 = clock64(); tw += t2 - t1;
+    if (!last && owns(bn)) {  // critical path: update the next block, solve it, push
+      if (crit) update(bn, Tc, bwd, Yb);
+      __syncthreads();
+      solve_and_push(s + 1, Ds + ((s + 1) & 1) * kTB * kPadT);
+    }
+    long long t3 = clock64(); tc += t3 - t2;
+    for (int ob = 0; ob < nown; ++ob) {  // remaining updates off the critical path
+
+      const int bp = cta + ob * C;
+      if (bwd ? bp >= b : bp <= b) continue;
+      if (crit && bp == bn) continue;
+      if (bp != first_other) {  // prefetched above otherwise
+        __syncthreads();
+        issue_tile(To, b, bp, bwd);
+        cp_async_commit();
+        cp_async_wait_all();
+        __syncthreads();
+      }
+      update(bp, To, bwd, Yb);
+    }
+    __syncthreads();
+    to += clock64() - t3;
+  }
+  if (cta == 0 && tid == 0 && g_trsm_trace) { g_trsm_trace[0] += tw; g_trsm_trace[1] += tc; g_trsm_trace[2] += to; g_trsm_trace[3] += 2 * nblk; }
+  cl.sync();  // no CTA exits while remote stores may still target it
+  for (int e = tid; e < nown * kTB * m; e += nt) {
+    const int ob = e / (kTB * m), rem = e % (kTB * m), q = rem / m, c = rem % m;
+    const int row = (cta + ob * C) * kTB + q;
+    if (row < n) X[(long long)row * ldx + c] = Rown[e];
+  }
+}
+
+static size_t trsm_cluster_smem(int n, int m, int C) {
+  const int nblk = (n + kTB - 1) / kTB;
+  const int nown = (nblk + C - 1) / C;
+  return (size_t(nown) * kTB * m + size_t(kRing) * kTB * m + 4 * size_t(kTB) * kPadT) * sizeof(double);
+}
+
 cudaError_t launch_trsm_pair(const double* F, long long ldf, double* X, long long ldx, int n, int m, int fwd, int bwd,
                              int num_sms, double* dinv_ws, cudaStream_t s) {
   if (n <= 0 || m <= 0) return cudaSuccess;
@@ -159,6 +378,34 @@ cudaError_t launch_trsm_pair(const double* F, long long ldf, double* X, long lon
     if (e != cudaSuccess) return e;
     attr_smem = smem;
   }
+  if (fwd && bwd && m <= kClusterMaxM && !std::getenv("RBPG_TRSM_GRID")) {
+    const int C = std::min(16, nblk);
+    const size_t csmem = trsm_cluster_smem(n, m, C);
+    if (csmem <= 220 * 1024) {
+      static size_t cattr = 0;
+      if (csmem > cattr) {
+        e = cudaFuncSetAttribute(trsm_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(trsm_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+        cattr = csmem;
+      }
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(C);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = csmem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      const double* Dc = dinv_ws;
+      return cudaLaunchKernelEx(&cfg, trsm_cluster_kernel, F, ldf, Dc, X, ldx, n, m);
+    }
+  }
   int blocks = std::min(num_sms, std::max(1, (n + kTB - 1) / kTB));
   const double* Dc = dinv_ws;
   for (int dir = 0; dir < 2; ++dir) {
@@ -171,4 +418,20 @@ cudaError_t launch_trsm_pair(const double* F, long long ldf, double* X, long lon
   return cudaSuccess;
 }
 
+}  // namespace rbpg
+namespace rbpg {
+void trsm_trace_dump() {
+  static long long* buf = nullptr;
+  if (!buf) {
+    cudaMalloc(&buf, 64);
+    cudaMemset(buf, 0, 64);
+    cudaMemcpyToSymbol(g_trsm_trace, &buf, sizeof(buf));
+    return;
+  }
+  long long h[4];
+  cudaMemcpy(h, buf, 32, cudaMemcpyDeviceToHost);
+  std::fprintf(stderr, "[trsm trace] steps %lld wait %.0f crit %.0f other %.0f cycles/step\n", h[3],
+               double(h[0]) / (h[3] ? h[3] : 1), double(h[1]) / (h[3] ? h[3] : 1), double(h[2]) / (h[3] ? h[3] : 1));
+  cudaMemset(buf, 0, 64);
+}
 }  // namespace rbpg
