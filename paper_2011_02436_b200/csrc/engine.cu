@@ -111,6 +111,20 @@ struct rbpg_context {
     return p;
   }
   double* dbuf(const std::string& name, size_t elems) { return static_cast<double*>(buf(name, elems * 8)); }
+  std::map<std::string, std::pair<void*, size_t>> hbufs;  // pinned host staging
+  void* pinned(const std::string& name, size_t bytes) {
+    auto it = hbufs.find(name);
+    if (it != hbufs.end() && it->second.second >= bytes) return it->second.first;
+    if (it != hbufs.end()) {
+      cudaStreamSynchronize(stream);
+      cudaFreeHost(it->second.first);
+      hbufs.erase(it);
+    }
+    void* p = nullptr;
+    ck(cudaMallocHost(&p, bytes < 64 ? 64 : bytes), ("cudaMallocHost " + name).c_str());
+    hbufs[name] = {p, bytes};
+    return p;
+  }
   // per-kernel-class device timing (bench.py roofline evidence), off by default
   bool profile = false;
   struct Prof {
@@ -277,13 +291,15 @@ struct FactorResult {
   const double* F = nullptr;  // factor rows by final position (n x n, ld ldF)
   size_t ldF = 0;
   const int* ord = nullptr;   // device: position -> original column
-  FactorState st{};
+  FactorState st{};           // host copy (valid after the stream reaches the factorisation's end)
+  FactorState* dst = nullptr; // device state
+  FactorState* hst = nullptr; // pinned host staging of the state
 };
 
 // Diagonal-pivoted (pivoting = 1, linalg.cpp:157-248) or unpivoted SpdFactor (pivoting = 0,
 // linalg.cpp:99-139) blocked Cholesky of the symmetric dG (n x n, ld ldg).  dG is not modified.
 FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t n, size_t rows_for_tol, double tol,
-                        int pivoting, const std::string& tag) {
+                        int pivoting, const std::string& tag, bool sync = true) {
   cudaStream_t s = ctx->stream;
   const size_t ldn = round_up(n, 8);
   double* Ga = ctx->dbuf(tag + ".Ga", n * ldn);
@@ -366,8 +382,15 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
   ctx->run("gather_factor", [&] { return launch_gather_factor(Fo, static_cast<long long>(ldn), ov[cur], static_cast<int>(n), F,
                                 static_cast<long long>(ldn), ctx->num_sms, s); });
   FactorResult r;
-  ck(cudaMemcpyAsync(&r.st, st, sizeof(FactorState), cudaMemcpyDeviceToHost, s), "read factor state");
-  ck(cudaStreamSynchronize(s), "factor sync");
+  r.dst = st;
+  // pinned staging so the state copy is truly asynchronous (sync = false: the caller reads it later)
+  FactorState* hs = static_cast<FactorState*>(ctx->pinned("factor.state", sizeof(FactorState)));
+  ck(cudaMemcpyAsync(hs, st, sizeof(FactorState), cudaMemcpyDeviceToHost, s), "read factor state");
+  r.hst = hs;
+  if (sync) {
+    ck(cudaStreamSynchronize(s), "factor sync");
+    r.st = *hs;
+  }
   if (trace) {
     unsigned long long h[6];
     cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
@@ -505,15 +528,23 @@ void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   if (sg.kind != RBPG_RANK_BASED) fail(RBPG_RUNTIME_ERROR, "solve_beta: unknown strategy");
   if (sg.rank_tol < 0.0 || !std::isfinite(sg.rank_tol))
     fail(RBPG_INVALID_ARGUMENT, "rank_revealing_permutation: tolerance must be >= 0");
-  FactorResult f = factor_dev(ctx, dG, ldg, L, rows, sg.rank_tol, 1, "rrf");
+  FactorResult f = factor_dev(ctx, dG, ldg, L, rows, sg.rank_tol, 1, "rrf", false);
+  // speculate the full-rank solve (elm.cpp:202-214) before the one host readback of the rank;
+  // with rank < L its result is discarded
+  const size_t lm = even(m);
+  double* rhs = ctx->dbuf("rank.rhs", L * lm);
+  ctx->run("gather rhs", [&] { return launch_gather_rows(dHtT, ldt, f.ord, L, m, rhs, lm, ctx->stream); });
+  trsm_pair_dev(ctx, f.F, f.ldF, rhs, lm, L, m);
+  ctx->run("unpermute beta", [&] { return launch_scatter_rows(rhs, lm, f.ord, L, m, dBeta, ldb, ctx->stream); });
+  int* ho = static_cast<int*>(ctx->pinned("order.out", L * 4));
+  if (order_out) ck(cudaMemcpyAsync(ho, f.ord, L * 4, cudaMemcpyDeviceToHost, ctx->stream), "read order");
+  ck(cudaStreamSynchronize(ctx->stream), "factor sync");
+  f.st = *f.hst;
   const size_t rank = static_cast<size_t>(f.st.rank);
   diag->rank = rank;
   diag->rank_known = 1;
-  if (order_out) {
-    std::vector<int> o(L);
-    ck(cudaMemcpy(o.data(), f.ord, L * 4, cudaMemcpyDeviceToHost), "read order");
-    for (size_t i = 0; i < L; ++i) order_out[i] = static_cast<size_t>(o[i]);
-  }
+  if (order_out)
+    for (size_t i = 0; i < L; ++i) order_out[i] = static_cast<size_t>(ho[i]);
   if (rank == 0 || L < 2) {
     diag->fallback_to_direct = 1;
     diag->split_lo = L;
@@ -524,14 +555,7 @@ void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   const size_t split = (rank == L) ? (L + 1) / 2 : rank;
   diag->split_lo = split;
   diag->split_hi = L - split;
-  if (rank == L) {
-    const size_t lm = even(m);
-    double* rhs = ctx->dbuf("rank.rhs", L * lm);
-    ctx->run("gather rhs", [&] { return launch_gather_rows(dHtT, ldt, f.ord, L, m, rhs, lm, ctx->stream); });
-    trsm_pair_dev(ctx, f.F, f.ldF, rhs, lm, L, m);
-    ctx->run("unpermute beta", [&] { return launch_scatter_rows(rhs, lm, f.ord, L, m, dBeta, ldb, ctx->stream); });
-    return;
-  }
+  if (rank == L) return;  // the speculated solve is the answer
   try {
     block_dev(ctx, dG, ldg, dHtT, ldt, L, m, rows, f.ord, split, dBeta, ldb, diag);
   } catch (const Fail& e) {
@@ -541,15 +565,19 @@ void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   }
 }
 
-void check_finite(rbpg_context* ctx, const double* dBeta, size_t ldb, size_t L, size_t m) {
+// non-finite beta check (elm.cpp:275-277); with defer the flag lands in pinned memory and the
+// caller tests it after its own synchronisation
+const int* check_finite(rbpg_context* ctx, const double* dBeta, size_t ldb, size_t L, size_t m, bool defer = false) {
   int* flag = static_cast<int*>(ctx->buf("nonfinite", 4));
   ck(cudaMemsetAsync(flag, 0, 4, ctx->stream), "memset flag");
   ctx->run("nonfinite", [&] { return launch_nonfinite(dBeta, static_cast<long long>(ldb), static_cast<int>(L), static_cast<int>(m), flag,
                             ctx->stream); });
-  int h = 0;
-  ck(cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, ctx->stream), "read flag");
+  int* h = static_cast<int*>(ctx->pinned("nonfinite", 4));
+  ck(cudaMemcpyAsync(h, flag, 4, cudaMemcpyDeviceToHost, ctx->stream), "read flag");
+  if (defer) return h;
   ck(cudaStreamSynchronize(ctx->stream), "sync");
-  if (h) fail(RBPG_RUNTIME_ERROR, "train: solver produced non-finite output weights");
+  if (*h) fail(RBPG_RUNTIME_ERROR, "train: solver produced non-finite output weights");
+  return h;
 }
 
 struct Padded {
@@ -602,14 +630,19 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
   }
   for (size_t r0 = 0; r0 < N; r0 += chunk) {
     const size_t nr = std::min(chunk, N - r0);
-    if (timed) cudaEventRecord(ctx->ev[0], ctx->stream);
+    // chunk 0 is timed by ev[0]/ev[1] without a sync (read by the caller after its own sync);
+    // further chunks (H larger than the budget) synchronise on ev[4]/ev[5]
+    cudaEvent_t ea = r0 == 0 ? ctx->ev[0] : ctx->ev[4], eb = r0 == 0 ? ctx->ev[1] : ctx->ev[5];
+    if (timed) cudaEventRecord(ea, ctx->stream);
     hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh);
     if (timed) {
-      cudaEventRecord(ctx->ev[1], ctx->stream);
-      cudaEventSynchronize(ctx->ev[1]);
-      float ms = 0.f;
-      cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
-      hidden_ms += ms;
+      cudaEventRecord(eb, ctx->stream);
+      if (r0 > 0) {
+        cudaEventSynchronize(eb);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ea, eb);
+        hidden_ms += ms;
+      }
     }
     if (m > 0)
       ck(cudaMemcpy2DAsync(dH + L, ldh * 8, dT + r0 * ldt_in, ldt_in * 8, m * 8, nr, cudaMemcpyDeviceToDevice,
@@ -644,7 +677,7 @@ void scores_dev(rbpg_context* ctx, const double* H, size_t ldh, size_t N, size_t
 
 uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* dT, size_t ldt_in, size_t N,
                         size_t d, size_t L, size_t m, const double* dW, size_t ldw, const double* db,
-                        const double* dBeta, size_t ldb) {
+                        const double* dBeta, size_t ldb, unsigned long long** deferred = nullptr) {
   unsigned long long* hits = static_cast<unsigned long long*>(ctx->buf("hits", 8));
   ck(cudaMemsetAsync(hits, 0, 8, ctx->stream), "memset hits");
   if (N > 0) {
@@ -675,10 +708,14 @@ uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const d
       }
     }
   }
-  unsigned long long h = 0;
-  ck(cudaMemcpyAsync(&h, hits, 8, cudaMemcpyDeviceToHost, ctx->stream), "read hits");
+  unsigned long long* h = static_cast<unsigned long long*>(ctx->pinned("hits", 8));
+  ck(cudaMemcpyAsync(h, hits, 8, cudaMemcpyDeviceToHost, ctx->stream), "read hits");
+  if (deferred) {
+    *deferred = h;
+    return 0;
+  }
   ck(cudaStreamSynchronize(ctx->stream), "sync");
-  return h;
+  return *h;
 }
 
 // train() body on device-resident X, T (elm.cpp:231-280 after validation and init_hidden)
@@ -700,15 +737,20 @@ void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* d
   float hidden_ms = gram_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, G, ldg, false, true, true);
   solve_dev(ctx, G, ldg, HtT, ldt, L, m, N, sg, dBeta, ldb, order_out, diag);
   cudaEventRecord(ctx->ev[3], ctx->stream);
-  cudaEventSynchronize(ctx->ev[3]);
-  float total_ms = 0.f;
+  // finiteness check and accuracy pass enqueued behind the solve; one synchronisation for both
+  const int* bad = check_finite(ctx, dBeta, ldb, L, m, true);
+  unsigned long long* hits = nullptr;
+  accuracy_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, dBeta, ldb, &hits);
+  ck(cudaStreamSynchronize(ctx->stream), "sync");
+  float total_ms = 0.f, first_hidden_ms = 0.f;
   cudaEventElapsedTime(&total_ms, ctx->ev[2], ctx->ev[3]);
+  if (N > 0) cudaEventElapsedTime(&first_hidden_ms, ctx->ev[0], ctx->ev[1]);
+  hidden_ms += first_hidden_ms;
   (void)wall0;
   diag->hidden_seconds = hidden_ms * 1e-3;
   diag->solve_seconds = std::max(0.f, total_ms - hidden_ms) * 1e-3;
-  check_finite(ctx, dBeta, ldb, L, m);
-  const uint64_t hits = accuracy_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, dBeta, ldb);
-  diag->training_accuracy = N ? static_cast<double>(hits) / static_cast<double>(N) : 0.0;
+  if (*bad) fail(RBPG_RUNTIME_ERROR, "train: solver produced non-finite output weights");
+  diag->training_accuracy = N ? static_cast<double>(*hits) / static_cast<double>(N) : 0.0;
 }
 
 template <typename F>
@@ -781,6 +823,7 @@ void rbpg_context_destroy(rbpg_context* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
+  for (auto& kv : ctx->hbufs) cudaFreeHost(kv.second.first);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->own);
   delete ctx;
