@@ -11,7 +11,7 @@ import os
 from ctypes import POINTER, c_char, c_double, c_int, c_size_t, c_uint64, c_void_p
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librbpelm_b200.so")
+LIB_PATH = os.environ.get("RBPG_LIB_PATH") or os.path.join(_HERE, "librbpelm_b200.so")  # override: debugging builds
 
 
 class rbpg_status(ctypes.Structure):

@@ -30,6 +30,7 @@
 #include <cooperative_groups.h>
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 
 namespace cg = cooperative_groups;
 
@@ -431,6 +432,305 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
 }
 
 // ---------------------------------------------------------------------------
+// Register-resident cluster variant (nl <= 16 * 64): one label per quad (4 lanes); lane q of the
+// quad holds its label's panel columns q, q+4, ..., q+60 in registers p[0..15], so the per-column
+// dot products read no shared memory for the label side.  Candidate rows travel in the same
+// "lane-major" order (row[q*16 + i] = P[label][q + 4i]), which is also how they are consumed.
+// Arithmetic is identical in the 4 lanes of a quad (xor-shuffle sums), so every lane holds the
+// same col and d; the reduction order is fixed and label-independent (exact twin ties persist).
+// ---------------------------------------------------------------------------
+constexpr int kRegLabels = kPThreads / 4;  // 64 labels per CTA
+constexpr int kRowQ = 18;                   // padded quarter of a lane-major row (16 used)
+constexpr int kRowLen = 4 * kRowQ;
+
+__global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int n = p.n, k = p.k, kb = p.kb, nl = n - k;
+  const int R = p.rows_per_cta;  // <= 64
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks()), cta = static_cast<int>(cl.block_rank());
+  int* lab_at = reinterpret_cast<int*>(smem_raw);  // [nl]
+  int* pos_of = lab_at + nl;                       // [nl]
+  __shared__ Cand cand_all[2][kMaxCluster];
+  // candidate rows, lane-major with a padded quarter stride (row[q*kRowQ + i] = P[label][q + 4i]):
+  // the 4 distinct 128-byte quarters a warp reads per step land on different banks
+  __shared__ __align__(16) double rows_all[2][kMaxCluster][kRowLen];
+  __shared__ __align__(16) double wrow[kPWarps][kRowLen];             // each warp's best row
+  __shared__ __align__(8) uint64_t cand_full[2];
+  __shared__ Cand wbest[kPWarps];
+  __shared__ int s_stop;
+  __shared__ unsigned long long s_wkey;
+  __shared__ int s_piv, s_xp, s_y, s_src;
+
+  FactorState* st = p.st;
+  if (st->stopped) {
+    if (cta == 0)
+      for (int i = tid; i < n; i += blockDim.x) p.ord_out[i] = p.ord_in[i];
+    return;
+  }
+  const int lbeg = k + cta * R;
+  const int nown = max(0, min(n, lbeg + R) - lbeg);
+  const int li = tid >> 2, q = tid & 3;
+  const int x = lbeg + li;
+  const bool mine = li < nown;
+  double pr[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) pr[i] = 0.0;
+  double dl = mine ? p.d_in[x] : -DBL_MAX;
+
+  for (int i = tid; i < nl; i += blockDim.x) {
+    lab_at[i] = k + i;
+    pos_of[i] = k + i;
+  }
+  if (tid == 0) {
+    s_stop = 0;
+    mbar_init(&cand_full[0], 1);
+    mbar_init(&cand_full[1], 1);
+    fence_mbar_init();
+  }
+  cl.sync();
+  const uint32_t kStepBytes = static_cast<uint32_t>(C) * (sizeof(Cand) + kPanelW * sizeof(double));
+  const double cut = st->cut;
+  const double thresh = st->thresh;
+  for (int i = tid; i < 2 * kMaxCluster * kRowLen; i += blockDim.x) (&rows_all[0][0][0])[i] = 0.0;
+  __syncthreads();
+
+  // stage this warp's best row (the quad holding label position `pos`) into wrow[warp]
+  auto stage_row = [&](unsigned long long key, int pos, int mypos, unsigned long long mykey) {
+    const unsigned who = __ballot_sync(0xffffffffu, q == 0 && mykey == key && mypos == pos && pos != INT_MAX);
+    if (who) {
+      const int lead = __ffs(who) - 1;  // lane of the quad leader
+      if ((lane >> 2) == (lead >> 2)) {
+        double2* dst = reinterpret_cast<double2*>(&wrow[warp][q * kRowQ]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = make_double2(pr[2 * i], pr[2 * i + 1]);
+      }
+    }
+  };
+  auto combine_publish = [&](int j) {
+    unsigned long long key = 0, k0 = 0;
+    int pos = INT_MAX, p0 = INT_MAX;
+    if (lane < kPWarps) {
+      k0 = key = wbest[lane].key;
+      p0 = pos = wbest[lane].pos;
+    }
+    warp_argmax(key, pos);
+    const int wsrc = __ffs(__ballot_sync(0xffffffffu, lane < kPWarps && k0 == key && p0 == pos)) - 1;
+    const int par = (j - k) & 1;
+    const int roff = (lane >> 3) * kRowQ + 2 * (lane & 7);  // lane's 16-byte chunk of the padded row
+    const double2 rv = *reinterpret_cast<const double2*>(&wrow[wsrc][roff]);
+    const uint32_t row_l = smem_u32(&rows_all[par][cta][roff]);
+    const uint32_t cand_l = smem_u32(&cand_all[par][cta]);
+    const uint32_t bar_l = smem_u32(&cand_full[par]);
+    for (int d = warp; d < C; d += kPWarps) {
+      const uint32_t rbar = mapa_u32(bar_l, d);
+      st_async_v2f64(mapa_u32(row_l, d), rv.x, rv.y, rbar);
+      if (lane == 0) st_async_v2b64(mapa_u32(cand_l, d), key, static_cast<unsigned long long>(pos), rbar);
+    }
+  };
+
+  // ---- initial candidates (rows are still zero)
+  {
+    unsigned long long key = 0;
+    int pos = INT_MAX;
+    if (mine && q == 0) {
+      if (p.pivoting) {
+        key = dkey(dl);
+        pos = x;
+      } else if (x == k) {
+        key = dkey(dl);
+        pos = k;
+      }
+    }
+    const unsigned long long mk = key;
+    const int mp = pos;
+    warp_argmax(key, pos);
+    stage_row(key, pos, mp, mk);
+    if (lane == 0) {
+      wbest[warp].key = key;
+      wbest[warp].pos = pos;
+    }
+    __syncthreads();
+    combine_publish(k);
+  }
+
+  long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  for (int c = 0; c < kb; ++c) {
+    const int j = k + c;
+    long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
+    if (p.trace) t0 = clock64();
+    if (warp == 0) {
+      if (lane == 0) mbar_arrive_expect_tx(&cand_full[c & 1], kStepBytes);
+      mbar_wait(&cand_full[c & 1], (c >> 1) & 1);
+      unsigned long long ck = 0;
+      int cp = INT_MAX;
+      if (lane < C) {
+        ck = cand_all[c & 1][lane].key;
+        cp = cand_all[c & 1][lane].pos;
+      }
+      unsigned long long wkey = ck;
+      int wpos = cp;
+      warp_argmax(wkey, wpos);
+      const int src = __ffs(__ballot_sync(0xffffffffu, lane < C && ck == wkey && cp == wpos)) - 1;
+      if (lane == 0) {
+        s_wkey = wkey;
+        s_piv = wpos;
+        s_xp = lab_at[wpos - k];
+        s_y = lab_at[j - k];
+        s_src = src;
+      }
+      named_bar_arrive(1, kPThreads);
+    } else {
+      named_bar_sync(1, kPThreads);
+    }
+    if (p.trace) t1 = clock64();
+    const int piv = s_piv, xp = s_xp, y = s_y;
+    const double dj = dkey_inv(s_wkey);
+    // this quad's label: position after this step's swap and G entry (load issued first)
+    int pos = -1;
+    if (mine) pos = (x == y) ? piv : (x == xp ? j : pos_of[x - k]);
+    const bool alive = pos > j;
+    const double gv = alive ? p.G[(long long)xp * p.ldg + x] : 0.0;
+    bool stop;
+    if (p.pivoting) {
+      stop = (dj > 0.0 ? sqrt(dj) : 0.0) <= cut;            // linalg.cpp:219-223
+    } else {
+      stop = !isfinite(dj) || dj <= thresh || dj <= 0.0;   // linalg.cpp:118-119
+    }
+    if (stop) {
+      __syncthreads();
+      if (tid == 0) {
+        if (piv != j) {
+          lab_at[j - k] = xp;
+          lab_at[piv - k] = y;
+          pos_of[xp - k] = j;
+          pos_of[y - k] = piv;
+        }
+        s_stop = p.pivoting ? 1 : 2;
+        if (cta == 0) {
+          st->stopped = 1;
+          st->rank = j;
+          if (!p.pivoting) {
+            st->fail = 1;
+            st->fail_index = j;
+            st->fail_value = dj;
+          }
+        }
+      }
+      __syncthreads();
+      break;
+    }
+    const double rjj = sqrt(dj);
+    const double inv_rjj = 1.0 / rjj;
+    if (p.trace) {
+      if (__double_as_longlong(gv) == 0x7ff0deadbeefll || __double_as_longlong(inv_rjj) == 0x7ff0deadbeefll)
+        p.trace[7] = 1;  // forces the G load and the reciprocal to complete before t2
+      t2 = clock64();
+    }
+    const double* prow = rows_all[c & 1][s_src];  // lane-major: prow[q*16 + i] = P[xp][q + 4i]
+    // ---- update: dot over columns cc = q + 4i < c from registers.  Entries at and beyond c are
+    // zero in both operands, so whole 16-column chunks are summed unpredicated; a chunk is skipped
+    // (warp-uniform) once c <= its first column.
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const double2* pv = reinterpret_cast<const double2*>(prow + q * kRowQ);
+#pragma unroll
+    for (int i = 0; i < 16; i += 4) {
+      if (c > 4 * i) {
+        const double2 v0 = pv[i / 2], v1 = pv[i / 2 + 1];
+        a0 = fma(pr[i], v0.x, a0);
+        a1 = fma(pr[i + 1], v0.y, a1);
+        a2 = fma(pr[i + 2], v1.x, a2);
+        a3 = fma(pr[i + 3], v1.y, a3);
+      }
+    }
+    double sq = (a0 + a1) + (a2 + a3);
+    sq = sq + __shfl_xor_sync(0xffffffffu, sq, 1);
+    sq = sq + __shfl_xor_sync(0xffffffffu, sq, 2);
+    const int slot = c >> 2, owner_lane = c & 3;
+    unsigned long long bkey = 0;
+    int bpos = INT_MAX;
+    const double col = (gv - sq) * inv_rjj;
+    // branch-free register write of the new column (alive labels) or of F(j, j) = rjj (the pivot)
+    const bool is_piv = mine && x == xp;
+    const bool wr = (alive || is_piv) && q == owner_lane;
+    const double wv = alive ? col : rjj;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pr[i] = (wr && i == slot) ? wv : pr[i];
+    if (alive) {
+      dl = fma(-col, col, dl);
+      if (q == 0 && (p.pivoting || pos == j + 1)) {
+        bkey = dkey(dl);
+        bpos = pos;
+      }
+    }
+    const unsigned long long mk = bkey;
+    const int mp = bpos;
+    warp_argmax(bkey, bpos);
+    if (p.trace) t3 = clock64();
+    if (c + 1 < kb) stage_row(bkey, bpos, mp, mk);
+    if (lane == 0) {
+      wbest[warp].key = bkey;
+      wbest[warp].pos = bpos;
+    }
+    __syncthreads();
+    if (p.trace) t4 = clock64();
+    if (c + 1 < kb) combine_publish(j + 1);
+    if (p.trace) {
+      const long long t5 = clock64();
+      tacc[0] += t1 - t0;
+      tacc[1] += t2 - t1;
+      tacc[2] += t3 - t2;
+      tacc[3] += t4 - t3;
+      tacc[4] += t5 - t4;
+      tacc[5] += 1;
+    }
+    if (tid == 0 && piv != j) {
+      lab_at[j - k] = xp;
+      lab_at[piv - k] = y;
+      pos_of[xp - k] = j;
+      pos_of[y - k] = piv;
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (p.trace && cta == 0 && tid == 0)
+    for (int i = 0; i < 6; ++i) atomicAdd(&p.trace[i], static_cast<unsigned long long>(tacc[i]));
+  cl.sync();  // no CTA leaves while remote st.async may target it
+
+  // ---- write back from registers: Fo rows by original column, trailing panel, d, order
+  if (mine) {
+    const int orig = p.ord_in[x];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int cc = q + 4 * i;
+      if (cc < kb) p.Fo[(long long)orig * p.ldf + k + cc] = pr[i];
+    }
+    if (!s_stop) {
+      const int t0 = k + kb;
+      const int ps = pos_of[x - k];
+      if (ps >= t0) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int cc = q + 4 * i;
+          if (cc < kb) p.PcT[(long long)cc * p.ldp + (ps - t0)] = pr[i];
+        }
+        if (q == 0) p.d_out[ps] = dl;
+      }
+    }
+  }
+  for (int ps = cta * blockDim.x + tid; ps < n; ps += C * blockDim.x) {
+    if (ps < k) {
+      p.ord_out[ps] = p.ord_in[ps];
+    } else {
+      const int lb = lab_at[ps - k];
+      p.ord_out[ps] = p.ord_in[lb];
+      p.lab_out[ps] = lb;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 size_t panel_smem_bytes(int nl, int R) {
   return size_t(kPanelW) * R * sizeof(double) + size_t(R) * sizeof(double) + size_t(2) * nl * sizeof(int);
 }
@@ -447,6 +747,33 @@ cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cuda
   const int nl = p.n - p.k;
   PanelParams pp = p;
   const int CL = panel_cluster_size(nl);
+  if (CL > 0 && (nl + CL - 1) / CL <= kRegLabels && !std::getenv("RBPG_PANEL_SMEM")) {
+    pp.rows_per_cta = (nl + CL - 1) / CL;
+    const size_t smem = size_t(2) * nl * sizeof(int);
+    static size_t attr = 0;
+    if (smem > attr || attr == 0) {
+      cudaError_t e = cudaFuncSetAttribute(panel_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)(smem > 0 ? smem : 16));
+      if (e != cudaSuccess) return e;
+      e = cudaFuncSetAttribute(panel_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+      attr = smem > 0 ? smem : 16;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CL);
+    cfg.blockDim = dim3(kPThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CL;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (ctas_used) *ctas_used = CL;
+    return cudaLaunchKernelEx(&cfg, panel_reg_kernel, pp);
+  }
   if (CL > 0) {
     pp.rows_per_cta = (nl + CL - 1) / CL;
     const size_t smem = panel_smem_bytes(nl, pp.rows_per_cta);
