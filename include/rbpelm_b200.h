@@ -117,6 +117,13 @@ int rbpg_rank_revealing_factor(rbpg_context* ctx, const double* a, size_t rows, 
 /* solve_factored_gram (linalg.cpp:254-270): out (n x m) = (F F^T)^{-1} rhs in permuted coordinates */
 int rbpg_solve_factored_gram(rbpg_context* ctx, const double* factor, const size_t* order, size_t n, size_t rank,
                              const double* rhs, size_t rrows, size_t m, double* out, rbpg_status* st);
+/* Rank-path pseudo-inverse (not a reference entry point -- the reference forms
+ * beta = H^+ T without materialising H^+): out (l x n) = P (F F^T)^{-1} P^T H^T, i.e. the
+ * full-rank solve of elm.cpp:202-214 / solve_factored_gram (linalg.cpp:254-270) with right-hand
+ * side H^T.  order (l) and rank are written; rank < l fails with RBPG_INVALID_ARGUMENT like
+ * solve_factored_gram (linalg.cpp:256-260).  tol as rank_revealing_factor. */
+int rbpg_pseudo_inverse(rbpg_context* ctx, const double* h, size_t n, size_t l, double tol, double* out,
+                        size_t* order, size_t* rank, rbpg_status* st);
 /* solve_spd (linalg.cpp:99-155): out = m^{-1} rhs through a blocked Cholesky */
 int rbpg_solve_spd(rbpg_context* ctx, const double* m, size_t mrows, size_t mcols, const double* rhs, size_t rrows,
                    size_t rcols, double* out, rbpg_status* st);
@@ -148,6 +155,15 @@ int rbpg_solve_stage_device(rbpg_context* ctx, const double* dg, size_t ldg, con
 int rbpg_accuracy_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in,
                                size_t n, size_t d, size_t l, size_t m, const double* dw, size_t ldw,
                                const double* db, const double* dbeta, size_t ldb, uint64_t* hits, rbpg_status* st);
+/* gram on a device matrix: G (cols x cols, ld ldg) (+)= A^T A, exactly symmetric (matrix.cpp:152-161) */
+int rbpg_gram_device(rbpg_context* ctx, const double* da, size_t lda, size_t rows, size_t cols, double* dg, size_t ldg,
+                     int accumulate, rbpg_status* st);
+/* Row-sharded pseudo-inverse: from the (all-reduced) Gram of all n_total rows, writes this shard's
+ * column block dout (l x n_local, ld ldo) = H^+[:, local rows] for the local rows dh (n_local x l).
+ * order/rank (host) optional. */
+int rbpg_pseudo_inverse_stage_device(rbpg_context* ctx, const double* dg, size_t ldg, size_t n_total,
+                                     const double* dh, size_t ldh, size_t n_local, size_t l, double tol, double* dout,
+                                     size_t ldo, size_t* order, size_t* rank, rbpg_status* st);
 /* Whole train() on device-resident X, T (W, b host arrays from init_hidden). */
 int rbpg_train_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in, size_t n,
                       size_t d, size_t l, size_t m, const double* w, const double* b, const rbpg_strategy* strategy,

@@ -107,6 +107,10 @@ struct RankRevealingFactor {
 };
 RankRevealingFactor rank_revealing_factor(const DenseMatrix& a, double tol = 0.0);
 DenseMatrix solve_factored_gram(const RankRevealingFactor& f, const DenseMatrix& rhs);
+// Extension (no reference counterpart): the rank-path pseudo-inverse
+// H^+ = P (F F^T)^{-1} P^T H^T (L x N) of a full-rank h; rank < L throws std::invalid_argument
+// like solve_factored_gram.  `perm` (optional) receives the pivot order and rank.
+DenseMatrix pseudo_inverse(const DenseMatrix& h, double tol = 0.0, ColumnPermutation* perm = nullptr);
 
 // ---- elm.hpp --------------------------------------------------------------
 enum class Activation { Sigmoid };

@@ -157,6 +157,19 @@ def solve_factored_gram(factor, order, rank, rhs):
     return out
 
 
+def pseudo_inverse(h, tol=0.0):
+    """Rank-path H^+ = P (F F^T)^-1 P^T H^T (full rank only).  Returns (hpinv, order, rank);
+    raises OracleFailure (code 2, invalid_argument) when rank < cols."""
+    h = _f(h)
+    n, l = h.shape
+    out = np.empty((l, n))
+    order = np.empty(l, dtype=np.uint64)
+    rank = c_size_t()
+    _call(lib().oracle_pseudo_inverse, _p(h), c_size_t(n), c_size_t(l), c_double(tol), _p(out), _p(order),
+          ctypes.byref(rank))
+    return out, [int(v) for v in order], int(rank.value)
+
+
 def solve_block_split(h1, h2, y, ridge=1e-8):
     h1, h2, y = _f(h1), _f(h2), _f(y)
     b1 = np.empty((h1.shape[1], y.shape[1]))

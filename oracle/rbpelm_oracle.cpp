@@ -822,6 +822,38 @@ int oracle_solve_factored_gram(const double* factor, const std::size_t* order, s
   });
 }
 
+// Rank-path pseudo-inverse H^+ = P (F F^T)^{-1} P^T H^T: the full-rank solve of
+// elm.cpp:202-214 with right-hand side H^T in place of H^T T, i.e. solve_factored_gram
+// (linalg.cpp:254-270) on the pivot-ordered rows of H^T, then invert_permutation_rows
+// (linalg.cpp:54-66).  rank < cols raises invalid_argument exactly like solve_factored_gram;
+// order and rank are written first.  The right-hand-side columns are independent, so they are
+// solved in column blocks on the worker threads (same arithmetic per column).
+int oracle_pseudo_inverse(const double* h, std::size_t rows, std::size_t cols, double tol, double* out,
+                          std::size_t* order, std::size_t* rank, oracle_error* err) {
+  return guarded(err, [&] {
+    if (rows == 0 || cols == 0) throw ShapeError("pseudo_inverse: empty matrix");
+    if (tol < 0.0 || !std::isfinite(tol)) throw std::invalid_argument("rank_revealing_permutation: tolerance must be >= 0");
+    Mat hm = from_ptr(h, rows, cols);
+    Factor f = factor_gram(gram(hm), rows, tol);
+    std::memcpy(order, f.order.data(), sizeof(std::size_t) * cols);
+    *rank = f.rank;
+    if (f.rank != cols)
+      throw std::invalid_argument("solve_factored_gram: factor is rank-deficient (" + std::to_string(f.rank) + " of " +
+                                  std::to_string(cols) + ")");
+    constexpr std::size_t kBlock = 256;
+    const std::size_t nblk = (rows + kBlock - 1) / kBlock;
+    parallel_for(nblk, nblk > 1, [&](std::size_t b) {
+      const std::size_t c0 = b * kBlock, nc = std::min(kBlock, rows - c0);
+      Mat x(cols, nc);
+      for (std::size_t i = 0; i < cols; ++i)
+        for (std::size_t j = 0; j < nc; ++j) x(i, j) = hm(c0 + j, f.order[i]);
+      tri_solve_pair(f.f, x);
+      for (std::size_t i = 0; i < cols; ++i)
+        for (std::size_t j = 0; j < nc; ++j) out[f.order[i] * rows + c0 + j] = x(i, j);
+    });
+  });
+}
+
 int oracle_solve_block_split(const double* h1, std::size_t n, std::size_t c1, const double* h2, std::size_t c2,
                              const double* y, std::size_t m, double ridge, double* beta1, double* beta2,
                              oracle_diag* diag, oracle_error* err) {

@@ -23,11 +23,14 @@ from .api import (  # noqa: F401
     context,
     duplicate_nodes,
     gram,
+    gram_device,
     gram_stage_device,
     hidden_matrix,
     init_hidden,
     invert_permutation_rows,
     predict,
+    pseudo_inverse,
+    pseudo_inverse_stage_device,
     rank_revealing_factor,
     rank_revealing_permutation,
     solve_beta,

@@ -346,6 +346,26 @@ def solve_factored_gram(f: RankRevealingFactor, rhs, ctx: Optional[Context] = No
     return out
 
 
+def pseudo_inverse(h, tol: float = 0.0, ctx: Optional[Context] = None):
+    """Rank-path pseudo-inverse H^+ = P (F F^T)^-1 P^T H^T (L x N) for full-rank H:
+    the full-rank solve of elm.cpp:202-214 with right-hand side H^T.  Returns (hpinv, order, rank).
+    Raises ValueError (invalid_argument, as solve_factored_gram at linalg.cpp:256-260) when rank < L."""
+    ctx = ctx or context()
+    h = np.asarray(h, dtype=np.float64)
+    if h.ndim != 2 or h.size == 0:
+        raise ShapeError("pseudo_inverse: empty matrix")
+    h = np.ascontiguousarray(h)
+    n, L = h.shape
+    out = np.empty((L, n))
+    order = np.empty(L, dtype=np.uint64)
+    rank = ctypes.c_size_t()
+    st = rbpg_status()
+    ctx.lib.rbpg_pseudo_inverse(ctx.handle, _ptr(h), n, L, float(tol), _ptr(out), _ptr(order), ctypes.byref(rank),
+                                ctypes.byref(st))
+    _raise(st)
+    return out, [int(v) for v in order], int(rank.value)
+
+
 def solve_spd(m, rhs, ctx: Optional[Context] = None) -> np.ndarray:
     """linalg.cpp:99-155 (SpdFactor + solve)."""
     ctx = ctx or context()
@@ -590,3 +610,36 @@ def accuracy_stage_device(x, t, w, b, beta, ctx: Optional[Context] = None) -> in
                                        ctypes.byref(hits), ctypes.byref(st))
     _raise(st)
     return int(hits.value)
+
+
+def gram_device(a, g, accumulate: bool = False, ctx: Optional[Context] = None) -> None:
+    """g (L x L torch tensor) (+)= a^T a for a device matrix a (rows x L)."""
+    import torch
+
+    ctx = ctx or context(a.device.index or 0)
+    ctx.set_stream(torch.cuda.current_stream(a.device).cuda_stream)
+    st = rbpg_status()
+    ctx.lib.rbpg_gram_device(ctx.handle, _tptr(a), _ld(a), a.shape[0], a.shape[1], _tptr(g), _ld(g), int(accumulate),
+                             ctypes.byref(st))
+    _raise(st)
+
+
+def pseudo_inverse_stage_device(g, h, n_total: int, tol: float = 0.0, ctx: Optional[Context] = None):
+    """Row-sharded H^+: from the all-reduced Gram g (L x L) of all n_total rows, this shard's column
+    block H^+[:, local rows] (L x n_local torch tensor) for the local rows h (n_local x L).
+    Returns (block, order, rank)."""
+    import torch
+
+    ctx = ctx or context(g.device.index or 0)
+    ctx.set_stream(torch.cuda.current_stream(g.device).cuda_stream)
+    L = g.shape[0]
+    n_local = h.shape[0]
+    out = torch.empty((L, max(n_local, 1) + (max(n_local, 1) & 1)), dtype=torch.float64, device=g.device)
+    order = np.zeros(L, dtype=np.uint64)
+    rank = ctypes.c_size_t()
+    st = rbpg_status()
+    ctx.lib.rbpg_pseudo_inverse_stage_device(ctx.handle, _tptr(g), _ld(g), n_total, _tptr(h), _ld(h), n_local, L,
+                                             float(tol), _tptr(out), _ld(out), _ptr(order), ctypes.byref(rank),
+                                             ctypes.byref(st))
+    _raise(st)
+    return out[:, :n_local], [int(v) for v in order], int(rank.value)

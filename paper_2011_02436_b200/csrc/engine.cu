@@ -753,6 +753,69 @@ void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* d
   diag->training_accuracy = N ? static_cast<double>(*hits) / static_cast<double>(N) : 0.0;
 }
 
+// ---------------------------------------------------------------------------
+// Rank-path pseudo-inverse H^+ (SURVEY §8 a11).  For rank(H) = L it is the full-rank solve of
+// elm.cpp:202-214 with right-hand side H^T: H^+ = P (F F^T)^{-1} P^T H^T.  Device form:
+//   Z    = (F F^T)^{-1}             triangular-solve pair on the identity (L right-hand sides)
+//   Ginv = P Z P^T                  gather (Ginv[a][b] = Z[pos a][pos b])
+//   H^+  = Ginv H^T                 one DMMA product over the rows of H (hidden_kernel, plain
+//                                   transposed epilogue): 2 L^2 N tensor-core flops instead of
+//                                   N / 128 latency-bound triangular sweeps.
+// The factorisation and Ginv depend only on G, so a row shard of H yields its column block of
+// H^+ from the all-reduced Gram with no further exchange.
+// ---------------------------------------------------------------------------
+struct PinvFactor {
+  const double* Ginv = nullptr;  // L x L (ld), original node order; null when rank < L
+  size_t ld = 0;
+  size_t rank = 0;
+  std::vector<int> order;
+};
+
+PinvFactor pinv_factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t L, size_t rows_for_tol,
+                           double tol) {
+  if (tol < 0.0 || !std::isfinite(tol)) fail(RBPG_INVALID_ARGUMENT, "rank_revealing_permutation: tolerance must be >= 0");
+  FactorResult f = factor_dev(ctx, dG, ldg, L, rows_for_tol, tol, 1, "pinv");
+  PinvFactor r;
+  r.rank = static_cast<size_t>(f.st.rank);
+  r.order.resize(L);
+  ck(cudaMemcpy(r.order.data(), f.ord, L * 4, cudaMemcpyDeviceToHost), "read order");
+  if (r.rank != L) return r;
+  const size_t ld = round_up(L, 8);
+  double* Z = ctx->dbuf("pinv.Z", L * ld);
+  ck(cudaMemsetAsync(Z, 0, sizeof(double) * L * ld, ctx->stream), "memset Z");
+  ctx->run("add_diag", [&] { return launch_add_diag(Z, static_cast<long long>(ld), static_cast<int>(L), 1.0, ctx->stream); });
+  trsm_pair_dev(ctx, f.F, f.ldF, Z, ld, L, L);
+  std::vector<int> pos(L);
+  for (size_t i = 0; i < L; ++i) pos[r.order[i]] = static_cast<int>(i);
+  int* dpos = static_cast<int*>(ctx->buf("pinv.pos", L * 4));
+  ck(cudaMemcpyAsync(dpos, pos.data(), L * 4, cudaMemcpyHostToDevice, ctx->stream), "upload pos");
+  double* Ginv = ctx->dbuf("pinv.Ginv", L * ld);
+  ctx->run("gather Ginv", [&] {
+    return launch_gather_block(Z, static_cast<long long>(ld), dpos, static_cast<int>(L), dpos, static_cast<int>(L),
+                               Ginv, static_cast<long long>(ld), ctx->stream);
+  });
+  ck(cudaStreamSynchronize(ctx->stream), "pinv sync");  // pos lives on the host stack
+  r.Ginv = Ginv;
+  r.ld = ld;
+  return r;
+}
+
+// out (L x N, ld ldo) = Ginv (L x L) * H^T for H (N x L, ld ldh)
+void pinv_apply_dev(rbpg_context* ctx, const double* Ginv, size_t ldgi, const double* dH, size_t ldh, size_t N, size_t L,
+                    double* dOut, size_t ldo) {
+  if (N == 0) return;
+  CUtensorMap tmH = make_map(ctx, dH, L, N, ldh, 16, kTile, true);
+  CUtensorMap tmG = make_map(ctx, Ginv, L, L, ldgi, kTile, kBK, false);
+  HiddenParams p{static_cast<int>(N), static_cast<int>(L), static_cast<int>(L), nullptr, dOut,
+                 static_cast<long long>(ldo), 1};
+  ctx->run("pinv_apply", [&] { return launch_hidden(tmH, tmG, p, ctx->stream); });
+}
+
+void rank_deficient_pinv(const PinvFactor& pf, size_t L) {
+  fail(RBPG_INVALID_ARGUMENT, "solve_factored_gram: factor is rank-deficient (" + std::to_string(pf.rank) + " of " +
+                                  std::to_string(L) + ")");
+}
+
 template <typename F>
 int guarded(rbpg_context* ctx, rbpg_status* st, F&& body) {
   if (st) std::memset(st, 0, sizeof(*st));
@@ -917,6 +980,51 @@ int rbpg_solve_factored_gram(rbpg_context* ctx, const double* factor, const size
     Padded X = upload(ctx, "rhs.in", rhs, n, m);
     trsm_pair_dev(ctx, F.p, F.ld, const_cast<double*>(X.p), X.ld, n, m);
     download(ctx, out, X.p, X.ld, n, m);
+  });
+}
+
+int rbpg_pseudo_inverse(rbpg_context* ctx, const double* h, size_t n, size_t l, double tol, double* out,
+                        size_t* order, size_t* rank, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (n == 0 || l == 0) fail(RBPG_SHAPE_ERROR, "pseudo_inverse: empty matrix");
+    Padded H = upload(ctx, "A.in", h, n, l);
+    const size_t ldg = round_up(l, 8);
+    double* G = ctx->dbuf("G0", l * ldg);
+    gram_dev(ctx, H.p, H.ld, n, l, nullptr, 0, 0, G, ldg, nullptr, 0, false);
+    PinvFactor pf = pinv_factor_dev(ctx, G, ldg, l, n, tol);
+    for (size_t i = 0; i < l; ++i) order[i] = static_cast<size_t>(pf.order[i]);
+    *rank = pf.rank;
+    if (pf.rank != l) rank_deficient_pinv(pf, l);
+    const size_t ldo = even(n);
+    double* O = ctx->dbuf("pinv.out", l * ldo);
+    pinv_apply_dev(ctx, pf.Ginv, pf.ld, H.p, H.ld, n, l, O, ldo);
+    download(ctx, out, O, ldo, l, n);
+  });
+}
+
+int rbpg_gram_device(rbpg_context* ctx, const double* da, size_t lda, size_t rows, size_t cols, double* dg, size_t ldg,
+                     int accumulate, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (cols == 0) fail(RBPG_SHAPE_ERROR, "gram: empty matrix");
+    Padded A = pad_device(ctx, "gram.a", da, lda, rows, cols);
+    gram_dev(ctx, A.p, A.ld, rows, cols, nullptr, 0, 0, dg, ldg, nullptr, 0, accumulate != 0);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int rbpg_pseudo_inverse_stage_device(rbpg_context* ctx, const double* dg, size_t ldg, size_t n_total,
+                                     const double* dh, size_t ldh, size_t n_local, size_t l, double tol, double* dout,
+                                     size_t ldo, size_t* order, size_t* rank, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (n_total == 0 || l == 0) fail(RBPG_SHAPE_ERROR, "pseudo_inverse: empty matrix");
+    PinvFactor pf = pinv_factor_dev(ctx, dg, ldg, l, n_total, tol);
+    if (order)
+      for (size_t i = 0; i < l; ++i) order[i] = static_cast<size_t>(pf.order[i]);
+    if (rank) *rank = pf.rank;
+    if (pf.rank != l) rank_deficient_pinv(pf, l);
+    Padded H = pad_device(ctx, "pinv.h", dh, ldh, n_local, l);
+    pinv_apply_dev(ctx, pf.Ginv, pf.ld, H.p, H.ld, n_local, l, dout, ldo);
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
   });
 }
 

@@ -113,6 +113,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
   }
 
+  if (p.transposed) {  // plain product stored transposed: H[c][r] (pseudo-inverse H^+ = G^-1 H^T)
+#pragma unroll
+    for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = n0 + wm + mt * 16 + g + (q >> 1) * 8;
+          const int c = l0 + wn + (nt >> 1) * 16 + 4 * t + 2 * (q & 1) + (nt & 1);
+          if (r < p.N && c < p.L) p.H[(long long)c * p.ldh + r] = acc[mt][nt][q];
+        }
+    return;
+  }
+
   // epilogue: bias after the full dot product, then sigmoid (elm.cpp:102, :27)
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {

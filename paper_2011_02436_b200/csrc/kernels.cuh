@@ -21,6 +21,7 @@ struct HiddenParams {
   const double* bias;
   double* H;
   long long ldh;
+  int transposed;  // 0: H = sigmoid(XW + b); 1: plain product stored transposed, H[c][r] = (XW)[r][c]
 };
 
 // ---- K2: lower-tile SYRK C = A^T A (+ A^T B tiles), TN layout (A is K x M row-major)

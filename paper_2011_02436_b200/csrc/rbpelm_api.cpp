@@ -277,6 +277,22 @@ DenseMatrix solve_factored_gram(const RankRevealingFactor& f, const DenseMatrix&
   return out;
 }
 
+DenseMatrix pseudo_inverse(const DenseMatrix& h, double tol, ColumnPermutation* perm) {
+  if (h.empty()) throw ShapeError("pseudo_inverse: empty matrix");
+  DenseMatrix out(h.cols(), h.rows(), 0.0);
+  std::vector<std::size_t> order(h.cols());
+  std::size_t rank = 0;
+  rbpg_status st;
+  rbpg_pseudo_inverse(ctx(), h.data(), h.rows(), h.cols(), tol, out.data(), order.data(), &rank, &st);
+  if (perm) {
+    perm->order = order;
+    perm->rank = rank;
+    perm->tolerance = tol > 0.0 ? tol : static_cast<double>(std::max(h.rows(), h.cols())) * 2.220446049250313e-16;
+  }
+  raise(st);
+  return out;
+}
+
 // ---- elm ---------------------------------------------------------------------
 std::string SolverStrategy::describe() const {  // elm.cpp:53-67
   switch (kind) {

@@ -53,6 +53,16 @@ class DeviceStages:
 
         return torch.as_tensor(x, dtype=torch.float64, device=like.device)
 
+    def gram_of(self, h):
+        import torch
+
+        g = torch.empty((h.shape[1], h.shape[1]), dtype=torch.float64, device=h.device)
+        api.gram_device(h, g, ctx=self.ctx)
+        return g
+
+    def pinv_block(self, g, h, n_total: int, tol: float):
+        return api.pseudo_inverse_stage_device(g, h, n_total, tol, ctx=self.ctx)
+
 
 def train_sharded(x_local, t_local, params: api.ElmParams, strategy: api.SolverStrategy, n_total: int,
                   stages=None, group=None, hidden: Optional[api.HiddenLayer] = None):
@@ -79,3 +89,17 @@ def train_sharded(x_local, t_local, params: api.ElmParams, strategy: api.SolverS
         dist.all_reduce(hits, group=group)
     diag.training_accuracy = float(hits.item()) / float(n_total)
     return beta, diag, hidden, order
+
+
+def pseudo_inverse_sharded(h_local, n_total: int, tol: float = 0.0, stages=None, group=None):
+    """Row-sharded rank-path pseudo-inverse: each rank holds a contiguous
+    row block H_p of H; one all-reduce of the local Grams H_p^T H_p, then every rank factors the
+    same G and writes its own column block H^+[:, rows of p] = P (F F^T)^-1 P^T H_p^T with no
+    further exchange.  Returns (block (L x n_local), order, rank)."""
+    import torch.distributed as dist
+
+    stages = stages or DeviceStages()
+    g = stages.gram_of(h_local)
+    if dist.is_available() and dist.is_initialized():
+        dist.all_reduce(g, group=group)
+    return stages.pinv_block(g, h_local, n_total, tol)

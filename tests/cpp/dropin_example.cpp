@@ -67,6 +67,20 @@ int main() {
     }
   CHECK(worst < 1e-10);
 
+  // rank-path pseudo-inverse extension: H^+ Y reproduces the rank-path beta
+  ColumnPermutation pp;
+  DenseMatrix Hp = pseudo_inverse(H, 0.0, &pp);
+  CHECK(Hp.rows() == L && Hp.cols() == n && pp.rank == L && pp.order == f.permutation.order);
+  double dmax = 0.0, bmax = 0.0;
+  for (std::size_t i = 0; i < L; ++i)
+    for (std::size_t j = 0; j < m; ++j) {
+      double s = 0.0;
+      for (std::size_t r = 0; r < n; ++r) s += Hp(i, r) * Y(r, j);
+      dmax = std::fmax(dmax, std::fabs(s - model.beta(i, j)));
+      bmax = std::fmax(bmax, std::fabs(model.beta(i, j)));
+    }
+  CHECK(dmax <= 1e-8 * bmax);
+
   // N < L with a block strategy names the direct strategy (elm.cpp:248-253)
   try {
     train(ElmParams{d, 1000, m, Activation::Sigmoid, 1}, X, Y, SolverStrategy::rank_based());

@@ -45,7 +45,7 @@ def test_cxx_dropin_api_symbols_exported():
     out = subprocess.run(["nm", "-DC", _native.LIB_PATH], capture_output=True, text=True, check=True).stdout
     for name in ["rbpelm::train(", "rbpelm::predict(", "rbpelm::solve_beta(", "rbpelm::rank_revealing_factor(",
                  "rbpelm::solve_factored_gram(", "rbpelm::SpdFactor::SpdFactor(", "rbpelm::hidden_matrix(",
-                 "rbpelm::gram(", "rbpelm::init_hidden("]:
+                 "rbpelm::gram(", "rbpelm::init_hidden(", "rbpelm::pseudo_inverse("]:
         assert name in out, name
 
 
