@@ -124,6 +124,11 @@ int rbpg_solve_factored_gram(rbpg_context* ctx, const double* factor, const size
  * solve_factored_gram (linalg.cpp:256-260).  tol as rank_revealing_factor. */
 int rbpg_pseudo_inverse(rbpg_context* ctx, const double* h, size_t n, size_t l, double tol, double* out,
                         size_t* order, size_t* rank, rbpg_status* st);
+/* pinv_svd (linalg.cpp:68-87): out (cols x rows) = V diag(1/s) U^T over s > rel * s_max,
+ * rel = tol > 0 ? tol : max(rows, cols) * eps.  Device block one-sided Jacobi SVD (k_svd.cu); the
+ * same SVD serves solve_direct's pseudo-inverse branch (elm.cpp:119-121) inside solve_beta/train. */
+int rbpg_pinv_svd(rbpg_context* ctx, const double* a, size_t rows, size_t cols, double tol, double* out,
+                  rbpg_status* st);
 /* solve_spd (linalg.cpp:99-155): out = m^{-1} rhs through a blocked Cholesky */
 int rbpg_solve_spd(rbpg_context* ctx, const double* m, size_t mrows, size_t mcols, const double* rhs, size_t rrows,
                    size_t rcols, double* out, rbpg_status* st);

@@ -6,8 +6,8 @@
 // entry point forwards to the C ABI in rbpelm_b200.h (device work on the
 // process-wide default context of device 0, or the one installed with
 // rbpelm::b200::set_device); status records are rethrown as the reference's
-// exceptions.  Not provided: pinv_svd (SVD fallback / test oracle, out of scope
-// for the device path) -- see INTEGRATION.md.
+// exceptions.  pinv_svd runs the device block one-sided Jacobi SVD (the same SVD
+// serves solve_direct's pseudo-inverse branch) -- see INTEGRATION.md.
 #pragma once
 
 #include <cstddef>
@@ -99,6 +99,7 @@ class SpdFactor {
 };
 
 DenseMatrix solve_spd(const DenseMatrix& m, const DenseMatrix& rhs);
+DenseMatrix pinv_svd(const DenseMatrix& a, double tol = 0.0);
 ColumnPermutation rank_revealing_permutation(const DenseMatrix& a, double tol = 0.0);
 
 struct RankRevealingFactor {

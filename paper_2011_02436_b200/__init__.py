@@ -28,6 +28,7 @@ from .api import (  # noqa: F401
     hidden_matrix,
     init_hidden,
     invert_permutation_rows,
+    pinv_svd,
     predict,
     pseudo_inverse,
     pseudo_inverse_stage_device,

@@ -346,6 +346,21 @@ def solve_factored_gram(f: RankRevealingFactor, rhs, ctx: Optional[Context] = No
     return out
 
 
+def pinv_svd(a, tol: float = 0.0, ctx: Optional[Context] = None) -> np.ndarray:
+    """SVD pseudo-inverse (linalg.cpp:68-87) on the device: block one-sided Jacobi SVD, singular
+    values above rel * s_max inverted (rel = tol or max(rows, cols) * eps)."""
+    ctx = ctx or context()
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2 or a.size == 0:
+        raise ShapeError("pinv_svd: empty matrix")
+    a = np.ascontiguousarray(a)
+    out = np.empty((a.shape[1], a.shape[0]))
+    st = rbpg_status()
+    ctx.lib.rbpg_pinv_svd(ctx.handle, _ptr(a), a.shape[0], a.shape[1], float(tol), _ptr(out), ctypes.byref(st))
+    _raise(st)
+    return out
+
+
 def pseudo_inverse(h, tol: float = 0.0, ctx: Optional[Context] = None):
     """Rank-path pseudo-inverse H^+ = P (F F^T)^-1 P^T H^T (L x N) for full-rank H:
     the full-rank solve of elm.cpp:202-214 with right-hand side H^T.  Returns (hpinv, order, rank).

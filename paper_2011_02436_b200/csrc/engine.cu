@@ -51,6 +51,13 @@ cudaError_t launch_symmetrize(double*, long long, int, cudaStream_t);
 cudaError_t launch_trace(const double*, long long, int, double*, cudaStream_t);
 cudaError_t launch_nonfinite(const double*, long long, int, int, int*, cudaStream_t);
 cudaError_t launch_add_block(double*, long long, const double*, long long, long long, long long, cudaStream_t);
+cudaError_t launch_svd_round(double*, long long, long long, double*, long long, long long, int, int, int, long long,
+                             int, long long, double, double, double*, double*, int*, int*, cudaStream_t);
+cudaError_t launch_col_sumsq(const double*, long long, long long, int, double*, cudaStream_t);
+cudaError_t launch_scale_rows(double*, long long, int, int, const double*, cudaStream_t);
+cudaError_t launch_scale_cols(double*, long long, long long, int, const double*, cudaStream_t);
+cudaError_t launch_transpose(const double*, long long, long long, long long, double*, long long, long long,
+                             cudaStream_t);
 cudaError_t launch_axpy_rows(const double*, long long, const double*, long long, int, int, double*, long long,
                              cudaStream_t);
 }  // namespace rbpg
@@ -94,6 +101,12 @@ struct rbpg_context {
   const double* kept_h = nullptr;
   size_t kept_n = 0, kept_l = 0, kept_ldh = 0;
   size_t h_budget_bytes = size_t(48) << 30;
+  // hidden matrix + targets of the current solve when resident (train / solve_beta): the SVD
+  // pseudo-inverse branch of solve_direct needs H itself, not only its Gram
+  const double* src_h = nullptr;
+  const double* src_y = nullptr;
+  size_t src_n = 0, src_ldh = 0, src_ldy = 0;
+  int svd_sweeps = 0;  // sweeps of the last SVD (diagnostics)
   std::mutex mu;
 
   void* buf(const std::string& name, size_t bytes) {
@@ -430,8 +443,138 @@ FactorResult spd_with_ridge(rbpg_context* ctx, const double* dA, size_t lda, siz
   return f;
 }
 
-// solve_direct (elm.cpp:108-122) on the Gram: SpdFactor(G) then two triangular solves; the SVD
-// pseudoinverse fallback exists on device only for H == 0 (pinv(0) = 0).
+// ---------------------------------------------------------------------------
+// SVD of H for pinv_svd (linalg.cpp:68-87) by block one-sided Jacobi (k_svd.cu).  Tall H (N >= L):
+// A = H (N x L); wide H: A = H^T (L x N).  Columns padded with zeros to a multiple of 32.  After
+// convergence A = U diag(s) (columns orthogonal), V accumulates the rotations, and w_j = 1/s_j^2
+// for the kept s_j > cut = rel * s_max (rel = tol or max(rows, cols) * eps), else 0.
+// ---------------------------------------------------------------------------
+struct SvdResult {
+  double* A = nullptr;  // M x Kp rotated columns (ld Kp)
+  double* V = nullptr;  // Kp x Kp (ld Kp)
+  double* w = nullptr;  // Kp weights 1/s^2 or 0 (device)
+  size_t M = 0, K = 0, Kp = 0;
+  bool tall = true;
+};
+
+SvdResult svd_dev(rbpg_context* ctx, const double* dH, size_t ldh, size_t N, size_t L, double tol) {
+  cudaStream_t s = ctx->stream;
+  constexpr double kEps = 2.220446049250313e-16;
+  SvdResult r;
+  r.tall = N >= L;
+  r.M = r.tall ? N : L;
+  r.K = r.tall ? L : N;
+  r.Kp = round_up(r.K, 32);
+  const size_t M = r.M, Kp = r.Kp;
+  r.A = ctx->dbuf("svd.A", M * Kp);
+  if (r.tall) {
+    if (Kp > L) ck(cudaMemsetAsync(r.A, 0, sizeof(double) * M * Kp, s), "memset A");
+    ck(cudaMemcpy2DAsync(r.A, Kp * 8, dH, ldh * 8, L * 8, N, cudaMemcpyDeviceToDevice, s), "copy H");
+  } else {
+    ctx->run("transpose", [&] {
+      return launch_transpose(dH, static_cast<long long>(ldh), static_cast<long long>(N), static_cast<long long>(L),
+                              r.A, static_cast<long long>(Kp), static_cast<long long>(Kp), s);
+    });
+  }
+  r.V = ctx->dbuf("svd.V", Kp * Kp);
+  ck(cudaMemsetAsync(r.V, 0, sizeof(double) * Kp * Kp, s), "memset V");
+  ctx->run("add_diag", [&] { return launch_add_diag(r.V, static_cast<long long>(Kp), static_cast<int>(Kp), 1.0, s); });
+  double* s2 = ctx->dbuf("svd.s2", Kp);
+  double* hs2 = static_cast<double*>(ctx->pinned("svd.s2", Kp * 8));
+  auto col_norms = [&] {
+    ctx->run("col_sumsq", [&] {
+      return launch_col_sumsq(r.A, static_cast<long long>(Kp), static_cast<long long>(M), static_cast<int>(Kp), s2, s);
+    });
+    ck(cudaMemcpyAsync(hs2, s2, Kp * 8, cudaMemcpyDeviceToHost, s), "read norms");
+    ck(cudaStreamSynchronize(s), "svd sync");
+  };
+  col_norms();
+  double fro2 = 0.0;
+  for (size_t j = 0; j < Kp; ++j) fro2 += hs2[j];
+
+  const int nb = static_cast<int>(Kp / 16), npairs = nb / 2;
+  const size_t want = 2 * static_cast<size_t>(ctx->num_sms);
+  auto split_rows = [&](size_t rows) {
+    size_t sp = std::max<size_t>(1, (want + npairs - 1) / npairs);
+    size_t per = round_up((rows + sp - 1) / sp, 64);
+    return std::max<size_t>(per, 64);
+  };
+  const size_t rows_a = split_rows(M), rows_v = split_rows(Kp);
+  const int splits = static_cast<int>((M + rows_a - 1) / rows_a);
+  const int vsplits = static_cast<int>((Kp + rows_v - 1) / rows_v);
+  double* ws = ctx->dbuf("svd.ws", static_cast<size_t>(npairs) * splits * 1024);
+  double* Q = ctx->dbuf("svd.Q", static_cast<size_t>(npairs) * 1024);
+  int* flags = static_cast<int*>(ctx->buf("svd.flags", npairs * 4));
+  int* rot = static_cast<int*>(ctx->buf("svd.rot", 4));
+  int* hrot = static_cast<int*>(ctx->pinned("svd.rot", 4));
+  const double otol = 4.0 * kEps * std::sqrt(static_cast<double>(M));
+  const double noise = 2.0 * kEps * std::sqrt(fro2);
+  constexpr int kMaxSweeps = 60;
+  int sweep = 0;
+  if (nb >= 2 && fro2 > 0.0) {
+    for (; sweep < kMaxSweeps; ++sweep) {
+      ck(cudaMemsetAsync(rot, 0, 4, s), "memset rot");
+      for (int rd = 0; rd < nb - 1; ++rd)
+        ctx->run("svd_round", [&] {
+          return launch_svd_round(r.A, static_cast<long long>(Kp), static_cast<long long>(M), r.V,
+                                  static_cast<long long>(Kp), static_cast<long long>(Kp), nb, rd, splits,
+                                  static_cast<long long>(rows_a), vsplits, static_cast<long long>(rows_v), otol,
+                                  noise, ws, Q, flags, rot, s);
+        });
+      ck(cudaMemcpyAsync(hrot, rot, 4, cudaMemcpyDeviceToHost, s), "read rot");
+      ck(cudaStreamSynchronize(s), "svd sweep sync");
+      if (*hrot == 0) break;
+    }
+  }
+  ctx->svd_sweeps = sweep + 1;
+  col_norms();
+  double smax = 0.0;
+  std::vector<double> sv(Kp), w(Kp, 0.0);
+  for (size_t j = 0; j < Kp; ++j) {
+    sv[j] = std::sqrt(hs2[j]);
+    smax = std::max(smax, sv[j]);
+  }
+  const double rel = tol > 0.0 ? tol : static_cast<double>(std::max(N, L)) * kEps;
+  const double cut = rel * smax;
+  for (size_t j = 0; j < Kp; ++j)
+    if (sv[j] > cut && sv[j] > 0.0) w[j] = 1.0 / (sv[j] * sv[j]);
+  r.w = ctx->dbuf("svd.w", Kp);
+  ck(cudaMemcpyAsync(r.w, w.data(), Kp * 8, cudaMemcpyHostToDevice, s), "upload w");
+  ck(cudaStreamSynchronize(s), "svd sync");  // w lives on the host stack
+  return r;
+}
+
+// beta (L x m) = pinv(H) Y = V diag(w) A^T Y (tall) or A diag(w) V^T Y (wide)
+void svd_solve_dev(rbpg_context* ctx, const double* dH, size_t ldh, size_t N, size_t L, const double* dY, size_t ldy,
+                   size_t m, double* dBeta, size_t ldb) {
+  SvdResult r = svd_dev(ctx, dH, ldh, N, L, 0.0);
+  const size_t lm = even(m);
+  double* C = ctx->dbuf("svd.C", r.Kp * lm);
+  const int Kp = static_cast<int>(r.Kp);
+  gemm_dev(ctx, Kp, static_cast<int>(m), static_cast<int>(N), r.tall ? r.A : r.V, r.Kp, true, dY, ldy, false, C, lm,
+           1.0, 0.0);
+  ctx->run("scale_rows", [&] { return launch_scale_rows(C, static_cast<long long>(lm), Kp, static_cast<int>(m), r.w, ctx->stream); });
+  gemm_dev(ctx, static_cast<int>(L), static_cast<int>(m), Kp, r.tall ? r.V : r.A, r.Kp, false, C, lm, false, dBeta,
+           ldb, 1.0, 0.0);
+}
+
+// pinv(H) (L x N, ld ldo) = V diag(w) A^T (tall) or A diag(w) V[0:N]^T (wide)
+void svd_pinv_dev(rbpg_context* ctx, const double* dH, size_t ldh, size_t N, size_t L, double tol, double* dOut,
+                  size_t ldo) {
+  SvdResult r = svd_dev(ctx, dH, ldh, N, L, tol);
+  ctx->run("scale_cols", [&] {
+    return launch_scale_cols(r.A, static_cast<long long>(r.Kp), static_cast<long long>(r.M), static_cast<int>(r.Kp),
+                             r.w, ctx->stream);
+  });
+  const int Kp = static_cast<int>(r.Kp);
+  if (r.tall)
+    gemm_dev(ctx, static_cast<int>(L), static_cast<int>(N), Kp, r.V, r.Kp, false, r.A, r.Kp, true, dOut, ldo, 1.0, 0.0);
+  else
+    gemm_dev(ctx, static_cast<int>(L), static_cast<int>(N), Kp, r.A, r.Kp, false, r.V, r.Kp, true, dOut, ldo, 1.0, 0.0);
+}
+
+// solve_direct (elm.cpp:108-122): SpdFactor(G) and two triangular solves; if N < L or the Gram
+// is singular, beta = pinv_svd(H) Y (linalg.cpp:68-87) on the resident H (ctx->src_h).
 void direct_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dHtT, size_t ldt, size_t L, size_t m,
                 size_t rows, double* dBeta, size_t ldb, rbpg_diagnostics* diag) {
   if (rows >= L) {
@@ -450,8 +593,29 @@ void direct_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* d
   } else {
     if (diag) diag->used_svd_path = 1;
   }
-  fail(RBPG_NOT_SUPPORTED, "solve_direct: SVD pseudoinverse fallback is not implemented on the device path");
+  if (!ctx->src_h || ctx->src_n != rows)
+    fail(RBPG_NOT_SUPPORTED,
+         "solve_direct: the SVD pseudoinverse branch needs the whole hidden matrix resident on one device "
+         "(not available through the row-sharded stage API)");
+  svd_solve_dev(ctx, ctx->src_h, ctx->src_ldh, rows, L, ctx->src_y, ctx->src_ldy, m, dBeta, ldb);
 }
+
+// RAII: the resident H / Y of the current call for the SVD branch
+struct SourceScope {
+  rbpg_context* ctx;
+  SourceScope(rbpg_context* c, const double* h, size_t ldh, const double* y, size_t ldy, size_t n) : ctx(c) {
+    c->src_h = h;
+    c->src_ldh = ldh;
+    c->src_y = y;
+    c->src_ldy = ldy;
+    c->src_n = n;
+  }
+  ~SourceScope() {
+    ctx->src_h = nullptr;
+    ctx->src_y = nullptr;
+    ctx->src_n = 0;
+  }
+};
 
 // Schur block solve (elm.cpp:124-156) on Gram sub-blocks.  ord: device position -> original
 // column; the first `split` positions form H1, the rest H2.  Writes beta in ORIGINAL order.
@@ -735,7 +899,13 @@ void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* d
   const auto wall0 = std::chrono::steady_clock::now();
   cudaEventRecord(ctx->ev[2], ctx->stream);
   float hidden_ms = gram_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, G, ldg, false, true, true);
-  solve_dev(ctx, G, ldg, HtT, ldt, L, m, N, sg, dBeta, ldb, order_out, diag);
+  {
+    // [H T] stays resident (unless H exceeded the memory budget) for solve_direct's SVD branch
+    const bool kept = ctx->kept_h && ctx->kept_n == N;
+    SourceScope src(ctx, kept ? ctx->kept_h : nullptr, ctx->kept_ldh, kept ? ctx->kept_h + L : nullptr,
+                    ctx->kept_ldh, kept ? N : 0);
+    solve_dev(ctx, G, ldg, HtT, ldt, L, m, N, sg, dBeta, ldb, order_out, diag);
+  }
   cudaEventRecord(ctx->ev[3], ctx->stream);
   // finiteness check and accuracy pass enqueued behind the solve; one synchronisation for both
   const int* bad = check_finite(ctx, dBeta, ldb, L, m, true);
@@ -1002,6 +1172,18 @@ int rbpg_pseudo_inverse(rbpg_context* ctx, const double* h, size_t n, size_t l, 
   });
 }
 
+int rbpg_pinv_svd(rbpg_context* ctx, const double* a, size_t rows, size_t cols, double tol, double* out,
+                  rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (rows == 0 || cols == 0) fail(RBPG_SHAPE_ERROR, "pinv_svd: empty matrix");
+    Padded A = upload(ctx, "A.in", a, rows, cols);
+    const size_t ldo = even(rows);
+    double* O = ctx->dbuf("pinv.out", cols * ldo);
+    svd_pinv_dev(ctx, A.p, A.ld, rows, cols, tol, O, ldo);
+    download(ctx, out, O, ldo, cols, rows);
+  });
+}
+
 int rbpg_gram_device(rbpg_context* ctx, const double* da, size_t lda, size_t rows, size_t cols, double* dg, size_t ldg,
                      int accumulate, rbpg_status* st) {
   return guarded(ctx, st, [&] {
@@ -1074,6 +1256,7 @@ int rbpg_solve_beta(rbpg_context* ctx, const double* h, size_t n, size_t l, cons
     double* HtT = G + l;
     double* B = ctx->dbuf("beta", l * lb);
     gram_dev(ctx, A, lda, n, l + m, nullptr, 0, 0, G, ldg, nullptr, 0, false);
+    SourceScope src(ctx, A, lda, A + l, lda, n);
     solve_dev(ctx, G, ldg, HtT, ldt, l, m, n, *strategy, B, lb, nullptr, diag);
     download(ctx, beta, B, lb, l, m);
   });

@@ -252,6 +252,14 @@ DenseMatrix SpdFactor::solve(const DenseMatrix& rhs) const {
   return out;
 }
 DenseMatrix solve_spd(const DenseMatrix& m, const DenseMatrix& rhs) { return SpdFactor(m).solve(rhs); }
+DenseMatrix pinv_svd(const DenseMatrix& a, double tol) {
+  if (a.empty()) throw ShapeError("pinv_svd: empty matrix");
+  DenseMatrix out(a.cols(), a.rows(), 0.0);
+  rbpg_status st;
+  rbpg_pinv_svd(ctx(), a.data(), a.rows(), a.cols(), tol, out.data(), &st);
+  raise(st);
+  return out;
+}
 
 RankRevealingFactor rank_revealing_factor(const DenseMatrix& a, double tol) {
   RankRevealingFactor out;

@@ -57,6 +57,9 @@ class OracleImpl:
     def solve_factored_gram(self, factor, order, rank, rhs):
         return self._call(oracle.solve_factored_gram, factor, order, rank, rhs)
 
+    def pinv_svd(self, a, tol=0.0):
+        return self._call(oracle.pinv_svd, a, tol)
+
     def solve_beta(self, h, y, kind="rank", split=0, tol=0.0):
         beta, diag, _ = self._call(oracle.solve_beta, h, y, kind, split, tol)
         return beta, diag
@@ -95,6 +98,9 @@ class B200Impl:
     def solve_factored_gram(self, factor, order, rank, rhs):
         perm = rb.ColumnPermutation(list(order), rank, 0.0)
         return rb.solve_factored_gram(rb.RankRevealingFactor(perm, np.asarray(factor, dtype=float)), rhs)
+
+    def pinv_svd(self, a, tol=0.0):
+        return rb.pinv_svd(a, tol)
 
     def _strategy(self, kind, split, tol):
         return {"rank": rb.SolverStrategy.rank_based(tol), "df": rb.SolverStrategy.df_split(split),

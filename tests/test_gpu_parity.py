@@ -91,14 +91,6 @@ def test_train_parity_ragged_shapes(shape):
     assert diag.training_accuracy == ref["diag"]["training_accuracy"]
 
 
-@pytest.mark.xfail(raises=rb.NotSupportedError, strict=True,
-                   reason="SVD pseudoinverse fallback (solve_direct after SingularSplit) not yet on device")
-def test_svd_fallback_branch():
-    # d=2 inputs, L=640: H is numerically rank-deficient, the Schur block stays singular after the
-    # ridge retry (SingularSplit) and the reference falls back to solve_direct -> pinv_svd.
-    train_both(700, 2, 640, 2, seeds=(700, 3, 642))
-
-
 def test_determinism_bitwise():
     x, t = rb.synth_classification(3000, 20, 4, 5, 6)
     p = rb.ElmParams(20, 300, 4, 7)

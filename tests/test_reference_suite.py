@@ -9,7 +9,7 @@ Random inputs use numpy's PCG64 instead of libstdc++'s uniform_real_distribution
 import numpy as np
 import pytest
 
-from impls import B200Impl, OracleImpl, ShapeError, SingularMatrix, SingularSplit, pinv, rel_err
+from impls import B200Impl, OracleImpl, ShapeError, SingularMatrix, SingularSplit, pinv, rel_err, rel_fro
 
 IMPLS = [pytest.param(OracleImpl(), id="oracle"), pytest.param(B200Impl(), id="b200", marks=pytest.mark.gpu)]
 
@@ -22,6 +22,47 @@ def one_hot(rng, n, m):
     y = np.zeros((n, m))
     y[np.arange(n), rng.integers(0, m, size=n)] = 1.0
     return y
+
+
+# ---------------------------------------------------------------- pinv_svd (test_linalg.cpp:26-58)
+@pytest.mark.parametrize("impl", IMPLS)
+def test_pinv_identity_and_rank_deficient_diagonal(impl):  # :26-32
+    assert np.abs(impl.pinv_svd(np.eye(4)) - np.eye(4)).max() < 1e-12
+    assert np.abs(impl.pinv_svd(np.array([[2.0, 0], [0, 0]])) - np.array([[0.5, 0], [0, 0]])).max() < 1e-14
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+def test_pinv_left_inverse_full_column_rank(impl):  # :34-38
+    a = rnd(11, 10, 4)
+    assert np.abs(impl.pinv_svd(a) @ a - np.eye(4)).max() < 1e-10
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+def test_pinv_penrose_conditions(impl):  # :40-58 (random shapes up to 50 x 50, half rank-deficient)
+    rng = np.random.default_rng(12)
+    for c in range(20):
+        rows, cols = 2 + int(rng.integers(0, 49)), 2 + int(rng.integers(0, 49))
+        a = rng.uniform(-1, 1, (rows, cols))
+        if c % 2 == 0:
+            a[:, cols - 1] = 2.0 * a[:, 0]
+        x = impl.pinv_svd(a)
+        assert rel_err(a @ x @ a, a) < 1e-8
+        assert rel_err(x @ a @ x, x) < 1e-8
+        assert rel_err(a @ x, (a @ x).T) < 1e-8
+        assert rel_err(x @ a, (x @ a).T) < 1e-8
+
+
+@pytest.mark.parametrize("impl", IMPLS)
+def test_pinv_matches_numpy_svd_with_cut(impl):  # linalg.cpp:76-83 cut rule, incl. explicit tol
+    rng = np.random.default_rng(21)
+    for rows, cols, rank, tol in [(70, 33, 33, 0.0), (33, 70, 33, 0.0), (90, 45, 12, 0.0), (45, 90, 12, 0.0),
+                                  (64, 64, 64, 1e-3), (130, 97, 60, 0.0)]:
+        a = rng.uniform(-1, 1, (rows, rank)) @ rng.uniform(-1, 1, (rank, cols))
+        if rank == min(rows, cols) and tol > 0:
+            u, _, vt = np.linalg.svd(a, full_matrices=False)
+            a = (u * np.logspace(0, -6, len(vt))) @ vt  # singular values straddle the explicit cut
+        want = pinv(a, tol)
+        assert rel_fro(impl.pinv_svd(a, tol), want) < 1e-9, (rows, cols, rank, tol)
 
 
 # ---------------------------------------------------------------- matrix (test_matrix.cpp)
@@ -271,12 +312,7 @@ def test_residual_optimality_every_strategy(impl):  # :191-210
         y = rng.uniform(-1, 1, (rows, 2))
         best = np.linalg.norm(h @ (pinv(h) @ y) - y)
         for kind, split, tol in [("direct", 0, 0.0), ("df", cols // 2, 0.0), ("rank", 0, 1e-6)]:
-            try:
-                beta = impl.solve_beta(h, y, kind, split, tol)[0]
-            except Exception as e:  # the device has no SVD fallback (documented NotSupported)
-                if impl.name == "b200" and "SVD" in str(e):
-                    continue
-                raise
+            beta = impl.solve_beta(h, y, kind, split, tol)[0]
             assert np.linalg.norm(h @ beta - y) <= best + 1e-6 * (1.0 + np.linalg.norm(y))
 
 
