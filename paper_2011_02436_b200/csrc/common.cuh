@@ -94,6 +94,20 @@ __device__ __forceinline__ void st_async_v2b64(uint32_t cluster_addr, unsigned l
 // ---------------------------------------------------------------------------
 // gpu-scope release/acquire helpers for inter-CTA flag exchange
 // ---------------------------------------------------------------------------
+// bulk copy (TMA engine) of `bytes` (multiple of 16) from this CTA's shared memory into another
+// cluster CTA's shared memory; the bytes complete on the receiver's mbarrier.  The source must be
+// made visible to the async proxy first (fence_proxy_async after the writes).
+__device__ __forceinline__ void bulk_s2s_cluster(uint32_t cluster_dst, uint32_t src, uint32_t bytes,
+                                                 uint32_t cluster_mbar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          cluster_dst),
+      "r"(src), "r"(bytes), "r"(cluster_mbar)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+
 __device__ __forceinline__ void st_release_u32(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }

@@ -34,8 +34,8 @@ cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams
 cudaError_t launch_syrk_finish(const SyrkParams&, int, int, int, cudaStream_t);
 cudaError_t launch_gemm(const GemmParams&, cudaStream_t);
 cudaError_t launch_scores(const CUtensorMap&, const CUtensorMap&, const ScoresParams&, cudaStream_t);
-cudaError_t launch_factor_setup(const double*, long long, int, long long, double, int, double*, int*, FactorState*,
-                                cudaStream_t);
+cudaError_t launch_factor_setup(const double*, long long, int, int, long long, double, int, double*, int*,
+                                FactorState*, cudaStream_t);
 cudaError_t launch_panel(const PanelParams&, int, int*, cudaStream_t);
 cudaError_t launch_gather_factor(const double*, long long, const int*, int, double*, long long, int, cudaStream_t);
 cudaError_t launch_gather_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
@@ -170,10 +170,32 @@ struct rbpg_context {
     if (profile) {
       cudaEventRecord(b, stream);
       prof[name].pending.emplace_back(a, b);
+      if (timeline_on) timeline.push_back({name, a, b});
     }
+  }
+  // RBPG_TIMELINE=1 (with profiling on): per-launch start / duration / gap dump on stderr
+  struct Mark {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  const bool timeline_on = std::getenv("RBPG_TIMELINE") != nullptr;
+  std::vector<Mark> timeline;
+  void dump_timeline() {
+    if (timeline.empty()) return;
+    float prev_end = 0.f;
+    for (size_t i = 0; i < timeline.size(); ++i) {
+      float st = 0.f, du = 0.f;
+      cudaEventElapsedTime(&st, timeline[0].a, timeline[i].a);
+      cudaEventElapsedTime(&du, timeline[i].a, timeline[i].b);
+      std::fprintf(stderr, "TL %-22s start %9.1f us  dur %8.1f us  gap %6.1f us\n", timeline[i].name, st * 1e3,
+                   du * 1e3, (st - prev_end) * 1e3);
+      prev_end = st + du;
+    }
+    timeline.clear();
   }
   void collect() {
     cudaStreamSynchronize(stream);
+    if (timeline_on) dump_timeline();
     for (auto& kv : prof) {
       for (auto& pr : kv.second.pending) {
         float ms = 0.f;
@@ -211,11 +233,13 @@ CUtensorMap make_map(rbpg_context* ctx, const double* base, uint64_t cols, uint6
 // device building blocks
 // ---------------------------------------------------------------------------
 void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_t d, const double* dW, size_t ldw,
-                const double* db, size_t L, double* dH, size_t ldh) {
+                const double* db, size_t L, double* dH, size_t ldh, const double* dT = nullptr, size_t ldt = 0,
+                size_t m = 0) {
   if (N == 0) return;
   CUtensorMap tmX = make_map(ctx, dX, d, N, ldx, 16, kTile, true);
   CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, kTile, kBK, false);
-  HiddenParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), db, dH, static_cast<long long>(ldh)};
+  HiddenParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), db, dH, static_cast<long long>(ldh),
+                 0, m > 0 ? dT : nullptr, static_cast<long long>(ldt), static_cast<int>(m)};
   ctx->run("hidden_kernel", [&] { return launch_hidden(tmX, tmW, p, ctx->stream); });
 }
 
@@ -286,7 +310,8 @@ void gemm_dev(rbpg_context* ctx, int M, int N, int K, const double* A, size_t ld
 }
 
 // X (n x m, ld ldx) <- (F F^T)^{-1} X, column chunks of <= 128 right-hand sides
-void trsm_pair_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X, size_t ldx, size_t n, size_t m) {
+void trsm_pair_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X, size_t ldx, size_t n, size_t m,
+                   bool fwd = true, bool bwd = true) {
   static const bool tr = std::getenv("RBPG_TRSM_TRACE") != nullptr;
   if (tr) { cudaStreamSynchronize(ctx->stream); trsm_trace_dump(); }
   struct Dump { bool on; cudaStream_t s; ~Dump() { if (on) { cudaStreamSynchronize(s); trsm_trace_dump(); } } } dump{tr, ctx->stream};
@@ -295,7 +320,7 @@ void trsm_pair_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X, si
     double* dinv = ctx->dbuf("trsm.dinv", ((n + 63) / 64) * 64 * 64);
     ctx->run("trsm_pair_kernel", [&] {
       return launch_trsm_pair(F, static_cast<long long>(ldf), X + c0, static_cast<long long>(ldx), static_cast<int>(n),
-                              mc, 1, 1, ctx->num_sms, dinv, ctx->stream);
+                              mc, fwd ? 1 : 0, bwd ? 1 : 0, ctx->num_sms, dinv, ctx->stream);
     });
   }
 }
@@ -311,9 +336,12 @@ struct FactorResult {
 
 // Diagonal-pivoted (pivoting = 1, linalg.cpp:157-248) or unpivoted SpdFactor (pivoting = 0,
 // linalg.cpp:99-139) blocked Cholesky of the symmetric dG (n x n, ld ldg).  dG is not modified.
+// neligible < n: the trailing n - neligible columns are right-hand sides carried through the
+// factorisation (never pivots): their factor rows become the forward-solved F^{-1} P^T b.
 FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t n, size_t rows_for_tol, double tol,
-                        int pivoting, const std::string& tag, bool sync = true) {
+                        int pivoting, const std::string& tag, bool sync = true, size_t neligible = SIZE_MAX) {
   cudaStream_t s = ctx->stream;
+  if (neligible > n) neligible = n;
   const size_t ldn = round_up(n, 8);
   double* Ga = ctx->dbuf(tag + ".Ga", n * ldn);
   double* Gb = ctx->dbuf(tag + ".Gb", n * ldn);
@@ -338,13 +366,15 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
   ck(cudaMemsetAsync(Pg, 0, sizeof(double) * n * 64, s), "memset Pg");
   ck(cudaMemsetAsync(slots, 0, sizeof(PivotSlot) * 2 * (max_ctas + 32), s), "memset slots");
   ck(cudaMemcpy2DAsync(Ga, ldn * 8, dG, ldg * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "copy G");
-  ctx->run("factor_setup", [&] { return launch_factor_setup(Ga, static_cast<long long>(ldn), static_cast<int>(n),
-                               static_cast<long long>(rows_for_tol), tol, pivoting, dv[0], ov[0], st, s); });
+  ctx->run("factor_setup", [&] {
+    return launch_factor_setup(Ga, static_cast<long long>(ldn), static_cast<int>(n), static_cast<int>(neligible),
+                               static_cast<long long>(rows_for_tol), tol, pivoting, dv[0], ov[0], st, s);
+  });
   double* gcur = Ga;
   double* gnext = Gb;
   int cur = 0;
-  for (size_t k = 0; k < n; k += 64) {
-    const int kb = static_cast<int>(std::min<size_t>(64, n - k));
+  for (size_t k = 0; k < neligible; k += 64) {
+    const int kb = static_cast<int>(std::min<size_t>(64, neligible - k));
     PanelParams pp{};
     pp.G = gcur;
     pp.ldg = static_cast<long long>(ldn);
@@ -365,10 +395,11 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     pp.ldf = static_cast<long long>(ldn);
     pp.pivoting = pivoting;
     pp.rows_per_cta = 0;  // chosen by launch_panel
+    pp.neligible = static_cast<int>(neligible);
     pp.trace = trace;
     ctx->run("panel_kernel", [&] { return launch_panel(pp, ctx->num_sms, nullptr, s); });
     const size_t t0 = k + kb;
-    if (t0 < n) {
+    if (t0 < neligible) {  // another panel follows
       const size_t nrem = n - t0;
       // 64-wide tiles while 128-wide ones would not fill two waves of SMs
       const size_t nb128 = (nrem + kTile - 1) / kTile;
@@ -659,9 +690,13 @@ void block_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
 }
 
 // solve_beta dispatch (elm.cpp:158-229) on device G (original coordinates) and HtT.
+// gaug: dG is the whole augmented Gram [H T]^T [H T] ((L+m) x (L+m), ld ldg) with dHtT = dG + L.
+// The rank path then factors it with the m target columns carried along as never-pivot labels, so
+// the factorisation itself forward-solves F y = P^T H^T T (y = their factor rows) and only the
+// backward substitution F^T x = y remains (cf. solve_factored_gram, linalg.cpp:254-270).
 void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dHtT, size_t ldt, size_t L, size_t m,
                size_t rows, const rbpg_strategy& sg, double* dBeta, size_t ldb, size_t* order_out,
-               rbpg_diagnostics* diag) {
+               rbpg_diagnostics* diag, bool gaug = false) {
   if (sg.kind == RBPG_DIRECT) {
     diag->split_lo = L;
     diag->split_hi = 0;
@@ -692,13 +727,23 @@ void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   if (sg.kind != RBPG_RANK_BASED) fail(RBPG_RUNTIME_ERROR, "solve_beta: unknown strategy");
   if (sg.rank_tol < 0.0 || !std::isfinite(sg.rank_tol))
     fail(RBPG_INVALID_ARGUMENT, "rank_revealing_permutation: tolerance must be >= 0");
-  FactorResult f = factor_dev(ctx, dG, ldg, L, rows, sg.rank_tol, 1, "rrf", false);
+  const bool aug = gaug && m > 0 && m <= 32 && !std::getenv("RBPG_NO_AUG");
+  FactorResult f = factor_dev(ctx, dG, ldg, aug ? L + m : L, rows, sg.rank_tol, 1, "rrf", false, L);
   // speculate the full-rank solve (elm.cpp:202-214) before the one host readback of the rank;
   // with rank < L its result is discarded
   const size_t lm = even(m);
   double* rhs = ctx->dbuf("rank.rhs", L * lm);
-  ctx->run("gather rhs", [&] { return launch_gather_rows(dHtT, ldt, f.ord, L, m, rhs, lm, ctx->stream); });
-  trsm_pair_dev(ctx, f.F, f.ldF, rhs, lm, L, m);
+  if (aug) {  // y (forward-solved, position order) = rows L.. of the factor, transposed
+    ctx->run("transpose y", [&] {
+      return launch_transpose(f.F + L * f.ldF, static_cast<long long>(f.ldF), static_cast<long long>(m),
+                              static_cast<long long>(L), rhs, static_cast<long long>(lm), static_cast<long long>(m),
+                              ctx->stream);
+    });
+    trsm_pair_dev(ctx, f.F, f.ldF, rhs, lm, L, m, false, true);
+  } else {
+    ctx->run("gather rhs", [&] { return launch_gather_rows(dHtT, ldt, f.ord, L, m, rhs, lm, ctx->stream); });
+    trsm_pair_dev(ctx, f.F, f.ldF, rhs, lm, L, m);
+  }
   ctx->run("unpermute beta", [&] { return launch_scatter_rows(rhs, lm, f.ord, L, m, dBeta, ldb, ctx->stream); });
   int* ho = static_cast<int*>(ctx->pinned("order.out", L * 4));
   if (order_out) ck(cudaMemcpyAsync(ho, f.ord, L * 4, cudaMemcpyDeviceToHost, ctx->stream), "read order");
@@ -798,7 +843,7 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
     // further chunks (H larger than the budget) synchronise on ev[4]/ev[5]
     cudaEvent_t ea = r0 == 0 ? ctx->ev[0] : ctx->ev[4], eb = r0 == 0 ? ctx->ev[1] : ctx->ev[5];
     if (timed) cudaEventRecord(ea, ctx->stream);
-    hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh);
+    hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh, dT + r0 * ldt_in, ldt_in, m);  // + T columns
     if (timed) {
       cudaEventRecord(eb, ctx->stream);
       if (r0 > 0) {
@@ -808,10 +853,6 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
         hidden_ms += ms;
       }
     }
-    if (m > 0)
-      ck(cudaMemcpy2DAsync(dH + L, ldh * 8, dT + r0 * ldt_in, ldt_in * 8, m * 8, nr, cudaMemcpyDeviceToDevice,
-                           ctx->stream),
-         "append T");
     gram_dev(ctx, dH, ldh, nr, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate || r0 > 0);
   }
   if (keep_h && chunk >= N) {
@@ -904,7 +945,7 @@ void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* d
     const bool kept = ctx->kept_h && ctx->kept_n == N;
     SourceScope src(ctx, kept ? ctx->kept_h : nullptr, ctx->kept_ldh, kept ? ctx->kept_h + L : nullptr,
                     ctx->kept_ldh, kept ? N : 0);
-    solve_dev(ctx, G, ldg, HtT, ldt, L, m, N, sg, dBeta, ldb, order_out, diag);
+    solve_dev(ctx, G, ldg, HtT, ldt, L, m, N, sg, dBeta, ldb, order_out, diag, true);
   }
   cudaEventRecord(ctx->ev[3], ctx->stream);
   // finiteness check and accuracy pass enqueued behind the solve; one synchronisation for both
@@ -1257,7 +1298,7 @@ int rbpg_solve_beta(rbpg_context* ctx, const double* h, size_t n, size_t l, cons
     double* B = ctx->dbuf("beta", l * lb);
     gram_dev(ctx, A, lda, n, l + m, nullptr, 0, 0, G, ldg, nullptr, 0, false);
     SourceScope src(ctx, A, lda, A + l, lda, n);
-    solve_dev(ctx, G, ldg, HtT, ldt, l, m, n, *strategy, B, lb, nullptr, diag);
+    solve_dev(ctx, G, ldg, HtT, ldt, l, m, n, *strategy, B, lb, nullptr, diag, true);
     download(ctx, beta, B, lb, l, m);
   });
 }

@@ -33,7 +33,9 @@ constexpr int kPanelThreads = 256;
 constexpr double kEps = 2.220446049250313e-16;
 
 // ---------------------------------------------------------------------------
-__global__ void factor_setup_kernel(const double* G, long long ldg, int n, long long rows, double tol,
+// neligible <= n: only the first neligible columns are pivot candidates (and set the tolerance);
+// the rest are augmented right-hand sides carried through the factorisation.
+__global__ void factor_setup_kernel(const double* G, long long ldg, int n, int neligible, long long rows, double tol,
                                     int pivoting, double* d, int* ord, FactorState* st) {
   __shared__ double red[kPanelThreads];
   double mx = -DBL_MAX;
@@ -41,7 +43,7 @@ __global__ void factor_setup_kernel(const double* G, long long ldg, int n, long 
     const double v = G[(long long)i * ldg + i];
     d[i] = v;
     ord[i] = i;
-    mx = fmax(mx, v);
+    if (i < neligible) mx = fmax(mx, v);
   }
   red[threadIdx.x] = mx;
   __syncthreads();
@@ -55,9 +57,9 @@ __global__ void factor_setup_kernel(const double* G, long long ldg, int n, long 
     st->fail = 0;
     st->fail_index = -1;
     st->fail_value = 0.0;
-    st->rank = n;
+    st->rank = neligible;
     st->stopped = 0;
-    const double rmax = static_cast<double>(rows > n ? rows : n);
+    const double rmax = static_cast<double>(rows > neligible ? rows : neligible);
     st->tolerance = tol > 0.0 ? tol : rmax * kEps;   // linalg.cpp:171
     if (pivoting) {
       if (!(dmax0 > 0.0)) {                           // linalg.cpp:189-193: rank 0, identity order
@@ -66,7 +68,7 @@ __global__ void factor_setup_kernel(const double* G, long long ldg, int n, long 
       }
       st->cut = st->tolerance * sqrt(dmax0 > 0.0 ? dmax0 : 0.0);
     } else {
-      st->thresh = static_cast<double>(n) * kEps * dmax0;  // linalg.cpp:109
+      st->thresh = static_cast<double>(neligible) * kEps * dmax0;  // linalg.cpp:109
     }
   }
 }
@@ -179,9 +181,9 @@ __global__ void axpy_rows_kernel(const double* A, long long lda, const double* B
 // ============================================================================
 // launchers
 // ============================================================================
-cudaError_t launch_factor_setup(const double* G, long long ldg, int n, long long rows, double tol, int pivoting,
-                                double* d, int* ord, FactorState* st, cudaStream_t s) {
-  factor_setup_kernel<<<1, kPanelThreads, 0, s>>>(G, ldg, n, rows, tol, pivoting, d, ord, st);
+cudaError_t launch_factor_setup(const double* G, long long ldg, int n, int neligible, long long rows, double tol,
+                                int pivoting, double* d, int* ord, FactorState* st, cudaStream_t s) {
+  factor_setup_kernel<<<1, kPanelThreads, 0, s>>>(G, ldg, n, neligible, rows, tol, pivoting, d, ord, st);
   return cudaGetLastError();
 }
 

@@ -127,6 +127,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     return;
   }
 
+  // augmented rows [H T]: the last column tile also copies this row tile's targets
+  if (p.T && blockIdx.x == gridDim.x - 1) {
+    for (int e = tid; e < kTile * p.m; e += kGemmThreads) {
+      const int rr = e / p.m, j = e - rr * p.m, r = n0 + rr;
+      if (r < p.N) p.H[(long long)r * p.ldh + p.L + j] = p.T[(long long)r * p.ldt + j];
+    }
+  }
+
   // epilogue: bias after the full dot product, then sigmoid (elm.cpp:102, :27)
 #pragma unroll
   for (int mt = 0; mt < 4; ++mt) {
@@ -264,6 +272,33 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
 
   // ---- epilogue.  Thread holds rows r, r+1 (r even) x cols c..c+3 per (mt, pp).
   const int split = blockIdx.y;
+  // trailing mode: every G_old gather is issued before the first store (the stores could alias
+  // the loads as far as the compiler knows, which would serialise one L2 round trip per element)
+  // (64-wide tiles only: the 128-wide kernel has no registers to spare for the staging)
+  constexpr bool kStageGold = TILE == 64;
+  double gold[kStageGold ? MT : 1][2][2][4];
+  if (kStageGold && p.mode == kSyrkTrailing && !isT) {
+    const int off = p.off;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const int r0 = i0 + wm + mt * 16 + 2 * g;
+        const int c0 = j0 + wn + pp * 16 + 4 * t;
+        int sc[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) sc[q] = (c0 + q < p.M) ? __ldg(p.lab + off + c0 + q) : 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + h;
+          const int sr = r < p.M ? __ldg(p.lab + off + r) : 0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            gold[mt][pp][h][q] =
+                (r < p.M && c0 + q < p.M && c0 + q <= r) ? __ldg(p.Gold + (long long)sr * p.ldg + sc[q]) : 0.0;
+        }
+      }
+  }
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
@@ -320,8 +355,12 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
           if (c >= p.M || c > r) continue;
           double val = v[h][q];
           if (p.mode == kSyrkTrailing) {
-            const int sr = p.lab[off + r], sc = p.lab[off + c];
-            val = sub_rn(p.Gold[(long long)sr * p.ldg + sc], val);
+            if constexpr (kStageGold) {
+              val = sub_rn(gold[mt][pp][h][q], val);
+            } else {
+              const int sr = p.lab[off + r], sc = p.lab[off + c];
+              val = sub_rn(p.Gold[(long long)sr * p.ldg + sc], val);
+            }
           }
           p.G[(long long)(off + r) * p.ldg + off + c] = val;
           p.G[(long long)(off + c) * p.ldg + off + r] = val;

@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
     unsigned long long key = 0;
     int pos = INT_MAX;
     if (p.pivoting) {
-      for (int i = tid; i < nown; i += kPThreads) {
+      for (int i = tid; i < nown && lbeg + i < p.neligible; i += kPThreads) {
         const unsigned long long kk = dkey(dl[i]);
         if (kk > key || (kk == key && lbeg + i < pos)) {
           key = kk;
@@ -358,7 +358,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
         dl[li] = dn;
         const unsigned long long kk = dkey(dn);
         if (p.pivoting) {
-          if (kk > bkey || (kk == bkey && pos < bpos)) {
+          if (x < p.neligible && (kk > bkey || (kk == bkey && pos < bpos))) {
             bkey = kk;
             bpos = pos;
           }
@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   {
     unsigned long long key = 0;
     int pos = INT_MAX;
-    if (mine && q == 0) {
+    if (mine && q == 0 && x < p.neligible) {
       if (p.pivoting) {
         key = dkey(dl);
         pos = x;
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     for (int i = 0; i < 16; ++i) pr[i] = (wr && i == slot) ? wv : pr[i];
     if (alive) {
       dl = fma(-col, col, dl);
-      if (q == 0 && (p.pivoting || pos == j + 1)) {
+      if (q == 0 && x < p.neligible && (p.pivoting || pos == j + 1)) {
         bkey = dkey(dl);
         bpos = pos;
       }

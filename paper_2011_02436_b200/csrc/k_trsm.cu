@@ -215,8 +215,36 @@ __device__ __forceinline__ void mma64(const double* A, int lda, bool aT, const d
   }
 }
 
-__global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, long long ldf, const double* Dinv,
-                                                              double* X, long long ldx, int n, int m) {
+// Inverse of the lower-triangular 64 x 64 tile T (rows/cols >= nb zero) into Dinv (64 x 64, row-major).
+// Column j is a forward substitution on e_j, shared by the two threads (j, h) of a lane pair: thread h
+// keeps the partial sums of rows 32h..32h+31 in registers; the owner of row c forms z_c and passes it
+// to its partner.  Same operation order as tri_inv_kernel (s_i accumulates F[i][c] z_c over
+// increasing c by fma; z_i = -s_i / F[i][i], z_j = 1 / F[j][j]).
+__device__ __forceinline__ void invert_tile(const double* T, int nb, double* Dinv, int tid) {
+  if (tid >= 2 * kTB) return;  // warps 0-3, fully active (shuffles)
+  const int j = tid >> 1, h = tid & 1, lane = tid & 31;
+  const double* Th = T + h * 32 * kPadT;
+  double sacc[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) sacc[r] = 0.0;
+#pragma unroll
+  for (int c = 0; c < kTB; ++c) {
+    const double zl = ((c == j ? 1.0 : 0.0) - sacc[c & 31]) / T[c * kPadT + c];
+    const double z0 = __shfl_sync(0xffffffffu, zl, (lane & ~1) | (c >> 5));
+    const double z = (c >= j && c < nb) ? z0 : 0.0;
+    if (h == (c >> 5)) Dinv[c * kTB + j] = z;
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (h * 32 + r > c) sacc[r] = fma(Th[r * kPadT + c], z, sacc[r]);
+  }
+}
+
+// Steps [s_begin, s_end) of the 2 * nblk block steps: forward steps s < nblk solve block s, backward
+// steps s >= nblk solve block 2 * nblk - 1 - s (s_begin = nblk: backward substitution only, the
+// right-hand side already forward-solved -- e.g. by the augmented factorisation).
+__global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, long long ldf, double* Dinv,
+                                                              double* X, long long ldx, int n, int m, int s_begin,
+                                                              int s_end) {
   extern __shared__ __align__(16) double csm[];
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), cta = static_cast<int>(cl.block_rank());
@@ -237,6 +265,17 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
     const int row = (cta + ob * C) * kTB + q;
     Rown[e] = row < n ? X[(long long)row * ldx + c] : 0.0;
   }
+  // inverses of the owned diagonal blocks (only the owner ever reads them), first-needed first
+  for (int oi = 0; oi < nown; ++oi) {
+    const int ob = s_begin == 0 ? oi : nown - 1 - oi;
+    const int b = cta + ob * C, nb = min(kTB, n - b * kTB);
+    load_tile_async(To, F, ldf, b * kTB, nb, b * kTB, nb, tid, nt);
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    invert_tile(To, nb, Dinv + (long long)b * kTB * kTB, tid);
+    __syncthreads();
+  }
   cl.sync();
   const uint32_t ybytes = static_cast<uint32_t>(kTB * m * sizeof(double));
   auto block_of = [&](int s) { return s < nblk ? s : 2 * nblk - 1 - s; };
@@ -247,19 +286,33 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
     const bool bwd = s >= nblk;
     const int b = block_of(s);
     double* Rb = Rown + (size_t)(b / C) * kTB * m;
-    const int slot = s % kRing;
+    const int slot = (s - s_begin) % kRing;
     double* Y = Ring + slot * kTB * m;
+    const long long q0 = clock64();
     mma64(D, kPadT, bwd, Rb, m, Y, false, tid);
+    const long long q1 = clock64();
     __syncthreads();
-    for (int e = tid; e < kTB * m; e += nt) Rb[e] = Y[e];  // the block's solution
+    const long long q2 = clock64();
     const uint32_t yl = smem_u32(Y), bl = smem_u32(&rbar[slot]);
-    for (int d = 0; d < C; ++d) {
-      if (d == cta) continue;
-      const uint32_t ry = mapa_u32(yl, d), rb = mapa_u32(bl, d);
-      for (int e = tid; e < kTB * m / 2; e += nt) st_async_v2f64(ry + 16 * e, Y[2 * e], Y[2 * e + 1], rb);
+    if (tid < C - 1) {
+      // one bulk DSMEM copy per destination (TMA engine), issued by C - 1 threads in parallel and
+      // in step order: the owner of the next block (the critical consumer) is served first
+      const int d = bwd ? (cta - 1 - tid + 2 * C) % C : (cta + 1 + tid) % C;
+      fence_proxy_async();
+      bulk_wait_read0();  // this thread's earlier push has finished reading its ring slot
+      bulk_s2s_cluster(mapa_u32(yl, d), yl, ybytes, mapa_u32(bl, d));
+      bulk_commit();
     }
-    if (tid == 0)  // the own copy was written in place
+    if (tid == 32)  // the own copy was written in place
       asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;\n" ::"r"(bl), "r"(ybytes) : "memory");
+    const long long q3 = clock64();
+    for (int e = tid; e < kTB * m; e += nt) Rb[e] = Y[e];  // the block's solution
+    if (tid == 0 && g_trsm_trace) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[8]), static_cast<unsigned long long>(q1 - q0));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[9]), static_cast<unsigned long long>(q2 - q1));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[10]), static_cast<unsigned long long>(q3 - q2));
+      atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[11]), 1ull);
+    }
   };
   // R_bp -= F-tile * Y (forward: tile = F[bp rows][b cols]; backward: tile = F[b rows][bp cols]^T)
   auto update = [&](int bp, const double* T, bool bwd, const double* Yb) {
@@ -278,23 +331,24 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
     }
   };
 
-  // step 0's solution needs no update
-  if (owns(block_of(0))) {
-    issue_dinv(Ds, block_of(0));
+  // the first step's solution needs no update
+  if (owns(block_of(s_begin))) {
+    issue_dinv(Ds, block_of(s_begin));
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
   }
   if (tid < kRing && tid == 0) mbar_arrive_expect_tx(&rbar[0], ybytes);
   __syncthreads();
-  if (owns(block_of(0))) solve_and_push(0, Ds);
+  if (owns(block_of(s_begin))) solve_and_push(s_begin, Ds);
 
   long long tw = 0, tc = 0, to = 0;
-  for (int s = 0; s < 2 * nblk; ++s) {
+  for (int s = s_begin; s < s_end; ++s) {
+    const int u = s - s_begin;
     const bool bwd = s >= nblk;
     const int b = block_of(s);
-    const int slot = s % kRing;
-    const bool last = s + 1 == 2 * nblk;
+    const int slot = u % kRing;
+    const bool last = s + 1 == s_end;
     const int bn = last ? -1 : block_of(s + 1);
     const bool bwd_n = s + 1 >= nblk;
     // does the next step's block need this step's Y? (not at the forward -> backward turn)
@@ -310,12 +364,12 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
       break;
     }
     if (first_other >= 0) issue_tile(To, b, first_other, bwd);
-    if (!last && owns(bn)) issue_dinv(Ds + ((s + 1) & 1) * kTB * kPadT, bn);
+    if (!last && owns(bn)) issue_dinv(Ds + ((u + 1) & 1) * kTB * kPadT, bn);
     cp_async_commit();
-    if (!last && tid == 0) mbar_arrive_expect_tx(&rbar[(s + 1) % kRing], ybytes);
-    if ((s + 1) % kSyncEvery == 0) cl.sync();  // skew < kRing steps
+    if (!last && tid == 0) mbar_arrive_expect_tx(&rbar[(u + 1) % kRing], ybytes);
+    if ((u + 1) % kSyncEvery == 0) cl.sync();  // skew < kRing steps
     long long t1 = clock64();
-    mbar_wait(&rbar[slot], (s / kRing) & 1);
+    mbar_wait(&rbar[slot], (u / kRing) & 1);
     const double* Yb = Ring + slot * kTB * m;
     cp_async_wait_all();
     __syncthreads();
@@ -323,7 +377,14 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
     if (!last && owns(bn)) {  // critical path: update the next block, solve it, push
       if (crit) update(bn, Tc, bwd, Yb);
       __syncthreads();
-      solve_and_push(s + 1, Ds + ((s + 1) & 1) * kTB * kPadT);
+      const long long ta = clock64();
+      solve_and_push(s + 1, Ds + ((u + 1) & 1) * kTB * kPadT);
+      if (tid == 0 && g_trsm_trace) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[4]), static_cast<unsigned long long>(ta - t2));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[5]),
+                  static_cast<unsigned long long>(clock64() - ta));
+        atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[6]), 1ull);
+      }
     }
     long long t3 = clock64(); tc += t3 - t2;
     for (int ob = 0; ob < nown; ++ob) {  // remaining updates off the critical path
@@ -343,7 +404,7 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
     __syncthreads();
     to += clock64() - t3;
   }
-  if (cta == 0 && tid == 0 && g_trsm_trace) { g_trsm_trace[0] += tw; g_trsm_trace[1] += tc; g_trsm_trace[2] += to; g_trsm_trace[3] += 2 * nblk; }
+  if (cta == 0 && tid == 0 && g_trsm_trace) { g_trsm_trace[0] += tw; g_trsm_trace[1] += tc; g_trsm_trace[2] += to; g_trsm_trace[3] += s_end - s_begin; }
   cl.sync();  // no CTA exits while remote stores may still target it
   for (int e = tid; e < nown * kTB * m; e += nt) {
     const int ob = e / (kTB * m), rem = e % (kTB * m), q = rem / m, c = rem % m;
@@ -368,9 +429,7 @@ cudaError_t launch_trsm_pair(const double* F, long long ldf, double* X, long lon
     cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kInvSmem);
     inv_attr = true;
   }
-  tri_inv_kernel<<<nblk, kTB, kInvSmem, s>>>(F, ldf, n, dinv_ws);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
   const size_t smem = (size_t(2) * kTB * m + size_t(kTB + kTR) * (kTB + 1)) * sizeof(double);
   static size_t attr_smem = 0;
   if (smem > attr_smem) {
@@ -378,7 +437,7 @@ cudaError_t launch_trsm_pair(const double* F, long long ldf, double* X, long lon
     if (e != cudaSuccess) return e;
     attr_smem = smem;
   }
-  if (fwd && bwd && m <= kClusterMaxM && !std::getenv("RBPG_TRSM_GRID")) {
+  if ((fwd || bwd) && m <= kClusterMaxM && !std::getenv("RBPG_TRSM_GRID")) {
     const int C = std::min(16, nblk);
     const size_t csmem = trsm_cluster_smem(n, m, C);
     if (csmem <= 220 * 1024) {
@@ -402,10 +461,14 @@ cudaError_t launch_trsm_pair(const double* F, long long ldf, double* X, long lon
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      const double* Dc = dinv_ws;
-      return cudaLaunchKernelEx(&cfg, trsm_cluster_kernel, F, ldf, Dc, X, ldx, n, m);
+      const int s_begin = fwd ? 0 : nblk, s_end = bwd ? 2 * nblk : nblk;
+      return cudaLaunchKernelEx(&cfg, trsm_cluster_kernel, F, ldf, dinv_ws, X, ldx, n, m, s_begin,
+                                s_end);  // inverts its diagonal blocks in-kernel
     }
   }
+  tri_inv_kernel<<<nblk, kTB, kInvSmem, s>>>(F, ldf, n, dinv_ws);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
   int blocks = std::min(num_sms, std::max(1, (n + kTB - 1) / kTB));
   const double* Dc = dinv_ws;
   for (int dir = 0; dir < 2; ++dir) {
@@ -423,15 +486,20 @@ namespace rbpg {
 void trsm_trace_dump() {
   static long long* buf = nullptr;
   if (!buf) {
-    cudaMalloc(&buf, 64);
-    cudaMemset(buf, 0, 64);
+    cudaMalloc(&buf, 128);
+    cudaMemset(buf, 0, 128);
     cudaMemcpyToSymbol(g_trsm_trace, &buf, sizeof(buf));
     return;
   }
-  long long h[4];
-  cudaMemcpy(h, buf, 32, cudaMemcpyDeviceToHost);
-  std::fprintf(stderr, "[trsm trace] steps %lld wait %.0f crit %.0f other %.0f cycles/step\n", h[3],
-               double(h[0]) / (h[3] ? h[3] : 1), double(h[1]) / (h[3] ? h[3] : 1), double(h[2]) / (h[3] ? h[3] : 1));
-  cudaMemset(buf, 0, 64);
+  long long h[12];
+  cudaMemcpy(h, buf, 96, cudaMemcpyDeviceToHost);
+  std::fprintf(stderr, "[trsm trace] solve_and_push x%lld: mma %.0f sync %.0f push-issue %.0f cycles\n", h[11],
+               double(h[8]) / (h[11] ? h[11] : 1), double(h[9]) / (h[11] ? h[11] : 1),
+               double(h[10]) / (h[11] ? h[11] : 1));
+  std::fprintf(stderr, "[trsm trace] steps %lld wait %.0f crit %.0f other %.0f cycles/step; owner steps %lld: "
+               "update %.0f solve+push %.0f cycles\n", h[3],
+               double(h[0]) / (h[3] ? h[3] : 1), double(h[1]) / (h[3] ? h[3] : 1), double(h[2]) / (h[3] ? h[3] : 1),
+               h[6], double(h[4]) / (h[6] ? h[6] : 1), double(h[5]) / (h[6] ? h[6] : 1));
+  cudaMemset(buf, 0, 128);
 }
 }  // namespace rbpg

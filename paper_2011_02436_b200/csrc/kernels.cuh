@@ -22,6 +22,9 @@ struct HiddenParams {
   double* H;
   long long ldh;
   int transposed;  // 0: H = sigmoid(XW + b); 1: plain product stored transposed, H[c][r] = (XW)[r][c]
+  const double* T;  // optional (transposed == 0): targets copied into H[:, L:L+m] (augmented [H T] rows)
+  long long ldt;
+  int m;
 };
 
 // ---- K2: lower-tile SYRK C = A^T A (+ A^T B tiles), TN layout (A is K x M row-major)
@@ -104,6 +107,7 @@ struct PanelParams {
   double* Fo; long long ldf;            // factor rows by original column
   int pivoting;                         // 1 = rank-revealing (diag pivot), 0 = SpdFactor (no pivot)
   int rows_per_cta;
+  int neligible;                        // labels >= neligible are never pivots (augmented right-hand sides)
   unsigned long long* trace;                   // optional per-phase cycle counters (CTA 0, thread 0)
 };
 
