@@ -29,7 +29,7 @@
 
 namespace rbpg {
 void trsm_trace_dump();
-cudaError_t launch_hidden(const CUtensorMap&, const CUtensorMap&, const HiddenParams&, cudaStream_t);
+cudaError_t launch_hidden(const CUtensorMap&, const CUtensorMap&, const HiddenParams&, int, cudaStream_t);
 cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams&, int, int, cudaStream_t);
 cudaError_t launch_syrk_finish(const SyrkParams&, int, int, int, cudaStream_t);
 cudaError_t launch_gemm(const GemmParams&, cudaStream_t);
@@ -237,10 +237,10 @@ void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_
                 size_t m = 0) {
   if (N == 0) return;
   CUtensorMap tmX = make_map(ctx, dX, d, N, ldx, 16, kTile, true);
-  CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, kTile, kBK, false);
+  CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, 64, kBK, false);
   HiddenParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), db, dH, static_cast<long long>(ldh),
                  0, m > 0 ? dT : nullptr, static_cast<long long>(ldt), static_cast<int>(m)};
-  ctx->run("hidden_kernel", [&] { return launch_hidden(tmX, tmW, p, ctx->stream); });
+  ctx->run("hidden_kernel", [&] { return launch_hidden(tmX, tmW, p, 64, ctx->stream); });
 }
 
 // G (+)= A^T A over rows [0, N) of A (N x L, ld lda); HtT (+)= A^T T when m > 0.
@@ -360,8 +360,8 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
   ck(cudaMemsetAsync(Fo, 0, sizeof(double) * n * ldn, s), "memset Fo");
   unsigned long long* trace = nullptr;
   if (std::getenv("RBPG_PANEL_TRACE")) {
-    trace = static_cast<unsigned long long*>(ctx->buf(tag + ".ptrace", 48));
-    ck(cudaMemsetAsync(trace, 0, 48, s), "memset trace");
+    trace = static_cast<unsigned long long*>(ctx->buf(tag + ".ptrace", 64));
+    ck(cudaMemsetAsync(trace, 0, 64, s), "memset trace");
   }
   ck(cudaMemsetAsync(Pg, 0, sizeof(double) * n * 64, s), "memset Pg");
   ck(cudaMemsetAsync(slots, 0, sizeof(PivotSlot) * 2 * (max_ctas + 32), s), "memset slots");
@@ -436,10 +436,11 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     r.st = *hs;
   }
   if (trace) {
-    unsigned long long h[6];
+    unsigned long long h[7];
     cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
     const double st = double(h[5] ? h[5] : 1);
-    std::fprintf(stderr, "[panel trace %s n=%zu] steps %llu cycles/step: barrier %.0f winner+row %.0f update %.0f reduce+sync %.0f publish %.0f\n",
+    std::fprintf(stderr, "[panel trace %s n=%zu] steps %llu cycles/step: barrier %.0f winner+row %.0f update %.0f "
+                 "reduce+sync %.0f publish %.0f\n",
                  tag.c_str(), n, h[5], h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st);
   }
   r.F = F;
@@ -1019,7 +1020,7 @@ void pinv_apply_dev(rbpg_context* ctx, const double* Ginv, size_t ldgi, const do
   CUtensorMap tmG = make_map(ctx, Ginv, L, L, ldgi, kTile, kBK, false);
   HiddenParams p{static_cast<int>(N), static_cast<int>(L), static_cast<int>(L), nullptr, dOut,
                  static_cast<long long>(ldo), 1};
-  ctx->run("pinv_apply", [&] { return launch_hidden(tmH, tmG, p, ctx->stream); });
+  ctx->run("pinv_apply", [&] { return launch_hidden(tmH, tmG, p, kTile, ctx->stream); });
 }
 
 void rank_deficient_pinv(const PinvFactor& pf, size_t L) {

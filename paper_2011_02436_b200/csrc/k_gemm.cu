@@ -36,23 +36,42 @@ __device__ __forceinline__ unsigned char* align1024(unsigned char* p) {
   return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
+// 1 / x for x >= 1 (x = 1 + exp(-z) in the sigmoid) without the XU pipe: an integer-subtraction
+// seed on the bit pattern (relative error < 5.1%), then four Newton-Raphson steps on DFMA
+// (error 5e-2 -> 2.6e-3 -> 6.5e-6 -> 4e-11 -> ~1e-21 before rounding), the last one giving the
+// correctly rounded quotient in all tested cases.  The DP reciprocal seed (MUFU.RCP64H) is the
+// bottleneck of the sigmoid epilogue on sm_100 (XU pipe ~90% busy), DFMA is not.
+__device__ __forceinline__ double recip_ge1(double x) {
+  double y = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(x));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+  }
+  return x <= 1.7976931348623157e308 ? y : (x > 0.0 ? 0.0 : x);  // 1/inf = 0, NaN propagates
+}
+
 }  // namespace
 
 // ============================================================================
-// K1: hidden-layer build
+// K1: hidden-layer build.  Row tile 128 (samples) x column tile BN (hidden nodes).  BN = 64 keeps
+// the accumulators at 32 per thread so two CTAs share an SM: one CTA's sigmoid epilogue (FP64
+// CUDA-core pipe) overlaps the other's DMMA main loop (tensor pipe).  BN = 128 (one CTA per SM)
+// serves the plain transposed product of the pseudo-inverse, which has no epilogue to hide.
 // ============================================================================
-__global__ void __launch_bounds__(kGemmThreads, 1)
+template <int BN>
+__global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
     hidden_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, HiddenParams p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = align1024(smem_raw);
   double* Xs = reinterpret_cast<double*>(smem);        // [stage][128 rows][16] swizzled
-  double* Ws = Xs + kStages * kTile * kBK;             // [stage][16][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(Ws + kStages * kBK * kTile);
+  double* Ws = Xs + kStages * kTile * kBK;             // [stage][16][BN]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Ws + kStages * kBK * BN);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int l0 = blockIdx.x * kTile, n0 = blockIdx.y * kTile;
+  const int l0 = blockIdx.x * BN, n0 = blockIdx.y * kTile;
   const int ktiles = (p.d + kBK - 1) / kBK;
-  constexpr uint32_t kStageBytes = 2u * kTile * kBK * sizeof(double);
+  constexpr uint32_t kStageBytes = (kTile + BN) * kBK * sizeof(double);
 
   if (tid == 0) {
     tma_prefetch_desc(&tmX);
@@ -65,14 +84,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int s = 0; s < kStages && s < ktiles; ++s) {
       mbar_arrive_expect_tx(&full[s], kStageBytes);
       tma_load_2d(Xs + s * kTile * kBK, &tmX, &full[s], s * kBK, n0);
-      tma_load_2d(Ws + s * kBK * kTile, &tmW, &full[s], l0, s * kBK);
+      tma_load_2d(Ws + s * kBK * BN, &tmW, &full[s], l0, s * kBK);
     }
   }
 
-  const int wm = (warp >> 2) * 64, wn = (warp & 3) * 32;
-  double acc[4][4][4];
+  // warp tile: 64 x 32 (BN = 128: 2 x 4 warps) or 32 x 32 (BN = 64: 4 x 2 warps)
+  constexpr int MT = BN == 128 ? 4 : 2;
+  constexpr int WARPS_N = BN / 32;
+  const int wm = (warp / WARPS_N) * (MT * 16), wn = (warp % WARPS_N) * 32;
+  double acc[MT][4][4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
@@ -82,25 +104,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int s = kt % kStages;
     mbar_wait(&full[s], (kt / kStages) & 1);
     const double* xs = Xs + s * kTile * kBK;
-    const double* ws = Ws + s * kBK * kTile;
+    const double* ws = Ws + s * kBK * BN;
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
       const int kc = ks * 4 + t;
-      double a[4][2], b[4];
+      double a[MT][2], b[4];
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) {
+      for (int mt = 0; mt < MT; ++mt) {
         const int r = wm + mt * 16 + g;
         a[mt][0] = xs[swz16(r, kc)];
         a[mt][1] = xs[swz16(r + 8, kc)];
       }
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp) {
-        const double2 w = *reinterpret_cast<const double2*>(ws + kc * kTile + wn + pp * 16 + 2 * g);
+        const double2 w = *reinterpret_cast<const double2*>(ws + kc * BN + wn + pp * 16 + 2 * g);
         b[2 * pp] = w.x;
         b[2 * pp + 1] = w.y;
       }
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
     }
@@ -109,13 +131,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int kn = kt + kStages;
       mbar_arrive_expect_tx(&full[s], kStageBytes);
       tma_load_2d(Xs + s * kTile * kBK, &tmX, &full[s], kn * kBK, n0);
-      tma_load_2d(Ws + s * kBK * kTile, &tmW, &full[s], l0, kn * kBK);
+      tma_load_2d(Ws + s * kBK * BN, &tmW, &full[s], l0, kn * kBK);
     }
   }
 
   if (p.transposed) {  // plain product stored transposed: H[c][r] (pseudo-inverse H^+ = G^-1 H^T)
 #pragma unroll
-    for (int mt = 0; mt < 4; ++mt)
+    for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
@@ -137,7 +159,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   // epilogue: bias after the full dot product, then sigmoid (elm.cpp:102, :27)
 #pragma unroll
-  for (int mt = 0; mt < 4; ++mt) {
+  for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
       const int cb = l0 + wn + pp * 16 + 4 * t;
@@ -152,7 +174,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int q = 0; q < 4; ++q) {
           const int c = cb + q;
           const double z = add_rn(v[q], c < p.L ? p.bias[c] : 0.0);
-          h[q] = 1.0 / (1.0 + exp(-z));
+          h[q] = recip_ge1(1.0 + exp(-z));
         }
         double* dst = p.H + (long long)r * p.ldh + cb;
         if (cb + 3 < p.L) {
@@ -487,14 +509,21 @@ __global__ void __launch_bounds__(128) gemm_kernel(GemmParams p) {
 // ============================================================================
 // launchers
 // ============================================================================
-cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const HiddenParams& p, cudaStream_t s) {
+// bn = 64 (sigmoid build, two CTAs per SM) or 128 (plain transposed product); tmW's box is {bn, kBK}
+cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const HiddenParams& p, int bn,
+                          cudaStream_t s) {
   static bool attr = false;
+  constexpr size_t kSmem64 = size_t(kStages) * (kTile + 64) * kBK * sizeof(double) + 1024 + 256;
   if (!attr) {
-    cudaFuncSetAttribute(hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+    cudaFuncSetAttribute(hidden_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+    cudaFuncSetAttribute(hidden_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem64);
     attr = true;
   }
-  dim3 grid((p.L + kTile - 1) / kTile, (p.N + kTile - 1) / kTile);
-  hidden_kernel<<<grid, kGemmThreads, kTmaSmemBytes, s>>>(tmX, tmW, p);
+  dim3 grid((p.L + bn - 1) / bn, (p.N + kTile - 1) / kTile);
+  if (bn == 64)
+    hidden_kernel<64><<<grid, kGemmThreads, kSmem64, s>>>(tmX, tmW, p);
+  else
+    hidden_kernel<128><<<grid, kGemmThreads, kTmaSmemBytes, s>>>(tmX, tmW, p);
   return cudaGetLastError();
 }
 
