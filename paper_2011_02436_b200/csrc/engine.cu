@@ -92,6 +92,8 @@ struct rbpg_context {
   int device = 0;
   int num_sms = 148;
   cudaStream_t own = nullptr;
+  cudaStream_t copy = nullptr;  // host -> device input uploads, overlapped with the hidden build
+  cudaEvent_t chunk_ev[8] = {};
   cudaStream_t stream = nullptr;
   std::map<std::string, std::pair<void*, size_t>> bufs;
   uint64_t launches = 0;
@@ -802,16 +804,24 @@ Padded pad_device(rbpg_context* ctx, const std::string& name, const double* d, s
   ck(cudaMemcpy2DAsync(q, nld * 8, d, ld * 8, cols * 8, rows, cudaMemcpyDeviceToDevice, ctx->stream), "pad copy");
   return {q, nld};
 }
+// host <-> device copies: one linear transfer when the rows are contiguous on both sides (a pitched
+// 2D copy of many short rows runs at a fraction of the link bandwidth)
+void copy_rows(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+               cudaMemcpyKind kind, cudaStream_t s, const char* what) {
+  if (!rows || !width) return;
+  if (dpitch == width && spitch == width)
+    ck(cudaMemcpyAsync(dst, src, width * rows, kind, s), what);
+  else
+    ck(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, s), what);
+}
 Padded upload(rbpg_context* ctx, const std::string& name, const double* h, size_t rows, size_t cols) {
   const size_t ld = even(cols);
   double* q = ctx->dbuf(name, std::max<size_t>(1, rows) * ld);
-  if (rows && cols)
-    ck(cudaMemcpy2DAsync(q, ld * 8, h, cols * 8, cols * 8, rows, cudaMemcpyHostToDevice, ctx->stream), "upload");
+  copy_rows(q, ld * 8, h, cols * 8, cols * 8, rows, cudaMemcpyHostToDevice, ctx->stream, "upload");
   return {q, ld};
 }
 void download(rbpg_context* ctx, double* h, const double* d, size_t ld, size_t rows, size_t cols) {
-  if (rows && cols)
-    ck(cudaMemcpy2DAsync(h, cols * 8, d, ld * 8, cols * 8, rows, cudaMemcpyDeviceToHost, ctx->stream), "download");
+  copy_rows(h, cols * 8, d, ld * 8, cols * 8, rows, cudaMemcpyDeviceToHost, ctx->stream, "download");
   ck(cudaStreamSynchronize(ctx->stream), "sync");
 }
 
@@ -826,9 +836,16 @@ size_t h_chunk_rows(rbpg_context* ctx, size_t N, size_t ldh) {
 // The Gram is taken of the augmented rows [H | T] (N x (L+m)): its lower triangle holds H^T H and,
 // mirrored, H^T T = Gaug[0:L, L:L+m], so the H^T T product rides in the SYRK's last tile row
 // instead of 128-wide tiles that would carry only m useful columns.
+// `ready` (optional): row blocks of X/T still being uploaded, as (end row, event recorded after the
+// block's copy); the hidden build then runs per block behind its upload (one Gram over all rows).
+struct RowReady {
+  size_t end;
+  cudaEvent_t ev;
+};
 float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* dT, size_t ldt_in, size_t N,
                  size_t d, size_t L, size_t m, const double* dW, size_t ldw, const double* db, double* dGaug,
-                 size_t ldga, bool accumulate, bool keep_h, bool timed) {
+                 size_t ldga, bool accumulate, bool keep_h, bool timed,
+                 const std::vector<RowReady>* ready = nullptr) {
   const size_t M = L + m;
   const size_t ldh = even(M);
   const size_t chunk = std::max<size_t>(1, h_chunk_rows(ctx, std::max<size_t>(N, 1), ldh));
@@ -836,6 +853,27 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
   float hidden_ms = 0.f;
   if (N == 0) {
     gram_dev(ctx, dH, ldh, 0, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate);
+    return 0.f;
+  }
+  if (ready && chunk >= N) {
+    if (timed) cudaEventRecord(ctx->ev[0], ctx->stream);
+    size_t r0 = 0;
+    for (const RowReady& rr : *ready) {
+      ck(cudaStreamWaitEvent(ctx->stream, rr.ev, 0), "wait upload");
+      hidden_dev(ctx, dX + r0 * ldx, ldx, rr.end - r0, d, dW, ldw, db, L, dH + r0 * ldh, ldh, dT + r0 * ldt_in,
+                 ldt_in, m);
+      r0 = rr.end;
+    }
+    if (timed) cudaEventRecord(ctx->ev[1], ctx->stream);
+    gram_dev(ctx, dH, ldh, N, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate);
+    if (keep_h) {
+      ctx->kept_h = dH;
+      ctx->kept_n = N;
+      ctx->kept_l = L;
+      ctx->kept_ldh = ldh;
+    } else {
+      ctx->kept_h = nullptr;
+    }
     return 0.f;
   }
   for (size_t r0 = 0; r0 < N; r0 += chunk) {
@@ -927,12 +965,16 @@ uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const d
 // train() body on device-resident X, T (elm.cpp:231-280 after validation and init_hidden)
 void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* dT, size_t ldt_in, size_t N, size_t d,
                 size_t L, size_t m, const double* w, const double* b, const rbpg_strategy& sg, double* dBeta,
-                size_t ldb, size_t* order_out, rbpg_diagnostics* diag) {
+                size_t ldb, size_t* order_out, rbpg_diagnostics* diag,
+                const std::vector<RowReady>* ready = nullptr, bool wb_uploaded = false) {
   Padded X = pad_device(ctx, "X.pad", dX, ldx, N, d);
   Padded T = pad_device(ctx, "T.pad", dT, ldt_in, N, m);
-  Padded W = upload(ctx, "W", w, d, L);
+  Padded W{ctx->dbuf("W", std::max<size_t>(1, d) * even(L)), even(L)};
   double* db = ctx->dbuf("b", L);
-  ck(cudaMemcpyAsync(db, b, L * 8, cudaMemcpyHostToDevice, ctx->stream), "upload b");
+  if (!wb_uploaded) {  // else already on the device (uploaded by the caller ahead of the inputs)
+    W = upload(ctx, "W", w, d, L);
+    ck(cudaMemcpyAsync(db, b, L * 8, cudaMemcpyHostToDevice, ctx->stream), "upload b");
+  }
   // augmented Gram [H T]^T [H T]: G = Gaug[0:L, 0:L], H^T T = Gaug[0:L, L:L+m] (same ld)
   const size_t ldg = round_up(L + m, 8), ldt = ldg;
   double* G = ctx->dbuf("G0", (L + m) * ldg);
@@ -940,7 +982,7 @@ void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* d
 
   const auto wall0 = std::chrono::steady_clock::now();
   cudaEventRecord(ctx->ev[2], ctx->stream);
-  float hidden_ms = gram_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, G, ldg, false, true, true);
+  float hidden_ms = gram_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, G, ldg, false, true, true, ready);
   {
     // [H T] stays resident (unless H exceeded the memory budget) for solve_direct's SVD branch
     const bool kept = ctx->kept_h && ctx->kept_n == N;
@@ -1081,6 +1123,8 @@ int rbpg_context_create(int device, rbpg_context** out, rbpg_status* st) {
     c->device = device;
     c->num_sms = prop.multiProcessorCount;
     ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking), "copy stream");
+    for (auto& e : c->chunk_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     c->stream = c->own;
     for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
     void* fn = nullptr;
@@ -1097,10 +1141,13 @@ void rbpg_context_destroy(rbpg_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->copy);
   for (auto& kv : ctx->bufs) cudaFree(kv.second.first);
   for (auto& kv : ctx->hbufs) cudaFreeHost(kv.second.first);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
+  for (auto& e : ctx->chunk_ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->own);
+  cudaStreamDestroy(ctx->copy);
   delete ctx;
 }
 
@@ -1325,14 +1372,56 @@ int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, 
     if (strategy->kind == RBPG_DF_SPLIT && (strategy->split_index < 1 || strategy->split_index >= hidden))
       fail(RBPG_INVALID_ARGUMENT, "train: df split index must be in (0, " + std::to_string(hidden) + "), got " +
                                       std::to_string(strategy->split_index));
-    rbpg_status s2;
-    if (rbpg_init_hidden(inputs, hidden, outputs, seed, w, b, &s2)) fail(s2.code, s2.message);
-    Padded X = upload(ctx, "X.in", x, n, xcols);
-    Padded T = upload(ctx, "T.in", y, n, ycols);
+    static const bool htrace = std::getenv("RBPG_HOST_TRACE") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    const auto h0 = now();
+    // X and T go up in row blocks on the copy stream; the hidden build of each block waits only for
+    // its own upload, and W, b are generated on the host meanwhile
+    const size_t ldx = even(xcols), ldy = even(ycols);
+    double* dX = ctx->dbuf("X.in", std::max<size_t>(1, n) * ldx);
+    double* dY = ctx->dbuf("T.in", std::max<size_t>(1, n) * ldy);
+    std::vector<RowReady> ready;
+    {
+      const size_t nblk = std::min<size_t>(4, std::max<size_t>(1, n / 8192));
+      const size_t per = round_up((n + nblk - 1) / nblk, kTile);
+      ck(cudaEventRecord(ctx->chunk_ev[7], ctx->stream), "event");  // buffers free (prior work done)
+      ck(cudaStreamWaitEvent(ctx->copy, ctx->chunk_ev[7], 0), "wait");
+      for (size_t r0 = 0, i = 0; r0 < n; r0 += per, ++i) {
+        const size_t nr = std::min(per, n - r0);
+        copy_rows(dX + r0 * ldx, ldx * 8, x + r0 * xcols, xcols * 8, xcols * 8, nr, cudaMemcpyHostToDevice,
+                  ctx->copy, "upload X");
+        copy_rows(dY + r0 * ldy, ldy * 8, y + r0 * ycols, ycols * 8, ycols * 8, nr, cudaMemcpyHostToDevice,
+                  ctx->copy, "upload Y");
+        if (i == 0) {  // W, b generated on the host while block 0 is in flight, then queued behind it
+          rbpg_status s2;
+          if (rbpg_init_hidden(inputs, hidden, outputs, seed, w, b, &s2)) fail(s2.code, s2.message);
+          double* dW = ctx->dbuf("W", inputs * even(hidden));
+          copy_rows(dW, even(hidden) * 8, w, hidden * 8, hidden * 8, inputs, cudaMemcpyHostToDevice, ctx->copy,
+                    "upload W");
+          ck(cudaMemcpyAsync(ctx->dbuf("b", hidden), b, hidden * 8, cudaMemcpyHostToDevice, ctx->copy), "upload b");
+        }
+        ck(cudaEventRecord(ctx->chunk_ev[i], ctx->copy), "event");
+        ready.push_back({r0 + nr, ctx->chunk_ev[i]});
+      }
+    }
+    if (ready.empty()) {  // no rows: W, b were not generated inside the loop
+      rbpg_status s2;
+      if (rbpg_init_hidden(inputs, hidden, outputs, seed, w, b, &s2)) fail(s2.code, s2.message);
+    }
+    const auto h1 = now();
+    const auto h2 = now();
     const size_t lb = even(outputs);
     double* B = ctx->dbuf("beta", hidden * lb);
-    train_core(ctx, X.p, X.ld, T.p, T.ld, n, inputs, hidden, outputs, w, b, *strategy, B, lb, order, diag);
+    train_core(ctx, dX, ldx, dY, ldy, n, inputs, hidden, outputs, w, b, *strategy, B, lb, order, diag, &ready,
+               !ready.empty());
+    const auto h3 = now();
     download(ctx, beta, B, lb, hidden, outputs);
+    const auto h4 = now();
+    if (htrace) {
+      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "[train host] init %.3f upload %.3f core %.3f download %.3f ms\n", ms(h0, h1), ms(h1, h2),
+                   ms(h2, h3), ms(h3, h4));
+    }
   });
 }
 
