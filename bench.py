@@ -209,7 +209,6 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    ctx.set_profiling(True)
     launches0 = ctx.launch_count
     with ClockSampler(local) as clk:
         for i in range(args.steps):
@@ -222,6 +221,13 @@ def main():
     if world > 1:
         dist.barrier()
     ms = sum(a.elapsed_time(b) for a, b in ev)
+    # per-kernel breakdown from a separate pass with per-launch events (events between launches
+    # would serialise the programmatic dependent launches of the timed steps)
+    ctx.set_profiling(True)
+    for i in range(args.steps):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
     syrk_ms, syrk_n = ctx.profile("syrk_kernel")
     hid_ms, hid_n = ctx.profile("hidden_kernel")
     panel_ms, panel_n = ctx.profile("panel_kernel")

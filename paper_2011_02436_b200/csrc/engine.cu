@@ -30,7 +30,7 @@
 namespace rbpg {
 void trsm_trace_dump();
 cudaError_t launch_hidden(const CUtensorMap&, const CUtensorMap&, const HiddenParams&, int, cudaStream_t);
-cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams&, int, int, cudaStream_t);
+cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams&, int, int, cudaStream_t, bool = false);
 cudaError_t launch_syrk_finish(const SyrkParams&, int, int, int, cudaStream_t);
 cudaError_t launch_gemm(const GemmParams&, cudaStream_t);
 cudaError_t launch_scores(const CUtensorMap&, const CUtensorMap&, const ScoresParams&, cudaStream_t);
@@ -420,7 +420,7 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
       sp.Gold = gcur;
       sp.lab = lab;
       sp.off = static_cast<int>(t0);
-      ctx->run("syrk_trailing", [&] { return launch_syrk(tm, tm, sp, 1, ttile, s); });
+      ctx->run("syrk_trailing", [&] { return launch_syrk(tm, tm, sp, 1, ttile, s, true); });
       std::swap(gcur, gnext);
     }
     cur = 1 - cur;

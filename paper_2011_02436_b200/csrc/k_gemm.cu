@@ -237,6 +237,8 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
+  pdl_trigger();
+  pdl_wait();  // trailing mode: the panel that wrote PcT / lab may still be finishing
   __syncthreads();
   if (tid == 0) {
     for (int s = 0; s < kStages && s < ktiles; ++s) {
@@ -530,28 +532,40 @@ cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
 // tile = 128 (256 threads, 1 CTA/SM: the Gram) or 64 (128 threads, several CTAs/SM: small
 // trailing updates, where 128-wide tiles would leave most SMs idle).  The tensor maps' boxes
 // must be {tile, kBK}.
+// pdl: launch as a programmatic dependent of the preceding kernel in the stream (trailing updates
+// behind a panel)
 cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const SyrkParams& p, int splits, int tile,
-                        cudaStream_t s) {
-  dim3 grid(p.nGram + p.nbI * p.nbT, splits);
+                        cudaStream_t s, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.nGram + p.nbI * p.nbT, splits);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
   if (tile == 128) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(syrk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
       attr = true;
     }
-    syrk_kernel<128><<<grid, 256, kTmaSmemBytes, s>>>(tmA, tmB, p);
-  } else if (tile == 64) {
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kTmaSmemBytes;
+    return cudaLaunchKernelEx(&cfg, syrk_kernel<128>, tmA, tmB, p);
+  }
+  if (tile == 64) {
     constexpr size_t smem = size_t(kStages) * 2 * 64 * kBK * sizeof(double) + 1024 + 256;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(syrk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr = true;
     }
-    syrk_kernel<64><<<grid, 128, smem, s>>>(tmA, tmB, p);
-  } else {
-    return cudaErrorInvalidValue;
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = smem;
+    return cudaLaunchKernelEx(&cfg, syrk_kernel<64>, tmA, tmB, p);
   }
-  return cudaGetLastError();
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_syrk_finish(const SyrkParams& p, int splits, int accumulate, int num_sms, cudaStream_t s) {

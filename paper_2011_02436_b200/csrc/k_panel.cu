@@ -463,6 +463,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   __shared__ unsigned long long s_wkey;
   __shared__ int s_piv, s_xp, s_y, s_src;
 
+  pdl_trigger();
+  pdl_wait();  // the previous trailing update / panel may still be finishing
   FactorState* st = p.st;
   if (st->stopped) {
     if (cta == 0)
@@ -764,13 +766,15 @@ cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cuda
     cfg.blockDim = dim3(kPThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     if (ctas_used) *ctas_used = CL;
     return cudaLaunchKernelEx(&cfg, panel_reg_kernel, pp);
   }
