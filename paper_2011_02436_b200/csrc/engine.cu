@@ -37,7 +37,8 @@ cudaError_t launch_scores(const CUtensorMap&, const CUtensorMap&, const ScoresPa
 cudaError_t launch_factor_setup(const double*, long long, int, int, long long, double, int, double*, int*,
                                 FactorState*, cudaStream_t);
 cudaError_t launch_panel(const PanelParams&, int, int*, cudaStream_t);
-cudaError_t launch_gather_factor(const double*, long long, const int*, int, double*, long long, int, cudaStream_t);
+cudaError_t launch_gather_factor(const double*, long long, const int*, int, double*, long long, const FactorState*,
+                                 int, cudaStream_t);
 cudaError_t launch_gather_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
 cudaError_t launch_scatter_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
 cudaError_t launch_trsm_pair(const double*, long long, double*, long long, int, int, int, int, int, double*,
@@ -359,27 +360,30 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
   PivotSlot* slots = static_cast<PivotSlot*>(ctx->buf(tag + ".slots", sizeof(PivotSlot) * 2 * (max_ctas + 32)));
   FactorState* st = static_cast<FactorState*>(ctx->buf(tag + ".state", sizeof(FactorState)));
 
-  ck(cudaMemsetAsync(Fo, 0, sizeof(double) * n * ldn, s), "memset Fo");
+
   unsigned long long* trace = nullptr;
   if (std::getenv("RBPG_PANEL_TRACE")) {
     trace = static_cast<unsigned long long*>(ctx->buf(tag + ".ptrace", 64));
     ck(cudaMemsetAsync(trace, 0, 64, s), "memset trace");
   }
-  ck(cudaMemsetAsync(Pg, 0, sizeof(double) * n * 64, s), "memset Pg");
-  ck(cudaMemsetAsync(slots, 0, sizeof(PivotSlot) * 2 * (max_ctas + 32), s), "memset slots");
-  ck(cudaMemcpy2DAsync(Ga, ldn * 8, dG, ldg * 8, n * 8, n, cudaMemcpyDeviceToDevice, s), "copy G");
+  if (n > 4096) {  // the grid panel variant's global mirror and exchange slots
+    ck(cudaMemsetAsync(Pg, 0, sizeof(double) * n * 64, s), "memset Pg");
+    ck(cudaMemsetAsync(slots, 0, sizeof(PivotSlot) * 2 * (max_ctas + 32), s), "memset slots");
+  }
   ctx->run("factor_setup", [&] {
-    return launch_factor_setup(Ga, static_cast<long long>(ldn), static_cast<int>(n), static_cast<int>(neligible),
+    return launch_factor_setup(dG, static_cast<long long>(ldg), static_cast<int>(n), static_cast<int>(neligible),
                                static_cast<long long>(rows_for_tol), tol, pivoting, dv[0], ov[0], st, s);
   });
-  double* gcur = Ga;
-  double* gnext = Gb;
+  // the first panel and trailing update read the caller's G in place; later ones ping-pong Ga / Gb
+  const double* gcur = dG;
+  size_t ldcur = ldg;
+  double* gnext = Ga;
   int cur = 0;
   for (size_t k = 0; k < neligible; k += 64) {
     const int kb = static_cast<int>(std::min<size_t>(64, neligible - k));
     PanelParams pp{};
     pp.G = gcur;
-    pp.ldg = static_cast<long long>(ldn);
+    pp.ldg = static_cast<long long>(ldcur);
     pp.d_in = dv[cur];
     pp.d_out = dv[1 - cur];
     pp.ord_in = ov[cur];
@@ -418,15 +422,19 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
       sp.G = gnext;
       sp.ldg = static_cast<long long>(ldn);
       sp.Gold = gcur;
+      sp.ldgo = static_cast<long long>(ldcur);
       sp.lab = lab;
       sp.off = static_cast<int>(t0);
       ctx->run("syrk_trailing", [&] { return launch_syrk(tm, tm, sp, 1, ttile, s, true); });
-      std::swap(gcur, gnext);
+      double* written = gnext;
+      gnext = (written == Ga) ? Gb : Ga;
+      gcur = written;
+      ldcur = ldn;
     }
     cur = 1 - cur;
   }
   ctx->run("gather_factor", [&] { return launch_gather_factor(Fo, static_cast<long long>(ldn), ov[cur], static_cast<int>(n), F,
-                                static_cast<long long>(ldn), ctx->num_sms, s); });
+                                static_cast<long long>(ldn), st, ctx->num_sms, s); });
   FactorResult r;
   r.dst = st;
   // pinned staging so the state copy is truly asynchronous (sync = false: the caller reads it later)

@@ -74,12 +74,15 @@ __global__ void factor_setup_kernel(const double* G, long long ldg, int n, int n
 }
 
 // factor rows by final position: F[a][:] = Fo[order[a]][:]
+// F[a][c] = Fo[ord[a]][c] on the computed part (c <= a, c < rank); zero elsewhere, so Fo needs no
+// clearing (entries above the diagonal or past an early stop are never written by the panels)
 __global__ void gather_factor_kernel(const double* Fo, long long ldf, const int* ord, int n, double* F,
-                                     long long ldF) {
+                                     long long ldF, const FactorState* st) {
+  const long long r = st->rank;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)n * n;
        e += (long long)gridDim.x * blockDim.x) {
     const long long a = e / n, c = e % n;
-    F[a * ldF + c] = Fo[(long long)ord[a] * ldf + c];
+    F[a * ldF + c] = (c <= a && c < r) ? Fo[(long long)ord[a] * ldf + c] : 0.0;
   }
 }
 
@@ -188,8 +191,9 @@ cudaError_t launch_factor_setup(const double* G, long long ldg, int n, int nelig
 }
 
 cudaError_t launch_gather_factor(const double* Fo, long long ldf, const int* ord, int n, double* F, long long ldF,
+                                 const FactorState* st,
                                  int num_sms, cudaStream_t s) {
-  gather_factor_kernel<<<num_sms * 4, 256, 0, s>>>(Fo, ldf, ord, n, F, ldF);
+  gather_factor_kernel<<<num_sms * 4, 256, 0, s>>>(Fo, ldf, ord, n, F, ldF, st);
   return cudaGetLastError();
 }
 

@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             gold[mt][pp][h][q] =
-                (r < p.M && c0 + q < p.M && c0 + q <= r) ? __ldg(p.Gold + (long long)sr * p.ldg + sc[q]) : 0.0;
+                (r < p.M && c0 + q < p.M && c0 + q <= r) ? __ldg(p.Gold + (long long)sr * p.ldgo + sc[q]) : 0.0;
         }
       }
   }
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
               val = sub_rn(gold[mt][pp][h][q], val);
             } else {
               const int sr = p.lab[off + r], sc = p.lab[off + c];
-              val = sub_rn(p.Gold[(long long)sr * p.ldg + sc], val);
+              val = sub_rn(p.Gold[(long long)sr * p.ldgo + sc], val);
             }
           }
           p.G[(long long)(off + r) * p.ldg + off + c] = val;

@@ -51,6 +51,7 @@ struct SyrkParams {
   double* wsT;           // partial HtT: wsT + s*wsTStride (ld = ldt)
   long long wsTStride;
   const double* Gold;    // trailing: source Gram (panel-start coordinates)
+  long long ldgo;        // trailing: leading dimension of Gold
   const int* lab;        // trailing: lab[p] = source index of position p (absolute)
   int off;               // trailing: first trailing position
 };
