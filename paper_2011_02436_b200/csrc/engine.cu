@@ -302,6 +302,7 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
   CUtensorMap tmA = make_map(ctx, dA, L, N, lda, kTile, kBK, false);
   CUtensorMap tmB = m > 0 ? make_map(ctx, dT, m, N, ldt_in, kTile, kBK, false) : tmA;
   ctx->run("syrk_kernel", [&] { return launch_syrk(tmA, tmB, p, splits, kTile, ctx->stream); });
+  if (p.nbI >= 2) ++ctx->launches;  // diagonal + off-diagonal grids
   if (!direct) ctx->run("syrk_finish", [&] { return launch_syrk_finish(p, splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
 }
 

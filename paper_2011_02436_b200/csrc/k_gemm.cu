@@ -194,7 +194,9 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
 // K2: SYRK-TN family.  A (kRows x M) row-major via tmA; B = A for Gram tiles,
 // B = T (kRows x mB) via tmB for the H^T T tiles.
 // ============================================================================
-template <int TILE>
+// PART 0: every lower tile (+ T tiles).  PART 1: off-diagonal lower tiles (+ T tiles) only -- the
+// diagonal ones go to syrk_diag_kernel, which this grid overlaps as its programmatic dependent.
+template <int TILE, int PART = 0>
 __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
     syrk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SyrkParams p) {
   extern __shared__ unsigned char smem_raw[];
@@ -209,15 +211,17 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
   const int bx = blockIdx.x;
   int I, J;
   bool isT;
-  if (bx < p.nGram) {
+  const int nLower = PART == 1 ? p.nbI * (p.nbI - 1) / 2 : p.nGram;
+  if (bx < nLower) {
     int i = static_cast<int>((sqrt(8.0 * bx + 1.0) - 1.0) * 0.5);
     while (i * (i + 1) / 2 > bx) --i;
     while ((i + 1) * (i + 2) / 2 <= bx) ++i;
     I = i;
     J = bx - i * (i + 1) / 2;
+    if (PART == 1) ++I;  // strictly lower: tile (i + 1, j), j <= i
     isT = false;
   } else {
-    const int tt = bx - p.nGram;
+    const int tt = bx - nLower;
     I = tt / p.nbT;
     J = tt % p.nbT;
     isT = true;
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
     fence_mbar_init();
   }
   pdl_trigger();
-  pdl_wait();  // trailing mode: the panel that wrote PcT / lab may still be finishing
+  if (PART == 0) pdl_wait();  // trailing mode: the panel that wrote PcT / lab may still be finishing
   __syncthreads();
   if (tid == 0) {
     for (int s = 0; s < kStages && s < ktiles; ++s) {
@@ -296,6 +300,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
 
   // ---- epilogue.  Thread holds rows r, r+1 (r even) x cols c..c+3 per (mt, pp).
   const int split = blockIdx.y;
+  if (PART == 1) pdl_wait();  // this grid completes only after the diagonal-tile grid
   // trailing mode: every G_old gather is issued before the first store (the stores could alias
   // the loads as far as the compiler knows, which would serialise one L2 round trip per element)
   // (64-wide tiles only: the 128-wide kernel has no registers to spare for the staging)
@@ -390,6 +395,115 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
           p.G[(long long)(off + c) * p.ldg + off + r] = val;
         }
       }
+    }
+  }
+}
+
+// One 16-deep k-slab of a diagonal 128-wide Gram tile for warp (DS, DH): its 9 lower-triangle
+// (m16, n8) fragments -- row groups DS and 7 - DS of SMSP DS, split 9 / 9 between the SMSP's two
+// warps -- accumulate into acc[i].
+template <int DS, int DH>
+__device__ __forceinline__ void diag_step(double (&acc)[9][4], const double* as, const double* bs, int g, int t) {
+#pragma unroll
+  for (int ks = 0; ks < kBK / 4; ++ks) {
+    const int kc = ks * 4 + t;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      constexpr int kFirst = 2 * DS + 2;
+      const int q = 9 * DH + i;
+      const int mt = q < kFirst ? DS : 7 - DS;
+      const int nt = q < kFirst ? q : q - kFirst;
+      const double2 a = *reinterpret_cast<const double2*>(as + kc * 128 + mt * 16 + 2 * g);
+      const double2 bw = *reinterpret_cast<const double2*>(bs + kc * 128 + (nt >> 1) * 16 + 2 * g);
+      dmma_16x8x4(acc[i], a.x, a.y, (nt & 1) ? bw.y : bw.x);
+    }
+  }
+}
+
+// Diagonal 128 x 128 Gram tiles (direct or split-K partial): only the 72 of 128 (m16, n8) fragments
+// that touch the lower triangle are computed.  SMSP s = warp & 3 owns row groups s and 7 - s
+// (18 fragments each: equal tensor-pipe work per SMSP), split 9 / 9 between its two warps.  Every
+// element sees the same DMMA k-sequence as in a full tile (exact twin ties survive).
+template <int DS, int DH>
+__device__ __forceinline__ void diag_tile_loop(double (&acc)[9][4], double* As, double* Bs,
+                                               uint64_t* full, const CUtensorMap* tmA, int i0, long long kbeg,
+                                               int ktiles, int tid, int g, int t) {
+  constexpr uint32_t kStageBytes = 2u * 128 * kBK * sizeof(double);
+  for (int kt = 0; kt < ktiles; ++kt) {
+    const int s = kt % kStages;
+    mbar_wait(&full[s], (kt / kStages) & 1);
+    diag_step<DS, DH>(acc, As + s * kBK * 128, Bs + s * kBK * 128, g, t);
+    __syncthreads();
+    if (tid == 0 && kt + kStages < ktiles) {
+      const int kr = static_cast<int>(kbeg + (long long)(kt + kStages) * kBK);
+      mbar_arrive_expect_tx(&full[s], kStageBytes);
+      tma_load_2d(As + s * kBK * 128, tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * 128, tmA, &full[s], i0, kr);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256, 1)
+    syrk_diag_kernel(const __grid_constant__ CUtensorMap tmA, SyrkParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = align1024(smem_raw);
+  double* As = reinterpret_cast<double*>(smem);
+  double* Bs = As + kStages * kBK * 128;
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBK * 128);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int I = blockIdx.x, i0 = I * 128;
+  const long long kbeg = (long long)blockIdx.y * p.kPerSplit;
+  long long kend = kbeg + p.kPerSplit;
+  if (kend > p.kRows) kend = p.kRows;
+  const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kBK - 1) / kBK) : 0;
+  constexpr uint32_t kStageBytes = 2u * 128 * kBK * sizeof(double);
+  if (tid == 0) {
+    tma_prefetch_desc(&tmA);
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  pdl_trigger();  // the off-diagonal grid may start right away (no data dependency)
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < kStages && s < ktiles; ++s) {
+      const int kr = static_cast<int>(kbeg + s * kBK);
+      mbar_arrive_expect_tx(&full[s], kStageBytes);
+      tma_load_2d(As + s * kBK * 128, &tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * 128, &tmA, &full[s], i0, kr);
+    }
+  }
+  double acc[9][4];
+#pragma unroll
+  for (int i = 0; i < 9; ++i)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
+  switch (warp) {  // compile-time fragment lists per warp
+    case 0: diag_tile_loop<0, 0>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
+    case 1: diag_tile_loop<1, 0>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
+    case 2: diag_tile_loop<2, 0>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
+    case 3: diag_tile_loop<3, 0>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
+    case 4: diag_tile_loop<0, 1>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
+    case 5: diag_tile_loop<1, 1>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
+    case 6: diag_tile_loop<2, 1>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
+    default: diag_tile_loop<3, 1>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
+  }
+  // fragment (mt, nt): MMA row g / g+8 <-> tile row mt*16 + 2g / +1; MMA col j <-> tile col
+  // (nt >> 1) * 16 + 2j + (nt & 1); lower elements only (mirrored in direct mode)
+  const int ds = warp & 3, dh = warp >> 2;
+  double* out = (p.mode == kSyrkPartial) ? p.ws + blockIdx.y * p.wsStride : p.G;
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const int q = 9 * dh + i;
+    const bool first = q < 2 * ds + 2;
+    const int mt = first ? ds : 7 - ds;
+    const int nt = first ? q : q - (2 * ds + 2);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = i0 + mt * 16 + 2 * g + (e >> 1);
+      const int c = i0 + (nt >> 1) * 16 + 2 * (2 * t + (e & 1)) + (nt & 1);
+      if (r >= p.M || c > r) continue;
+      out[(long long)r * p.ldg + c] = acc[i][e];
+      if (p.mode != kSyrkPartial) out[(long long)c * p.ldg + r] = acc[i][e];
     }
   }
 }
@@ -536,6 +650,30 @@ cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
 // behind a panel)
 cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const SyrkParams& p, int splits, int tile,
                         cudaStream_t s, bool pdl) {
+  if (tile == 128 && p.mode != kSyrkTrailing && p.nbI >= 2) {
+    // Gram: diagonal tiles by syrk_diag_kernel, the rest by syrk_kernel<128, 1> as its
+    // programmatic dependent (the two grids share the machine)
+    static bool dattr = false;
+    if (!dattr) {
+      cudaFuncSetAttribute(syrk_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+      cudaFuncSetAttribute(syrk_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+      dattr = true;
+    }
+    syrk_diag_kernel<<<dim3(p.nbI, splits), 256, kTmaSmemBytes, s>>>(tmA, p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t c2 = {};
+    c2.gridDim = dim3(p.nbI * (p.nbI - 1) / 2 + p.nbI * p.nbT, splits);
+    c2.blockDim = dim3(256);
+    c2.dynamicSmemBytes = kTmaSmemBytes;
+    c2.stream = s;
+    cudaLaunchAttribute a2[1];
+    a2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a2[0].val.programmaticStreamSerializationAllowed = 1;
+    c2.attrs = a2;
+    c2.numAttrs = 1;
+    return cudaLaunchKernelEx(&c2, syrk_kernel<128, 1>, tmA, tmB, p);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.nGram + p.nbI * p.nbT, splits);
   cfg.stream = s;
