@@ -460,8 +460,6 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   __shared__ __align__(8) uint64_t cand_full[2];
   __shared__ Cand wbest[kPWarps];
   __shared__ int s_stop;
-  __shared__ unsigned long long s_wkey;
-  __shared__ int s_piv, s_xp, s_y, s_src;
 
   pdl_trigger();
   pdl_wait();  // the previous trailing update / panel may still be finishing
@@ -558,40 +556,37 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   }
 
   long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  // Every warp resolves the winner itself from the exchanged candidates (no intra-CTA broadcast).
+  // The position swap of step c is written by tid 0 after step c's barrier, so a warp reading the
+  // maps during step c + 1 applies that last swap itself (pivp <-> jp, labels xpp / ypp).
+  int pivp = -1, xpp = -1, ypp = -1;
   for (int c = 0; c < kb; ++c) {
     const int j = k + c;
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
     if (p.trace) t0 = clock64();
-    if (warp == 0) {
-      if (lane == 0) mbar_arrive_expect_tx(&cand_full[c & 1], kStepBytes);
-      mbar_wait(&cand_full[c & 1], (c >> 1) & 1);
-      unsigned long long ck = 0;
-      int cp = INT_MAX;
-      if (lane < C) {
-        ck = cand_all[c & 1][lane].key;
-        cp = cand_all[c & 1][lane].pos;
-      }
-      unsigned long long wkey = ck;
-      int wpos = cp;
-      warp_argmax(wkey, wpos);
-      const int src = __ffs(__ballot_sync(0xffffffffu, lane < C && ck == wkey && cp == wpos)) - 1;
-      if (lane == 0) {
-        s_wkey = wkey;
-        s_piv = wpos;
-        s_xp = lab_at[wpos - k];
-        s_y = lab_at[j - k];
-        s_src = src;
-      }
-      named_bar_arrive(1, kPThreads);
-    } else {
-      named_bar_sync(1, kPThreads);
+    const int jp = j - 1;
+    auto lab_eff = [&](int ps) { return ps == jp ? xpp : (ps == pivp ? ypp : lab_at[ps - k]); };
+    auto pos_eff = [&](int lb) { return lb == xpp ? jp : (lb == ypp ? pivp : pos_of[lb - k]); };
+    const int mypos = mine ? pos_eff(x) : -1;   // before the exchange wait
+    const int y = lab_eff(j);
+    if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&cand_full[c & 1], kStepBytes);
+    mbar_wait(&cand_full[c & 1], (c >> 1) & 1);
+    unsigned long long ck = 0;
+    int cp = INT_MAX;
+    if (lane < C) {
+      ck = cand_all[c & 1][lane].key;
+      cp = cand_all[c & 1][lane].pos;
     }
+    unsigned long long wkey = ck;
+    int piv = cp;
+    warp_argmax(wkey, piv);
+    const int src = __ffs(__ballot_sync(0xffffffffu, lane < C && ck == wkey && cp == piv)) - 1;
+    const int xp = lab_eff(piv);
     if (p.trace) t1 = clock64();
-    const int piv = s_piv, xp = s_xp, y = s_y;
-    const double dj = dkey_inv(s_wkey);
+    const double dj = dkey_inv(wkey);
     // this quad's label: position after this step's swap and G entry (load issued first)
     int pos = -1;
-    if (mine) pos = (x == y) ? piv : (x == xp ? j : pos_of[x - k]);
+    if (mine) pos = (x == y) ? piv : (x == xp ? j : mypos);
     const bool alive = pos > j;
     const double gv = alive ? p.G[(long long)xp * p.ldg + x] : 0.0;
     bool stop;
@@ -630,7 +625,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
         p.trace[7] = 1;  // forces the G load and the reciprocal to complete before t2
       t2 = clock64();
     }
-    const double* prow = rows_all[c & 1][s_src];  // lane-major: prow[q*16 + i] = P[xp][q + 4i]
+    const double* prow = rows_all[c & 1][src];  // lane-major: prow[q*16 + i] = P[xp][q + 4i]
     // ---- update: dot over columns cc = q + 4i < c from registers.  Entries at and beyond c are
     // zero in both operands, so whole 16-column chunks are summed unpredicated; a chunk is skipped
     // (warp-uniform) once c <= its first column.
@@ -693,7 +688,9 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
       pos_of[xp - k] = j;
       pos_of[y - k] = piv;
     }
-    __syncwarp();
+    pivp = piv;
+    xpp = xp;
+    ypp = y;
   }
   __syncthreads();
   if (p.trace && cta == 0 && tid == 0)
