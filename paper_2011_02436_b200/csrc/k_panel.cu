@@ -497,7 +497,10 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   __syncthreads();
 
   // stage this warp's best row (the quad holding label position `pos`) into wrow[warp]
-  auto stage_row = [&](unsigned long long key, int pos, int mypos, unsigned long long mykey) {
+  // (the candidate's row is staged with this step's column `wv` patched in at `slot` when `wr`:
+  // the register copy itself is updated after the publication, off the critical path)
+  auto stage_row = [&](unsigned long long key, int pos, int mypos, unsigned long long mykey, bool wr, int slot,
+                       double wv) {
     const unsigned who = __ballot_sync(0xffffffffu, q == 0 && mykey == key && mypos == pos && pos != INT_MAX);
     if (who) {
       const int lead = __ffs(who) - 1;  // lane of the quad leader
@@ -505,6 +508,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
         double2* dst = reinterpret_cast<double2*>(&wrow[warp][q * kRowQ]);
 #pragma unroll
         for (int i = 0; i < 8; ++i) dst[i] = make_double2(pr[2 * i], pr[2 * i + 1]);
+        if (wr) wrow[warp][q * kRowQ + slot] = wv;  // this step's column (lane q == c & 3)
       }
     }
   };
@@ -546,7 +550,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const unsigned long long mk = key;
     const int mp = pos;
     warp_argmax(key, pos);
-    stage_row(key, pos, mp, mk);
+    stage_row(key, pos, mp, mk, false, 0, 0.0);
     if (lane == 0) {
       wbest[warp].key = key;
       wbest[warp].pos = pos;
@@ -652,8 +656,6 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const bool is_piv = mine && x == xp;
     const bool wr = (alive || is_piv) && q == owner_lane;
     const double wv = alive ? col : rjj;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) pr[i] = (wr && i == slot) ? wv : pr[i];
     if (alive) {
       dl = fma(-col, col, dl);
       if (q == 0 && x < p.neligible && (p.pivoting || pos == j + 1)) {
@@ -665,7 +667,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const int mp = bpos;
     warp_argmax(bkey, bpos);
     if (p.trace) t3 = clock64();
-    if (c + 1 < kb) stage_row(bkey, bpos, mp, mk);
+    if (c + 1 < kb) stage_row(bkey, bpos, mp, mk, wr, slot, wv);
     if (lane == 0) {
       wbest[warp].key = bkey;
       wbest[warp].pos = bpos;
@@ -673,6 +675,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     __syncthreads();
     if (p.trace) t4 = clock64();
     if (c + 1 < kb) combine_publish(j + 1);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pr[i] = (wr && i == slot) ? wv : pr[i];
     if (p.trace) {
       const long long t5 = clock64();
       tacc[0] += t1 - t0;
