@@ -177,6 +177,99 @@ std::pair<ElmModel, SolveDiagnostics> train(const ElmParams& params, const Dense
 DenseMatrix predict(const ElmModel& model, const DenseMatrix& x);
 double accuracy(const DenseMatrix& pred, const DenseMatrix& y);
 
+// ---- data.hpp (host-side data formats feeding train()) ----
+/// Feature matrix plus one-hot targets; classes in first-appearance order; feature_ranges holds
+/// the per-feature (min, max) captured by normalize() (empty for raw datasets).
+struct Dataset {
+  DenseMatrix x;  // N x n
+  DenseMatrix y;  // N x m, one-hot rows
+  std::vector<std::string> class_names;
+  std::vector<std::pair<double, double>> feature_ranges;
+  std::size_t samples() const { return x.rows(); }
+  std::size_t features() const { return x.cols(); }
+  std::size_t classes() const { return y.cols(); }
+};
+
+class DataError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+/// Comma-separated numeric features and one label column (label_column < 0: the last one).
+Dataset load_csv(const std::string& path, int label_column = -1, bool has_header = false);
+/// Sparse "label idx:val ..." lines, 1-based indices, absent entries 0.
+Dataset load_libsvm(const std::string& path);
+/// libsvm text with round-trip-exact values.
+void save_libsvm(const Dataset& ds, const std::string& path);
+/// Per-feature min-max map onto [-1, 1]; constant features map to 0.
+Dataset normalize(const Dataset& ds);
+Dataset normalize_with(const Dataset& ds, const std::vector<std::pair<double, double>>& ranges);
+/// Deterministic Gaussian-cluster dataset (one cluster per class), normalized.
+Dataset synth(std::size_t samples, std::size_t features, std::size_t classes, std::uint64_t seed);
+
+// ---- bench.hpp (trial protocol and report formats) ----------
+struct TrialRecord {
+  std::uint64_t seed = 0;
+  double total_seconds = 0.0;   // H construction through beta completion (host wall clock)
+  double solve_seconds = 0.0;   // beta computation (device time)
+  double hidden_seconds = 0.0;  // H construction (device time)
+  double accuracy = 0.0;
+  std::size_t rank = 0;
+  bool rank_known = false;
+  bool ridge_applied = false;
+  bool fallback_to_direct = false;
+};
+
+struct TrialStats {
+  std::string strategy;
+  std::size_t hidden_nodes = 0;
+  std::size_t trials = 0;
+  double mean_seconds = 0.0;
+  double min_seconds = 0.0;
+  double max_seconds = 0.0;
+  double stddev_seconds = 0.0;
+  double mean_solve_seconds = 0.0;
+  double mean_accuracy = 0.0;
+  std::vector<TrialRecord> records;
+};
+
+struct DatasetInfo {
+  std::string name;
+  std::size_t samples = 0;
+  std::size_t features = 0;
+  std::size_t classes = 0;
+};
+
+struct BenchmarkReport {
+  std::string machine;
+  DatasetInfo dataset;
+  std::vector<std::size_t> node_counts;
+  std::vector<std::size_t> split_points;
+  std::vector<TrialStats> stats;
+};
+
+struct SweepResult {
+  std::vector<TrialStats> stats;
+  std::size_t best_index = 0;   // argmin of mean_seconds
+  std::size_t worst_index = 0;  // argmax of mean_seconds
+};
+
+/// `trials` trainings reseeded with base seed + index, after one discarded warm-up trial.
+TrialStats run_trials(const Dataset& ds, const ElmParams& params_template, const SolverStrategy& strategy,
+                      std::size_t trials);
+SweepResult sweep_df_splits(const Dataset& ds, const ElmParams& params_template,
+                            const std::vector<std::size_t>& split_points, std::size_t trials);
+BenchmarkReport sweep_nodes(const Dataset& ds, const ElmParams& params_template,
+                            const std::vector<std::size_t>& node_counts,
+                            const std::vector<SolverStrategy>& strategies, std::size_t trials,
+                            const std::string& machine = "", const std::string& dataset_name = "");
+/// format "json" (schema 1) or "csv".
+void emit_report(const BenchmarkReport& report, const std::string& format, const std::string& path);
+/// One tab-separated series per strategy: path_prefix.<strategy>.tsv (hidden_nodes, mean, min, max).
+std::vector<std::string> emit_plot_data(const BenchmarkReport& report, const std::string& path_prefix);
+std::string report_to_json(const BenchmarkReport& report);
+BenchmarkReport report_from_json(const std::string& text);
+
 // ---- B200 extras ----------------------------------------------------------
 namespace b200 {
 /// Select the CUDA device used by the calls above (default 0).

@@ -10,9 +10,9 @@ SRC = os.path.join(ROOT, "tests", "cpp", "dropin_example.cpp")
 LIBDIR = os.path.join(ROOT, "paper_2011_02436_b200")
 
 
-def build(tmp_path):
-    exe = os.path.join(str(tmp_path), "dropin_example")
-    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), SRC, "-L", LIBDIR,
+def build(tmp_path, src=SRC):
+    exe = os.path.join(str(tmp_path), os.path.splitext(os.path.basename(src))[0])
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"), src, "-L", LIBDIR,
                     "-lrbpelm_b200", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
     return exe
 
@@ -24,5 +24,22 @@ def test_cpp_dropin_compiles_and_links(tmp_path):
 @pytest.mark.gpu
 def test_cpp_dropin_runs_on_device(tmp_path):
     out = subprocess.run([build(tmp_path)], capture_output=True, text=True, timeout=300)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+
+
+def test_cpp_host_formats_data_layer_and_reports(tmp_path):
+    """Data layer (reference test_data.cpp) and report formats (test_bench.cpp): host only, CPU."""
+    out = subprocess.run([build(tmp_path, os.path.join(ROOT, "tests", "cpp", "host_formats.cpp"))],
+                         capture_output=True, text=True, timeout=120)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+
+
+@pytest.mark.gpu
+def test_cpp_bench_protocol_on_device(tmp_path):
+    """Trial / sweep protocol (reference test_bench.cpp:18-84) through the device train()."""
+    out = subprocess.run([build(tmp_path, os.path.join(ROOT, "tests", "cpp", "bench_protocol.cpp"))],
+                         capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
