@@ -1391,7 +1391,7 @@ int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, 
     double* dY = ctx->dbuf("T.in", std::max<size_t>(1, n) * ldy);
     std::vector<RowReady> ready;
     {
-      const size_t nblk = std::min<size_t>(4, std::max<size_t>(1, n / 8192));
+      const size_t nblk = std::min<size_t>(7, std::max<size_t>(1, n / 4096));
       const size_t per = round_up((n + nblk - 1) / nblk, kTile);
       ck(cudaEventRecord(ctx->chunk_ev[7], ctx->stream), "event");  // buffers free (prior work done)
       ck(cudaStreamWaitEvent(ctx->copy, ctx->chunk_ev[7], 0), "wait");
