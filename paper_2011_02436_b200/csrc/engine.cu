@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <mutex>
 #include <stdexcept>
@@ -706,9 +707,14 @@ void block_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
 // The rank path then factors it with the m target columns carried along as never-pivot labels, so
 // the factorisation itself forward-solves F y = P^T H^T T (y = their factor rows) and only the
 // backward substitution F^T x = y remains (cf. solve_factored_gram, linalg.cpp:254-270).
+// post (optional): work enqueued behind the speculative full-rank solve before the single rank
+// readback (train()'s finiteness check and accuracy pass); *post_valid tells the caller whether that
+// work ran on the final beta (rank == L) or must be repeated after the fallback solve.
 void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dHtT, size_t ldt, size_t L, size_t m,
                size_t rows, const rbpg_strategy& sg, double* dBeta, size_t ldb, size_t* order_out,
-               rbpg_diagnostics* diag, bool gaug = false) {
+               rbpg_diagnostics* diag, bool gaug = false, const std::function<void()>* post = nullptr,
+               bool* post_valid = nullptr) {
+  if (post_valid) *post_valid = false;
   if (sg.kind == RBPG_DIRECT) {
     diag->split_lo = L;
     diag->split_hi = 0;
@@ -759,6 +765,7 @@ void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   ctx->run("unpermute beta", [&] { return launch_scatter_rows(rhs, lm, f.ord, L, m, dBeta, ldb, ctx->stream); });
   int* ho = static_cast<int*>(ctx->pinned("order.out", L * 4));
   if (order_out) ck(cudaMemcpyAsync(ho, f.ord, L * 4, cudaMemcpyDeviceToHost, ctx->stream), "read order");
+  if (post) (*post)();
   ck(cudaStreamSynchronize(ctx->stream), "factor sync");
   f.st = *f.hst;
   const size_t rank = static_cast<size_t>(f.st.rank);
@@ -776,7 +783,10 @@ void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   const size_t split = (rank == L) ? (L + 1) / 2 : rank;
   diag->split_lo = split;
   diag->split_hi = L - split;
-  if (rank == L) return;  // the speculated solve is the answer
+  if (rank == L) {  // the speculated solve is the answer
+    if (post_valid) *post_valid = post != nullptr;
+    return;
+  }
   try {
     block_dev(ctx, dG, ldg, dHtT, ldt, L, m, rows, f.ord, split, dBeta, ldb, diag);
   } catch (const Fail& e) {
@@ -990,6 +1000,8 @@ void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* d
   double* HtT = G + L;
 
   const auto wall0 = std::chrono::steady_clock::now();
+  const int* bad = nullptr;
+  unsigned long long* hits = nullptr;
   cudaEventRecord(ctx->ev[2], ctx->stream);
   float hidden_ms = gram_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, G, ldg, false, true, true, ready);
   {
@@ -997,13 +1009,17 @@ void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* d
     const bool kept = ctx->kept_h && ctx->kept_n == N;
     SourceScope src(ctx, kept ? ctx->kept_h : nullptr, ctx->kept_ldh, kept ? ctx->kept_h + L : nullptr,
                     ctx->kept_ldh, kept ? N : 0);
-    solve_dev(ctx, G, ldg, HtT, ldt, L, m, N, sg, dBeta, ldb, order_out, diag, true);
+    // finiteness check and accuracy pass enqueued behind the (speculative) solve: one
+    // synchronisation for the rank, the check and the hit count
+    const std::function<void()> post = [&] {
+      cudaEventRecord(ctx->ev[3], ctx->stream);
+      bad = check_finite(ctx, dBeta, ldb, L, m, true);
+      accuracy_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, dBeta, ldb, &hits);
+    };
+    bool done = false;
+    solve_dev(ctx, G, ldg, HtT, ldt, L, m, N, sg, dBeta, ldb, order_out, diag, true, &post, &done);
+    if (!done) post();  // other strategies, or the rank < L fallback changed beta
   }
-  cudaEventRecord(ctx->ev[3], ctx->stream);
-  // finiteness check and accuracy pass enqueued behind the solve; one synchronisation for both
-  const int* bad = check_finite(ctx, dBeta, ldb, L, m, true);
-  unsigned long long* hits = nullptr;
-  accuracy_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, dBeta, ldb, &hits);
   ck(cudaStreamSynchronize(ctx->stream), "sync");
   float total_ms = 0.f, first_hidden_ms = 0.f;
   cudaEventElapsedTime(&total_ms, ctx->ev[2], ctx->ev[3]);
