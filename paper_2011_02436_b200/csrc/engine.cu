@@ -241,7 +241,7 @@ void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_
                 size_t m = 0) {
   if (N == 0) return;
   CUtensorMap tmX = make_map(ctx, dX, d, N, ldx, 16, kTile, true);
-  CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, 64, kBK, false);
+  CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, 64 + 4, kBK, false);  // padded smem rows
   HiddenParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), db, dH, static_cast<long long>(ldh),
                  0, m > 0 ? dT : nullptr, static_cast<long long>(ldt), static_cast<int>(m)};
   ctx->run("hidden_kernel", [&] { return launch_hidden(tmX, tmW, p, 64, ctx->stream); });
@@ -1084,7 +1084,7 @@ void pinv_apply_dev(rbpg_context* ctx, const double* Ginv, size_t ldgi, const do
                     double* dOut, size_t ldo) {
   if (N == 0) return;
   CUtensorMap tmH = make_map(ctx, dH, L, N, ldh, 16, kTile, true);
-  CUtensorMap tmG = make_map(ctx, Ginv, L, L, ldgi, kTile, kBK, false);
+  CUtensorMap tmG = make_map(ctx, Ginv, L, L, ldgi, kTile + 4, kBK, false);  // padded smem rows
   HiddenParams p{static_cast<int>(N), static_cast<int>(L), static_cast<int>(L), nullptr, dOut,
                  static_cast<long long>(ldo), 1};
   ctx->run("pinv_apply", [&] { return launch_hidden(tmH, tmG, p, kTile, ctx->stream); });

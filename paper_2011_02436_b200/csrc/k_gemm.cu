@@ -17,6 +17,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <algorithm>
 #include <cstdio>
 
 namespace rbpg {
@@ -65,13 +66,17 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = align1024(smem_raw);
   double* Xs = reinterpret_cast<double*>(smem);        // [stage][128 rows][16] swizzled
-  double* Ws = Xs + kStages * kTile * kBK;             // [stage][16][BN]
-  uint64_t* full = reinterpret_cast<uint64_t*>(Ws + kStages * kBK * BN);
+  // W rows padded by 4 doubles (TMA box {BN + 4, 16}): the k rows of a quarter-warp's 16-byte
+  // fragment loads then start on different banks (an unpadded 512 / 1024-byte row stride maps
+  // the 4 k rows onto the same banks: 4-way conflicts)
+  constexpr int BNP = BN + 4;
+  double* Ws = Xs + kStages * kTile * kBK;             // [stage][16][BNP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Ws + kStages * kBK * BNP);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int l0 = blockIdx.x * BN, n0 = blockIdx.y * kTile;
   const int ktiles = (p.d + kBK - 1) / kBK;
-  constexpr uint32_t kStageBytes = (kTile + BN) * kBK * sizeof(double);
+  constexpr uint32_t kStageBytes = (kTile + BNP) * kBK * sizeof(double);
 
   if (tid == 0) {
     tma_prefetch_desc(&tmX);
@@ -84,7 +89,7 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
     for (int s = 0; s < kStages && s < ktiles; ++s) {
       mbar_arrive_expect_tx(&full[s], kStageBytes);
       tma_load_2d(Xs + s * kTile * kBK, &tmX, &full[s], s * kBK, n0);
-      tma_load_2d(Ws + s * kBK * BN, &tmW, &full[s], l0, s * kBK);
+      tma_load_2d(Ws + s * kBK * BNP, &tmW, &full[s], l0, s * kBK);
     }
   }
 
@@ -104,7 +109,7 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
     const int s = kt % kStages;
     mbar_wait(&full[s], (kt / kStages) & 1);
     const double* xs = Xs + s * kTile * kBK;
-    const double* ws = Ws + s * kBK * BN;
+    const double* ws = Ws + s * kBK * BNP;
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
       const int kc = ks * 4 + t;
@@ -117,7 +122,7 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
       }
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp) {
-        const double2 w = *reinterpret_cast<const double2*>(ws + kc * BN + wn + pp * 16 + 2 * g);
+        const double2 w = *reinterpret_cast<const double2*>(ws + kc * BNP + wn + pp * 16 + 2 * g);
         b[2 * pp] = w.x;
         b[2 * pp + 1] = w.y;
       }
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
       const int kn = kt + kStages;
       mbar_arrive_expect_tx(&full[s], kStageBytes);
       tma_load_2d(Xs + s * kTile * kBK, &tmX, &full[s], kn * kBK, n0);
-      tma_load_2d(Ws + s * kBK * BN, &tmW, &full[s], l0, kn * kBK);
+      tma_load_2d(Ws + s * kBK * BNP, &tmW, &full[s], l0, kn * kBK);
     }
   }
 
@@ -625,13 +630,14 @@ __global__ void __launch_bounds__(128) gemm_kernel(GemmParams p) {
 // ============================================================================
 // launchers
 // ============================================================================
-// bn = 64 (sigmoid build, two CTAs per SM) or 128 (plain transposed product); tmW's box is {bn, kBK}
+// bn = 64 (sigmoid build, two CTAs per SM) or 128 (plain transposed product); tmW's box is {bn + 4, kBK}
 cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const HiddenParams& p, int bn,
                           cudaStream_t s) {
   static bool attr = false;
-  constexpr size_t kSmem64 = size_t(kStages) * (kTile + 64) * kBK * sizeof(double) + 1024 + 256;
+  constexpr size_t kSmem64 = size_t(kStages) * (kTile + 68) * kBK * sizeof(double) + 1024 + 256;
+  constexpr size_t kSmem128 = size_t(kStages) * (kTile + 132) * kBK * sizeof(double) + 1024 + 256;
   if (!attr) {
-    cudaFuncSetAttribute(hidden_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+    cudaFuncSetAttribute(hidden_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem128);
     cudaFuncSetAttribute(hidden_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem64);
     attr = true;
   }
@@ -639,7 +645,7 @@ cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
   if (bn == 64)
     hidden_kernel<64><<<grid, kGemmThreads, kSmem64, s>>>(tmX, tmW, p);
   else
-    hidden_kernel<128><<<grid, kGemmThreads, kTmaSmemBytes, s>>>(tmX, tmW, p);
+    hidden_kernel<128><<<grid, kGemmThreads, kSmem128, s>>>(tmX, tmW, p);
   return cudaGetLastError();
 }
 
