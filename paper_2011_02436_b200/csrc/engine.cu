@@ -300,8 +300,8 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
     }
     return;
   }
-  CUtensorMap tmA = make_map(ctx, dA, L, N, lda, kTile, kBK, false);
-  CUtensorMap tmB = m > 0 ? make_map(ctx, dT, m, N, ldt_in, kTile, kBK, false) : tmA;
+  CUtensorMap tmA = make_map(ctx, dA, L, N, lda, kTile + 4, kBK, false);  // padded smem rows
+  CUtensorMap tmB = m > 0 ? make_map(ctx, dT, m, N, ldt_in, kTile + 4, kBK, false) : tmA;
   ctx->run("syrk_kernel", [&] { return launch_syrk(tmA, tmB, p, splits, kTile, ctx->stream); });
   if (p.nbI >= 2) ++ctx->launches;  // diagonal + off-diagonal grids
   if (!direct) ctx->run("syrk_finish", [&] { return launch_syrk_finish(p, splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
@@ -412,7 +412,7 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
       // 64-wide tiles while 128-wide ones would not fill two waves of SMs
       const size_t nb128 = (nrem + kTile - 1) / kTile;
       const int ttile = (nb128 * (nb128 + 1) / 2 < size_t(2 * ctx->num_sms)) ? 64 : kTile;
-      CUtensorMap tm = make_map(ctx, PcT, nrem, static_cast<uint64_t>(kb), ldp, ttile, kBK, false);
+      CUtensorMap tm = make_map(ctx, PcT, nrem, static_cast<uint64_t>(kb), ldp, ttile + 4, kBK, false);
       SyrkParams sp{};
       sp.M = static_cast<int>(nrem);
       sp.nbI = static_cast<int>((nrem + ttile - 1) / ttile);

@@ -206,9 +206,12 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
     syrk_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, SyrkParams p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = align1024(smem_raw);
-  double* As = reinterpret_cast<double*>(smem);   // [stage][16][128]
-  double* Bs = As + kStages * kBK * TILE;        // [stage][16][128]
-  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBK * TILE);
+  // operand rows padded by 4 doubles (TMA box {TILE + 4, 16}): a quarter-warp's 16-byte fragment
+  // loads from 4 consecutive k rows then start on different banks (no 4-way conflicts)
+  constexpr int TP = TILE + 4;
+  double* As = reinterpret_cast<double*>(smem);   // [stage][16][TP]
+  double* Bs = As + kStages * kBK * TP;          // [stage][16][TP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBK * TP);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
 
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
   long long kend = kbeg + p.kPerSplit;
   if (kend > p.kRows) kend = p.kRows;
   const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kBK - 1) / kBK) : 0;
-  constexpr uint32_t kStageBytes = 2u * TILE * kBK * sizeof(double);
+  constexpr uint32_t kStageBytes = 2u * TP * kBK * sizeof(double);
 
   if (tid == 0) {
     tma_prefetch_desc(&tmA);
@@ -253,8 +256,8 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
     for (int s = 0; s < kStages && s < ktiles; ++s) {
       const int kr = static_cast<int>(kbeg + s * kBK);
       mbar_arrive_expect_tx(&full[s], kStageBytes);
-      tma_load_2d(As + s * kBK * TILE, &tmA, &full[s], i0, kr);
-      tma_load_2d(Bs + s * kBK * TILE, mapB, &full[s], j0, kr);
+      tma_load_2d(As + s * kBK * TP, &tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * TP, mapB, &full[s], j0, kr);
     }
   }
 
@@ -271,21 +274,21 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
   for (int kt = 0; kt < ktiles; ++kt) {
     const int s = kt % kStages;
     mbar_wait(&full[s], (kt / kStages) & 1);
-    const double* as = As + s * kBK * TILE;
-    const double* bs = Bs + s * kBK * TILE;
+    const double* as = As + s * kBK * TP;
+    const double* bs = Bs + s * kBK * TP;
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
       const int kc = ks * 4 + t;
       double a[MT][2], b[4];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        const double2 v = *reinterpret_cast<const double2*>(as + kc * TILE + wm + mt * 16 + 2 * g);
+        const double2 v = *reinterpret_cast<const double2*>(as + kc * TP + wm + mt * 16 + 2 * g);
         a[mt][0] = v.x;   // MMA row g   <-> tile row 2g
         a[mt][1] = v.y;   // MMA row g+8 <-> tile row 2g+1
       }
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp) {
-        const double2 w = *reinterpret_cast<const double2*>(bs + kc * TILE + wn + pp * 16 + 2 * g);
+        const double2 w = *reinterpret_cast<const double2*>(bs + kc * TP + wn + pp * 16 + 2 * g);
         b[2 * pp] = w.x;       // n-tile 2pp   col g <-> tile col 16pp + 2g
         b[2 * pp + 1] = w.y;   // n-tile 2pp+1 col g <-> tile col 16pp + 2g + 1
       }
@@ -298,8 +301,8 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
     if (tid == 0 && kt + kStages < ktiles) {
       const int kr = static_cast<int>(kbeg + (long long)(kt + kStages) * kBK);
       mbar_arrive_expect_tx(&full[s], kStageBytes);
-      tma_load_2d(As + s * kBK * TILE, &tmA, &full[s], i0, kr);
-      tma_load_2d(Bs + s * kBK * TILE, mapB, &full[s], j0, kr);
+      tma_load_2d(As + s * kBK * TP, &tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * TP, mapB, &full[s], j0, kr);
     }
   }
 
@@ -418,8 +421,8 @@ __device__ __forceinline__ void diag_step(double (&acc)[9][4], const double* as,
       const int q = 9 * DH + i;
       const int mt = q < kFirst ? DS : 7 - DS;
       const int nt = q < kFirst ? q : q - kFirst;
-      const double2 a = *reinterpret_cast<const double2*>(as + kc * 128 + mt * 16 + 2 * g);
-      const double2 bw = *reinterpret_cast<const double2*>(bs + kc * 128 + (nt >> 1) * 16 + 2 * g);
+      const double2 a = *reinterpret_cast<const double2*>(as + kc * 132 + mt * 16 + 2 * g);
+      const double2 bw = *reinterpret_cast<const double2*>(bs + kc * 132 + (nt >> 1) * 16 + 2 * g);
       dmma_16x8x4(acc[i], a.x, a.y, (nt & 1) ? bw.y : bw.x);
     }
   }
@@ -433,17 +436,17 @@ template <int DS, int DH>
 __device__ __forceinline__ void diag_tile_loop(double (&acc)[9][4], double* As, double* Bs,
                                                uint64_t* full, const CUtensorMap* tmA, int i0, long long kbeg,
                                                int ktiles, int tid, int g, int t) {
-  constexpr uint32_t kStageBytes = 2u * 128 * kBK * sizeof(double);
+  constexpr uint32_t kStageBytes = 2u * 132 * kBK * sizeof(double);
   for (int kt = 0; kt < ktiles; ++kt) {
     const int s = kt % kStages;
     mbar_wait(&full[s], (kt / kStages) & 1);
-    diag_step<DS, DH>(acc, As + s * kBK * 128, Bs + s * kBK * 128, g, t);
+    diag_step<DS, DH>(acc, As + s * kBK * 132, Bs + s * kBK * 132, g, t);
     __syncthreads();
     if (tid == 0 && kt + kStages < ktiles) {
       const int kr = static_cast<int>(kbeg + (long long)(kt + kStages) * kBK);
       mbar_arrive_expect_tx(&full[s], kStageBytes);
-      tma_load_2d(As + s * kBK * 128, tmA, &full[s], i0, kr);
-      tma_load_2d(Bs + s * kBK * 128, tmA, &full[s], i0, kr);
+      tma_load_2d(As + s * kBK * 132, tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * 132, tmA, &full[s], i0, kr);
     }
   }
 }
@@ -453,15 +456,15 @@ __global__ void __launch_bounds__(256, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = align1024(smem_raw);
   double* As = reinterpret_cast<double*>(smem);
-  double* Bs = As + kStages * kBK * 128;
-  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBK * 128);
+  double* Bs = As + kStages * kBK * 132;  // padded rows, as in syrk_kernel
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBK * 132);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int I = blockIdx.x, i0 = I * 128;
   const long long kbeg = (long long)blockIdx.y * p.kPerSplit;
   long long kend = kbeg + p.kPerSplit;
   if (kend > p.kRows) kend = p.kRows;
   const int ktiles = kend > kbeg ? static_cast<int>((kend - kbeg + kBK - 1) / kBK) : 0;
-  constexpr uint32_t kStageBytes = 2u * 128 * kBK * sizeof(double);
+  constexpr uint32_t kStageBytes = 2u * 132 * kBK * sizeof(double);
   if (tid == 0) {
     tma_prefetch_desc(&tmA);
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
@@ -473,8 +476,8 @@ __global__ void __launch_bounds__(256, 1)
     for (int s = 0; s < kStages && s < ktiles; ++s) {
       const int kr = static_cast<int>(kbeg + s * kBK);
       mbar_arrive_expect_tx(&full[s], kStageBytes);
-      tma_load_2d(As + s * kBK * 128, &tmA, &full[s], i0, kr);
-      tma_load_2d(Bs + s * kBK * 128, &tmA, &full[s], i0, kr);
+      tma_load_2d(As + s * kBK * 132, &tmA, &full[s], i0, kr);
+      tma_load_2d(Bs + s * kBK * 132, &tmA, &full[s], i0, kr);
     }
   }
   double acc[9][4];
@@ -654,6 +657,10 @@ cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
 // must be {tile, kBK}.
 // pdl: launch as a programmatic dependent of the preceding kernel in the stream (trailing updates
 // behind a panel)
+constexpr size_t kSyrkSmem128 = size_t(kStages) * 2 * 132 * kBK * sizeof(double) + 1024 + 256;
+constexpr size_t kSyrkSmem64 = size_t(kStages) * 2 * 68 * kBK * sizeof(double) + 1024 + 256;
+
+// tensor-map boxes must be {tile + 4, kBK} (padded shared-memory rows)
 cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const SyrkParams& p, int splits, int tile,
                         cudaStream_t s, bool pdl) {
   if (tile == 128 && p.mode != kSyrkTrailing && p.nbI >= 2) {
@@ -661,17 +668,17 @@ cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const Sy
     // programmatic dependent (the two grids share the machine)
     static bool dattr = false;
     if (!dattr) {
-      cudaFuncSetAttribute(syrk_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
-      cudaFuncSetAttribute(syrk_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+      cudaFuncSetAttribute(syrk_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem128);
+      cudaFuncSetAttribute(syrk_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem128);
       dattr = true;
     }
-    syrk_diag_kernel<<<dim3(p.nbI, splits), 256, kTmaSmemBytes, s>>>(tmA, p);
+    syrk_diag_kernel<<<dim3(p.nbI, splits), 256, kSyrkSmem128, s>>>(tmA, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t c2 = {};
     c2.gridDim = dim3(p.nbI * (p.nbI - 1) / 2 + p.nbI * p.nbT, splits);
     c2.blockDim = dim3(256);
-    c2.dynamicSmemBytes = kTmaSmemBytes;
+    c2.dynamicSmemBytes = kSyrkSmem128;
     c2.stream = s;
     cudaLaunchAttribute a2[1];
     a2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -691,15 +698,15 @@ cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const Sy
   if (tile == 128) {
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(syrk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmemBytes);
+      cudaFuncSetAttribute(syrk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem128);
       attr = true;
     }
     cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = kTmaSmemBytes;
+    cfg.dynamicSmemBytes = kSyrkSmem128;
     return cudaLaunchKernelEx(&cfg, syrk_kernel<128>, tmA, tmB, p);
   }
   if (tile == 64) {
-    constexpr size_t smem = size_t(kStages) * 2 * 64 * kBK * sizeof(double) + 1024 + 256;
+    constexpr size_t smem = kSyrkSmem64;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(syrk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
