@@ -257,22 +257,55 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
   p.nGram = p.nbI * (p.nbI + 1) / 2;
   p.nbT = m > 0 ? static_cast<int>((m + kTile - 1) / kTile) : 0;
   const int tiles = p.nGram + p.nbI * p.nbT;
-  // split-K count: fill whole waves of one CTA per SM (wave quantisation), each split >= 1024 rows
+  // split-K count S (uniform row splits for every tile, so every Gram element sees the same
+  // arithmetic): greedy list scheduling of the tile x split CTAs on the SMs -- off-diagonal and
+  // H^T T tiles first, then the diagonal ones at ~0.56 of their work (72 of 128 fragments) --
+  // plus the fixed-order reduction of the S partials
   int splits = 1;
   if (tiles < 4 * ctx->num_sms) {
-    double best = -1.0;
-    for (int s = 1; s <= 32; ++s) {
-      if (s > 1 && N / static_cast<size_t>(s) < 1024) break;
-      const long long ctas = static_cast<long long>(tiles) * s;
-      const long long waves = (ctas + ctx->num_sms - 1) / ctx->num_sms;
-      const double eff = static_cast<double>(ctas) / static_cast<double>(waves * ctx->num_sms);
-      const double score = eff - 0.004 * s;
-      if (score > best + 1e-12) {
-        best = score;
-        splits = s;
+    const int P = ctx->num_sms;
+    const int nfull = tiles - (p.nbI >= 2 ? p.nbI : 0), ndiag = p.nbI >= 2 ? p.nbI : 0;
+    const double us_per_row = 2.0 * kTile * kTile / (35.7e12 / P) * 1e6;
+    // fixed-order reduction: ~1 us per partial at L + m = 1010 (measured), quadratic in L + m
+    const double finish_us_per_split = double(L + m) * double(L + m) / (1010.0 * 1010.0);
+    const double ws_bytes_per_split = double(L + m) * double(L + m) * 8.0;
+    std::vector<std::pair<double, int>> cand;  // (modelled time, S)
+    for (int sp = 1; sp <= 40; ++sp) {
+      if (sp > 1 && N / static_cast<size_t>(sp) < 768) break;
+      if (sp > 1 && sp * ws_bytes_per_split > 2.0e9) break;  // split workspace <= 2 GB
+      const double dur = double(N) / sp * us_per_row + 2.0;  // + per-CTA prologue / partial store
+      // equal full-tile CTAs: every SM gets q or q + 1 of them; then the diagonal CTAs go, one
+      // at a time, to the least-loaded SM (loads kept as a histogram of levels)
+      const long long nf = 1LL * nfull * sp;
+      std::map<double, long long> level;
+      level[double(nf / P) * dur] += P - nf % P;
+      if (nf % P) level[double(nf / P + 1) * dur] += nf % P;
+      const double ddur = 0.5625 * (dur - 2.0) + 2.0;
+      for (long long c = 0; c < 1LL * ndiag * sp; ++c) {
+        auto it = level.begin();
+        const double l = it->first;
+        if (--it->second == 0) level.erase(it);
+        level[l + ddur] += 1;
+      }
+      cand.emplace_back(level.rbegin()->first + (sp > 1 ? sp * finish_us_per_split + 3.0 : 0.0), sp);
+    }
+    // the greedy model misses the launch order of the two grids: among the near-best candidates
+    // prefer the split count that fills the last off-diagonal wave (measured best at C2: S = 37,
+    // 28 x 37 = 7 x 148)
+    double tmin = 1e300;
+    for (const auto& c : cand) tmin = std::min(tmin, c.first);
+    long long best_rem = P + 1;
+    for (const auto& c : cand) {
+      if (c.first > 1.01 * tmin) continue;
+      const long long rem = (1LL * nfull * c.second) % P;
+      const long long waste = rem == 0 ? 0 : P - rem;
+      if (waste < best_rem) {
+        best_rem = waste;
+        splits = c.second;
       }
     }
   }
+  if (const char* e = std::getenv("RBPG_GRAM_SPLITS")) splits = std::max(1, std::atoi(e));  // tuning experiments
   long long per = static_cast<long long>(round_up((N + splits - 1) / splits, kBK));
   if (per == 0) per = kBK;
   splits = static_cast<int>((N + per - 1) / per);

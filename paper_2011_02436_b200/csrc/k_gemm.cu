@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
-  pdl_trigger();
+  pdl_trigger();  // PART 1: the diagonal-tile grid (this grid's dependent) may start launching
   if (PART == 0) pdl_wait();  // trailing mode: the panel that wrote PcT / lab may still be finishing
   __syncthreads();
   if (tid == 0) {
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
 
   // ---- epilogue.  Thread holds rows r, r+1 (r even) x cols c..c+3 per (mt, pp).
   const int split = blockIdx.y;
-  if (PART == 1) pdl_wait();  // this grid completes only after the diagonal-tile grid
+
   // trailing mode: every G_old gather is issued before the first store (the stores could alias
   // the loads as far as the compiler knows, which would serialise one L2 round trip per element)
   // (64-wide tiles only: the 128-wide kernel has no registers to spare for the staging)
@@ -470,7 +470,6 @@ __global__ void __launch_bounds__(256, 1)
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
-  pdl_trigger();  // the off-diagonal grid may start right away (no data dependency)
   __syncthreads();
   if (tid == 0) {
     for (int s = 0; s < kStages && s < ktiles; ++s) {
@@ -495,6 +494,7 @@ __global__ void __launch_bounds__(256, 1)
     case 6: diag_tile_loop<2, 1>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
     default: diag_tile_loop<3, 1>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
   }
+  pdl_wait();  // completes only after the off-diagonal grid (its primary): the reduction follows
   // fragment (mt, nt): MMA row g / g+8 <-> tile row mt*16 + 2g / +1; MMA col j <-> tile col
   // (nt >> 1) * 16 + 2j + (nt & 1); lower elements only (mirrored in direct mode)
   const int ds = warp & 3, dh = warp >> 2;
@@ -516,30 +516,49 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-// Fixed-order split reduction: G[i][j] = G[j][i] = (acc ? G[i][j] : 0) + sum_s ws[s][i][j]
-// over the lower triangle (i >= j), plus the H^T T partials.
-__global__ void syrk_finish_kernel(SyrkParams p, int splits, int accumulate) {
-  const long long Mg = p.M;
-  const long long total = Mg * Mg;
-  const long long totalT = (long long)p.M * p.mB;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total + totalT;
-       e += (long long)gridDim.x * blockDim.x) {
-    if (e < total) {
-      const long long i = e / Mg, j = e % Mg;
-      if (j > i) continue;
-      double v = p.ws[i * p.ldg + j];
-      for (int s = 1; s < splits; ++s) v = add_rn(v, p.ws[s * p.wsStride + i * p.ldg + j]);
-      if (accumulate) v = add_rn(p.G[i * p.ldg + j], v);
-      p.G[i * p.ldg + j] = v;
-      p.G[j * p.ldg + i] = v;
-    } else {
-      const long long f = e - total;
-      const long long i = f / p.mB, j = f % p.mB;
-      double v = p.wsT[i * p.ldt + j];
-      for (int s = 1; s < splits; ++s) v = add_rn(v, p.wsT[s * p.wsTStride + i * p.ldt + j]);
-      if (accumulate) v = add_rn(p.HtT[i * p.ldt + j], v);
-      p.HtT[i * p.ldt + j] = v;
+// Fixed-order split reduction: G[i][j] = G[j][i] = (acc ? G[i][j] : 0) + sum_s ws[s][i][j] over the
+// lower triangle (i >= j), plus the H^T T partials.  One CTA per 32 x 32 block of the lower
+// triangle: the summed block is staged in shared memory and written both ways with coalesced rows
+// (the mirrored half is a transpose, not a column scatter).  Blocks past the triangle reduce the
+// H^T T partials.
+__global__ void __launch_bounds__(256) syrk_finish_kernel(SyrkParams p, int splits, int accumulate) {
+  __shared__ double blk[32][33];
+  const int M = p.M, nb = (M + 31) / 32, nlow = nb * (nb + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  int b = blockIdx.x;
+  if (b < nlow) {
+    int bi = static_cast<int>((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+    while (bi * (bi + 1) / 2 > b) --bi;
+    while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
+    const int bj = b - bi * (bi + 1) / 2;
+    const int i0 = bi * 32, j0 = bj * 32;
+    for (int r = ty; r < 32; r += 8) {
+      const int i = i0 + r, j = j0 + tx;
+      double v = 0.0;
+      if (i < M && j < M && j <= i) {
+        const long long off = (long long)i * p.ldg + j;
+        v = p.ws[off];
+        for (int sp = 1; sp < splits; ++sp) v = add_rn(v, p.ws[sp * p.wsStride + off]);
+        if (accumulate) v = add_rn(p.G[off], v);
+        p.G[off] = v;
+      }
+      blk[r][tx] = v;
     }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {  // mirror: G[j0 + r][i0 + tx] = blk[tx][r]
+      const int j = j0 + r, i = i0 + tx;
+      if (i < M && j < M && (bi != bj || r < tx)) p.G[(long long)j * p.ldg + i] = blk[tx][r];
+    }
+    return;
+  }
+  b -= nlow;
+  const long long totalT = (long long)p.M * p.mB;
+  for (long long f = (long long)b * blockDim.x + threadIdx.x; f < totalT; f += (long long)(gridDim.x - nlow) * blockDim.x) {
+    const long long i = f / p.mB, j = f % p.mB;
+    double v = p.wsT[i * p.ldt + j];
+    for (int sp = 1; sp < splits; ++sp) v = add_rn(v, p.wsT[sp * p.wsTStride + i * p.ldt + j]);
+    if (accumulate) v = add_rn(p.HtT[i * p.ldt + j], v);
+    p.HtT[i * p.ldt + j] = v;
   }
 }
 
@@ -672,11 +691,13 @@ cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const Sy
       cudaFuncSetAttribute(syrk_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem128);
       dattr = true;
     }
-    syrk_diag_kernel<<<dim3(p.nbI, splits), 256, kSyrkSmem128, s>>>(tmA, p);
+    // off-diagonal (long) CTAs first, the diagonal (short) ones as its programmatic dependent:
+    // they fill the SMs the last off-diagonal wave leaves idle
+    syrk_kernel<128, 1><<<dim3(p.nbI * (p.nbI - 1) / 2 + p.nbI * p.nbT, splits), 256, kSyrkSmem128, s>>>(tmA, tmB, p);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t c2 = {};
-    c2.gridDim = dim3(p.nbI * (p.nbI - 1) / 2 + p.nbI * p.nbT, splits);
+    c2.gridDim = dim3(p.nbI, splits);
     c2.blockDim = dim3(256);
     c2.dynamicSmemBytes = kSyrkSmem128;
     c2.stream = s;
@@ -685,7 +706,7 @@ cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const Sy
     a2[0].val.programmaticStreamSerializationAllowed = 1;
     c2.attrs = a2;
     c2.numAttrs = 1;
-    return cudaLaunchKernelEx(&c2, syrk_kernel<128, 1>, tmA, tmB, p);
+    return cudaLaunchKernelEx(&c2, syrk_diag_kernel, tmA, p);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.nGram + p.nbI * p.nbT, splits);
@@ -720,7 +741,9 @@ cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const Sy
 }
 
 cudaError_t launch_syrk_finish(const SyrkParams& p, int splits, int accumulate, int num_sms, cudaStream_t s) {
-  syrk_finish_kernel<<<num_sms * 4, 256, 0, s>>>(p, splits, accumulate);
+  const int nb = (p.M + 31) / 32;
+  const int tblocks = p.mB > 0 ? num_sms : 0;
+  syrk_finish_kernel<<<nb * (nb + 1) / 2 + tblocks, 256, 0, s>>>(p, splits, accumulate);
   return cudaGetLastError();
 }
 
