@@ -184,17 +184,16 @@ def main():
     N_total = n * world
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
 
-    G = torch.empty((L, L), dtype=torch.float64, device=dev)
-    HtT = torch.empty((L, m), dtype=torch.float64, device=dev)
+    Gaug = torch.empty((L + m, L + m), dtype=torch.float64, device=dev)
 
     def step():
         if world == 1:
             beta, diag, _ = rb.train_device(X, T, params, strat, hidden=hidden, ctx=ctx)
             return diag
-        rb.gram_stage_device(X, T, W, B, G, HtT, ctx=ctx)
-        dist.all_reduce(G)
-        dist.all_reduce(HtT)
-        beta, diag = rb.solve_stage_device(G, HtT, N_total, strat, ctx=ctx)
+        # row shard -> augmented Gram [H T]^T [H T] -> ONE all-reduce -> replicated solve
+        rb.gram_stage_device_aug(X, T, W, B, Gaug, ctx=ctx)
+        dist.all_reduce(Gaug)
+        beta, diag = rb.solve_stage_device_aug(Gaug, L, m, N_total, strat, ctx=ctx)
         hits = torch.tensor([rb.accuracy_stage_device(X, T, W, B, beta, ctx=ctx)], dtype=torch.int64, device=dev)
         dist.all_reduce(hits)
         diag.training_accuracy = hits.item() / N_total

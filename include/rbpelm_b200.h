@@ -155,6 +155,16 @@ int rbpg_gram_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, cons
 int rbpg_solve_stage_device(rbpg_context* ctx, const double* dg, size_t ldg, const double* dhtt, size_t ldt,
                             size_t l, size_t m, size_t n_total, const rbpg_strategy* strategy, double* dbeta,
                             size_t ldb, size_t* order_out, rbpg_diagnostics* diag, rbpg_status* st);
+/* Augmented form of stages 1 and 2: stage 1 writes (adds, with accumulate) the whole
+ * (L+m) x (L+m) Gram of [H T] (ld ldga >= L+m), so a sharded job all-reduces ONE buffer; stage 2
+ * then factors it with the targets carried along (forward substitution inside the factorisation,
+ * backward sweep only) -- the single-GPU train() pipeline. */
+int rbpg_gram_stage_device_aug(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in,
+                               size_t n, size_t d, size_t l, size_t m, const double* dw, size_t ldw, const double* db,
+                               double* dgaug, size_t ldga, int accumulate, int keep_h, rbpg_status* st);
+int rbpg_solve_stage_device_aug(rbpg_context* ctx, const double* dgaug, size_t ldga, size_t l, size_t m,
+                                size_t n_total, const rbpg_strategy* strategy, double* dbeta, size_t ldb,
+                                size_t* order_out, rbpg_diagnostics* diag, rbpg_status* st);
 /* Stage 3 (per shard): number of local rows whose argmax(H beta) equals argmax(T).  Uses the H kept
  * by stage 1 when available, otherwise rebuilds it from X. */
 int rbpg_accuracy_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in,

@@ -77,6 +77,10 @@ SIGNATURES = {
     "rbpg_predict": (c_int, [P, P, P, c_size_t, c_size_t, P, c_size_t, P, c_size_t, c_size_t, P, ST]),
     "rbpg_gram_stage_device": (c_int, [P, P, c_size_t, P, c_size_t, c_size_t, c_size_t, c_size_t, c_size_t, P, c_size_t,
                                        P, P, c_size_t, P, c_size_t, c_int, c_int, ST]),
+    "rbpg_gram_stage_device_aug": (c_int, [P, P, c_size_t, P, c_size_t, c_size_t, c_size_t, c_size_t, c_size_t, P,
+                                           c_size_t, P, P, c_size_t, c_int, c_int, ST]),
+    "rbpg_solve_stage_device_aug": (c_int, [P, P, c_size_t, c_size_t, c_size_t, c_size_t, POINTER(rbpg_strategy), P,
+                                            c_size_t, P, P, ST]),
     "rbpg_solve_stage_device": (c_int, [P, P, c_size_t, P, c_size_t, c_size_t, c_size_t, c_size_t, POINTER(rbpg_strategy),
                                         P, c_size_t, P, POINTER(rbpg_diagnostics), ST]),
     "rbpg_accuracy_stage_device": (c_int, [P, P, c_size_t, P, c_size_t, c_size_t, c_size_t, c_size_t, c_size_t, P,

@@ -612,6 +612,42 @@ def solve_stage_device(g, htt, n_total: int, strategy: SolverStrategy, ctx: Opti
     return beta, diag
 
 
+def gram_stage_device_aug(x, t, w, b, gaug, accumulate: bool = False, keep_h: bool = True,
+                          ctx: Optional[Context] = None) -> None:
+    """Stage 1, augmented: gaug ((L+m) x (L+m) torch tensor) (+)= [H T]^T [H T] of the local rows."""
+    import torch
+
+    ctx = ctx or context(x.device.index or 0)
+    ctx.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
+    st = rbpg_status()
+    ctx.lib.rbpg_gram_stage_device_aug(ctx.handle, _tptr(x), _ld(x), _tptr(t), _ld(t), x.shape[0], x.shape[1],
+                                       w.shape[1], t.shape[1], _tptr(w), _ld(w), _tptr(b), _tptr(gaug), _ld(gaug),
+                                       int(accumulate), int(keep_h), ctypes.byref(st))
+    _raise(st)
+
+
+def solve_stage_device_aug(gaug, L: int, m: int, n_total: int, strategy: SolverStrategy,
+                           ctx: Optional[Context] = None, return_order: bool = False):
+    """Stage 2 on the all-reduced augmented Gram.  Returns (beta, diag[, order])."""
+    import torch
+
+    ctx = ctx or context(gaug.device.index or 0)
+    ctx.set_stream(torch.cuda.current_stream(gaug.device).cuda_stream)
+    beta = torch.empty((L, m), dtype=torch.float64, device=gaug.device)
+    order = np.zeros(L, dtype=np.uint64)
+    s = strategy._c()
+    d = rbpg_diagnostics()
+    st = rbpg_status()
+    ctx.lib.rbpg_solve_stage_device_aug(ctx.handle, _tptr(gaug), _ld(gaug), L, m, n_total, ctypes.byref(s),
+                                        _tptr(beta), m, _ptr(order) if return_order else None, ctypes.byref(d),
+                                        ctypes.byref(st))
+    _raise(st)
+    diag = SolveDiagnostics(strategy=strategy.describe())._fill(d)
+    if return_order:
+        return beta, diag, [int(v) for v in order]
+    return beta, diag
+
+
 def accuracy_stage_device(x, t, w, b, beta, ctx: Optional[Context] = None) -> int:
     """Stage 3: number of local rows whose argmax(H beta) matches argmax(T)."""
     import torch

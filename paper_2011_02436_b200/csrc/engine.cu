@@ -1535,6 +1535,31 @@ int rbpg_gram_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, cons
   });
 }
 
+int rbpg_gram_stage_device_aug(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in,
+                               size_t n, size_t d, size_t l, size_t m, const double* dw, size_t ldw, const double* db,
+                               double* dgaug, size_t ldga, int accumulate, int keep_h, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (ldga < l + m) fail(RBPG_SHAPE_ERROR, "gram_stage_device_aug: leading dimension below l + m");
+    Padded X = pad_device(ctx, "X.pad", dx, ldx, n, d);
+    Padded T = pad_device(ctx, "T.pad", dt, ldt_in, n, m);
+    Padded W = pad_device(ctx, "W.pad", dw, ldw, d, l);
+    gram_stage(ctx, X.p, X.ld, T.p, T.ld, n, d, l, m, W.p, W.ld, db, dgaug, ldga, accumulate != 0, keep_h != 0, false);
+  });
+}
+
+int rbpg_solve_stage_device_aug(rbpg_context* ctx, const double* dgaug, size_t ldga, size_t l, size_t m,
+                                size_t n_total, const rbpg_strategy* strategy, double* dbeta, size_t ldb,
+                                size_t* order_out, rbpg_diagnostics* diag, rbpg_status* st) {
+  rbpg_diagnostics local;
+  if (!diag) diag = &local;
+  zero_diag(diag);
+  return guarded(ctx, st, [&] {
+    if (ldga < l + m) fail(RBPG_SHAPE_ERROR, "solve_stage_device_aug: leading dimension below l + m");
+    solve_dev(ctx, dgaug, ldga, dgaug + l, ldga, l, m, n_total, *strategy, dbeta, ldb, order_out, diag, true);
+    check_finite(ctx, dbeta, ldb, l, m);
+  });
+}
+
 int rbpg_solve_stage_device(rbpg_context* ctx, const double* dg, size_t ldg, const double* dhtt, size_t ldt,
                             size_t l, size_t m, size_t n_total, const rbpg_strategy* strategy, double* dbeta,
                             size_t ldb, size_t* order_out, rbpg_diagnostics* diag, rbpg_status* st) {

@@ -1,10 +1,11 @@
 """Row-sharded training across ranks (one process per GPU).
 
 The hot path shards naturally by rows: each rank builds H for its
-contiguous block of rows and its local Gram blocks G_p = H_p^T H_p, (H^T T)_p;
-one all-reduce (sum) of G and H^T T; every rank then runs the identical
-pivoted-Cholesky + triangular solves, so beta is bitwise identical on all
-ranks; training-accuracy hits are a local count plus an all-reduce.
+contiguous block of rows and its local augmented Gram [H_p T_p]^T [H_p T_p]
+((L+m) x (L+m): G_p and (H^T T)_p in one buffer); ONE all-reduce (sum); every
+rank then runs the identical pivoted-Cholesky + triangular solve, so beta is
+bitwise identical on all ranks; training-accuracy hits are a local count plus an
+all-reduce.
 
 ``train_sharded`` is the orchestration; the per-rank numerical stages are a
 pluggable object.  ``DeviceStages`` (the product) runs them through the C ABI on
@@ -33,17 +34,16 @@ class DeviceStages:
     def __init__(self, ctx: Optional[api.Context] = None):
         self.ctx = ctx
 
-    def gram(self, x, t, w, b):
+    def gram_aug(self, x, t, w, b):
         import torch
 
-        L, m = w.shape[1], t.shape[1]
-        g = torch.empty((L, L), dtype=torch.float64, device=x.device)
-        htt = torch.empty((L, m), dtype=torch.float64, device=x.device)
-        api.gram_stage_device(x, t, w, b, g, htt, keep_h=True, ctx=self.ctx)
-        return g, htt
+        M = w.shape[1] + t.shape[1]
+        g = torch.empty((M, M), dtype=torch.float64, device=x.device)
+        api.gram_stage_device_aug(x, t, w, b, g, keep_h=True, ctx=self.ctx)
+        return g
 
-    def solve(self, g, htt, n_total: int, strategy: api.SolverStrategy):
-        return api.solve_stage_device(g, htt, n_total, strategy, ctx=self.ctx, return_order=True)
+    def solve_aug(self, gaug, L: int, m: int, n_total: int, strategy: api.SolverStrategy):
+        return api.solve_stage_device_aug(gaug, L, m, n_total, strategy, ctx=self.ctx, return_order=True)
 
     def hits(self, x, t, w, b, beta) -> int:
         return api.accuracy_stage_device(x, t, w, b, beta, ctx=self.ctx)
@@ -78,13 +78,13 @@ def train_sharded(x_local, t_local, params: api.ElmParams, strategy: api.SolverS
     hidden = hidden or api.init_hidden(params)  # identical on every rank (seeded mt19937_64)
     w = stages.as_tensor(hidden.weights, x_local)
     b = stages.as_tensor(hidden.biases.reshape(-1), x_local)
-    g, htt = stages.gram(x_local, t_local, w, b)
+    gaug = stages.gram_aug(x_local, t_local, w, b)
     distributed = dist.is_available() and dist.is_initialized()
     if distributed:
-        dist.all_reduce(g, group=group)
-        dist.all_reduce(htt, group=group)
-    beta, diag, order = stages.solve(g, htt, n_total, strategy)
-    hits = torch.tensor([stages.hits(x_local, t_local, w, b, beta)], dtype=torch.int64, device=g.device)
+        dist.all_reduce(gaug, group=group)  # the one exchange step of the path
+    L, m = w.shape[1], t_local.shape[1]
+    beta, diag, order = stages.solve_aug(gaug, L, m, n_total, strategy)
+    hits = torch.tensor([stages.hits(x_local, t_local, w, b, beta)], dtype=torch.int64, device=gaug.device)
     if distributed:
         dist.all_reduce(hits, group=group)
     diag.training_accuracy = float(hits.item()) / float(n_total)

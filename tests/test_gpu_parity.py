@@ -268,3 +268,33 @@ def test_triangular_solve_pair_sizes(n, m):
     perm = rb.ColumnPermutation(list(range(n)), n, 0.0)
     x = rb.solve_factored_gram(rb.RankRevealingFactor(perm, f), rhs)
     assert rel_fro(x, np.linalg.solve(f @ f.T, rhs)) < 1e-13
+
+
+def test_augmented_stage_api_row_shards():
+    """Row-sharded augmented stages on one device (the multi-GPU path without NCCL): three row
+    blocks accumulate [H T]^T [H T] in one buffer, one solve on it.  Pivots, rank and accuracy equal
+    the unsharded train(); beta within the reduction-order floor."""
+    import torch
+
+    n, d, L, m = 30000, 48, 600, 6
+    x, t = rb.synth_classification(n, d, m, 11, 12)
+    params = rb.ElmParams(d, L, m, 13)
+    hid = rb.init_hidden(params)
+    model, diag0, order0 = rb.train(params, x, t, rb.SolverStrategy.rank_based(), return_order=True)
+    W = torch.from_numpy(hid.weights).cuda()
+    B = torch.from_numpy(hid.biases.reshape(-1)).cuda()
+    gaug = torch.empty((L + m, L + m), dtype=torch.float64, device="cuda")
+    hits = 0
+    bounds = [(0, 9000), (9000, 21111), (21111, n)]
+    for i, (a, b) in enumerate(bounds):
+        X = torch.from_numpy(np.ascontiguousarray(x[a:b])).cuda()
+        T = torch.from_numpy(np.ascontiguousarray(t[a:b])).cuda()
+        rb.gram_stage_device_aug(X, T, W, B, gaug, accumulate=i > 0, keep_h=False)
+    beta, diag, order = rb.solve_stage_device_aug(gaug, L, m, n, rb.SolverStrategy.rank_based(), return_order=True)
+    for a, b in bounds:
+        X = torch.from_numpy(np.ascontiguousarray(x[a:b])).cuda()
+        T = torch.from_numpy(np.ascontiguousarray(t[a:b])).cuda()
+        hits += rb.accuracy_stage_device(X, T, W, B, beta)
+    assert diag.rank == diag0.rank == L and order == order0
+    assert hits / n == diag0.training_accuracy
+    assert rel_fro(beta.cpu().numpy(), model.beta) < 1e-9

@@ -24,18 +24,20 @@ class OracleStages:
     def as_tensor(self, x, like):
         return torch.as_tensor(np.asarray(x, dtype=np.float64))
 
-    def gram(self, x, t, w, b):
+    def gram_aug(self, x, t, w, b):
         import oracle
 
         h = oracle.hidden_matrix(w.numpy(), b.numpy().reshape(1, -1), x.numpy())
         self._h = h
-        return torch.from_numpy(oracle.gram(h)), torch.from_numpy(h.T @ t.numpy())
+        return torch.from_numpy(oracle.gram(np.hstack([h, t.numpy()])))
 
-    def solve(self, g, htt, n_total, strategy):
+    def solve_aug(self, gaug, L, m, n_total, strategy):
         import oracle
         import paper_2011_02436_b200 as rb
 
-        order, rank, _, f, _ = oracle.factor_gram(g.numpy(), n_total, strategy.rank_tol)
+        g = np.ascontiguousarray(gaug.numpy()[:L, :L])
+        htt = torch.from_numpy(np.ascontiguousarray(gaug.numpy()[:L, L:L + m]))
+        order, rank, _, f, _ = oracle.factor_gram(g, n_total, strategy.rank_tol)
         assert rank == g.shape[0]
         x = oracle.solve_factored_gram(f, order, rank, htt.numpy()[order])
         beta = np.empty_like(x)
