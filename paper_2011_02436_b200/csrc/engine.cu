@@ -248,23 +248,15 @@ void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_
 }
 
 // G (+)= A^T A over rows [0, N) of A (N x L, ld lda); HtT (+)= A^T T when m > 0.
-void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t L, const double* dT, size_t ldt_in,
-              size_t m, double* dG, size_t ldg, double* dHtT, size_t ldt, bool accumulate) {
-  SyrkParams p{};
-  p.M = static_cast<int>(L);
-  p.mB = static_cast<int>(m);
-  p.nbI = static_cast<int>((L + kTile - 1) / kTile);
-  p.nGram = p.nbI * (p.nbI + 1) / 2;
-  p.nbT = m > 0 ? static_cast<int>((m + kTile - 1) / kTile) : 0;
-  const int tiles = p.nGram + p.nbI * p.nbT;
-  // split-K count S (uniform row splits for every tile, so every Gram element sees the same
-  // arithmetic): greedy list scheduling of the tile x split CTAs on the SMs -- off-diagonal and
-  // H^T T tiles first, then the diagonal ones at ~0.56 of their work (72 of 128 fragments) --
-  // plus the fixed-order reduction of the S partials
+// split-K count S for a Gram of N rows (uniform row splits for every tile, so every Gram element
+// sees the same arithmetic): greedy list scheduling of the tile x split CTAs on the SMs --
+// off-diagonal and H^T T tiles first, then the diagonal ones at ~0.56 of their work (72 of 128
+// fragments) -- plus the fixed-order reduction of the S partials
+int gram_splits(rbpg_context* ctx, size_t N, size_t L, size_t m, int tiles, int nbI) {
   int splits = 1;
   if (tiles < 4 * ctx->num_sms) {
     const int P = ctx->num_sms;
-    const int nfull = tiles - (p.nbI >= 2 ? p.nbI : 0), ndiag = p.nbI >= 2 ? p.nbI : 0;
+    const int nfull = tiles - (nbI >= 2 ? nbI : 0), ndiag = nbI >= 2 ? nbI : 0;
     const double us_per_row = 2.0 * kTile * kTile / (35.7e12 / P) * 1e6;
     // fixed-order reduction: ~1 us per partial at L + m = 1010 (measured), quadratic in L + m
     const double finish_us_per_split = double(L + m) * double(L + m) / (1010.0 * 1010.0);
@@ -305,6 +297,19 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
       }
     }
   }
+  return splits;
+}
+
+void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t L, const double* dT, size_t ldt_in,
+              size_t m, double* dG, size_t ldg, double* dHtT, size_t ldt, bool accumulate) {
+  SyrkParams p{};
+  p.M = static_cast<int>(L);
+  p.mB = static_cast<int>(m);
+  p.nbI = static_cast<int>((L + kTile - 1) / kTile);
+  p.nGram = p.nbI * (p.nbI + 1) / 2;
+  p.nbT = m > 0 ? static_cast<int>((m + kTile - 1) / kTile) : 0;
+  const int tiles = p.nGram + p.nbI * p.nbT;
+  int splits = gram_splits(ctx, N, L, m, tiles, p.nbI);
   if (const char* e = std::getenv("RBPG_GRAM_SPLITS")) splits = std::max(1, std::atoi(e));  // tuning experiments
   long long per = static_cast<long long>(round_up((N + splits - 1) / splits, kBK));
   if (per == 0) per = kBK;
@@ -917,6 +922,8 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
       r0 = rr.end;
     }
     if (timed) cudaEventRecord(ctx->ev[1], ctx->stream);
+    // (a row-blocked Gram behind the uploads was measured slower: its per-block wave
+    // quantisation costs more than the hidden upload tail)
     gram_dev(ctx, dH, ldh, N, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate);
     if (keep_h) {
       ctx->kept_h = dH;

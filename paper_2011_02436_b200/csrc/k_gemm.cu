@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
   }
 
   // ---- epilogue.  Thread holds rows r, r+1 (r even) x cols c..c+3 per (mt, pp).
-  const int split = blockIdx.y;
+  const int split = p.split0 + blockIdx.y;
 
   // trailing mode: every G_old gather is issued before the first store (the stores could alias
   // the loads as far as the compiler knows, which would serialise one L2 round trip per element)
@@ -498,7 +498,7 @@ __global__ void __launch_bounds__(256, 1)
   // fragment (mt, nt): MMA row g / g+8 <-> tile row mt*16 + 2g / +1; MMA col j <-> tile col
   // (nt >> 1) * 16 + 2j + (nt & 1); lower elements only (mirrored in direct mode)
   const int ds = warp & 3, dh = warp >> 2;
-  double* out = (p.mode == kSyrkPartial) ? p.ws + blockIdx.y * p.wsStride : p.G;
+  double* out = (p.mode == kSyrkPartial) ? p.ws + (p.split0 + blockIdx.y) * p.wsStride : p.G;
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
     const int q = 9 * dh + i;

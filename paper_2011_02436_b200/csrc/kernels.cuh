@@ -54,6 +54,7 @@ struct SyrkParams {
   long long ldgo;        // trailing: leading dimension of Gold
   const int* lab;        // trailing: lab[p] = source index of position p (absolute)
   int off;               // trailing: first trailing position
+  int split0;            // partial: index of this launch's first split in ws (row-blocked Grams)
 };
 
 // ---- generic DMMA GEMM: C = alpha * op(A) op(B) + beta * C (row-major)
