@@ -241,10 +241,11 @@ void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_
                 size_t m = 0) {
   if (N == 0) return;
   CUtensorMap tmX = make_map(ctx, dX, d, N, ldx, 16, kTile, true);
-  CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, 64 + 4, kBK, false);  // padded smem rows
+  static const int bn = std::getenv("RBPG_HIDDEN_BN") ? std::atoi(std::getenv("RBPG_HIDDEN_BN")) : 32;
+  CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, bn + 4, kBK, false);  // padded smem rows
   HiddenParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), db, dH, static_cast<long long>(ldh),
                  0, m > 0 ? dT : nullptr, static_cast<long long>(ldt), static_cast<int>(m)};
-  ctx->run("hidden_kernel", [&] { return launch_hidden(tmX, tmW, p, 64, ctx->stream); });
+  ctx->run("hidden_kernel", [&] { return launch_hidden(tmX, tmW, p, bn, ctx->stream); });
 }
 
 // G (+)= A^T A over rows [0, N) of A (N x L, ld lda); HtT (+)= A^T T when m > 0.

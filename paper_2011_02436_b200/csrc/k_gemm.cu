@@ -60,8 +60,8 @@ __device__ __forceinline__ double recip_ge1(double x) {
 // CUDA-core pipe) overlaps the other's DMMA main loop (tensor pipe).  BN = 128 (one CTA per SM)
 // serves the plain transposed product of the pseudo-inverse, which has no epilogue to hide.
 // ============================================================================
-template <int BN>
-__global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
+template <int BN, int NS = 4>
+__global__ void __launch_bounds__(kGemmThreads, BN == 32 ? 3 : (BN == 64 ? 2 : 1))
     hidden_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, HiddenParams p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = align1024(smem_raw);
@@ -70,8 +70,8 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
   // fragment loads then start on different banks (an unpadded 512 / 1024-byte row stride maps
   // the 4 k rows onto the same banks: 4-way conflicts)
   constexpr int BNP = BN + 4;
-  double* Ws = Xs + kStages * kTile * kBK;             // [stage][16][BNP]
-  uint64_t* full = reinterpret_cast<uint64_t*>(Ws + kStages * kBK * BNP);
+  double* Ws = Xs + NS * kTile * kBK;             // [stage][16][BNP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Ws + NS * kBK * BNP);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int l0 = blockIdx.x * BN, n0 = blockIdx.y * kTile;
@@ -81,12 +81,12 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
   if (tid == 0) {
     tma_prefetch_desc(&tmX);
     tma_prefetch_desc(&tmW);
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid == 0) {
-    for (int s = 0; s < kStages && s < ktiles; ++s) {
+    for (int s = 0; s < NS && s < ktiles; ++s) {
       mbar_arrive_expect_tx(&full[s], kStageBytes);
       tma_load_2d(Xs + s * kTile * kBK, &tmX, &full[s], s * kBK, n0);
       tma_load_2d(Ws + s * kBK * BNP, &tmW, &full[s], l0, s * kBK);
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
   }
 
   // warp tile: 64 x 32 (BN = 128: 2 x 4 warps) or 32 x 32 (BN = 64: 4 x 2 warps)
-  constexpr int MT = BN == 128 ? 4 : 2;
+  constexpr int MT = BN == 128 ? 4 : (BN == 64 ? 2 : 1);
   constexpr int WARPS_N = BN / 32;
   const int wm = (warp / WARPS_N) * (MT * 16), wn = (warp % WARPS_N) * 32;
   double acc[MT][4][4];
@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
       for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
 
   for (int kt = 0; kt < ktiles; ++kt) {
-    const int s = kt % kStages;
-    mbar_wait(&full[s], (kt / kStages) & 1);
+    const int s = kt % NS;
+    mbar_wait(&full[s], (kt / NS) & 1);
     const double* xs = Xs + s * kTile * kBK;
     const double* ws = Ws + s * kBK * BNP;
 #pragma unroll
@@ -132,8 +132,8 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 64 ? 2 : 1)
         for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
     }
     __syncthreads();
-    if (tid == 0 && kt + kStages < ktiles) {
-      const int kn = kt + kStages;
+    if (tid == 0 && kt + NS < ktiles) {
+      const int kn = kt + NS;
       mbar_arrive_expect_tx(&full[s], kStageBytes);
       tma_load_2d(Xs + s * kTile * kBK, &tmX, &full[s], kn * kBK, n0);
       tma_load_2d(Ws + s * kBK * BNP, &tmW, &full[s], l0, kn * kBK);
@@ -664,7 +664,15 @@ cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const 
     attr = true;
   }
   dim3 grid((p.L + bn - 1) / bn, (p.N + kTile - 1) / kTile);
-  if (bn == 64)
+  if (bn == 32) {
+    constexpr size_t kSmem32 = size_t(3) * (kTile + 36) * kBK * sizeof(double) + 1024 + 256;
+    static bool a32 = false;
+    if (!a32) {
+      cudaFuncSetAttribute(hidden_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem32);
+      a32 = true;
+    }
+    hidden_kernel<32, 3><<<grid, kGemmThreads, kSmem32, s>>>(tmX, tmW, p);
+  } else if (bn == 64)
     hidden_kernel<64><<<grid, kGemmThreads, kSmem64, s>>>(tmX, tmW, p);
   else
     hidden_kernel<128><<<grid, kGemmThreads, kSmem128, s>>>(tmX, tmW, p);
