@@ -75,7 +75,12 @@ def test_hidden_matrix_parity_c1():
 
 
 @pytest.mark.parametrize("shape", [(5, 3, 1, 1), (40, 5, 10, 3), (129, 7, 65, 3), (300, 33, 129, 5),
-                                   (1000, 17, 257, 7), (4097, 130, 300, 1), (700, 3, 64, 2)])
+                                   (1000, 17, 257, 7), (4097, 130, 300, 1), (700, 3, 64, 2),
+                                   # m = 32 / 33: the augmented-factorisation boundary (forward sweep
+                                   # inside the panels vs. the two-sweep TRSM)
+                                   (3000, 20, 200, 32), (3000, 20, 200, 33),
+                                   # L + m = 1025: the first panel on the shared-memory cluster variant
+                                   (6000, 40, 1015, 10), (8000, 30, 1200, 4)])
 def test_train_parity_ragged_shapes(shape):
     n, d, L, m = shape
     x, t, model, diag, order, ref = train_both(n, d, L, m, seeds=(n, d + 1, L + 2))
@@ -298,3 +303,23 @@ def test_augmented_stage_api_row_shards():
     assert diag.rank == diag0.rank == L and order == order0
     assert hits / n == diag0.training_accuracy
     assert rel_fro(beta.cpu().numpy(), model.beta) < 1e-9
+
+
+@pytest.mark.parametrize("kind,split", [("direct", 0), ("df", 400), ("df", 1)])
+def test_other_strategies_at_scale(kind, split):
+    """direct (unpivoted SpdFactor panels, elm.cpp:108-122) and df splits (Schur block path on Gram
+    sub-blocks, elm.cpp:124-185) at N = 20000, L = 800 against the oracle."""
+    n, d, L, m = 20000, 32, 800, 5
+    x, t = rb.synth_classification(n, d, m, 41, 42)
+    params = rb.ElmParams(d, L, m, 43)
+    strat = rb.SolverStrategy.direct() if kind == "direct" else rb.SolverStrategy.df_split(split)
+    model, diag = rb.train(params, x, t, strat)
+    ref = oracle.train(d, L, m, 43, x, t, kind, split, 0.0)
+    h = oracle.hidden_matrix(ref["w"], ref["b"], x)
+    for k in ("ridge_applied", "fallback_to_direct", "used_svd_path"):
+        assert getattr(diag, k) == bool(ref["diag"][k]), k
+    floor = rel_fro(h @ (np.linalg.pinv(h) @ t), h @ ref["beta"])
+    err = rel_fro(h @ model.beta, h @ ref["beta"])
+    print(f"{kind}:{split}: fitted rel {err:.2e} (floor {floor:.2e}), beta rel {rel_fro(model.beta, ref['beta']):.2e}")
+    assert err <= max(1e-9, 4 * floor)
+    assert diag.training_accuracy == ref["diag"]["training_accuracy"]
