@@ -32,6 +32,51 @@ inline double normal01(std::mt19937_64& gen) {
   return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
 }
 
+// std::mt19937_64 (the C++ standard's parameters: n = 312, m = 156, r = 31,
+// a = 0xB5026F5AA96619E9, tempering u = 29 / d = 0x5555555555555555, s = 17 / b = 0x71D67FFFEDA60000,
+// t = 37 / c = 0xFFF7EEE000000000, l = 43, seeding f = 6364136223846793005), generated a whole
+// 312-word block at a time: the twist and the tempering are straight loops the compiler
+// vectorises.  Output-identical to std::mt19937_64 (pinned in the CPU tests); init_hidden sits on
+// the end-to-end critical path (the hidden build waits for W).
+class Mt64Block {
+ public:
+  explicit Mt64Block(std::uint64_t seed) {
+    mt_[0] = seed;
+    for (int i = 1; i < kN; ++i) mt_[i] = 6364136223846793005ull * (mt_[i - 1] ^ (mt_[i - 1] >> 62)) + i;
+    pos_ = kN;
+  }
+  std::uint64_t operator()() {
+    if (pos_ == kN) refill();
+    return out_[pos_++];
+  }
+
+ private:
+  static constexpr int kN = 312, kM = 156;
+  static constexpr std::uint64_t kA = 0xB5026F5AA96619E9ull, kUpper = 0xFFFFFFFF80000000ull,
+                                 kLower = 0x7FFFFFFFull;
+  static inline std::uint64_t twist(std::uint64_t a, std::uint64_t b, std::uint64_t c) {
+    const std::uint64_t y = (a & kUpper) | (b & kLower);
+    return c ^ (y >> 1) ^ ((y & 1ull) ? kA : 0ull);
+  }
+  void refill() {
+    for (int i = 0; i < kN - kM; ++i) mt_[i] = twist(mt_[i], mt_[i + 1], mt_[i + kM]);
+    for (int i = kN - kM; i < kN - 1; ++i) mt_[i] = twist(mt_[i], mt_[i + 1], mt_[i + kM - kN]);
+    mt_[kN - 1] = twist(mt_[kN - 1], mt_[0], mt_[kM - 1]);
+    for (int i = 0; i < kN; ++i) {
+      std::uint64_t z = mt_[i];
+      z ^= (z >> 29) & 0x5555555555555555ull;
+      z ^= (z << 17) & 0x71D67FFFEDA60000ull;
+      z ^= (z << 37) & 0xFFF7EEE000000000ull;
+      z ^= z >> 43;
+      out_[i] = z;
+    }
+    pos_ = 0;
+  }
+  std::uint64_t mt_[kN];
+  std::uint64_t out_[kN];
+  int pos_;
+};
+
 constexpr std::size_t kBlockRows = 65536;
 inline std::uint64_t block_seed(std::uint64_t seed, std::size_t block) {
   return seed ^ (0x9E3779B97F4A7C15ull * static_cast<std::uint64_t>(block + 1));
@@ -49,10 +94,10 @@ int rbpg_init_hidden(size_t inputs, size_t hidden, size_t outputs, uint64_t seed
     set_status(st, RBPG_INVALID_ARGUMENT, "ElmParams: inputs, hidden_nodes and outputs must be >= 1");
     return RBPG_INVALID_ARGUMENT;
   }
-  std::mt19937_64 gen(seed);
+  Mt64Block gen(seed);
   for (size_t i = 0; i < inputs; ++i)
-    for (size_t j = 0; j < hidden; ++j) w[i * hidden + j] = 2.0 * unit53(gen) - 1.0;
-  for (size_t j = 0; j < hidden; ++j) b[j] = 2.0 * unit53(gen) - 1.0;
+    for (size_t j = 0; j < hidden; ++j) w[i * hidden + j] = 2.0 * (static_cast<double>(gen() >> 11) * 0x1.0p-53) - 1.0;
+  for (size_t j = 0; j < hidden; ++j) b[j] = 2.0 * (static_cast<double>(gen() >> 11) * 0x1.0p-53) - 1.0;
   set_status(st, RBPG_OK, "");
   return RBPG_OK;
 }
