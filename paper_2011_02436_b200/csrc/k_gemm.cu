@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 32 ? 3 : (BN == 64 ? 2 : 1
     }
   }
 
-  // warp tile: 64 x 32 (BN = 128: 2 x 4 warps) or 32 x 32 (BN = 64: 4 x 2 warps)
+  // warp tile: 64 x 32 (BN = 128: 2 x 4 warps), 32 x 32 (BN = 64: 4 x 2 warps) or 16 x 32 (BN = 32: 8 x 1)
   constexpr int MT = BN == 128 ? 4 : (BN == 64 ? 2 : 1);
   constexpr int WARPS_N = BN / 32;
   const int wm = (warp / WARPS_N) * (MT * 16), wn = (warp % WARPS_N) * 32;
