@@ -105,6 +105,9 @@ __device__ __forceinline__ void bulk_s2s_cluster(uint32_t cluster_dst, uint32_t 
       "r"(src), "r"(bytes), "r"(cluster_mbar)
       : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
@@ -136,5 +139,19 @@ __device__ __forceinline__ double ld_volatile_f64(const double* p) {
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+// Optional device timeline (RBPG_DEVICE_TIMELINE): slot s of tl holds {first entry, first start
+// of work, last exit} over a launch's CTAs, in globaltimer nanoseconds.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void tl_mark(unsigned long long* tl, int slot, int phase) {
+  if (tl == nullptr || threadIdx.x != 0) return;
+  const unsigned long long t = gtimer();
+  if (phase < 2) atomicMin(&tl[3 * slot + phase], t);
+  else atomicMax(&tl[3 * slot + 2], t);
+}
 
 }  // namespace rbpg

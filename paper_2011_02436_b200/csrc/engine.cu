@@ -38,6 +38,8 @@ cudaError_t launch_scores(const CUtensorMap&, const CUtensorMap&, const ScoresPa
 cudaError_t launch_factor_setup(const double*, long long, int, int, long long, double, int, double*, int*,
                                 FactorState*, cudaStream_t);
 cudaError_t launch_panel(const PanelParams&, int, int*, cudaStream_t);
+bool panel_is_reg(int nl);
+cudaError_t launch_trail(const CUtensorMap&, const SyrkParams&, int, cudaStream_t);
 cudaError_t launch_gather_factor(const double*, long long, const int*, int, double*, long long, const FactorState*,
                                  int, cudaStream_t);
 cudaError_t launch_gather_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
@@ -407,6 +409,21 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     trace = static_cast<unsigned long long*>(ctx->buf(tag + ".ptrace", 64));
     ck(cudaMemsetAsync(trace, 0, 64, s), "memset trace");
   }
+  // RBPG_DEVICE_TIMELINE: {entry, start of work, exit} of every panel / trailing launch
+  unsigned long long* tl = nullptr;
+  const int tl_max = 512;
+  int tl_n = 0;
+  std::vector<char> tl_kind;
+  if (std::getenv("RBPG_DEVICE_TIMELINE")) {
+    tl = static_cast<unsigned long long*>(ctx->buf(tag + ".tl", sizeof(unsigned long long) * 3 * tl_max));
+    std::vector<unsigned long long> init(3 * tl_max);
+    for (int i = 0; i < tl_max; ++i) {
+      init[3 * i] = init[3 * i + 1] = ~0ull;
+      init[3 * i + 2] = 0;
+    }
+    ck(cudaMemcpyAsync(tl, init.data(), sizeof(unsigned long long) * 3 * tl_max, cudaMemcpyHostToDevice, s), "tl init");
+    ck(cudaStreamSynchronize(s), "tl init sync");
+  }
   if (n > 4096) {  // the grid panel variant's global mirror and exchange slots
     ck(cudaMemsetAsync(Pg, 0, sizeof(double) * n * 64, s), "memset Pg");
     ck(cudaMemsetAsync(slots, 0, sizeof(PivotSlot) * 2 * (max_ctas + 32), s), "memset slots");
@@ -444,13 +461,22 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     pp.rows_per_cta = 0;  // chosen by launch_panel
     pp.neligible = static_cast<int>(neligible);
     pp.trace = trace;
+    if (tl && tl_n < tl_max) {
+      pp.tl = tl;
+      pp.tl_slot = tl_n++;
+      tl_kind.push_back('P');
+    }
     ctx->run("panel_kernel", [&] { return launch_panel(pp, ctx->num_sms, nullptr, s); });
     const size_t t0 = k + kb;
     if (t0 < neligible) {  // another panel follows
       const size_t nrem = n - t0;
-      // 64-wide tiles while 128-wide ones would not fill two waves of SMs
-      const size_t nb128 = (nrem + kTile - 1) / kTile;
-      const int ttile = (nb128 * (nb128 + 1) / 2 < size_t(2 * ctx->num_sms)) ? 64 : kTile;
+      // 32-wide tiles while they fit in three waves (the late, small updates: their DMMA work per
+      // SM is what bounds the update), then 64-wide while 128-wide ones would not fill two waves
+      const size_t nb32 = (nrem + 31) / 32, nb64 = (nrem + 63) / 64, nb128 = (nrem + kTile - 1) / kTile;
+      const int ttile = (nb32 * (nb32 + 1) / 2 <= size_t(3 * ctx->num_sms))   ? 32
+                        : (nb128 * (nb128 + 1) / 2 < size_t(2 * ctx->num_sms)) ? 64
+                                                                                : kTile;
+      (void)nb64;
       CUtensorMap tm = make_map(ctx, PcT, nrem, static_cast<uint64_t>(kb), ldp, ttile + 4, kBK, false);
       SyrkParams sp{};
       sp.M = static_cast<int>(nrem);
@@ -466,7 +492,18 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
       sp.ldgo = static_cast<long long>(ldcur);
       sp.lab = lab;
       sp.off = static_cast<int>(t0);
-      ctx->run("syrk_trailing", [&] { return launch_syrk(tm, tm, sp, 1, ttile, s, true); });
+      // the register-resident panel reads G through its lower triangle; the others read rows
+      sp.mirror = panel_is_reg(static_cast<int>(n - t0)) ? 0 : 1;
+      if (tl && tl_n < tl_max) {
+        sp.tl = tl;
+        sp.tl_slot = tl_n++;
+        tl_kind.push_back('T');
+      }
+      if (ttile == kTile) {
+        ctx->run("syrk_trailing", [&] { return launch_syrk(tm, tm, sp, 1, ttile, s, true); });
+      } else {
+        ctx->run("syrk_trailing", [&] { return launch_trail(tm, sp, ttile, s); });
+      }
       double* written = gnext;
       gnext = (written == Ga) ? Gb : Ga;
       gcur = written;
@@ -485,6 +522,20 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
   if (sync) {
     ck(cudaStreamSynchronize(s), "factor sync");
     r.st = *hs;
+  }
+  if (tl) {
+    std::vector<unsigned long long> h(3 * tl_n);
+    ck(cudaStreamSynchronize(s), "tl sync");
+    ck(cudaMemcpy(h.data(), tl, sizeof(unsigned long long) * 3 * tl_n, cudaMemcpyDeviceToHost), "tl read");
+    const unsigned long long base = h.empty() ? 0 : h[0];
+    unsigned long long prev_end = base;
+    for (int i = 0; i < tl_n; ++i) {
+      std::fprintf(stderr, "[tl %s] %c%-3d entry %8.2f start %8.2f end %8.2f  dur %7.2f  gap %6.2f us\n", tag.c_str(),
+                   tl_kind[i], i, (h[3 * i] - base) * 1e-3, (h[3 * i + 1] - base) * 1e-3, (h[3 * i + 2] - base) * 1e-3,
+                   (double(h[3 * i + 2]) - double(h[3 * i + 1])) * 1e-3,
+                   (double(h[3 * i + 1]) - double(prev_end)) * 1e-3);
+      prev_end = h[3 * i + 2];
+    }
   }
   if (trace) {
     unsigned long long h[7];

@@ -249,8 +249,10 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
+  tl_mark(p.tl, p.tl_slot, 0);
   pdl_trigger();  // PART 1: the diagonal-tile grid (this grid's dependent) may start launching
   if (PART == 0) pdl_wait();  // trailing mode: the panel that wrote PcT / lab may still be finishing
+  tl_mark(p.tl, p.tl_slot, 1);
   __syncthreads();
   if (tid == 0) {
     for (int s = 0; s < kStages && s < ktiles; ++s) {
@@ -405,6 +407,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
       }
     }
   }
+  tl_mark(p.tl, p.tl_slot, 2);
 }
 
 // One 16-deep k-slab of a diagonal 128-wide Gram tile for warp (DS, DH): its 9 lower-triangle
@@ -514,6 +517,164 @@ __global__ void __launch_bounds__(256, 1)
       if (p.mode != kSyrkPartial) out[(long long)c * p.ldg + r] = acc[i][e];
     }
   }
+}
+
+// Trailing update of the blocked pivoted Cholesky (K2 in trailing mode, behind every panel but
+// the last): G_new[t0 + r][t0 + c] = G_old[lab[t0 + r]][lab[t0 + c]] - sum_cc PcT[cc][r] PcT[cc][c]
+// for r >= c.  K = the panel width (<= 64), so every k-stage is loaded up front.  The G_old gathers
+// (two dependent L2 round trips: label, then entry) are issued as cp.async into shared memory
+// before the DMMAs, in a thread-interleaved layout (element e of thread t at [e][t]: conflict-free),
+// so their latency hides under the tensor-core work.  G_old is read through its lower triangle
+// (G[max][min]) and G_new is written lower-only unless p.mirror (the next panel reads whole rows).
+// TILE 32 (64 threads) for the small late updates: four times the CTAs per DMMA of a 64-wide tile.
+template <int TILE>
+__global__ void __launch_bounds__(2 * TILE, 1)
+    trail_kernel(const __grid_constant__ CUtensorMap tmP, SyrkParams p) {
+  constexpr int NT = 2 * TILE;      // threads: warps of (TILE / 2) x 32
+  constexpr int TP = TILE + 4;      // padded smem rows (TMA box {TILE + 4, 16})
+  constexpr int MT = TILE / 32;     // m16 fragments per warp
+  constexpr int WARPS_N = TILE / 32;
+  constexpr int NG = MT * 2 * 2 * 4;  // G_old entries per thread
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = align1024(smem_raw);
+  double* As = reinterpret_cast<double*>(smem);  // [stage][16][TP]
+  double* Bs = As + kStages * kBK * TP;          // [stage][16][TP]
+  double* gsm = Bs + kStages * kBK * TP;         // [NG][NT]
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm + NG * NT);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  int I, J;
+  {
+    const int bx = blockIdx.x;
+    int i = static_cast<int>((sqrtf(8.0f * bx + 1.0f) - 1.0f) * 0.5f);
+    while (i * (i + 1) / 2 > bx) --i;
+    while ((i + 1) * (i + 2) / 2 <= bx) ++i;
+    I = i;
+    J = bx - i * (i + 1) / 2;
+  }
+  const int i0 = I * TILE, j0 = J * TILE;
+  const bool diag = I == J;
+  const int ktiles = static_cast<int>((p.kRows + kBK - 1) / kBK);  // <= kStages (launcher checks)
+  const uint32_t stage_bytes = (diag ? 1u : 2u) * TP * kBK * sizeof(double);
+  if (tid == 0) {
+    tma_prefetch_desc(&tmP);
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  tl_mark(p.tl, p.tl_slot, 0);
+  if (!p.late_trigger) pdl_trigger();
+  pdl_wait();  // the panel that wrote PcT / lab may still be finishing
+  if (p.late_trigger) pdl_trigger();
+  tl_mark(p.tl, p.tl_slot, 1);
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < ktiles; ++s) {
+      mbar_arrive_expect_tx(&full[s], stage_bytes);
+      tma_load_2d(As + s * kBK * TP, &tmP, &full[s], i0, s * kBK);
+      if (!diag) tma_load_2d(Bs + s * kBK * TP, &tmP, &full[s], j0, s * kBK);
+    }
+  }
+  const int wm = (warp / WARPS_N) * (TILE / 2), wn = (warp % WARPS_N) * 32;
+  const int M = p.M, off = p.off;
+  {  // G_old gathers -> gsm
+    int sr[MT][2], sc[2][4];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = i0 + wm + mt * 16 + 2 * g + h;
+        sr[mt][h] = r < M ? __ldg(p.lab + off + r) : 0;
+      }
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = j0 + wn + pp * 16 + 4 * t + q;
+        sc[pp][q] = c < M ? __ldg(p.lab + off + c) : 0;
+      }
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = i0 + wm + mt * 16 + 2 * g + h, c = j0 + wn + pp * 16 + 4 * t + q;
+            if (r < M && c <= r) {
+              const int a = max(sr[mt][h], sc[pp][q]), b = min(sr[mt][h], sc[pp][q]);
+              cp_async8(gsm + (((mt * 2 + pp) * 2 + h) * 4 + q) * NT + tid, p.Gold + (long long)a * p.ldgo + b);
+            }
+          }
+    cp_async_commit();
+  }
+
+  double acc[MT][4][4];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
+  for (int kt = 0; kt < ktiles; ++kt) {
+    mbar_wait(&full[kt], 0);
+    const double* as = As + kt * kBK * TP;
+    const double* bs = diag ? as : Bs + kt * kBK * TP;
+#pragma unroll
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const int kc = ks * 4 + t;
+      double a[MT][2], b[4];
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const double2 v = *reinterpret_cast<const double2*>(as + kc * TP + wm + mt * 16 + 2 * g);
+        a[mt][0] = v.x;
+        a[mt][1] = v.y;
+      }
+#pragma unroll
+      for (int pp = 0; pp < 2; ++pp) {
+        const double2 w = *reinterpret_cast<const double2*>(bs + kc * TP + wn + pp * 16 + 2 * g);
+        b[2 * pp] = w.x;
+        b[2 * pp + 1] = w.y;
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_16x8x4(acc[mt][nt], a[mt][0], a[mt][1], b[nt]);
+    }
+  }
+  cp_async_wait_all();  // this thread's own gathers (it reads nothing another thread copied)
+
+  // ---- epilogue.  Thread holds rows r, r+1 x cols c..c+3 per (mt, pp) (see syrk_kernel).
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = i0 + wm + mt * 16 + 2 * g + h, c0 = j0 + wn + pp * 16 + 4 * t;
+        if (r >= M || c0 > r) continue;
+        double v[4];
+        v[0] = acc[mt][2 * pp][2 * h];
+        v[1] = acc[mt][2 * pp + 1][2 * h];
+        v[2] = acc[mt][2 * pp][2 * h + 1];
+        v[3] = acc[mt][2 * pp + 1][2 * h + 1];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = sub_rn(gsm[(((mt * 2 + pp) * 2 + h) * 4 + q) * NT + tid], v[q]);
+        double* dst = p.G + (long long)(off + r) * p.ldg + off + c0;
+        if (c0 + 3 <= r) {
+          reinterpret_cast<double2*>(dst)[0] = make_double2(v[0], v[1]);
+          reinterpret_cast<double2*>(dst)[1] = make_double2(v[2], v[3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c0 + q <= r) dst[q] = v[q];
+        }
+        if (p.mirror) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c0 + q < r) p.G[(long long)(off + c0 + q) * p.ldg + off + r] = v[q];
+        }
+      }
+  tl_mark(p.tl, p.tl_slot, 2);
 }
 
 // Fixed-order split reduction: G[i][j] = G[j][i] = (acc ? G[i][j] : 0) + sum_s ws[s][i][j] over the
@@ -744,6 +905,46 @@ cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const Sy
     cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = smem;
     return cudaLaunchKernelEx(&cfg, syrk_kernel<64>, tmA, tmB, p);
+  }
+  return cudaErrorInvalidValue;
+}
+
+template <int TILE>
+constexpr size_t trail_smem() {
+  return size_t(kStages) * 2 * (TILE + 4) * kBK * sizeof(double) + size_t(TILE / 32) * 16 * 2 * TILE * sizeof(double) +
+         1024 + 256;
+}
+
+// Trailing update (tile 32 or 64); the tensor map covers PcT with box {tile + 4, 16}.
+cudaError_t launch_trail(const CUtensorMap& tmP, const SyrkParams& p, int tile, cudaStream_t s) {
+  if (p.kRows > kStages * kBK) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.nbI * (p.nbI + 1) / 2);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (tile == 64) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(trail_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trail_smem<64>());
+      attr = true;
+    }
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = trail_smem<64>();
+    return cudaLaunchKernelEx(&cfg, trail_kernel<64>, tmP, p);
+  }
+  if (tile == 32) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(trail_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trail_smem<32>());
+      attr = true;
+    }
+    cfg.blockDim = dim3(64);
+    cfg.dynamicSmemBytes = trail_smem<32>();
+    return cudaLaunchKernelEx(&cfg, trail_kernel<32>, tmP, p);
   }
   return cudaErrorInvalidValue;
 }

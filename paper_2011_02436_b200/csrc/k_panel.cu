@@ -461,12 +461,15 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   __shared__ Cand wbest[kPWarps];
   __shared__ int s_stop;
 
+  tl_mark(p.tl, p.tl_slot, 0);
   pdl_trigger();
   pdl_wait();  // the previous trailing update / panel may still be finishing
+  tl_mark(p.tl, p.tl_slot, 1);
   FactorState* st = p.st;
   if (st->stopped) {
     if (cta == 0)
       for (int i = tid; i < n; i += blockDim.x) p.ord_out[i] = p.ord_in[i];
+    tl_mark(p.tl, p.tl_slot, 2);
     return;
   }
   const int lbeg = k + cta * R;
@@ -592,7 +595,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     int pos = -1;
     if (mine) pos = (x == y) ? piv : (x == xp ? j : mypos);
     const bool alive = pos > j;
-    const double gv = alive ? p.G[(long long)xp * p.ldg + x] : 0.0;
+    // G through its lower triangle (trailing updates behind this variant write only that half)
+    const double gv = alive ? p.G[(long long)max(xp, x) * p.ldg + min(xp, x)] : 0.0;
     bool stop;
     if (p.pivoting) {
       stop = (dj > 0.0 ? sqrt(dj) : 0.0) <= cut;            // linalg.cpp:219-223
@@ -731,6 +735,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
       p.lab_out[ps] = lb;
     }
   }
+  tl_mark(p.tl, p.tl_slot, 2);
 }
 
 // ---------------------------------------------------------------------------
@@ -746,11 +751,17 @@ int panel_cluster_size(int nl) {
   return 0;
 }
 
+// Whether a panel of nl labels runs panel_reg_kernel (which reads G through its lower triangle).
+bool panel_is_reg(int nl) {
+  const int CL = panel_cluster_size(nl);
+  return CL > 0 && (nl + CL - 1) / CL <= kRegLabels && !std::getenv("RBPG_PANEL_SMEM");
+}
+
 cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cudaStream_t s) {
   const int nl = p.n - p.k;
   PanelParams pp = p;
   const int CL = panel_cluster_size(nl);
-  if (CL > 0 && (nl + CL - 1) / CL <= kRegLabels && !std::getenv("RBPG_PANEL_SMEM")) {
+  if (panel_is_reg(nl)) {
     pp.rows_per_cta = (nl + CL - 1) / CL;
     const size_t smem = size_t(2) * nl * sizeof(int);
     static size_t attr = 0;

@@ -55,6 +55,9 @@ struct SyrkParams {
   const int* lab;        // trailing: lab[p] = source index of position p (absolute)
   int off;               // trailing: first trailing position
   int split0;            // partial: index of this launch's first split in ws (row-blocked Grams)
+  unsigned long long* tl; int tl_slot;  // optional device timeline
+  int late_trigger;      // trailing: release the dependent launch only after the panel before has completed
+  int mirror;            // trailing: also write the upper triangle (the next panel reads whole rows)
 };
 
 // ---- generic DMMA GEMM: C = alpha * op(A) op(B) + beta * C (row-major)
@@ -111,6 +114,7 @@ struct PanelParams {
   int rows_per_cta;
   int neligible;                        // labels >= neligible are never pivots (augmented right-hand sides)
   unsigned long long* trace;                   // optional per-phase cycle counters (CTA 0, thread 0)
+  unsigned long long* tl; int tl_slot;         // optional device timeline
 };
 
 }  // namespace rbpg
