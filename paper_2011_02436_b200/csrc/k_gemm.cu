@@ -116,9 +116,11 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 32 ? 3 : (BN == 64 ? 2 : 1
       double a[MT][2], b[4];
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) {
-        const int r = wm + mt * 16 + g;
+        // MMA rows g, g + 8 <-> tile rows 2g, 2g + 1: a half-warp's 8-byte loads then cover the
+        // 8 swizzled 16-byte chunks once (rows g, g + 1 would pair up on the same chunks)
+        const int r = wm + mt * 16 + 2 * g;
         a[mt][0] = xs[swz16(r, kc)];
-        a[mt][1] = xs[swz16(r + 8, kc)];
+        a[mt][1] = xs[swz16(r + 1, kc)];
       }
 #pragma unroll
       for (int pp = 0; pp < 2; ++pp) {
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 32 ? 3 : (BN == 64 ? 2 : 1
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int r = n0 + wm + mt * 16 + g + (q >> 1) * 8;
+          const int r = n0 + wm + mt * 16 + 2 * g + (q >> 1);
           const int c = l0 + wn + (nt >> 1) * 16 + 4 * t + 2 * (q & 1) + (nt & 1);
           if (r < p.N && c < p.L) p.H[(long long)c * p.ldh + r] = acc[mt][nt][q];
         }
@@ -170,7 +172,7 @@ __global__ void __launch_bounds__(kGemmThreads, BN == 32 ? 3 : (BN == 64 ? 2 : 1
       const int cb = l0 + wn + pp * 16 + 4 * t;
 #pragma unroll
       for (int half = 0; half < 2; ++half) {
-        const int r = n0 + wm + mt * 16 + g + half * 8;
+        const int r = n0 + wm + mt * 16 + 2 * g + half;
         if (r >= p.N) continue;
         double v[4] = {acc[mt][2 * pp][2 * half], acc[mt][2 * pp + 1][2 * half], acc[mt][2 * pp][2 * half + 1],
                        acc[mt][2 * pp + 1][2 * half + 1]};
@@ -970,8 +972,9 @@ __global__ void __launch_bounds__(kGemmThreads)
   unsigned char* smem = align1024(smem_raw);
   constexpr int kS = 4;
   double* Hs = reinterpret_cast<double*>(smem);        // [stage][128][16] swizzled
-  double* Bs = Hs + kS * kTile * kBK;                  // [stage][16][BN]
-  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kS * kBK * BN);
+  constexpr int BNP = BN + 4;                          // padded B rows (TMA box {BN + 4, 16})
+  double* Bs = Hs + kS * kTile * kBK;                  // [stage][16][BNP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kS * kBK * BNP);
   double* sc = reinterpret_cast<double*>(smem);  // [128][BN+1], aliases the drained pipeline
   constexpr int SCL = BN + 1;
   __shared__ unsigned long long blk_hits;
@@ -979,7 +982,7 @@ __global__ void __launch_bounds__(kGemmThreads)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int r0 = blockIdx.x * kTile;
   const int ktiles = (p.L + kBK - 1) / kBK;
-  constexpr uint32_t kStageBytes = (kTile * kBK + kBK * BN) * sizeof(double);
+  constexpr uint32_t kStageBytes = (kTile * kBK + kBK * BNP) * sizeof(double);
   if (tid == 0) {
     tma_prefetch_desc(&tmH);
     tma_prefetch_desc(&tmB);
@@ -992,7 +995,7 @@ __global__ void __launch_bounds__(kGemmThreads)
     for (int s = 0; s < kS && s < ktiles; ++s) {
       mbar_arrive_expect_tx(&full[s], kStageBytes);
       tma_load_2d(Hs + s * kTile * kBK, &tmH, &full[s], s * kBK, r0);
-      tma_load_2d(Bs + s * kBK * BN, &tmB, &full[s], 0, s * kBK);
+      tma_load_2d(Bs + s * kBK * BNP, &tmB, &full[s], 0, s * kBK);
     }
   }
   constexpr int NT = BN / 8;
@@ -1006,15 +1009,16 @@ __global__ void __launch_bounds__(kGemmThreads)
     const int s = kt % kS;
     mbar_wait(&full[s], (kt / kS) & 1);
     const double* hs = Hs + s * kTile * kBK;
-    const double* bs = Bs + s * kBK * BN;
+    const double* bs = Bs + s * kBK * BNP;
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
       const int kc = ks * 4 + t;
-      const double a0 = hs[swz16(wm + g, kc)];
-      const double a1 = hs[swz16(wm + g + 8, kc)];
+      // MMA rows g, g + 8 <-> tile rows 2g, 2g + 1 (conflict-free swizzled loads, as in K1)
+      const double a0 = hs[swz16(wm + 2 * g, kc)];
+      const double a1 = hs[swz16(wm + 2 * g + 1, kc)];
 #pragma unroll
       for (int pp = 0; pp < NT / 2; ++pp) {
-        const double2 w = *reinterpret_cast<const double2*>(bs + kc * BN + pp * 16 + 2 * g);
+        const double2 w = *reinterpret_cast<const double2*>(bs + kc * BNP + pp * 16 + 2 * g);
         dmma_16x8x4(acc[2 * pp], a0, a1, w.x);
         dmma_16x8x4(acc[2 * pp + 1], a0, a1, w.y);
       }
@@ -1024,7 +1028,7 @@ __global__ void __launch_bounds__(kGemmThreads)
       const int kn = kt + kS;
       mbar_arrive_expect_tx(&full[s], kStageBytes);
       tma_load_2d(Hs + s * kTile * kBK, &tmH, &full[s], kn * kBK, r0);
-      tma_load_2d(Bs + s * kBK * BN, &tmB, &full[s], 0, kn * kBK);
+      tma_load_2d(Bs + s * kBK * BNP, &tmB, &full[s], 0, kn * kBK);
     }
   }
   // scatter the accumulators to smem in natural column order
@@ -1033,7 +1037,7 @@ __global__ void __launch_bounds__(kGemmThreads)
     const int cb = pp * 16 + 4 * t;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int r = wm + g + 8 * h;
+      const int r = wm + 2 * g + h;
       sc[r * SCL + cb + 0] = acc[2 * pp][2 * h];
       sc[r * SCL + cb + 1] = acc[2 * pp + 1][2 * h];
       sc[r * SCL + cb + 2] = acc[2 * pp][2 * h + 1];
@@ -1062,7 +1066,7 @@ __global__ void __launch_bounds__(kGemmThreads)
 cudaError_t launch_scores(const CUtensorMap& tmH, const CUtensorMap& tmB, const ScoresParams& p, cudaStream_t s) {
   const int grid = (p.N + kTile - 1) / kTile;
   auto go = [&](auto kern, int bn) -> cudaError_t {
-    const size_t pipe = size_t(4) * (kTile * kBK + kBK * bn) * sizeof(double) + 64;
+    const size_t pipe = size_t(4) * (kTile * kBK + kBK * (bn + 4)) * sizeof(double) + 64;
     const size_t scb = size_t(kTile) * (bn + 1) * sizeof(double);
     const size_t smem = (pipe > scb ? pipe : scb) + 1024;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
