@@ -432,16 +432,20 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// Register-resident cluster variant (nl <= 16 * 64): one label per quad (4 lanes); lane q of the
-// quad holds its label's panel columns q, q+4, ..., q+60 in registers p[0..15], so the per-column
-// dot products read no shared memory for the label side.  Candidate rows travel in the same
-// "lane-major" order (row[q*16 + i] = P[label][q + 4i]), which is also how they are consumed.
+// Quad-per-label cluster variant (nl <= 16 * 64): one label per quad (4 lanes); lane q of the
+// quad owns its label's panel columns q, q+4, ..., q+60, kept in the CTA's shared memory in the
+// padded "lane-major" order (row[q*kRowQ + i] = P[label][q + 4i]) in which candidate rows also
+// travel and are consumed.  The owner lane stores each new column with one 8-byte store (a
+// register copy would need a select over all 16 slots, the slot being a run-time value), the
+// label's row is re-read (8 x 16 B per lane, issued before the exchange wait) for the dot product,
+// and the CTA's candidate row is pushed straight from this array.
 // Arithmetic is identical in the 4 lanes of a quad (xor-shuffle sums), so every lane holds the
 // same col and d; the reduction order is fixed and label-independent (exact twin ties persist).
 // ---------------------------------------------------------------------------
 constexpr int kRegLabels = kPThreads / 4;  // 64 labels per CTA
 constexpr int kRowQ = 18;                   // padded quarter of a lane-major row (16 used)
 constexpr int kRowLen = 4 * kRowQ;
+constexpr size_t kQrowBytes = size_t(kRegLabels) * kRowLen * sizeof(double);
 
 __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -450,13 +454,13 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), cta = static_cast<int>(cl.block_rank());
-  int* lab_at = reinterpret_cast<int*>(smem_raw);  // [nl]
-  int* pos_of = lab_at + nl;                       // [nl]
+  double (*qrow)[kRowLen] = reinterpret_cast<double (*)[kRowLen]>(smem_raw);  // [kRegLabels] own rows
+  int* lab_at = reinterpret_cast<int*>(smem_raw + kQrowBytes);  // [nl]
+  int* pos_of = lab_at + nl;                                     // [nl]
   __shared__ Cand cand_all[2][kMaxCluster];
   // candidate rows, lane-major with a padded quarter stride (row[q*kRowQ + i] = P[label][q + 4i]):
   // the 4 distinct 128-byte quarters a warp reads per step land on different banks
   __shared__ __align__(16) double rows_all[2][kMaxCluster][kRowLen];
-  __shared__ __align__(16) double wrow[kPWarps][kRowLen];             // each warp's best row
   __shared__ __align__(8) uint64_t cand_full[2];
   __shared__ Cand wbest[kPWarps];
   __shared__ int s_stop;
@@ -477,9 +481,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   const int li = tid >> 2, q = tid & 3;
   const int x = lbeg + li;
   const bool mine = li < nown;
-  double pr[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) pr[i] = 0.0;
+  double* myrow = &qrow[li][q * kRowQ];  // this lane's 16 slots of its label's row
   double dl = mine ? p.d_in[x] : -DBL_MAX;
 
   for (int i = tid; i < nl; i += blockDim.x) {
@@ -497,23 +499,13 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   const double cut = st->cut;
   const double thresh = st->thresh;
   for (int i = tid; i < 2 * kMaxCluster * kRowLen; i += blockDim.x) (&rows_all[0][0][0])[i] = 0.0;
+  for (int i = tid; i < kRegLabels * kRowLen; i += blockDim.x) (&qrow[0][0])[i] = 0.0;
   __syncthreads();
 
-  // stage this warp's best row (the quad holding label position `pos`) into wrow[warp]
-  // (the candidate's row is staged with this step's column `wv` patched in at `slot` when `wr`:
-  // the register copy itself is updated after the publication, off the critical path)
-  auto stage_row = [&](unsigned long long key, int pos, int mypos, unsigned long long mykey, bool wr, int slot,
-                       double wv) {
+  // the CTA row index (label - lbeg) of this warp's best candidate (any valid row when none)
+  auto best_row = [&](unsigned long long key, int pos, int mypos, unsigned long long mykey) {
     const unsigned who = __ballot_sync(0xffffffffu, q == 0 && mykey == key && mypos == pos && pos != INT_MAX);
-    if (who) {
-      const int lead = __ffs(who) - 1;  // lane of the quad leader
-      if ((lane >> 2) == (lead >> 2)) {
-        double2* dst = reinterpret_cast<double2*>(&wrow[warp][q * kRowQ]);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) dst[i] = make_double2(pr[2 * i], pr[2 * i + 1]);
-        if (wr) wrow[warp][q * kRowQ + slot] = wv;  // this step's column (lane q == c & 3)
-      }
-    }
+    return who ? warp * 8 + ((__ffs(who) - 1) >> 2) : 0;
   };
   auto combine_publish = [&](int j) {
     unsigned long long key = 0, k0 = 0;
@@ -526,7 +518,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const int wsrc = __ffs(__ballot_sync(0xffffffffu, lane < kPWarps && k0 == key && p0 == pos)) - 1;
     const int par = (j - k) & 1;
     const int roff = (lane >> 3) * kRowQ + 2 * (lane & 7);  // lane's 16-byte chunk of the padded row
-    const double2 rv = *reinterpret_cast<const double2*>(&wrow[wsrc][roff]);
+    const double2 rv = *reinterpret_cast<const double2*>(&qrow[wbest[wsrc].pad][roff]);
     const uint32_t row_l = smem_u32(&rows_all[par][cta][roff]);
     const uint32_t cand_l = smem_u32(&cand_all[par][cta]);
     const uint32_t bar_l = smem_u32(&cand_full[par]);
@@ -553,10 +545,11 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const unsigned long long mk = key;
     const int mp = pos;
     warp_argmax(key, pos);
-    stage_row(key, pos, mp, mk, false, 0, 0.0);
+    const int brow = best_row(key, pos, mp, mk);
     if (lane == 0) {
       wbest[warp].key = key;
       wbest[warp].pos = pos;
+      wbest[warp].pad = brow;
     }
     __syncthreads();
     combine_publish(k);
@@ -576,6 +569,11 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     auto pos_eff = [&](int lb) { return lb == xpp ? jp : (lb == ypp ? pivp : pos_of[lb - k]); };
     const int mypos = mine ? pos_eff(x) : -1;   // before the exchange wait
     const int y = lab_eff(j);
+    // this label's row so far (slot chunks that can hold columns < c), read before the wait
+    double2 own[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) own[i] = (c > 16 * (i >> 1)) ? reinterpret_cast<const double2*>(myrow)[i]
+                                                              : make_double2(0.0, 0.0);
     if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&cand_full[c & 1], kStepBytes);
     mbar_wait(&cand_full[c & 1], (c >> 1) & 1);
     unsigned long long ck = 0;
@@ -643,10 +641,11 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     for (int i = 0; i < 16; i += 4) {
       if (c > 4 * i) {
         const double2 v0 = pv[i / 2], v1 = pv[i / 2 + 1];
-        a0 = fma(pr[i], v0.x, a0);
-        a1 = fma(pr[i + 1], v0.y, a1);
-        a2 = fma(pr[i + 2], v1.x, a2);
-        a3 = fma(pr[i + 3], v1.y, a3);
+        const double2 u0 = own[i / 2], u1 = own[i / 2 + 1];
+        a0 = fma(u0.x, v0.x, a0);
+        a1 = fma(u0.y, v0.y, a1);
+        a2 = fma(u1.x, v1.x, a2);
+        a3 = fma(u1.y, v1.y, a3);
       }
     }
     double sq = (a0 + a1) + (a2 + a3);
@@ -660,6 +659,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const bool is_piv = mine && x == xp;
     const bool wr = (alive || is_piv) && q == owner_lane;
     const double wv = alive ? col : rjj;
+    if (wr) myrow[slot] = wv;  // read by this step's publication (after the barrier) and later steps
     if (alive) {
       dl = fma(-col, col, dl);
       if (q == 0 && x < p.neligible && (p.pivoting || pos == j + 1)) {
@@ -671,16 +671,15 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const int mp = bpos;
     warp_argmax(bkey, bpos);
     if (p.trace) t3 = clock64();
-    if (c + 1 < kb) stage_row(bkey, bpos, mp, mk, wr, slot, wv);
+    const int brow = best_row(bkey, bpos, mp, mk);
     if (lane == 0) {
       wbest[warp].key = bkey;
       wbest[warp].pos = bpos;
+      wbest[warp].pad = brow;
     }
     __syncthreads();
     if (p.trace) t4 = clock64();
     if (c + 1 < kb) combine_publish(j + 1);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) pr[i] = (wr && i == slot) ? wv : pr[i];
     if (p.trace) {
       const long long t5 = clock64();
       tacc[0] += t1 - t0;
@@ -705,13 +704,13 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     for (int i = 0; i < 6; ++i) atomicAdd(&p.trace[i], static_cast<unsigned long long>(tacc[i]));
   cl.sync();  // no CTA leaves while remote st.async may target it
 
-  // ---- write back from registers: Fo rows by original column, trailing panel, d, order
+  // ---- write back: Fo rows by original column, trailing panel, d, order
   if (mine) {
     const int orig = p.ord_in[x];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int cc = q + 4 * i;
-      if (cc < kb) p.Fo[(long long)orig * p.ldf + k + cc] = pr[i];
+      if (cc < kb) p.Fo[(long long)orig * p.ldf + k + cc] = myrow[i];
     }
     if (!s_stop) {
       const int t0 = k + kb;
@@ -720,7 +719,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int cc = q + 4 * i;
-          if (cc < kb) p.PcT[(long long)cc * p.ldp + (ps - t0)] = pr[i];
+          if (cc < kb) p.PcT[(long long)cc * p.ldp + (ps - t0)] = myrow[i];
         }
         if (q == 0) p.d_out[ps] = dl;
       }
@@ -763,7 +762,7 @@ cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cuda
   const int CL = panel_cluster_size(nl);
   if (panel_is_reg(nl)) {
     pp.rows_per_cta = (nl + CL - 1) / CL;
-    const size_t smem = size_t(2) * nl * sizeof(int);
+    const size_t smem = kQrowBytes + size_t(2) * nl * sizeof(int);
     static size_t attr = 0;
     if (smem > attr || attr == 0) {
       cudaError_t e = cudaFuncSetAttribute(panel_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
