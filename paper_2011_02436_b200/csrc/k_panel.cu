@@ -447,6 +447,8 @@ constexpr int kRowQ = 18;                   // padded quarter of a lane-major ro
 constexpr int kRowLen = 4 * kRowQ;
 constexpr size_t kQrowBytes = size_t(kRegLabels) * kRowLen * sizeof(double);
 
+// kTrace: per-phase cycle counters (RBPG_PANEL_TRACE), compiled out of the production variant
+template <bool kTrace>
 __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = p.n, k = p.k, kb = p.kb, nl = n - k;
@@ -563,17 +565,16 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   for (int c = 0; c < kb; ++c) {
     const int j = k + c;
     long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
-    if (p.trace) t0 = clock64();
+    if (kTrace) t0 = clock64();
     const int jp = j - 1;
     auto lab_eff = [&](int ps) { return ps == jp ? xpp : (ps == pivp ? ypp : lab_at[ps - k]); };
     auto pos_eff = [&](int lb) { return lb == xpp ? jp : (lb == ypp ? pivp : pos_of[lb - k]); };
     const int mypos = mine ? pos_eff(x) : -1;   // before the exchange wait
     const int y = lab_eff(j);
-    // this label's row so far (slot chunks that can hold columns < c), read before the wait
+    // this label's row so far (slots not yet written hold zeros), read before the wait
     double2 own[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) own[i] = (c > 16 * (i >> 1)) ? reinterpret_cast<const double2*>(myrow)[i]
-                                                              : make_double2(0.0, 0.0);
+    for (int i = 0; i < 8; ++i) own[i] = reinterpret_cast<const double2*>(myrow)[i];
     if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&cand_full[c & 1], kStepBytes);
     mbar_wait(&cand_full[c & 1], (c >> 1) & 1);
     unsigned long long ck = 0;
@@ -587,7 +588,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     warp_argmax(wkey, piv);
     const int src = __ffs(__ballot_sync(0xffffffffu, lane < C && ck == wkey && cp == piv)) - 1;
     const int xp = lab_eff(piv);
-    if (p.trace) t1 = clock64();
+    if (kTrace) t1 = clock64();
     const double dj = dkey_inv(wkey);
     // this quad's label: position after this step's swap and G entry (load issued first)
     int pos = -1;
@@ -595,9 +596,32 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const bool alive = pos > j;
     // G through its lower triangle (trailing updates behind this variant write only that half)
     const double gv = alive ? p.G[(long long)max(xp, x) * p.ldg + min(xp, x)] : 0.0;
+    // the dot product and sqrt(dj) go before the stop test: one basic block, so their latency
+    // chains interleave (dj <= 0 or NaN always stops; rjj is then unused)
+    const double* prow = rows_all[c & 1][src];  // lane-major: prow[q*16 + i] = P[xp][q + 4i]
+    // ---- update: dot over columns cc = q + 4i < c from registers.  Entries at and beyond c are
+    // zero in both operands, so whole 16-column chunks are summed unpredicated; a chunk is skipped
+    // (warp-uniform) once c <= its first column.
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const double2* pv = reinterpret_cast<const double2*>(prow + q * kRowQ);
+#pragma unroll
+    for (int i = 0; i < 16; i += 4) {
+      if (c > 4 * i) {
+        const double2 v0 = pv[i / 2], v1 = pv[i / 2 + 1];
+        const double2 u0 = own[i / 2], u1 = own[i / 2 + 1];
+        a0 = fma(u0.x, v0.x, a0);
+        a1 = fma(u0.y, v0.y, a1);
+        a2 = fma(u1.x, v1.x, a2);
+        a3 = fma(u1.y, v1.y, a3);
+      }
+    }
+    double sq = (a0 + a1) + (a2 + a3);
+    sq = sq + __shfl_xor_sync(0xffffffffu, sq, 1);
+    sq = sq + __shfl_xor_sync(0xffffffffu, sq, 2);
+    const double rjj = sqrt(dj);
     bool stop;
     if (p.pivoting) {
-      stop = (dj > 0.0 ? sqrt(dj) : 0.0) <= cut;            // linalg.cpp:219-223
+      stop = (dj > 0.0 ? rjj : 0.0) <= cut;            // linalg.cpp:219-223
     } else {
       stop = !isfinite(dj) || dj <= thresh || dj <= 0.0;   // linalg.cpp:118-119
     }
@@ -624,33 +648,12 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
       __syncthreads();
       break;
     }
-    const double rjj = sqrt(dj);
     const double inv_rjj = 1.0 / rjj;
-    if (p.trace) {
+    if (kTrace) {
       if (__double_as_longlong(gv) == 0x7ff0deadbeefll || __double_as_longlong(inv_rjj) == 0x7ff0deadbeefll)
         p.trace[7] = 1;  // forces the G load and the reciprocal to complete before t2
       t2 = clock64();
     }
-    const double* prow = rows_all[c & 1][src];  // lane-major: prow[q*16 + i] = P[xp][q + 4i]
-    // ---- update: dot over columns cc = q + 4i < c from registers.  Entries at and beyond c are
-    // zero in both operands, so whole 16-column chunks are summed unpredicated; a chunk is skipped
-    // (warp-uniform) once c <= its first column.
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    const double2* pv = reinterpret_cast<const double2*>(prow + q * kRowQ);
-#pragma unroll
-    for (int i = 0; i < 16; i += 4) {
-      if (c > 4 * i) {
-        const double2 v0 = pv[i / 2], v1 = pv[i / 2 + 1];
-        const double2 u0 = own[i / 2], u1 = own[i / 2 + 1];
-        a0 = fma(u0.x, v0.x, a0);
-        a1 = fma(u0.y, v0.y, a1);
-        a2 = fma(u1.x, v1.x, a2);
-        a3 = fma(u1.y, v1.y, a3);
-      }
-    }
-    double sq = (a0 + a1) + (a2 + a3);
-    sq = sq + __shfl_xor_sync(0xffffffffu, sq, 1);
-    sq = sq + __shfl_xor_sync(0xffffffffu, sq, 2);
     const int slot = c >> 2, owner_lane = c & 3;
     unsigned long long bkey = 0;
     int bpos = INT_MAX;
@@ -670,7 +673,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const unsigned long long mk = bkey;
     const int mp = bpos;
     warp_argmax(bkey, bpos);
-    if (p.trace) t3 = clock64();
+    if (kTrace) t3 = clock64();
     const int brow = best_row(bkey, bpos, mp, mk);
     if (lane == 0) {
       wbest[warp].key = bkey;
@@ -678,9 +681,9 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
       wbest[warp].pad = brow;
     }
     __syncthreads();
-    if (p.trace) t4 = clock64();
+    if (kTrace) t4 = clock64();
     if (c + 1 < kb) combine_publish(j + 1);
-    if (p.trace) {
+    if (kTrace) {
       const long long t5 = clock64();
       tacc[0] += t1 - t0;
       tacc[1] += t2 - t1;
@@ -763,14 +766,16 @@ cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cuda
   if (panel_is_reg(nl)) {
     pp.rows_per_cta = (nl + CL - 1) / CL;
     const size_t smem = kQrowBytes + size_t(2) * nl * sizeof(int);
-    static size_t attr = 0;
-    if (smem > attr || attr == 0) {
-      cudaError_t e = cudaFuncSetAttribute(panel_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kern = p.trace ? panel_reg_kernel<true> : panel_reg_kernel<false>;
+    static size_t attr[2] = {0, 0};
+    size_t& a = attr[p.trace ? 1 : 0];
+    if (smem > a || a == 0) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(smem > 0 ? smem : 16));
       if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(panel_reg_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       if (e != cudaSuccess) return e;
-      attr = smem > 0 ? smem : 16;
+      a = smem > 0 ? smem : 16;
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL);
@@ -787,7 +792,7 @@ cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cuda
     cfg.attrs = at;
     cfg.numAttrs = 2;
     if (ctas_used) *ctas_used = CL;
-    return cudaLaunchKernelEx(&cfg, panel_reg_kernel, pp);
+    return cudaLaunchKernelEx(&cfg, kern, pp);
   }
   if (CL > 0) {
     pp.rows_per_cta = (nl + CL - 1) / CL;
