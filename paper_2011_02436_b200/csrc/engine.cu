@@ -406,8 +406,8 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
 
   unsigned long long* trace = nullptr;
   if (std::getenv("RBPG_PANEL_TRACE")) {
-    trace = static_cast<unsigned long long*>(ctx->buf(tag + ".ptrace", 64));
-    ck(cudaMemsetAsync(trace, 0, 64, s), "memset trace");
+    trace = static_cast<unsigned long long*>(ctx->buf(tag + ".ptrace", 128));
+    ck(cudaMemsetAsync(trace, 0, 128, s), "memset trace");
   }
   // RBPG_DEVICE_TIMELINE: {entry, start of work, exit} of every panel / trailing launch
   unsigned long long* tl = nullptr;
@@ -538,12 +538,13 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     }
   }
   if (trace) {
-    unsigned long long h[7];
+    unsigned long long h[16];
     cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
-    const double st = double(h[5] ? h[5] : 1);
-    std::fprintf(stderr, "[panel trace %s n=%zu] steps %llu cycles/step: barrier %.0f winner+row %.0f update %.0f "
-                 "reduce+sync %.0f publish %.0f\n",
-                 tag.c_str(), n, h[5], h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st);
+    const double st = double(h[9] ? h[9] : 1);
+    std::fprintf(stderr, "[panel trace %s n=%zu] steps %llu cycles/step: pre+wait %.0f resolve %.0f dot %.0f "
+                 "sqrt+stop %.0f rcp %.0f col(G) %.0f argmax %.0f bar %.0f publish %.0f\n",
+                 tag.c_str(), n, h[9], h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st, h[5] / st, h[6] / st,
+                 h[7] / st, h[8] / st);
   }
   r.F = F;
   r.ldF = ldn;

@@ -557,26 +557,50 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     combine_publish(k);
   }
 
-  long long tacc[6] = {0, 0, 0, 0, 0, 0};
+  // kTrace: stamps T0..T9 per step (values forced in consumption order), deltas accumulated
+  long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long ts[10];
+#define PANEL_TS(i) \
+  do {              \
+    if (kTrace) ts[i] = clock64(); \
+  } while (0)
+#define PANEL_FORCE(v)                                                           \
+  do {                                                                           \
+    if (kTrace && __double_as_longlong(double(v)) == 0x7ff0deadbeefll) p.trace[15] = 1; \
+  } while (0)
   // Every warp resolves the winner itself from the exchanged candidates (no intra-CTA broadcast).
   // The position swap of step c is written by tid 0 after step c's barrier, so a warp reading the
   // maps during step c + 1 applies that last swap itself (pivp <-> jp, labels xpp / ypp).
   int pivp = -1, xpp = -1, ypp = -1;
-  for (int c = 0; c < kb; ++c) {
+  // Steps run in 4 groups of 16 (the outer loop is unrolled, so the group ch is a compile-time
+  // constant): group ch writes only slot chunk ch of the rows, so the label's own row stays in
+  // registers and only that chunk (plus, on entry, the previous one) is re-read per step.
+  double2 own[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) own[i] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) {
+#pragma unroll 1
+  for (int u = 0; u < 16; ++u) {
+    const int c = 16 * ch + u;
+    if (c >= kb) goto panel_done;
     const int j = k + c;
-    long long t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0;
-    if (kTrace) t0 = clock64();
+    PANEL_TS(0);
     const int jp = j - 1;
     auto lab_eff = [&](int ps) { return ps == jp ? xpp : (ps == pivp ? ypp : lab_at[ps - k]); };
     auto pos_eff = [&](int lb) { return lb == xpp ? jp : (lb == ypp ? pivp : pos_of[lb - k]); };
     const int mypos = mine ? pos_eff(x) : -1;   // before the exchange wait
     const int y = lab_eff(j);
-    // this label's row so far (slots not yet written hold zeros), read before the wait
-    double2 own[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) own[i] = reinterpret_cast<const double2*>(myrow)[i];
+    // this label's row: the chunk written by this group (and the previous group's last column)
+    own[2 * ch] = reinterpret_cast<const double2*>(myrow)[2 * ch];
+    own[2 * ch + 1] = reinterpret_cast<const double2*>(myrow)[2 * ch + 1];
+    if (ch > 0 && u == 0) {
+      own[2 * ch - 1] = reinterpret_cast<const double2*>(myrow)[2 * ch - 1];
+      own[2 * ch - 2] = reinterpret_cast<const double2*>(myrow)[2 * ch - 2];
+    }
     if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&cand_full[c & 1], kStepBytes);
     mbar_wait(&cand_full[c & 1], (c >> 1) & 1);
+    PANEL_TS(1);
     unsigned long long ck = 0;
     int cp = INT_MAX;
     if (lane < C) {
@@ -588,7 +612,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     warp_argmax(wkey, piv);
     const int src = __ffs(__ballot_sync(0xffffffffu, lane < C && ck == wkey && cp == piv)) - 1;
     const int xp = lab_eff(piv);
-    if (kTrace) t1 = clock64();
+    PANEL_FORCE(xp);
+    PANEL_TS(2);
     const double dj = dkey_inv(wkey);
     // this quad's label: position after this step's swap and G entry (load issued first)
     int pos = -1;
@@ -606,7 +631,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const double2* pv = reinterpret_cast<const double2*>(prow + q * kRowQ);
 #pragma unroll
     for (int i = 0; i < 16; i += 4) {
-      if (c > 4 * i) {
+      if (i / 4 < ch || (i / 4 == ch && u > 0)) {  // == (c > 4 * i)
         const double2 v0 = pv[i / 2], v1 = pv[i / 2 + 1];
         const double2 u0 = own[i / 2], u1 = own[i / 2 + 1];
         a0 = fma(u0.x, v0.x, a0);
@@ -618,6 +643,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     double sq = (a0 + a1) + (a2 + a3);
     sq = sq + __shfl_xor_sync(0xffffffffu, sq, 1);
     sq = sq + __shfl_xor_sync(0xffffffffu, sq, 2);
+    PANEL_FORCE(sq);
+    PANEL_TS(3);
     const double rjj = sqrt(dj);
     bool stop;
     if (p.pivoting) {
@@ -646,18 +673,18 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
         }
       }
       __syncthreads();
-      break;
+      goto panel_done;
     }
+    PANEL_TS(4);
     const double inv_rjj = 1.0 / rjj;
-    if (kTrace) {
-      if (__double_as_longlong(gv) == 0x7ff0deadbeefll || __double_as_longlong(inv_rjj) == 0x7ff0deadbeefll)
-        p.trace[7] = 1;  // forces the G load and the reciprocal to complete before t2
-      t2 = clock64();
-    }
+    PANEL_FORCE(inv_rjj);
+    PANEL_TS(5);
     const int slot = c >> 2, owner_lane = c & 3;
     unsigned long long bkey = 0;
     int bpos = INT_MAX;
     const double col = (gv - sq) * inv_rjj;
+    PANEL_FORCE(col);
+    PANEL_TS(6);
     // branch-free register write of the new column (alive labels) or of F(j, j) = rjj (the pivot)
     const bool is_piv = mine && x == xp;
     const bool wr = (alive || is_piv) && q == owner_lane;
@@ -673,7 +700,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const unsigned long long mk = bkey;
     const int mp = bpos;
     warp_argmax(bkey, bpos);
-    if (kTrace) t3 = clock64();
+    PANEL_FORCE(bpos);
+    PANEL_TS(7);
     const int brow = best_row(bkey, bpos, mp, mk);
     if (lane == 0) {
       wbest[warp].key = bkey;
@@ -681,16 +709,13 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
       wbest[warp].pad = brow;
     }
     __syncthreads();
-    if (kTrace) t4 = clock64();
+    PANEL_TS(8);
     if (c + 1 < kb) combine_publish(j + 1);
+    PANEL_TS(9);
     if (kTrace) {
-      const long long t5 = clock64();
-      tacc[0] += t1 - t0;
-      tacc[1] += t2 - t1;
-      tacc[2] += t3 - t2;
-      tacc[3] += t4 - t3;
-      tacc[4] += t5 - t4;
-      tacc[5] += 1;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) tacc[i] += ts[i + 1] - ts[i];
+      tacc[9] += 1;
     }
     if (tid == 0 && piv != j) {
       lab_at[j - k] = xp;
@@ -702,9 +727,11 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     xpp = xp;
     ypp = y;
   }
+  }
+panel_done:
   __syncthreads();
   if (p.trace && cta == 0 && tid == 0)
-    for (int i = 0; i < 6; ++i) atomicAdd(&p.trace[i], static_cast<unsigned long long>(tacc[i]));
+    for (int i = 0; i < 10; ++i) atomicAdd(&p.trace[i], static_cast<unsigned long long>(tacc[i]));
   cl.sync();  // no CTA leaves while remote st.async may target it
 
   // ---- write back: Fo rows by original column, trailing panel, d, order
