@@ -542,9 +542,9 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
     const double st = double(h[9] ? h[9] : 1);
     std::fprintf(stderr, "[panel trace %s n=%zu] steps %llu cycles/step: pre+wait %.0f resolve %.0f dot %.0f "
-                 "sqrt+stop %.0f rcp %.0f col(G) %.0f argmax %.0f bar %.0f publish %.0f\n",
+                 "sqrt+stop %.0f rcp %.0f col(G) %.0f argmax %.0f bar %.0f publish %.0f (dot: first row chunk at %.0f)\n",
                  tag.c_str(), n, h[9], h[0] / st, h[1] / st, h[2] / st, h[3] / st, h[4] / st, h[5] / st, h[6] / st,
-                 h[7] / st, h[8] / st);
+                 h[7] / st, h[8] / st, h[10] / st);
   }
   r.F = F;
   r.ldF = ldn;

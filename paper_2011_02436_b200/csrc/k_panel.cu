@@ -497,7 +497,6 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     fence_mbar_init();
   }
   cl.sync();
-  const uint32_t kStepBytes = static_cast<uint32_t>(C) * (sizeof(Cand) + kPanelW * sizeof(double));
   const double cut = st->cut;
   const double thresh = st->thresh;
   for (int i = tid; i < 2 * kMaxCluster * kRowLen; i += blockDim.x) (&rows_all[0][0][0])[i] = 0.0;
@@ -509,7 +508,9 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const unsigned who = __ballot_sync(0xffffffffu, q == 0 && mykey == key && mypos == pos && pos != INT_MAX);
     return who ? warp * 8 + ((__ffs(who) - 1) >> 2) : 0;
   };
-  auto combine_publish = [&](int j) {
+  // publish for step j: the CTA's candidate and its row's first nch slot chunks (the receiving
+  // step reads no later chunk; columns beyond those are zero or not yet summed)
+  auto combine_publish = [&](int j, int nch) {
     unsigned long long key = 0, k0 = 0;
     int pos = INT_MAX, p0 = INT_MAX;
     if (lane < kPWarps) {
@@ -524,9 +525,10 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const uint32_t row_l = smem_u32(&rows_all[par][cta][roff]);
     const uint32_t cand_l = smem_u32(&cand_all[par][cta]);
     const uint32_t bar_l = smem_u32(&cand_full[par]);
+    const bool push_row = ((lane & 7) >> 1) < nch;
     for (int d = warp; d < C; d += kPWarps) {
       const uint32_t rbar = mapa_u32(bar_l, d);
-      st_async_v2f64(mapa_u32(row_l, d), rv.x, rv.y, rbar);
+      if (push_row) st_async_v2f64(mapa_u32(row_l, d), rv.x, rv.y, rbar);
       if (lane == 0) st_async_v2b64(mapa_u32(cand_l, d), key, static_cast<unsigned long long>(pos), rbar);
     }
   };
@@ -554,12 +556,12 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
       wbest[warp].pad = brow;
     }
     __syncthreads();
-    combine_publish(k);
+    combine_publish(k, 0);
   }
 
   // kTrace: stamps T0..T9 per step (values forced in consumption order), deltas accumulated
-  long long tacc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
-  long long ts[10];
+  long long tacc[11] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  long long ts[11];
 #define PANEL_TS(i) \
   do {              \
     if (kTrace) ts[i] = clock64(); \
@@ -598,7 +600,9 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
       own[2 * ch - 1] = reinterpret_cast<const double2*>(myrow)[2 * ch - 1];
       own[2 * ch - 2] = reinterpret_cast<const double2*>(myrow)[2 * ch - 2];
     }
-    if (warp == 0 && lane == 0) mbar_arrive_expect_tx(&cand_full[c & 1], kStepBytes);
+    if (warp == 0 && lane == 0)
+      mbar_arrive_expect_tx(&cand_full[c & 1],
+                            static_cast<uint32_t>(C) * (sizeof(Cand) + (c == 0 ? 0u : 128u * (((c - 1) >> 4) + 1))));
     mbar_wait(&cand_full[c & 1], (c >> 1) & 1);
     PANEL_TS(1);
     unsigned long long ck = 0;
@@ -629,6 +633,11 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     // (warp-uniform) once c <= its first column.
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     const double2* pv = reinterpret_cast<const double2*>(prow + q * kRowQ);
+    if (kTrace) {  // diagnostic split of the dot phase: first row chunk landed
+      const double2 t = pv[0];
+      PANEL_FORCE(t.x + t.y);
+      PANEL_TS(10);
+    }
 #pragma unroll
     for (int i = 0; i < 16; i += 4) {
       if (i / 4 < ch || (i / 4 == ch && u > 0)) {  // == (c > 4 * i)
@@ -710,12 +719,13 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     }
     __syncthreads();
     PANEL_TS(8);
-    if (c + 1 < kb) combine_publish(j + 1);
+    if (c + 1 < kb) combine_publish(j + 1, ch + 1);
     PANEL_TS(9);
     if (kTrace) {
 #pragma unroll
       for (int i = 0; i < 9; ++i) tacc[i] += ts[i + 1] - ts[i];
       tacc[9] += 1;
+      tacc[10] += ts[10] - ts[2];
     }
     if (tid == 0 && piv != j) {
       lab_at[j - k] = xp;
@@ -731,7 +741,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
 panel_done:
   __syncthreads();
   if (p.trace && cta == 0 && tid == 0)
-    for (int i = 0; i < 10; ++i) atomicAdd(&p.trace[i], static_cast<unsigned long long>(tacc[i]));
+    for (int i = 0; i < 11; ++i) atomicAdd(&p.trace[i], static_cast<unsigned long long>(tacc[i]));
   cl.sync();  // no CTA leaves while remote st.async may target it
 
   // ---- write back: Fo rows by original column, trailing panel, d, order
