@@ -35,6 +35,9 @@ sys.path.insert(0, HERE)
 CONFIGS = {
     "c1": (2000, 16, 200, 2),
     "c2": (50000, 64, 1000, 10),
+    "c4_250": (100000, 128, 250, 10),
+    "c4_500": (100000, 128, 500, 10),
+    "c4_1000": (100000, 128, 1000, 10),
     "c4_2000": (100000, 128, 2000, 10),
     "c4_4000": (100000, 128, 4000, 10),
     "c4_8000": (100000, 128, 8000, 10),
@@ -119,7 +122,7 @@ def reference_arm(args, n, d, L, m, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    rows = int(os.environ.get("RBPG_REF_ROWS", "10000"))
+    rows = int(os.environ.get("RBPG_REF_ROWS", str(n)))
     samples = []
     for i in range(args.warmup + args.steps):
         v, dt = cpu_oracle_sample(n, d, L, m, threads, rows)
@@ -278,7 +281,7 @@ def main():
                 traffic = None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            rows = int(os.environ.get("RBPG_CPU_ROWS", "4000"))
+            rows = int(os.environ.get("RBPG_CPU_ROWS", str(n)))
             v, dt = cpu_oracle_sample(n, d, L, m, 1, rows)
             cpu = {"value": v, "unit": "TFLOP/s", "cores": 1, "kind": "port",
                    "sample": f"oracle restatement train() (single thread, as the reference build) on the first "
