@@ -264,7 +264,7 @@ def main():
         e2e_s = statistics.median(t_e)
         e2e = {"value": flops / e2e_s / 1e12, "unit": "TFLOP/s", "seconds": e2e_s,
                "h2d_bytes_per_step": int(n * d * 8 + n * m * 8),
-               "d2h_bytes_per_step": int(L * m * 8 + d * L * 8 + L * 8),
+               "d2h_bytes_per_step": int(L * m * 8),  # beta (W, b are generated on the host)
                "api": "rbpg_train (C ABI, host buffers)"}
 
     if rank == 0:

@@ -97,7 +97,9 @@ struct rbpg_context {
   int num_sms = 148;
   cudaStream_t own = nullptr;
   cudaStream_t copy = nullptr;  // host -> device input uploads, overlapped with the hidden build
-  cudaEvent_t chunk_ev[8] = {};
+  cudaStream_t aux = nullptr;   // hidden builds of late upload blocks, concurrent with the first Gram part
+  cudaEvent_t chunk_ev[16] = {};
+  cudaEvent_t aux_ev[8] = {};
   cudaStream_t stream = nullptr;
   std::map<std::string, std::pair<void*, size_t>> bufs;
   uint64_t launches = 0;
@@ -346,6 +348,58 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
   ctx->run("syrk_kernel", [&] { return launch_syrk(tmA, tmB, p, splits, kTile, ctx->stream); });
   if (p.nbI >= 2) ++ctx->launches;  // diagonal + off-diagonal grids
   if (!direct) ctx->run("syrk_finish", [&] { return launch_syrk_finish(p, splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
+}
+
+// Row-blocked Gram G = A^T A over rows [0, N) for the e2e path: part q covers rows
+// [ends[q-1], ends[q]) with its own uniform split count, every split writes its own partial slot
+// (split0 offset), and one fixed-order reduction sums all parts' partials.  Each part is launched
+// by `launch_part(q)` ordering: the caller interleaves its launches with the producers of its rows.
+struct GramParts {
+  SyrkParams p{};
+  std::vector<size_t> ends;
+  std::vector<int> splits, split0;
+  std::vector<long long> per;
+  int total = 0;
+};
+GramParts gram_parts_plan(rbpg_context* ctx, size_t L, const std::vector<size_t>& ends, double* dG, size_t ldg) {
+  GramParts gp;
+  gp.ends = ends;
+  SyrkParams& p = gp.p;
+  p.M = static_cast<int>(L);
+  p.nbI = static_cast<int>((L + kTile - 1) / kTile);
+  p.nGram = p.nbI * (p.nbI + 1) / 2;
+  p.G = dG;
+  p.ldg = static_cast<long long>(ldg);
+  p.mode = kSyrkPartial;
+  size_t r0 = 0;
+  for (size_t e : ends) {
+    const size_t rows = e - r0;
+    int sp = gram_splits(ctx, rows, L, 0, p.nGram, p.nbI);
+    long long per = static_cast<long long>(round_up((rows + sp - 1) / sp, kBK));
+    if (per == 0) per = kBK;
+    sp = static_cast<int>((rows + per - 1) / per);
+    gp.split0.push_back(gp.total);
+    gp.splits.push_back(sp);
+    gp.per.push_back(per);
+    gp.total += sp;
+    r0 = e;
+  }
+  p.ws = ctx->dbuf("syrk_ws", size_t(gp.total) * L * ldg);
+  p.wsStride = static_cast<long long>(L * ldg);
+  return gp;
+}
+void gram_parts_launch(rbpg_context* ctx, GramParts& gp, int q, const double* dA, size_t lda) {
+  const size_t r0 = q == 0 ? 0 : gp.ends[q - 1], rows = gp.ends[q] - r0;
+  SyrkParams p = gp.p;
+  p.kRows = static_cast<long long>(rows);
+  p.kPerSplit = gp.per[q];
+  p.split0 = gp.split0[q];
+  CUtensorMap tmA = make_map(ctx, dA + r0 * lda, p.M, rows, lda, kTile + 4, kBK, false);
+  ctx->run("syrk_kernel", [&] { return launch_syrk(tmA, tmA, p, gp.splits[q], kTile, ctx->stream); });
+  if (p.nbI >= 2) ++ctx->launches;
+}
+void gram_parts_finish(rbpg_context* ctx, GramParts& gp, bool accumulate) {
+  ctx->run("syrk_finish", [&] { return launch_syrk_finish(gp.p, gp.total, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
 }
 
 void gemm_dev(rbpg_context* ctx, int M, int N, int K, const double* A, size_t lda, bool tA, const double* B,
@@ -965,6 +1019,75 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
     gram_dev(ctx, dH, ldh, 0, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate);
     return 0.f;
   }
+  // Gram parts behind the uploads: part 0 covers the first upload blocks and runs while the later
+  // blocks arrive; their hidden builds go on the aux stream, concurrently with the Gram parts on
+  // the main stream; part q > 0 starts once the aux stream has built its last block.
+  // Default cuts (measured on one B200, PCIe ~40 GB/s): after block 2 when the Gram + hidden work
+  // outlasts the upload (C2: 3.83 -> 3.74 ms e2e), every 2 blocks when the upload dominates
+  // (C4 L = 250: 3.32 -> 2.96 ms).  RBPG_E2E_PARTS overrides: the upload-block counts at which
+  // parts end, e.g. "2" or "1,3" (the last part always ends at N; "0" = one Gram after all blocks).
+  const double upload_s = double(N) * double(d + m) * 8.0 / 40e9;
+  const double compute_s = (2.0 * N * d * L + double(N) * M * M) / 30e12;
+  const char* parts_env = std::getenv("RBPG_E2E_PARTS");
+  const std::vector<size_t> part_cuts = [&] {
+    std::vector<size_t> v;
+    std::string str = parts_env ? parts_env : (upload_s > compute_s ? "2,4,6,8,10,12,14" : "2");
+    size_t pos = 0;
+    while (pos < str.size()) {
+      const size_t c = str.find(',', pos);
+      const int x = std::atoi(str.substr(pos, c == std::string::npos ? std::string::npos : c - pos).c_str());
+      if (x > 0 && (v.empty() || size_t(x) > v.back()) && v.size() < 6) v.push_back(size_t(x));
+      if (c == std::string::npos) break;
+      pos = c + 1;
+    }
+    return v;
+  }();
+  std::vector<size_t> cuts;  // block counts ending parts 0 .. P-2
+  if (ready && chunk >= N && M >= 2 * kTile)
+    for (size_t c : part_cuts)
+      if (c < ready->size()) cuts.push_back(c);
+  if (!cuts.empty()) {
+    std::vector<size_t> ends;
+    for (size_t c : cuts) ends.push_back((*ready)[c - 1].end);
+    ends.push_back(N);
+    GramParts gp = gram_parts_plan(ctx, M, ends, dGaug, ldga);
+    if (timed) cudaEventRecord(ctx->ev[0], ctx->stream);
+    ck(cudaEventRecord(ctx->aux_ev[0], ctx->stream), "event");  // H rows free (earlier work done)
+    ck(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0), "wait");
+    size_t r0 = 0, q = 0;
+    for (size_t i = 0; i < ready->size(); ++i) {
+      const RowReady& rr = (*ready)[i];
+      const bool on_aux = i >= cuts[0];
+      ck(cudaStreamWaitEvent(on_aux ? ctx->aux : ctx->stream, rr.ev, 0), "wait upload");
+      if (on_aux) std::swap(ctx->stream, ctx->aux);
+      hidden_dev(ctx, dX + r0 * ldx, ldx, rr.end - r0, d, dW, ldw, db, L, dH + r0 * ldh, ldh, dT + r0 * ldt_in,
+                 ldt_in, m);
+      if (on_aux) std::swap(ctx->stream, ctx->aux);
+      r0 = rr.end;
+      if (q < cuts.size() && i + 1 == cuts[q]) {  // part q's rows are built: launch it on the main stream
+        if (q > 0) {
+          ck(cudaEventRecord(ctx->aux_ev[1 + q], ctx->aux), "event");
+          ck(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1 + q], 0), "wait hidden");
+        }
+        gram_parts_launch(ctx, gp, static_cast<int>(q), dH, ldh);
+        ++q;
+      }
+    }
+    ck(cudaEventRecord(ctx->aux_ev[1], ctx->aux), "event");
+    ck(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0), "wait hidden");
+    if (timed) cudaEventRecord(ctx->ev[1], ctx->stream);
+    gram_parts_launch(ctx, gp, static_cast<int>(cuts.size()), dH, ldh);
+    gram_parts_finish(ctx, gp, accumulate);
+    if (keep_h) {
+      ctx->kept_h = dH;
+      ctx->kept_n = N;
+      ctx->kept_l = L;
+      ctx->kept_ldh = ldh;
+    } else {
+      ctx->kept_h = nullptr;
+    }
+    return 0.f;
+  }
   if (ready && chunk >= N) {
     if (timed) cudaEventRecord(ctx->ev[0], ctx->stream);
     size_t r0 = 0;
@@ -1242,7 +1365,9 @@ int rbpg_context_create(int device, rbpg_context** out, rbpg_status* st) {
     c->num_sms = prop.multiProcessorCount;
     ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking), "copy stream");
+    ck(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking), "aux stream");
     for (auto& e : c->chunk_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    for (auto& e : c->aux_ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     c->stream = c->own;
     for (auto& e : c->ev) ck(cudaEventCreate(&e), "event");
     void* fn = nullptr;
@@ -1264,6 +1389,7 @@ void rbpg_context_destroy(rbpg_context* ctx) {
   for (auto& kv : ctx->hbufs) cudaFreeHost(kv.second.first);
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   for (auto& e : ctx->chunk_ev) cudaEventDestroy(e);
+  for (auto& e : ctx->aux_ev) cudaEventDestroy(e);
   cudaStreamDestroy(ctx->own);
   cudaStreamDestroy(ctx->copy);
   delete ctx;
@@ -1500,10 +1626,12 @@ int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, 
     double* dY = ctx->dbuf("T.in", std::max<size_t>(1, n) * ldy);
     std::vector<RowReady> ready;
     {
-      const size_t nblk = std::min<size_t>(7, std::max<size_t>(1, n / 4096));
+      static const size_t max_blk =
+          std::getenv("RBPG_E2E_BLOCKS") ? std::min(15, std::max(1, std::atoi(std::getenv("RBPG_E2E_BLOCKS")))) : 7;
+      const size_t nblk = std::min<size_t>(max_blk, std::max<size_t>(1, n / 4096));
       const size_t per = round_up((n + nblk - 1) / nblk, kTile);
-      ck(cudaEventRecord(ctx->chunk_ev[7], ctx->stream), "event");  // buffers free (prior work done)
-      ck(cudaStreamWaitEvent(ctx->copy, ctx->chunk_ev[7], 0), "wait");
+      ck(cudaEventRecord(ctx->chunk_ev[15], ctx->stream), "event");  // buffers free (prior work done)
+      ck(cudaStreamWaitEvent(ctx->copy, ctx->chunk_ev[15], 0), "wait");
       for (size_t r0 = 0, i = 0; r0 < n; r0 += per, ++i) {
         const size_t nr = std::min(per, n - r0);
         copy_rows(dX + r0 * ldx, ldx * 8, x + r0 * xcols, xcols * 8, xcols * 8, nr, cudaMemcpyHostToDevice,
