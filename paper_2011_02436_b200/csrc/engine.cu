@@ -44,6 +44,8 @@ cudaError_t launch_gather_factor(const double*, long long, const int*, int, doub
                                  int, cudaStream_t);
 cudaError_t launch_gather_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
 cudaError_t launch_scatter_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
+cudaError_t launch_tri_inv(const double*, long long, int, double*, cudaStream_t);
+bool trsm_cluster_fits(int n, int m);
 cudaError_t launch_trsm_pair(const double*, long long, double*, long long, int, int, int, int, int, double*,
                              cudaStream_t);
 cudaError_t launch_accuracy(const double*, long long, const double*, long long, long long, int, unsigned long long*,
@@ -403,15 +405,67 @@ void gram_parts_finish(rbpg_context* ctx, GramParts& gp, bool accumulate) {
 }
 
 void gemm_dev(rbpg_context* ctx, int M, int N, int K, const double* A, size_t lda, bool tA, const double* B,
-              size_t ldb, bool tB, double* C, size_t ldc, double alpha, double beta) {
+              size_t ldb, bool tB, double* C, size_t ldc, double alpha, double beta,
+              const char* name = "gemm_kernel") {
   GemmParams p{M, N, K, A, static_cast<long long>(lda), tA ? 1 : 0, B, static_cast<long long>(ldb), tB ? 1 : 0,
                C, static_cast<long long>(ldc), alpha, beta};
-  ctx->run("gemm_kernel", [&] { return launch_gemm(p, ctx->stream); });
+  ctx->run(name, [&] { return launch_gemm(p, ctx->stream); });
+}
+
+// Blocked TRSM pair for right-hand sides the cluster kernel cannot hold (m > 32, or n too large
+// for its shared-memory ring): the 64 x 64 diagonal blocks of F are inverted once, then every block
+// step is two DMMA GEMMs -- the block solution W_b = D_b^-1 X_b (D_b^-T backward) and the rank-64
+// update of the rows still to solve.  Forward writes X -> W, backward W -> X (or X -> W, copied
+// back), so the pair needs no copy.
+void trsm_blocked_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X, size_t ldx, size_t n, size_t m,
+                      bool fwd, bool bwd) {
+  const size_t nblk = (n + 63) / 64;
+  double* dinv = ctx->dbuf("trsm.dinv", nblk * 64 * 64);
+  ctx->run("trsm_pair_kernel", [&] { return launch_tri_inv(F, static_cast<long long>(ldf), static_cast<int>(n), dinv, ctx->stream); });
+  const size_t ldw = even(m);
+  double* W = ctx->dbuf("trsm.w", n * ldw);
+  double* src = X;
+  size_t lds = ldx;
+  double* dst = W;
+  size_t ldd = ldw;
+  const int mi = static_cast<int>(m);
+  if (fwd) {
+    for (size_t b = 0; b < nblk; ++b) {
+      const size_t r0 = b * 64, nb = std::min<size_t>(64, n - r0);
+      gemm_dev(ctx, static_cast<int>(nb), mi, static_cast<int>(nb), dinv + b * 4096, 64, false, src + r0 * lds, lds,
+               false, dst + r0 * ldd, ldd, 1.0, 0.0, "trsm_pair_kernel");
+      if (r0 + nb < n)
+        gemm_dev(ctx, static_cast<int>(n - r0 - nb), mi, static_cast<int>(nb), F + (r0 + nb) * ldf + r0, ldf, false,
+                 dst + r0 * ldd, ldd, false, src + (r0 + nb) * lds, lds, -1.0, 1.0, "trsm_pair_kernel");
+    }
+    std::swap(src, dst);
+    std::swap(lds, ldd);
+  }
+  if (bwd) {
+    for (size_t b = nblk; b-- > 0;) {
+      const size_t r0 = b * 64, nb = std::min<size_t>(64, n - r0);
+      gemm_dev(ctx, static_cast<int>(nb), mi, static_cast<int>(nb), dinv + b * 4096, 64, true, src + r0 * lds, lds,
+               false, dst + r0 * ldd, ldd, 1.0, 0.0, "trsm_pair_kernel");
+      if (r0 > 0)
+        gemm_dev(ctx, static_cast<int>(r0), mi, static_cast<int>(nb), F + r0 * ldf, ldf, true, dst + r0 * ldd, ldd,
+                 false, src, lds, -1.0, 1.0, "trsm_pair_kernel");
+    }
+    std::swap(src, dst);
+    std::swap(lds, ldd);
+  }
+  if (src != X)
+    ck(cudaMemcpy2DAsync(X, ldx * 8, src, lds * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream), "trsm copy");
 }
 
 // X (n x m, ld ldx) <- (F F^T)^{-1} X, column chunks of <= 128 right-hand sides
 void trsm_pair_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X, size_t ldx, size_t n, size_t m,
                    bool fwd = true, bool bwd = true) {
+  static const bool legacy = std::getenv("RBPG_TRSM_LEGACY") != nullptr;  // the cooperative sweep for every m
+  if (n > 0 && m > 0 && (fwd || bwd) && !legacy &&
+      !trsm_cluster_fits(static_cast<int>(n), static_cast<int>(std::min<size_t>(m, 128)))) {
+    trsm_blocked_dev(ctx, F, ldf, X, ldx, n, m, fwd, bwd);
+    return;
+  }
   static const bool tr = std::getenv("RBPG_TRSM_TRACE") != nullptr;
   if (tr) { cudaStreamSynchronize(ctx->stream); trsm_trace_dump(); }
   struct Dump { bool on; cudaStream_t s; ~Dump() { if (on) { cudaStreamSynchronize(s); trsm_trace_dump(); } } } dump{tr, ctx->stream};
@@ -525,12 +579,13 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     if (t0 < neligible) {  // another panel follows
       const size_t nrem = n - t0;
       // 32-wide tiles while they fit in three waves (the late, small updates: their DMMA work per
-      // SM is what bounds the update), then 64-wide while 128-wide ones would not fill two waves
-      const size_t nb32 = (nrem + 31) / 32, nb64 = (nrem + 63) / 64, nb128 = (nrem + kTile - 1) / kTile;
-      const int ttile = (nb32 * (nb32 + 1) / 2 <= size_t(3 * ctx->num_sms))   ? 32
-                        : (nb128 * (nb128 + 1) / 2 < size_t(2 * ctx->num_sms)) ? 64
-                                                                                : kTile;
-      (void)nb64;
+      // SM is what bounds the update), 64-wide beyond.  The 128-wide trailing SYRK (RBPG_TRAIL_TILE
+      // = 128) gathers G_old element by element in its epilogue (no registers to stage them) and
+      // measured 1.5x slower at L = 8000 (C4: 21.5 -> 14.7 ms of trailing updates per train).
+      const size_t nb32 = (nrem + 31) / 32;
+      static const int force_tile = std::getenv("RBPG_TRAIL_TILE") ? std::atoi(std::getenv("RBPG_TRAIL_TILE")) : 0;
+      int ttile = (nb32 * (nb32 + 1) / 2 <= size_t(3 * ctx->num_sms)) ? 32 : 64;
+      if (force_tile == 128 && ttile == 64) ttile = kTile;
       CUtensorMap tm = make_map(ctx, PcT, nrem, static_cast<uint64_t>(kb), ldp, ttile + 4, kBK, false);
       SyrkParams sp{};
       sp.M = static_cast<int>(nrem);

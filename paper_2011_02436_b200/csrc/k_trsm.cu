@@ -417,6 +417,27 @@ static size_t trsm_cluster_smem(int n, int m, int C) {
   return (size_t(nown) * kTB * m + size_t(kRing) * kTB * m + 4 * size_t(kTB) * kPadT) * sizeof(double);
 }
 
+// The 64 x 64 diagonal-block inverses of F (blocked TRSM path of the engine).
+cudaError_t launch_tri_inv(const double* F, long long ldf, int n, double* dinv, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  constexpr size_t kInvSmem = size_t(2) * kTB * (kTB + 1) * sizeof(double);
+  static bool inv_attr = false;
+  if (!inv_attr) {
+    cudaError_t e = cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kInvSmem);
+    if (e != cudaSuccess) return e;
+    inv_attr = true;
+  }
+  tri_inv_kernel<<<(n + kTB - 1) / kTB, kTB, kInvSmem, s>>>(F, ldf, n, dinv);
+  return cudaGetLastError();
+}
+
+// Whether launch_trsm_pair runs its cluster kernel for n rows and m (<= 128) right-hand sides.
+bool trsm_cluster_fits(int n, int m) {
+  if (m > kClusterMaxM || std::getenv("RBPG_TRSM_GRID")) return false;
+  const int nblk = (n + kTB - 1) / kTB;
+  return trsm_cluster_smem(n, m, std::min(16, nblk)) <= 220 * 1024;
+}
+
 cudaError_t launch_trsm_pair(const double* F, long long ldf, double* X, long long ldx, int n, int m, int fwd, int bwd,
                              int num_sms, double* dinv_ws, cudaStream_t s) {
   if (n <= 0 || m <= 0) return cudaSuccess;
