@@ -45,6 +45,8 @@ cudaError_t launch_gather_factor(const double*, long long, const int*, int, doub
 cudaError_t launch_gather_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
 cudaError_t launch_scatter_rows(const double*, long long, const int*, int, int, double*, long long, cudaStream_t);
 cudaError_t launch_tri_inv(const double*, long long, int, double*, cudaStream_t);
+cudaError_t launch_trsm_step(const double*, long long, const double*, double*, long long, double*, long long, int, int,
+                             int, int, int, cudaStream_t);
 bool trsm_cluster_fits(int n, int m);
 cudaError_t launch_trsm_pair(const double*, long long, double*, long long, int, int, int, int, int, double*,
                              cudaStream_t);
@@ -429,26 +431,17 @@ void trsm_blocked_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X,
   double* dst = W;
   size_t ldd = ldw;
   const int mi = static_cast<int>(m);
-  if (fwd) {
-    for (size_t b = 0; b < nblk; ++b) {
+  const long long lf = static_cast<long long>(ldf);
+  for (int dir = 0; dir < 2; ++dir) {
+    if ((dir == 0 && !fwd) || (dir == 1 && !bwd)) continue;
+    for (size_t i = 0; i < nblk; ++i) {
+      const size_t b = dir == 0 ? i : nblk - 1 - i;
       const size_t r0 = b * 64, nb = std::min<size_t>(64, n - r0);
-      gemm_dev(ctx, static_cast<int>(nb), mi, static_cast<int>(nb), dinv + b * 4096, 64, false, src + r0 * lds, lds,
-               false, dst + r0 * ldd, ldd, 1.0, 0.0, "trsm_pair_kernel");
-      if (r0 + nb < n)
-        gemm_dev(ctx, static_cast<int>(n - r0 - nb), mi, static_cast<int>(nb), F + (r0 + nb) * ldf + r0, ldf, false,
-                 dst + r0 * ldd, ldd, false, src + (r0 + nb) * lds, lds, -1.0, 1.0, "trsm_pair_kernel");
-    }
-    std::swap(src, dst);
-    std::swap(lds, ldd);
-  }
-  if (bwd) {
-    for (size_t b = nblk; b-- > 0;) {
-      const size_t r0 = b * 64, nb = std::min<size_t>(64, n - r0);
-      gemm_dev(ctx, static_cast<int>(nb), mi, static_cast<int>(nb), dinv + b * 4096, 64, true, src + r0 * lds, lds,
-               false, dst + r0 * ldd, ldd, 1.0, 0.0, "trsm_pair_kernel");
-      if (r0 > 0)
-        gemm_dev(ctx, static_cast<int>(r0), mi, static_cast<int>(nb), F + r0 * ldf, ldf, true, dst + r0 * ldd, ldd,
-                 false, src, lds, -1.0, 1.0, "trsm_pair_kernel");
+      ctx->run("trsm_pair_kernel", [&] {
+        return launch_trsm_step(F, lf, dinv + b * 4096, src, static_cast<long long>(lds), dst,
+                                static_cast<long long>(ldd), static_cast<int>(n), mi, static_cast<int>(r0),
+                                static_cast<int>(nb), dir, ctx->stream);
+      });
     }
     std::swap(src, dst);
     std::swap(lds, ldd);

@@ -417,6 +417,155 @@ static size_t trsm_cluster_smem(int n, int m, int C) {
   return (size_t(nown) * kTB * m + size_t(kRing) * kTB * m + 4 * size_t(kTB) * kPadT) * sizeof(double);
 }
 
+// One block step of the blocked TRSM pair (engine trsm_blocked_dev), fused: every CTA forms the
+// block solution W = op(D_b) S_b for its NC-column slice (D_b = inverse of the 64 x 64 diagonal
+// block, op = transpose on the backward sweep; recomputed per CTA instead of a second launch), then
+// row-tile CTAs apply the rank-64 update of the rows still to solve,
+//   backward: src[R, :] -= F[r0 : r0+nb, R]^T W      (R in [0, r0))
+//   forward:  src[R, :] -= F[R, r0 : r0+nb] W        (R in [r0+nb, n))
+// and CTA row 0 stores W into dst[r0 : r0+nb, :].  Grid (ceil(m/NC), 1 + row tiles of 64), 256
+// threads; NC = 128 for m > 64 keeps the grid to one wave at n = 8192.
+template <int NC>
+__global__ void __launch_bounds__(256) trsm_step_kernel(const double* __restrict__ F, long long ldf,
+                                                        const double* __restrict__ Db, double* src, long long lds,
+                                                        double* dst, long long ldd, int n, int m, int r0, int nb,
+                                                        int bwd) {
+  constexpr int SP = NC + 2, DP = 66;   // padded smem rows (doubles)
+  constexpr int NF = NC / 16;           // n8 fragments per warp (warp tile 16 x NC/2)
+  constexpr int NE = 64 * NC / 256;     // S / W elements per thread
+  extern __shared__ __align__(16) double tsm[];
+  double(*S)[SP] = reinterpret_cast<double(*)[SP]>(tsm);                  // S_b slice [k][c]
+  double(*Wt)[SP] = reinterpret_cast<double(*)[SP]>(tsm + 64 * SP);       // W [k][c]
+  double(*D)[DP] = reinterpret_cast<double(*)[DP]>(tsm + 128 * SP);       // D_b [row][col]
+  double(*A)[DP] = reinterpret_cast<double(*)[DP]>(tsm + 128 * SP + 64 * DP);  // A(i, k) at [k][i]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int j0 = blockIdx.x * NC, y = blockIdx.y;
+  const int R0 = bwd ? (y - 1) * 64 : r0 + nb + (y - 1) * 64;
+  const int Rend = bwd ? r0 : n;
+  // every load of this thread in flight at once (a load-store loop would serialise the round trips)
+  double sv[NE], dv[16], av[16];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const int e = tid + 256 * i, r = e / NC, c = e % NC;
+    sv[i] = (r < nb && j0 + c < m) ? src[(long long)(r0 + r) * lds + j0 + c] : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int e = tid + 256 * i, r = e >> 6, c = e & 63;
+    dv[i] = (r < nb && c < nb) ? Db[r * 64 + c] : 0.0;
+    av[i] = 0.0;
+    if (y > 0) {  // bwd: A(i, k) = F[r0 + k][R0 + i] (coalesced in i); fwd: A(i, k) = F[R0 + i][r0 + k]
+      if (bwd) {
+        if (r < nb && R0 + c < Rend) av[i] = F[(long long)(r0 + r) * ldf + R0 + c];
+      } else {
+        if (c < nb && R0 + r < Rend) av[i] = F[(long long)(R0 + r) * ldf + r0 + c];
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const int e = tid + 256 * i;
+    S[e / NC][e % NC] = sv[i];
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int e = tid + 256 * i, r = e >> 6, c = e & 63;
+    D[r][c] = dv[i];
+    if (bwd) A[r][c] = av[i]; else A[c][r] = av[i];
+  }
+  __syncthreads();
+  // warp tile: rows 16 * (warp & 3) .. +16, cols (NC / 2) * (warp >> 2) .. + NC / 2
+  const int wi = 16 * (warp & 3), wc = (NC / 2) * (warp >> 2);
+  double acc[NF][4];
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[f][q] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < 64; k += 4) {
+    // W(i, c) = sum_k op(D)(i, k) S[k][c]; op(D)(i, k) = D[k][i] (bwd) or D[i][k] (fwd)
+    const double a0 = bwd ? D[k + t][wi + g] : D[wi + g][k + t];
+    const double a1 = bwd ? D[k + t][wi + g + 8] : D[wi + g + 8][k + t];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) dmma_16x8x4(acc[f], a0, a1, S[k + t][wc + 8 * f + g]);
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int c = wc + 8 * f + 2 * t;
+    Wt[wi + g][c] = acc[f][0];
+    Wt[wi + g][c + 1] = acc[f][1];
+    Wt[wi + g + 8][c] = acc[f][2];
+    Wt[wi + g + 8][c + 1] = acc[f][3];
+  }
+  __syncthreads();
+  if (y == 0) {
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = tid + 256 * i, r = e / NC, c = e % NC;
+      if (r < nb && j0 + c < m) dst[(long long)(r0 + r) * ldd + j0 + c] = Wt[r][c];
+    }
+    return;
+  }
+  // read every old value first (the stores could alias later loads as far as the compiler knows);
+  // the loads fly under the update DMMAs
+  double old[NF][4];
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int c = j0 + wc + 8 * f + 2 * t;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = R0 + wi + g + 8 * h;
+      const double* row = src + (long long)r * lds;
+      old[f][2 * h] = (r < Rend && c < m) ? row[c] : 0.0;
+      old[f][2 * h + 1] = (r < Rend && c + 1 < m) ? row[c + 1] : 0.0;
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[f][q] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < 64; k += 4) {
+    const double a0 = A[k + t][wi + g], a1 = A[k + t][wi + g + 8];
+#pragma unroll
+    for (int f = 0; f < NF; ++f) dmma_16x8x4(acc[f], a0, a1, Wt[k + t][wc + 8 * f + g]);
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+    const int c = j0 + wc + 8 * f + 2 * t;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = R0 + wi + g + 8 * h;
+      if (r >= Rend) continue;
+      double* row = src + (long long)r * lds;
+      if (c < m) row[c] = old[f][2 * h] - acc[f][2 * h];
+      if (c + 1 < m) row[c + 1] = old[f][2 * h + 1] - acc[f][2 * h + 1];
+    }
+  }
+}
+
+cudaError_t launch_trsm_step(const double* F, long long ldf, const double* Db, double* src, long long lds,
+                             double* dst, long long ldd, int n, int m, int r0, int nb, int bwd, cudaStream_t s) {
+  const int rows = bwd ? r0 : n - r0 - nb;
+  auto go = [&](auto kern, int nc) -> cudaError_t {
+    const size_t smem = (size_t(128) * (nc + 2) + size_t(128) * 66) * sizeof(double);
+    static size_t attr[2] = {0, 0};
+    size_t& a = attr[nc == 128 ? 1 : 0];  // (per instantiation: the lambda is a template)
+    if (a < smem) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      a = smem;
+    }
+    dim3 grid((m + nc - 1) / nc, 1 + (rows + 63) / 64);
+    kern<<<grid, 256, smem, s>>>(F, ldf, Db, src, lds, dst, ldd, n, m, r0, nb, bwd);
+    return cudaGetLastError();
+  };
+  static const int nc = std::getenv("RBPG_TRSM_NC") ? std::atoi(std::getenv("RBPG_TRSM_NC")) : 32;
+  if (nc == 128) return go(trsm_step_kernel<128>, 128);
+  if (nc == 64) return go(trsm_step_kernel<64>, 64);
+  return go(trsm_step_kernel<32>, 32);
+}
+
 // The 64 x 64 diagonal-block inverses of F (blocked TRSM path of the engine).
 cudaError_t launch_tri_inv(const double* F, long long ldf, int n, double* dinv, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
