@@ -169,10 +169,17 @@ def main():
 
     import paper_2011_02436_b200 as rb
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # RBPG_DIST_BACKEND=gloo + more ranks than GPUs: a functional check of the sharded orchestration
+    # on one GPU (host-staged all-reduce; not a scaling measurement)
+    backend = os.environ.get("RBPG_DIST_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     # ---- inputs: this rank's contiguous row shard of the global matrix, resident in HBM
     xh, th = rb.synth_classification(n, d, m, SEED_X, SEED_TEACHER, row0=rank * n)
@@ -182,7 +189,7 @@ def main():
     hidden = rb.init_hidden(params)
     W = torch.from_numpy(hidden.weights).to(dev)
     B = torch.from_numpy(hidden.biases.reshape(-1)).to(dev)
-    ctx = rb.context(local)
+    ctx = rb.context(local_dev)
     strat = rb.SolverStrategy.rank_based()
     N_total = n * world
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
@@ -195,9 +202,13 @@ def main():
             return diag
         # row shard -> augmented Gram [H T]^T [H T] -> ONE all-reduce -> replicated solve
         rb.gram_stage_device_aug(X, T, W, B, Gaug, ctx=ctx)
+        if backend != "nccl":
+            torch.cuda.synchronize()  # host-staged backends do not order against the stream
         dist.all_reduce(Gaug)
         beta, diag = rb.solve_stage_device_aug(Gaug, L, m, N_total, strat, ctx=ctx)
         hits = torch.tensor([rb.accuracy_stage_device(X, T, W, B, beta, ctx=ctx)], dtype=torch.int64, device=dev)
+        if backend != "nccl":
+            torch.cuda.synchronize()
         dist.all_reduce(hits)
         diag.training_accuracy = hits.item() / N_total
         return diag
@@ -212,7 +223,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = ctx.launch_count
-    with ClockSampler(local) as clk:
+    with ClockSampler(local_dev) as clk:
         for i in range(args.steps):
             flush.zero_()  # L2 flush between timed steps (outside the events)
             ev[i][0].record(stream)
@@ -246,6 +257,39 @@ def main():
 
     # ---- e2e: the reference-facing C-ABI call with host (pinned) buffers, copies inside the timed region
     e2e = None
+    if world > 1:
+        # the sharded train() through the Python API from this rank's pinned host shard: H2D of the
+        # shard, augmented Gram, all-reduce, replicated solve, hit-count all-reduce, beta back to host
+        from paper_2011_02436_b200 import sharded
+
+        xp = torch.empty((n, d), dtype=torch.float64).pin_memory()
+        tp = torch.empty((n, m), dtype=torch.float64).pin_memory()
+        xp.copy_(torch.from_numpy(xh))
+        tp.copy_(torch.from_numpy(th))
+        stages = sharded.DeviceStages(ctx)
+
+        def e2e_step():
+            xd = xp.to(dev, non_blocking=True)
+            td = tp.to(dev, non_blocking=True)
+            beta, dg, _, _ = sharded.train_sharded(xd, td, params, strat, N_total, stages=stages, hidden=hidden)
+            return beta.cpu()
+
+        e2e_step()
+        t_e = []
+        for _ in range(max(3, args.steps)):
+            flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            e2e_step()
+            torch.cuda.synchronize()
+            te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            t_e.append(float(te.item()))
+        e2e_s = statistics.median(t_e)
+        e2e = {"value": flops / e2e_s / 1e12, "unit": "TFLOP/s", "seconds": e2e_s,
+               "h2d_bytes_per_step": int(n * d * 8 + n * m * 8), "d2h_bytes_per_step": int(L * m * 8),
+               "api": "sharded.train_sharded (Python API, pinned host shard per rank; max over ranks)"}
     if world == 1:
         xp = torch.empty((n, d), dtype=torch.float64).pin_memory()
         tp = torch.empty((n, m), dtype=torch.float64).pin_memory()

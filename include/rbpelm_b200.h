@@ -70,7 +70,8 @@ typedef struct rbpg_context rbpg_context;
 /* ---- context (one per device; per-call stream-safe when not shared across threads) */
 int rbpg_context_create(int device, rbpg_context** out, rbpg_status* st);
 void rbpg_context_destroy(rbpg_context* ctx);
-/* stream the device entry points run on (cudaStream_t); NULL = context's own stream */
+/* stream the device entry points run on (cudaStream_t); NULL = the context's own non-blocking stream
+ * (pass cudaStreamLegacy, 0x1, for the legacy default stream) */
 int rbpg_context_set_stream(rbpg_context* ctx, void* stream, rbpg_status* st);
 int rbpg_context_synchronize(rbpg_context* ctx, rbpg_status* st);
 /* number of kernels this context has launched (evidence counter for bench.py) */

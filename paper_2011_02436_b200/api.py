@@ -235,6 +235,16 @@ _ctx_lock = threading.Lock()
 _contexts = {}
 
 
+def _torch_stream(device) -> int:
+    """Handle of torch's current stream on `device` for the device entry points.  torch's default
+    stream is the legacy NULL stream (handle 0), which rbpg_context_set_stream would read as "the
+    context's own (non-blocking) stream" -- unordered with torch's work -- so it is passed as
+    cudaStreamLegacy (0x1) instead."""
+    import torch
+
+    return torch.cuda.current_stream(device).cuda_stream or 1
+
+
 def context(device: int = 0) -> Context:
     with _ctx_lock:
         c = _contexts.get(device)
@@ -555,7 +565,7 @@ def train_device(x, t, params: ElmParams, strategy: SolverStrategy, hidden: Opti
     import torch
 
     ctx = ctx or context(x.device.index or 0)
-    ctx.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
+    ctx.set_stream(_torch_stream(x.device))
     hidden = hidden or init_hidden(params)
     w = _f64(hidden.weights)
     b = _f64(hidden.biases)
@@ -581,7 +591,7 @@ def gram_stage_device(x, t, w, b, g, htt, accumulate: bool = False, keep_h: bool
     import torch
 
     ctx = ctx or context(x.device.index or 0)
-    ctx.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
+    ctx.set_stream(_torch_stream(x.device))
     st = rbpg_status()
     ctx.lib.rbpg_gram_stage_device(ctx.handle, _tptr(x), _ld(x), _tptr(t), _ld(t), x.shape[0], x.shape[1],
                                    w.shape[1], t.shape[1], _tptr(w), _ld(w), _tptr(b), _tptr(g), _ld(g), _tptr(htt),
@@ -595,7 +605,7 @@ def solve_stage_device(g, htt, n_total: int, strategy: SolverStrategy, ctx: Opti
     import torch
 
     ctx = ctx or context(g.device.index or 0)
-    ctx.set_stream(torch.cuda.current_stream(g.device).cuda_stream)
+    ctx.set_stream(_torch_stream(g.device))
     L, m = htt.shape
     beta = torch.empty((L, m), dtype=torch.float64, device=g.device)
     order = np.zeros(L, dtype=np.uint64)
@@ -618,7 +628,7 @@ def gram_stage_device_aug(x, t, w, b, gaug, accumulate: bool = False, keep_h: bo
     import torch
 
     ctx = ctx or context(x.device.index or 0)
-    ctx.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
+    ctx.set_stream(_torch_stream(x.device))
     st = rbpg_status()
     ctx.lib.rbpg_gram_stage_device_aug(ctx.handle, _tptr(x), _ld(x), _tptr(t), _ld(t), x.shape[0], x.shape[1],
                                        w.shape[1], t.shape[1], _tptr(w), _ld(w), _tptr(b), _tptr(gaug), _ld(gaug),
@@ -632,7 +642,7 @@ def solve_stage_device_aug(gaug, L: int, m: int, n_total: int, strategy: SolverS
     import torch
 
     ctx = ctx or context(gaug.device.index or 0)
-    ctx.set_stream(torch.cuda.current_stream(gaug.device).cuda_stream)
+    ctx.set_stream(_torch_stream(gaug.device))
     beta = torch.empty((L, m), dtype=torch.float64, device=gaug.device)
     order = np.zeros(L, dtype=np.uint64)
     s = strategy._c()
@@ -653,7 +663,7 @@ def accuracy_stage_device(x, t, w, b, beta, ctx: Optional[Context] = None) -> in
     import torch
 
     ctx = ctx or context(x.device.index or 0)
-    ctx.set_stream(torch.cuda.current_stream(x.device).cuda_stream)
+    ctx.set_stream(_torch_stream(x.device))
     hits = ctypes.c_uint64()
     st = rbpg_status()
     ctx.lib.rbpg_accuracy_stage_device(ctx.handle, _tptr(x), _ld(x), _tptr(t), _ld(t), x.shape[0], x.shape[1],
@@ -668,7 +678,7 @@ def gram_device(a, g, accumulate: bool = False, ctx: Optional[Context] = None) -
     import torch
 
     ctx = ctx or context(a.device.index or 0)
-    ctx.set_stream(torch.cuda.current_stream(a.device).cuda_stream)
+    ctx.set_stream(_torch_stream(a.device))
     st = rbpg_status()
     ctx.lib.rbpg_gram_device(ctx.handle, _tptr(a), _ld(a), a.shape[0], a.shape[1], _tptr(g), _ld(g), int(accumulate),
                              ctypes.byref(st))
@@ -682,7 +692,7 @@ def pseudo_inverse_stage_device(g, h, n_total: int, tol: float = 0.0, ctx: Optio
     import torch
 
     ctx = ctx or context(g.device.index or 0)
-    ctx.set_stream(torch.cuda.current_stream(g.device).cuda_stream)
+    ctx.set_stream(_torch_stream(g.device))
     L = g.shape[0]
     n_local = h.shape[0]
     out = torch.empty((L, max(n_local, 1) + (max(n_local, 1) & 1)), dtype=torch.float64, device=g.device)

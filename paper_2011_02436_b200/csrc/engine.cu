@@ -1570,7 +1570,16 @@ int rbpg_gram_device(rbpg_context* ctx, const double* da, size_t lda, size_t row
   return guarded(ctx, st, [&] {
     if (cols == 0) fail(RBPG_SHAPE_ERROR, "gram: empty matrix");
     Padded A = pad_device(ctx, "gram.a", da, lda, rows, cols);
-    gram_dev(ctx, A.p, A.ld, rows, cols, nullptr, 0, 0, dg, ldg, nullptr, 0, accumulate != 0);
+    if (ldg % 2 == 0 && (reinterpret_cast<uintptr_t>(dg) & 15) == 0) {
+      gram_dev(ctx, A.p, A.ld, rows, cols, nullptr, 0, 0, dg, ldg, nullptr, 0, accumulate != 0);
+    } else {  // 16-byte vector stores: stage an odd leading dimension / unaligned base
+      const size_t lds = round_up(cols, 8);
+      double* S = ctx->dbuf("gram.stage", cols * lds);
+      if (accumulate)
+        ck(cudaMemcpy2DAsync(S, lds * 8, dg, ldg * 8, cols * 8, cols, cudaMemcpyDeviceToDevice, ctx->stream), "stage");
+      gram_dev(ctx, A.p, A.ld, rows, cols, nullptr, 0, 0, S, lds, nullptr, 0, accumulate != 0);
+      ck(cudaMemcpy2DAsync(dg, ldg * 8, S, lds * 8, cols * 8, cols, cudaMemcpyDeviceToDevice, ctx->stream), "store");
+    }
     ck(cudaStreamSynchronize(ctx->stream), "sync");
   });
 }
@@ -1779,7 +1788,19 @@ int rbpg_gram_stage_device_aug(rbpg_context* ctx, const double* dx, size_t ldx, 
     Padded X = pad_device(ctx, "X.pad", dx, ldx, n, d);
     Padded T = pad_device(ctx, "T.pad", dt, ldt_in, n, m);
     Padded W = pad_device(ctx, "W.pad", dw, ldw, d, l);
-    gram_stage(ctx, X.p, X.ld, T.p, T.ld, n, d, l, m, W.p, W.ld, db, dgaug, ldga, accumulate != 0, keep_h != 0, false);
+    // the Gram kernels store 16-byte vectors: an odd leading dimension (or unaligned base) goes
+    // through an aligned staging buffer
+    if (ldga % 2 == 0 && (reinterpret_cast<uintptr_t>(dgaug) & 15) == 0) {
+      gram_stage(ctx, X.p, X.ld, T.p, T.ld, n, d, l, m, W.p, W.ld, db, dgaug, ldga, accumulate != 0, keep_h != 0,
+                 false);
+      return;
+    }
+    const size_t M = l + m, lds = round_up(M, 8);
+    double* S = ctx->dbuf("Gaug.stage", M * lds);
+    if (accumulate)
+      ck(cudaMemcpy2DAsync(S, lds * 8, dgaug, ldga * 8, M * 8, M, cudaMemcpyDeviceToDevice, ctx->stream), "stage G");
+    gram_stage(ctx, X.p, X.ld, T.p, T.ld, n, d, l, m, W.p, W.ld, db, S, lds, accumulate != 0, keep_h != 0, false);
+    ck(cudaMemcpy2DAsync(dgaug, ldga * 8, S, lds * 8, M * 8, M, cudaMemcpyDeviceToDevice, ctx->stream), "store G");
   });
 }
 

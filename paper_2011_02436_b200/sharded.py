@@ -81,11 +81,15 @@ def train_sharded(x_local, t_local, params: api.ElmParams, strategy: api.SolverS
     gaug = stages.gram_aug(x_local, t_local, w, b)
     distributed = dist.is_available() and dist.is_initialized()
     if distributed:
+        if gaug.is_cuda and dist.get_backend(group) != "nccl":
+            torch.cuda.synchronize(gaug.device)  # host-staged backends (gloo) do not order against the stream
         dist.all_reduce(gaug, group=group)  # the one exchange step of the path
     L, m = w.shape[1], t_local.shape[1]
     beta, diag, order = stages.solve_aug(gaug, L, m, n_total, strategy)
     hits = torch.tensor([stages.hits(x_local, t_local, w, b, beta)], dtype=torch.int64, device=gaug.device)
     if distributed:
+        if hits.is_cuda and dist.get_backend(group) != "nccl":
+            torch.cuda.synchronize(hits.device)
         dist.all_reduce(hits, group=group)
     diag.training_accuracy = float(hits.item()) / float(n_total)
     return beta, diag, hidden, order
