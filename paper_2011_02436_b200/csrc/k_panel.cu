@@ -448,16 +448,17 @@ constexpr int kRowLen = 4 * kRowQ;
 constexpr size_t kQrowBytes = size_t(kRegLabels) * kRowLen * sizeof(double);
 
 // kTrace: per-phase cycle counters (RBPG_PANEL_TRACE), compiled out of the production variant
-template <bool kTrace>
+template <bool kTrace, int LPQ>
 __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) {
+  constexpr int kLabels = kRegLabels * LPQ;  // labels per CTA: LPQ per quad
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = p.n, k = p.k, kb = p.kb, nl = n - k;
-  const int R = p.rows_per_cta;  // <= 64
+  const int R = p.rows_per_cta;  // <= kLabels
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), cta = static_cast<int>(cl.block_rank());
   double (*qrow)[kRowLen] = reinterpret_cast<double (*)[kRowLen]>(smem_raw);  // [kRegLabels] own rows
-  int* lab_at = reinterpret_cast<int*>(smem_raw + kQrowBytes);  // [nl]
+  int* lab_at = reinterpret_cast<int*>(smem_raw + kQrowBytes * LPQ);  // [nl]
   int* pos_of = lab_at + nl;                                     // [nl]
   __shared__ Cand cand_all[2][kMaxCluster];
   // candidate rows, lane-major with a padded quarter stride (row[q*kRowQ + i] = P[label][q + 4i]):
@@ -480,11 +481,20 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   }
   const int lbeg = k + cta * R;
   const int nown = max(0, min(n, lbeg + R) - lbeg);
-  const int li = tid >> 2, q = tid & 3;
-  const int x = lbeg + li;
-  const bool mine = li < nown;
-  double* myrow = &qrow[li][q * kRowQ];  // this lane's 16 slots of its label's row
-  double dl = mine ? p.d_in[x] : -DBL_MAX;
+  const int qi = tid >> 2, q = tid & 3;
+  // quad qi holds labels lbeg + qi + 64 l (l < LPQ): consecutive quads, consecutive labels
+  int x[LPQ];
+  bool mine[LPQ];
+  double* myrow[LPQ];  // this lane's 16 slots of each of its labels' rows
+  double dl[LPQ];
+#pragma unroll
+  for (int l = 0; l < LPQ; ++l) {
+    const int li = qi + kRegLabels * l;
+    x[l] = lbeg + li;
+    mine[l] = li < nown;
+    myrow[l] = &qrow[li][q * kRowQ];
+    dl[l] = mine[l] ? p.d_in[x[l]] : -DBL_MAX;
+  }
 
   for (int i = tid; i < nl; i += blockDim.x) {
     lab_at[i] = k + i;
@@ -500,13 +510,28 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   const double cut = st->cut;
   const double thresh = st->thresh;
   for (int i = tid; i < 2 * kMaxCluster * kRowLen; i += blockDim.x) (&rows_all[0][0][0])[i] = 0.0;
-  for (int i = tid; i < kRegLabels * kRowLen; i += blockDim.x) (&qrow[0][0])[i] = 0.0;
+  for (int i = tid; i < kLabels * kRowLen; i += blockDim.x) (&qrow[0][0])[i] = 0.0;
   __syncthreads();
 
   // the CTA row index (label - lbeg) of this warp's best candidate (any valid row when none)
-  auto best_row = [&](unsigned long long key, int pos, int mypos, unsigned long long mykey) {
+  // (myl: which of the lane's labels the lane's own candidate is)
+  auto best_row = [&](unsigned long long key, int pos, int mypos, unsigned long long mykey, int myl) {
     const unsigned who = __ballot_sync(0xffffffffu, q == 0 && mykey == key && mypos == pos && pos != INT_MAX);
-    return who ? warp * 8 + ((__ffs(who) - 1) >> 2) : 0;
+    if constexpr (LPQ == 1) {
+      return who ? warp * 8 + ((__ffs(who) - 1) >> 2) : 0;
+    } else {
+      const int src = who ? __ffs(who) - 1 : 0;
+      const int bl = __shfl_sync(0xffffffffu, myl, src);
+      return who ? warp * 8 + (src >> 2) + kRegLabels * bl : 0;
+    }
+  };
+  // the lane's best candidate over its LPQ labels: larger key, then smaller position
+  auto lane_best = [](unsigned long long& key, int& pos, int& bl, unsigned long long kk, int pp, int l) {
+    if (kk > key || (kk == key && pp < pos)) {
+      key = kk;
+      pos = pp;
+      bl = l;
+    }
   };
   // publish for step j: the CTA's candidate and its row's first nch slot chunks (the receiving
   // step reads no later chunk; columns beyond those are zero or not yet summed)
@@ -536,20 +561,21 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   // ---- initial candidates (rows are still zero)
   {
     unsigned long long key = 0;
-    int pos = INT_MAX;
-    if (mine && q == 0 && x < p.neligible) {
-      if (p.pivoting) {
-        key = dkey(dl);
-        pos = x;
-      } else if (x == k) {
-        key = dkey(dl);
-        pos = k;
+    int pos = INT_MAX, bl = 0;
+#pragma unroll
+    for (int l = 0; l < LPQ; ++l) {
+      if (mine[l] && q == 0 && x[l] < p.neligible) {
+        if (p.pivoting) {
+          lane_best(key, pos, bl, dkey(dl[l]), x[l], l);
+        } else if (x[l] == k) {
+          lane_best(key, pos, bl, dkey(dl[l]), k, l);
+        }
       }
     }
     const unsigned long long mk = key;
     const int mp = pos;
     warp_argmax(key, pos);
-    const int brow = best_row(key, pos, mp, mk);
+    const int brow = best_row(key, pos, mp, mk, bl);
     if (lane == 0) {
       wbest[warp].key = key;
       wbest[warp].pos = pos;
@@ -577,9 +603,11 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   // Steps run in 4 groups of 16 (the outer loop is unrolled, so the group ch is a compile-time
   // constant): group ch writes only slot chunk ch of the rows, so the label's own row stays in
   // registers and only that chunk (plus, on entry, the previous one) is re-read per step.
-  double2 own[8];
+  double2 own[LPQ][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) own[i] = make_double2(0.0, 0.0);
+  for (int l = 0; l < LPQ; ++l)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) own[l][i] = make_double2(0.0, 0.0);
 #pragma unroll
   for (int ch = 0; ch < 4; ++ch) {
 #pragma unroll 1
@@ -591,14 +619,19 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const int jp = j - 1;
     auto lab_eff = [&](int ps) { return ps == jp ? xpp : (ps == pivp ? ypp : lab_at[ps - k]); };
     auto pos_eff = [&](int lb) { return lb == xpp ? jp : (lb == ypp ? pivp : pos_of[lb - k]); };
-    const int mypos = mine ? pos_eff(x) : -1;   // before the exchange wait
+    int mypos[LPQ];
+#pragma unroll
+    for (int l = 0; l < LPQ; ++l) mypos[l] = mine[l] ? pos_eff(x[l]) : -1;  // before the exchange wait
     const int y = lab_eff(j);
     // this label's row: the chunk written by this group (and the previous group's last column)
-    own[2 * ch] = reinterpret_cast<const double2*>(myrow)[2 * ch];
-    own[2 * ch + 1] = reinterpret_cast<const double2*>(myrow)[2 * ch + 1];
-    if (ch > 0 && u == 0) {
-      own[2 * ch - 1] = reinterpret_cast<const double2*>(myrow)[2 * ch - 1];
-      own[2 * ch - 2] = reinterpret_cast<const double2*>(myrow)[2 * ch - 2];
+#pragma unroll
+    for (int l = 0; l < LPQ; ++l) {
+      own[l][2 * ch] = reinterpret_cast<const double2*>(myrow[l])[2 * ch];
+      own[l][2 * ch + 1] = reinterpret_cast<const double2*>(myrow[l])[2 * ch + 1];
+      if (ch > 0 && u == 0) {
+        own[l][2 * ch - 1] = reinterpret_cast<const double2*>(myrow[l])[2 * ch - 1];
+        own[l][2 * ch - 2] = reinterpret_cast<const double2*>(myrow[l])[2 * ch - 2];
+      }
     }
     if (warp == 0 && lane == 0)
       mbar_arrive_expect_tx(&cand_full[c & 1],
@@ -620,18 +653,26 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     PANEL_TS(2);
     const double dj = dkey_inv(wkey);
     // this quad's label: position after this step's swap and G entry (load issued first)
-    int pos = -1;
-    if (mine) pos = (x == y) ? piv : (x == xp ? j : mypos);
-    const bool alive = pos > j;
-    // G through its lower triangle (trailing updates behind this variant write only that half)
-    const double gv = alive ? p.G[(long long)max(xp, x) * p.ldg + min(xp, x)] : 0.0;
+    int pos[LPQ];
+    bool alive[LPQ];
+    double gv[LPQ];
+#pragma unroll
+    for (int l = 0; l < LPQ; ++l) {
+      pos[l] = -1;
+      if (mine[l]) pos[l] = (x[l] == y) ? piv : (x[l] == xp ? j : mypos[l]);
+      alive[l] = pos[l] > j;
+      // G through its lower triangle (trailing updates behind this variant write only that half)
+      gv[l] = alive[l] ? p.G[(long long)max(xp, x[l]) * p.ldg + min(xp, x[l])] : 0.0;
+    }
     // the dot product and sqrt(dj) go before the stop test: one basic block, so their latency
     // chains interleave (dj <= 0 or NaN always stops; rjj is then unused)
     const double* prow = rows_all[c & 1][src];  // lane-major: prow[q*16 + i] = P[xp][q + 4i]
     // ---- update: dot over columns cc = q + 4i < c from registers.  Entries at and beyond c are
     // zero in both operands, so whole 16-column chunks are summed unpredicated; a chunk is skipped
     // (warp-uniform) once c <= its first column.
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double a0[LPQ], a1[LPQ], a2[LPQ], a3[LPQ];
+#pragma unroll
+    for (int l = 0; l < LPQ; ++l) a0[l] = a1[l] = a2[l] = a3[l] = 0.0;
     const double2* pv = reinterpret_cast<const double2*>(prow + q * kRowQ);
     if (kTrace) {  // diagnostic split of the dot phase: first row chunk landed
       const double2 t = pv[0];
@@ -642,17 +683,24 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     for (int i = 0; i < 16; i += 4) {
       if (i / 4 < ch || (i / 4 == ch && u > 0)) {  // == (c > 4 * i)
         const double2 v0 = pv[i / 2], v1 = pv[i / 2 + 1];
-        const double2 u0 = own[i / 2], u1 = own[i / 2 + 1];
-        a0 = fma(u0.x, v0.x, a0);
-        a1 = fma(u0.y, v0.y, a1);
-        a2 = fma(u1.x, v1.x, a2);
-        a3 = fma(u1.y, v1.y, a3);
+#pragma unroll
+        for (int l = 0; l < LPQ; ++l) {
+          const double2 u0 = own[l][i / 2], u1 = own[l][i / 2 + 1];
+          a0[l] = fma(u0.x, v0.x, a0[l]);
+          a1[l] = fma(u0.y, v0.y, a1[l]);
+          a2[l] = fma(u1.x, v1.x, a2[l]);
+          a3[l] = fma(u1.y, v1.y, a3[l]);
+        }
       }
     }
-    double sq = (a0 + a1) + (a2 + a3);
-    sq = sq + __shfl_xor_sync(0xffffffffu, sq, 1);
-    sq = sq + __shfl_xor_sync(0xffffffffu, sq, 2);
-    PANEL_FORCE(sq);
+    double sq[LPQ];
+#pragma unroll
+    for (int l = 0; l < LPQ; ++l) {
+      sq[l] = (a0[l] + a1[l]) + (a2[l] + a3[l]);
+      sq[l] = sq[l] + __shfl_xor_sync(0xffffffffu, sq[l], 1);
+      sq[l] = sq[l] + __shfl_xor_sync(0xffffffffu, sq[l], 2);
+    }
+    PANEL_FORCE(sq[0]);
     PANEL_TS(3);
     const double rjj = sqrt(dj);
     bool stop;
@@ -690,20 +738,23 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     PANEL_TS(5);
     const int slot = c >> 2, owner_lane = c & 3;
     unsigned long long bkey = 0;
-    int bpos = INT_MAX;
-    const double col = (gv - sq) * inv_rjj;
-    PANEL_FORCE(col);
+    int bpos = INT_MAX, bl = 0;
+    double col[LPQ];
+#pragma unroll
+    for (int l = 0; l < LPQ; ++l) col[l] = (gv[l] - sq[l]) * inv_rjj;
+    PANEL_FORCE(col[0]);
     PANEL_TS(6);
-    // branch-free register write of the new column (alive labels) or of F(j, j) = rjj (the pivot)
-    const bool is_piv = mine && x == xp;
-    const bool wr = (alive || is_piv) && q == owner_lane;
-    const double wv = alive ? col : rjj;
-    if (wr) myrow[slot] = wv;  // read by this step's publication (after the barrier) and later steps
-    if (alive) {
-      dl = fma(-col, col, dl);
-      if (q == 0 && x < p.neligible && (p.pivoting || pos == j + 1)) {
-        bkey = dkey(dl);
-        bpos = pos;
+#pragma unroll
+    for (int l = 0; l < LPQ; ++l) {
+      // branch-free write of the new column (alive labels) or of F(j, j) = rjj (the pivot)
+      const bool is_piv = mine[l] && x[l] == xp;
+      const bool wr = (alive[l] || is_piv) && q == owner_lane;
+      const double wv = alive[l] ? col[l] : rjj;
+      if (wr) myrow[l][slot] = wv;  // read by this step's publication (after the barrier) and later steps
+      if (alive[l]) {
+        dl[l] = fma(-col[l], col[l], dl[l]);
+        if (q == 0 && x[l] < p.neligible && (p.pivoting || pos[l] == j + 1))
+          lane_best(bkey, bpos, bl, dkey(dl[l]), pos[l], l);
       }
     }
     const unsigned long long mk = bkey;
@@ -711,7 +762,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     warp_argmax(bkey, bpos);
     PANEL_FORCE(bpos);
     PANEL_TS(7);
-    const int brow = best_row(bkey, bpos, mp, mk);
+    const int brow = best_row(bkey, bpos, mp, mk, bl);
     if (lane == 0) {
       wbest[warp].key = bkey;
       wbest[warp].pos = bpos;
@@ -745,23 +796,25 @@ panel_done:
   cl.sync();  // no CTA leaves while remote st.async may target it
 
   // ---- write back: Fo rows by original column, trailing panel, d, order
-  if (mine) {
-    const int orig = p.ord_in[x];
+#pragma unroll
+  for (int l = 0; l < LPQ; ++l) {
+    if (!mine[l]) continue;
+    const int orig = p.ord_in[x[l]];
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       const int cc = q + 4 * i;
-      if (cc < kb) p.Fo[(long long)orig * p.ldf + k + cc] = myrow[i];
+      if (cc < kb) p.Fo[(long long)orig * p.ldf + k + cc] = myrow[l][i];
     }
     if (!s_stop) {
       const int t0 = k + kb;
-      const int ps = pos_of[x - k];
+      const int ps = pos_of[x[l] - k];
       if (ps >= t0) {
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int cc = q + 4 * i;
-          if (cc < kb) p.PcT[(long long)cc * p.ldp + (ps - t0)] = myrow[i];
+          if (cc < kb) p.PcT[(long long)cc * p.ldp + (ps - t0)] = myrow[l][i];
         }
-        if (q == 0) p.d_out[ps] = dl;
+        if (q == 0) p.d_out[ps] = dl[l];
       }
     }
   }
@@ -790,22 +843,35 @@ int panel_cluster_size(int nl) {
   return 0;
 }
 
-// Whether a panel of nl labels runs panel_reg_kernel (which reads G through its lower triangle).
-bool panel_is_reg(int nl) {
+// Labels per quad of panel_reg_kernel for a panel of nl labels (0: another variant).  Up to 4
+// labels per quad (256 per CTA, 4096 per 16-CTA cluster); RBPG_PANEL_REG_LPQ caps it (1 = the
+// round-1 limit of 1024 labels) and RBPG_PANEL_SMEM disables the variant.
+int panel_reg_lpq(int nl) {
+  static const int cap = std::getenv("RBPG_PANEL_SMEM") ? 0
+                         : std::getenv("RBPG_PANEL_REG_LPQ") ? std::atoi(std::getenv("RBPG_PANEL_REG_LPQ"))
+                                                               : 4;
   const int CL = panel_cluster_size(nl);
-  return CL > 0 && (nl + CL - 1) / CL <= kRegLabels && !std::getenv("RBPG_PANEL_SMEM");
+  if (CL <= 0) return 0;
+  const int R = (nl + CL - 1) / CL;
+  const int lpq = R <= kRegLabels ? 1 : (R <= 2 * kRegLabels ? 2 : (R <= 4 * kRegLabels ? 4 : 0));
+  return lpq <= cap ? lpq : 0;
 }
+
+// Whether a panel of nl labels runs panel_reg_kernel (which reads G through its lower triangle).
+bool panel_is_reg(int nl) { return panel_reg_lpq(nl) > 0; }
 
 cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cudaStream_t s) {
   const int nl = p.n - p.k;
   PanelParams pp = p;
   const int CL = panel_cluster_size(nl);
-  if (panel_is_reg(nl)) {
+  if (const int lpq = panel_reg_lpq(nl)) {
     pp.rows_per_cta = (nl + CL - 1) / CL;
-    const size_t smem = kQrowBytes + size_t(2) * nl * sizeof(int);
-    auto kern = p.trace ? panel_reg_kernel<true> : panel_reg_kernel<false>;
-    static size_t attr[2] = {0, 0};
-    size_t& a = attr[p.trace ? 1 : 0];
+    const size_t smem = kQrowBytes * lpq + size_t(2) * nl * sizeof(int);
+    auto kern = lpq == 1 ? (p.trace ? panel_reg_kernel<true, 1> : panel_reg_kernel<false, 1>)
+                : lpq == 2 ? (p.trace ? panel_reg_kernel<true, 2> : panel_reg_kernel<false, 2>)
+                           : (p.trace ? panel_reg_kernel<true, 4> : panel_reg_kernel<false, 4>);
+    static size_t attr[6] = {0, 0, 0, 0, 0, 0};
+    size_t& a = attr[(p.trace ? 1 : 0) + 2 * (lpq == 1 ? 0 : (lpq == 2 ? 1 : 2))];
     if (smem > a || a == 0) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            (int)(smem > 0 ? smem : 16));
