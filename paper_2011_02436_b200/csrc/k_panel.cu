@@ -927,6 +927,8 @@ cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cuda
   // grid variant: ~ceil(nl / num_sms) labels per CTA, every CTA co-resident (cooperative launch)
   int R = (nl + num_sms - 1) / num_sms;
   if (R < 32) R = 32;
+  static const int min_r = std::getenv("RBPG_PANEL_GRID_R") ? std::atoi(std::getenv("RBPG_PANEL_GRID_R")) : 0;
+  if (R < min_r) R = std::min(min_r, kMaxLabelsPerCta);
   if (R > kMaxLabelsPerCta) return cudaErrorInvalidValue;  // n > 256 * num_sms unsupported
   const int C = (nl + R - 1) / R;
   pp.rows_per_cta = R;
