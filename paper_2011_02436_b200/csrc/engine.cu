@@ -594,8 +594,8 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
       sp.ldgo = static_cast<long long>(ldcur);
       sp.lab = lab;
       sp.off = static_cast<int>(t0);
-      // the register-resident panel reads G through its lower triangle; the others read rows
-      sp.mirror = panel_is_reg(static_cast<int>(n - t0)) ? 0 : 1;
+      // every panel variant reads G through its lower triangle: no mirrored upper half
+      sp.mirror = 0;
       if (tl && tl_n < tl_max) {
         sp.tl = tl;
         sp.tl_slot = tl_n++;

@@ -276,11 +276,12 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
       prow = prow_g;
     }
     // this warp's first-pass G entries, issued before the FP64 math
-    const double* grow = p.G + (long long)xp * p.ldg;
+    // G through its lower triangle (the trailing updates write only that half)
+    auto gat = [&](int xl) { return p.G[(long long)max(xp, xl) * p.ldg + min(xp, xl)]; };
     double gpre = 0.0;
     {
       const int li0 = warp * 8 + (lane >> 2);
-      if ((lane & 3) == 0 && li0 < nown) gpre = grow[lbeg + li0];
+      if ((lane & 3) == 0 && li0 < nown) gpre = gat(lbeg + li0);
     }
     bool stop;
     if (p.pivoting) {
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
       int pos = -1;
       if (li < nown) pos = (x == y) ? piv : (x == xp ? j : pos_of[x - k]);
       const bool alive = pos > j;
-      const double gv = (alive && q == 0) ? (base == warp * 8 ? gpre : grow[x]) : 0.0;
+      const double gv = (alive && q == 0) ? (base == warp * 8 ? gpre : gat(x)) : 0.0;
       double s = 0.0;
       if (alive) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
