@@ -17,6 +17,8 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstdio>
 
@@ -529,7 +531,9 @@ __global__ void __launch_bounds__(256, 1)
 // so their latency hides under the tensor-core work.  G_old is read through its lower triangle
 // (G[max][min]) and G_new is written lower-only unless p.mirror (the next panel reads whole rows).
 // TILE 32 (64 threads) for the small late updates: four times the CTAs per DMMA of a 64-wide tile.
-template <int TILE>
+// KS: k-stages resident (4 = the whole rank-64 panel loaded up front; 2 = two halves through two
+// stages, ~35 KB less shared memory so a third CTA fits on an SM)
+template <int TILE, int KS = kStages>
 __global__ void __launch_bounds__(2 * TILE, 1)
     trail_kernel(const __grid_constant__ CUtensorMap tmP, SyrkParams p) {
   constexpr int NT = 2 * TILE;      // threads: warps of (TILE / 2) x 32
@@ -540,8 +544,8 @@ __global__ void __launch_bounds__(2 * TILE, 1)
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = align1024(smem_raw);
   double* As = reinterpret_cast<double*>(smem);  // [stage][16][TP]
-  double* Bs = As + kStages * kBK * TP;          // [stage][16][TP]
-  double* gsm = Bs + kStages * kBK * TP;         // [NG][NT]
+  double* Bs = As + KS * kBK * TP;               // [stage][16][TP]
+  double* gsm = Bs + KS * kBK * TP;              // [NG][NT]
   uint64_t* full = reinterpret_cast<uint64_t*>(gsm + NG * NT);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   int I, J;
@@ -559,7 +563,7 @@ __global__ void __launch_bounds__(2 * TILE, 1)
   const uint32_t stage_bytes = (diag ? 1u : 2u) * TP * kBK * sizeof(double);
   if (tid == 0) {
     tma_prefetch_desc(&tmP);
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < KS; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
   }
   tl_mark(p.tl, p.tl_slot, 0);
@@ -569,7 +573,7 @@ __global__ void __launch_bounds__(2 * TILE, 1)
   tl_mark(p.tl, p.tl_slot, 1);
   __syncthreads();
   if (tid == 0) {
-    for (int s = 0; s < ktiles; ++s) {
+    for (int s = 0; s < ktiles && s < KS; ++s) {
       mbar_arrive_expect_tx(&full[s], stage_bytes);
       tma_load_2d(As + s * kBK * TP, &tmP, &full[s], i0, s * kBK);
       if (!diag) tma_load_2d(Bs + s * kBK * TP, &tmP, &full[s], j0, s * kBK);
@@ -618,9 +622,18 @@ __global__ void __launch_bounds__(2 * TILE, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
   for (int kt = 0; kt < ktiles; ++kt) {
-    mbar_wait(&full[kt], 0);
-    const double* as = As + kt * kBK * TP;
-    const double* bs = diag ? as : Bs + kt * kBK * TP;
+    if (KS < kStages && kt == KS) {  // first half consumed: the second half into the same stages
+      __syncthreads();
+      if (tid == 0)
+        for (int s = 0; s < KS && KS + s < ktiles; ++s) {
+          mbar_arrive_expect_tx(&full[s], stage_bytes);
+          tma_load_2d(As + s * kBK * TP, &tmP, &full[s], i0, (KS + s) * kBK);
+          if (!diag) tma_load_2d(Bs + s * kBK * TP, &tmP, &full[s], j0, (KS + s) * kBK);
+        }
+    }
+    mbar_wait(&full[kt % KS], (kt / KS) & 1);
+    const double* as = As + (kt % KS) * kBK * TP;
+    const double* bs = diag ? as : Bs + (kt % KS) * kBK * TP;
 #pragma unroll
     for (int ks = 0; ks < kBK / 4; ++ks) {
       const int kc = ks * 4 + t;
@@ -911,9 +924,9 @@ cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const Sy
   return cudaErrorInvalidValue;
 }
 
-template <int TILE>
+template <int TILE, int KS = kStages>
 constexpr size_t trail_smem() {
-  return size_t(kStages) * 2 * (TILE + 4) * kBK * sizeof(double) + size_t(TILE / 32) * 16 * 2 * TILE * sizeof(double) +
+  return size_t(KS) * 2 * (TILE + 4) * kBK * sizeof(double) + size_t(TILE / 32) * 16 * 2 * TILE * sizeof(double) +
          1024 + 256;
 }
 
@@ -929,12 +942,20 @@ cudaError_t launch_trail(const CUtensorMap& tmP, const SyrkParams& p, int tile, 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (tile == 64) {
+    // RBPG_TRAIL_KS=4: the whole panel resident (two CTAs per SM); default two stages (three CTAs)
+    static const int ks = std::getenv("RBPG_TRAIL_KS") ? std::atoi(std::getenv("RBPG_TRAIL_KS")) : 2;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(trail_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trail_smem<64>());
+      cudaFuncSetAttribute(trail_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)trail_smem<64, 2>());
       attr = true;
     }
     cfg.blockDim = dim3(128);
+    if (ks == 2) {
+      cfg.dynamicSmemBytes = trail_smem<64, 2>();
+      return cudaLaunchKernelEx(&cfg, trail_kernel<64, 2>, tmP, p);
+    }
     cfg.dynamicSmemBytes = trail_smem<64>();
     return cudaLaunchKernelEx(&cfg, trail_kernel<64>, tmP, p);
   }
