@@ -622,13 +622,13 @@ __global__ void __launch_bounds__(2 * TILE, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[i][j][q] = 0.0;
   for (int kt = 0; kt < ktiles; ++kt) {
-    if (KS < kStages && kt == KS) {  // first half consumed: the second half into the same stages
+    if (KS < kStages && kt > 0 && kt % KS == 0) {  // stages consumed: the next k-tiles into them
       __syncthreads();
       if (tid == 0)
-        for (int s = 0; s < KS && KS + s < ktiles; ++s) {
+        for (int s = 0; s < KS && kt + s < ktiles; ++s) {
           mbar_arrive_expect_tx(&full[s], stage_bytes);
-          tma_load_2d(As + s * kBK * TP, &tmP, &full[s], i0, (KS + s) * kBK);
-          if (!diag) tma_load_2d(Bs + s * kBK * TP, &tmP, &full[s], j0, (KS + s) * kBK);
+          tma_load_2d(As + s * kBK * TP, &tmP, &full[s], i0, (kt + s) * kBK);
+          if (!diag) tma_load_2d(Bs + s * kBK * TP, &tmP, &full[s], j0, (kt + s) * kBK);
         }
     }
     mbar_wait(&full[kt % KS], (kt / KS) & 1);
@@ -942,16 +942,23 @@ cudaError_t launch_trail(const CUtensorMap& tmP, const SyrkParams& p, int tile, 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (tile == 64) {
-    // RBPG_TRAIL_KS=4: the whole panel resident (two CTAs per SM); default two stages (three CTAs)
-    static const int ks = std::getenv("RBPG_TRAIL_KS") ? std::atoi(std::getenv("RBPG_TRAIL_KS")) : 2;
+    // RBPG_TRAIL_KS: k-stages resident -- 4 = the whole panel (two CTAs per SM), 2 = halves (three),
+    // default 1 = one 16-deep stage reloaded four times (four CTAs per SM; C4 L=8000: 11.4 / 9.5 / 9.1 ms)
+    static const int ks = std::getenv("RBPG_TRAIL_KS") ? std::atoi(std::getenv("RBPG_TRAIL_KS")) : 1;
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(trail_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trail_smem<64>());
       cudaFuncSetAttribute(trail_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)trail_smem<64, 2>());
+      cudaFuncSetAttribute(trail_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)trail_smem<64, 1>());
       attr = true;
     }
     cfg.blockDim = dim3(128);
+    if (ks == 1) {
+      cfg.dynamicSmemBytes = trail_smem<64, 1>();
+      return cudaLaunchKernelEx(&cfg, trail_kernel<64, 1>, tmP, p);
+    }
     if (ks == 2) {
       cfg.dynamicSmemBytes = trail_smem<64, 2>();
       return cudaLaunchKernelEx(&cfg, trail_kernel<64, 2>, tmP, p);
