@@ -531,8 +531,8 @@ __global__ void __launch_bounds__(256, 1)
 // so their latency hides under the tensor-core work.  G_old is read through its lower triangle
 // (G[max][min]) and G_new is written lower-only unless p.mirror (the next panel reads whole rows).
 // TILE 32 (64 threads) for the small late updates: four times the CTAs per DMMA of a 64-wide tile.
-// KS: k-stages resident (4 = the whole rank-64 panel loaded up front; 2 = two halves through two
-// stages, ~35 KB less shared memory so a third CTA fits on an SM)
+// KS: k-stages resident (4 = the whole rank-64 panel loaded up front; 2 or 1 = the panel streamed
+// through fewer stages, reloaded as they are consumed, so three or four CTAs fit on an SM)
 template <int TILE, int KS = kStages>
 __global__ void __launch_bounds__(2 * TILE, 1)
     trail_kernel(const __grid_constant__ CUtensorMap tmP, SyrkParams p) {
