@@ -226,3 +226,30 @@ def accuracy(pred, y):
     _call(lib().oracle_accuracy, _p(pred), c_size_t(pred.shape[0]), c_size_t(pred.shape[1]), _p(y),
           c_size_t(y.shape[0]), c_size_t(y.shape[1]), ctypes.byref(out))
     return float(out.value)
+
+
+def synth_classification(n, d, m, seed, teacher_seed, noise_sigma=0.1, row0=0):
+    """SURVEY §8(d) synthetic classification rows [row0, row0 + n): the generator definition the
+    product's rbpg_synth_classification implements, restated so that bench.py's CPU legs never load
+    the product library.  Returns (X n x d, one-hot T n x m)."""
+    x = np.empty((n, d))
+    t = np.empty((n, m))
+    _call(lib().oracle_synth_classification, c_size_t(row0), c_size_t(n), c_size_t(d), c_size_t(m), c_uint64(seed),
+          c_uint64(teacher_seed), c_double(noise_sigma), _p(x), _p(t))
+    return x, t
+
+
+PHASES = ("hidden", "gram", "factor", "solve", "accuracy")
+
+
+def train_phase_times(inputs, hidden, outputs, seed, x, y, ridge=1e-2):
+    """Seconds per phase of train(rank) on the sample rows x, y (see oracle_train_phase_times):
+    dict over PHASES plus 'rank'.  hidden/gram/accuracy are linear in the row count."""
+    x, y = _f(x), _f(y)
+    times = np.zeros(5)
+    rank = c_size_t()
+    _call(lib().oracle_train_phase_times, c_size_t(inputs), c_size_t(hidden), c_size_t(outputs), c_uint64(seed),
+          _p(x), c_size_t(x.shape[0]), _p(y), c_double(ridge), _p(times), ctypes.byref(rank))
+    out = dict(zip(PHASES, (float(v) for v in times)))
+    out["rank"] = int(rank.value)
+    return out

@@ -13,7 +13,9 @@
 // cites the reference file:line it follows.  Bit-level parity with Eigen's
 // kernels is unpinned (no golden vectors exist in the reference);
 // the oracle is pinned by porting the reference's own known-answer and
-// tolerance tests (tests/test_oracle_*.py).
+// tolerance tests (tests/test_reference_suite.py, run on this oracle in the CPU
+// suite), and its blocked/threaded loops are pinned bitwise against its own
+// scalar-loop transcription (tests/golden/oracle_digests.json).
 //
 // Floating-point contract: compiled with -ffp-contract=off so that every
 // a*b+c is a rounded multiply followed by a rounded add, as in the reference's
@@ -29,9 +31,15 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <chrono>
 
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
+
+#include <emmintrin.h>
 
 namespace oracle {
 
@@ -78,24 +86,103 @@ static bool all_finite(const Mat& m) {
 
 static int g_threads = 1;
 
+// Persistent worker pool behind parallel_for (thread start-up per call would dominate the many
+// short parallel loops of the blocked Gram and factorisation).
+class Pool {
+ public:
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  // fn() on `nt` threads (the caller included); returns when all have finished
+  void run(int nt, const std::function<void()>& fn) {
+    std::lock_guard<std::mutex> run_lk(run_mu_);
+    while (static_cast<int>(th_.size()) < nt - 1) {
+      const int idx = static_cast<int>(th_.size());
+      th_.emplace_back([this, idx] { worker(idx); });
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &fn;
+      want_ = nt - 1;
+      pending_ = nt - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void worker(int idx) {
+    std::size_t seen = 0;
+    for (;;) {
+      const std::function<void()>* job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        if (idx >= want_) continue;
+        job = job_;
+      }
+      (*job)();
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_all();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void()>* job_ = nullptr;
+  std::size_t gen_ = 0;
+  int want_ = 0, pending_ = 0;
+  bool stop_ = false;
+};
+static Pool& pool() {
+  static Pool p;
+  return p;
+}
+
 // Dynamic-schedule parallel loop over [0, count).  Each index is processed by
 // exactly one thread with the same arithmetic as the serial loop, so results
 // are bitwise independent of the thread count.
+static thread_local bool t_in_parallel = false;  // nested loops run serially on their thread
 template <typename F>
 static void parallel_for(std::size_t count, bool enable, F&& fn) {
-  const int nt = enable ? std::min<int>(g_threads, static_cast<int>(count)) : 1;
+  const int nt = (enable && !t_in_parallel) ? std::min<int>(g_threads, static_cast<int>(count)) : 1;
   if (nt <= 1) {
     for (std::size_t i = 0; i < count; ++i) fn(i);
     return;
   }
   std::atomic<std::size_t> next{0};
-  auto worker = [&] {
+  const std::function<void()> worker = [&] {
+    t_in_parallel = true;
     for (std::size_t i; (i = next.fetch_add(1)) < count;) fn(i);
+    t_in_parallel = false;
   };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < nt; ++t) pool.emplace_back(worker);
-  worker();
-  for (auto& th : pool) th.join();
+  pool().run(nt, worker);
+}
+
+// 4 x 4 block of products over k in increasing order: acc[a][b] = acc[a][b] + A[k][a] * B[k][b]
+// with A, B packed as [k][4].  SSE2 (baseline x86-64) multiplies and adds are the separately
+// rounded IEEE operations of the scalar loop, so every element equals the scalar sum bitwise.
+static inline void mk44(const double* A4, const double* B4, std::size_t K, __m128d acc[4][2]) {
+  for (std::size_t k = 0; k < K; ++k) {
+    const __m128d b01 = _mm_loadu_pd(B4 + 4 * k), b23 = _mm_loadu_pd(B4 + 4 * k + 2);
+    for (int a = 0; a < 4; ++a) {
+      const __m128d av = _mm_set1_pd(A4[4 * k + a]);
+      acc[a][0] = _mm_add_pd(acc[a][0], _mm_mul_pd(av, b01));
+      acc[a][1] = _mm_add_pd(acc[a][1], _mm_mul_pd(av, b23));
+    }
+  }
 }
 
 // matrix.cpp:69-77
@@ -113,16 +200,21 @@ static Mat matmul(const Mat& a, const Mat& b) {
   return out;
 }
 
-// matrix.cpp:79-87 (a^T b)
+// matrix.cpp:79-87 (a^T b).  Each output element sums a(n, i) * b(n, j) over n in increasing
+// order; output rows go in blocks of 8 so that a row of `a` is read one cache line at a time.
 static Mat matmul_at(const Mat& a, const Mat& b) {
   if (a.r != b.r) throw ShapeError("matmul_at: row counts differ, " + a.shape() + "^T times " + b.shape());
   Mat out(a.c, b.c, 0.0);
-  parallel_for(a.c, a.r * a.c * b.c > 1000000, [&](std::size_t i) {
-    double* o = &out.v[i * b.c];
+  constexpr std::size_t kI = 8;
+  parallel_for((a.c + kI - 1) / kI, a.r * a.c * b.c > 1000000, [&](std::size_t ib) {
+    const std::size_t i0 = ib * kI, i1 = std::min(a.c, i0 + kI);
     for (std::size_t n = 0; n < a.r; ++n) {
-      const double s = a(n, i);
       const double* br = &b.v[n * b.c];
-      for (std::size_t j = 0; j < b.c; ++j) o[j] = o[j] + s * br[j];
+      for (std::size_t i = i0; i < i1; ++i) {
+        const double s = a(n, i);
+        double* o = &out.v[i * b.c];
+        for (std::size_t j = 0; j < b.c; ++j) o[j] = o[j] + s * br[j];
+      }
     }
   });
   return out;
@@ -164,48 +256,63 @@ static Mat vstack(const Mat& t, const Mat& b) {  // matrix.cpp:130-139
 // and shards are added in shard order (shards = 1 is the reference's single
 // pass; shards > 1 reproduces a row-sharded multi-GPU reduction order and is
 // used to measure the oracle's own conditioning floor).
+// Loop structure: rows go in chunks of kKC packed as 4-column blocks [block][row][4]; every lower
+// 4 x 4 block of G carries its running sums across chunks (a stored double is exact, so the
+// chunking does not change any value).
 static Mat gram_sharded(const Mat& a, std::size_t shards) {
   const std::size_t n = a.c, rows = a.r;
   if (shards < 1) shards = 1;
-  Mat acm = transpose(a);  // column-major copy, as linalg.cpp:181
-  Mat g(n, n, 0.0);
+  constexpr std::size_t kKC = 256;
+  const std::size_t nb = (n + 3) / 4, nblk = nb * (nb + 1) / 2;
+  std::vector<double> acc(nblk * 16, 0.0), tot;
+  std::vector<double> q(nb * kKC * 4);
   const std::size_t per = (rows + shards - 1) / shards;
-  const std::size_t B = 4;
-  parallel_for((n + B - 1) / B, true, [&](std::size_t ib) {
-    const std::size_t i0 = ib * B;
-    for (std::size_t j0 = 0; j0 <= i0; j0 += B) {
-      double tot[B][B] = {};
-      for (std::size_t s = 0; s < shards; ++s) {
-        const std::size_t r0 = s * per, r1 = std::min(rows, r0 + per);
-        double acc[B][B] = {};
-        const double* hi[B];
-        const double* hj[B];
-        for (std::size_t q = 0; q < B; ++q) {
-          hi[q] = &acm.v[std::min(i0 + q, n - 1) * rows];
-          hj[q] = &acm.v[std::min(j0 + q, n - 1) * rows];
+  for (std::size_t s = 0; s < shards; ++s) {
+    const std::size_t r0 = std::min(rows, s * per), r1 = std::min(rows, r0 + per);
+    if (s > 0) std::fill(acc.begin(), acc.end(), 0.0);
+    for (std::size_t c0 = r0; c0 < r1; c0 += kKC) {
+      const std::size_t kc = std::min(kKC, r1 - c0);
+      parallel_for(nb, n * kc > 65536, [&](std::size_t cb) {
+        double* dst = &q[cb * kKC * 4];
+        for (std::size_t k = 0; k < kc; ++k) {
+          const double* src = &a.v[(c0 + k) * n];
+          for (std::size_t t = 0; t < 4; ++t) dst[4 * k + t] = (4 * cb + t < n) ? src[4 * cb + t] : 0.0;
         }
-        // 16 independent chains; each element still adds its products in row order
-        for (std::size_t k = r0; k < r1; ++k) {
-          const double a0 = hi[0][k], a1 = hi[1][k], a2 = hi[2][k], a3 = hi[3][k];
-          const double b0 = hj[0][k], b1 = hj[1][k], b2 = hj[2][k], b3 = hj[3][k];
-          acc[0][0] = acc[0][0] + a0 * b0; acc[0][1] = acc[0][1] + a0 * b1;
-          acc[0][2] = acc[0][2] + a0 * b2; acc[0][3] = acc[0][3] + a0 * b3;
-          acc[1][0] = acc[1][0] + a1 * b0; acc[1][1] = acc[1][1] + a1 * b1;
-          acc[1][2] = acc[1][2] + a1 * b2; acc[1][3] = acc[1][3] + a1 * b3;
-          acc[2][0] = acc[2][0] + a2 * b0; acc[2][1] = acc[2][1] + a2 * b1;
-          acc[2][2] = acc[2][2] + a2 * b2; acc[2][3] = acc[2][3] + a2 * b3;
-          acc[3][0] = acc[3][0] + a3 * b0; acc[3][1] = acc[3][1] + a3 * b1;
-          acc[3][2] = acc[3][2] + a3 * b2; acc[3][3] = acc[3][3] + a3 * b3;
+      });
+      parallel_for(nb, n * kc > 65536, [&](std::size_t rev) {
+        const std::size_t ib = nb - 1 - rev;  // longest block rows first
+        for (std::size_t jb = 0; jb <= ib; ++jb) {
+          double* ap = &acc[(ib * (ib + 1) / 2 + jb) * 16];
+          __m128d r[4][2];
+          for (int x = 0; x < 4; ++x) {
+            r[x][0] = _mm_loadu_pd(ap + 4 * x);
+            r[x][1] = _mm_loadu_pd(ap + 4 * x + 2);
+          }
+          mk44(&q[ib * kKC * 4], &q[jb * kKC * 4], kc, r);
+          for (int x = 0; x < 4; ++x) {
+            _mm_storeu_pd(ap + 4 * x, r[x][0]);
+            _mm_storeu_pd(ap + 4 * x + 2, r[x][1]);
+          }
         }
-        for (std::size_t ii = 0; ii < B; ++ii)
-          for (std::size_t jj = 0; jj < B; ++jj) tot[ii][jj] = (s == 0) ? acc[ii][jj] : tot[ii][jj] + acc[ii][jj];
-      }
-      for (std::size_t ii = 0; ii < B; ++ii)
-        for (std::size_t jj = 0; jj < B; ++jj) {
-          const std::size_t i = i0 + ii, j = j0 + jj;
-          if (i < n && j < n && j <= i) {
-            g(i, j) = tot[ii][jj];
-            g(j, i) = tot[ii][jj];
+      });
+    }
+    if (s == 0) {
+      tot = acc;
+    } else {
+      for (std::size_t e = 0; e < tot.size(); ++e) tot[e] = tot[e] + acc[e];
+    }
+  }
+  if (shards == 1 && tot.empty()) tot = acc;
+  Mat g(n, n, 0.0);
+  parallel_for(nb, n > 256, [&](std::size_t ib) {
+    for (std::size_t jb = 0; jb <= ib; ++jb) {
+      const double* ap = &tot[(ib * (ib + 1) / 2 + jb) * 16];
+      for (std::size_t x = 0; x < 4; ++x)
+        for (std::size_t y = 0; y < 4; ++y) {
+          const std::size_t i = 4 * ib + x, j = 4 * jb + y;
+          if (i < n && j <= i) {
+            g(i, j) = ap[4 * x + y];
+            g(j, i) = ap[4 * x + y];
           }
         }
     }
@@ -355,25 +462,42 @@ static Spd spd_factor(const Mat& m) {
   return f;
 }
 
-// L y = rhs then L^T x = y, in place (linalg.cpp:147-149, 267-268)
+// L y = rhs then L^T x = y, in place (linalg.cpp:147-149, 267-268).  Right-hand-side columns are
+// independent, so they go in column blocks on the worker threads (same arithmetic per column); the
+// backward sweep reads L^T row-wise from a transposed copy.
 static void tri_solve_pair(const Mat& l, Mat& x) {
   const std::size_t n = l.r, m = x.c;
-  for (std::size_t i = 0; i < n; ++i) {
-    for (std::size_t c = 0; c < i; ++c) {
-      const double s = l(i, c);
-      if (s == 0.0) continue;
-      for (std::size_t j = 0; j < m; ++j) x(i, j) = x(i, j) - s * x(c, j);
+  if (n == 0 || m == 0) return;
+  Mat lt(n, n);
+  parallel_for(n, n > 512, [&](std::size_t i) {
+    for (std::size_t j = 0; j < n; ++j) lt(j, i) = l(i, j);
+  });
+  const std::size_t w = std::max<std::size_t>(1, std::min<std::size_t>(8, m / std::max(1, g_threads)));
+  parallel_for((m + w - 1) / w, n * n * m > 4000000, [&](std::size_t blk) {
+    const std::size_t j0 = blk * w, j1 = std::min(m, j0 + w);
+    for (std::size_t i = 0; i < n; ++i) {
+      const double* li = &l.v[i * n];
+      double* xi = &x.v[i * m];
+      for (std::size_t c = 0; c < i; ++c) {
+        const double s = li[c];
+        if (s == 0.0) continue;
+        const double* xc = &x.v[c * m];
+        for (std::size_t j = j0; j < j1; ++j) xi[j] = xi[j] - s * xc[j];
+      }
+      for (std::size_t j = j0; j < j1; ++j) xi[j] = xi[j] / li[i];
     }
-    for (std::size_t j = 0; j < m; ++j) x(i, j) = x(i, j) / l(i, i);
-  }
-  for (std::size_t ii = n; ii-- > 0;) {
-    for (std::size_t c = ii + 1; c < n; ++c) {
-      const double s = l(c, ii);
-      if (s == 0.0) continue;
-      for (std::size_t j = 0; j < m; ++j) x(ii, j) = x(ii, j) - s * x(c, j);
+    for (std::size_t ii = n; ii-- > 0;) {
+      const double* lr = &lt.v[ii * n];
+      double* xi = &x.v[ii * m];
+      for (std::size_t c = ii + 1; c < n; ++c) {
+        const double s = lr[c];
+        if (s == 0.0) continue;
+        const double* xc = &x.v[c * m];
+        for (std::size_t j = j0; j < j1; ++j) xi[j] = xi[j] - s * xc[j];
+      }
+      for (std::size_t j = j0; j < j1; ++j) xi[j] = xi[j] / lr[ii];
     }
-    for (std::size_t j = 0; j < m; ++j) x(ii, j) = x(ii, j) / l(ii, ii);
-  }
+  });
 }
 
 static Mat spd_solve(const Spd& f, const Mat& rhs) {
@@ -417,9 +541,28 @@ static Factor factor_gram(Mat g, std::size_t rows, double tol) {
   const double cut = out.tolerance * r00;
   std::size_t rank = n;
   const std::size_t nb = 64;
-  std::vector<double> col(n);
+  // Loop structure only (not arithmetic) differs from a literal transcription of :186-247:
+  //  * within a panel the G swaps (:215-216) are tracked as a position -> row map `lab` into the
+  //    panel-start G (exactly symmetric, so column j of the swapped G is row lab[j] gathered at
+  //    lab[i]); rows and columns before the panel are never read again, so nothing else observes
+  //    the physical swaps;
+  //  * the trailing update writes the next panel's G (position order, both triangles, i.e. the
+  //    reference's lower update plus mirror) into a second buffer, in 4 x 4 blocks on the worker
+  //    threads, from the panel's factor columns packed as [row block][column][4];
+  //  * column-update rows go four at a time so their dot-product chains overlap.
+  // Every element still sums its products in increasing column order from 0.0 with separately
+  // rounded multiplies and adds, so F, the order and the rank are bitwise those of the scalar
+  // loops (pinned by the CPU tests).
+  //  * the panel's own factor columns live in a compact n x 64 array `pc` during the panel (the
+  //    same values F receives at panel end).
+  Mat g2(n, n, 0.0);
+  std::vector<std::size_t> lab(n);
+  std::vector<double> pk, pc(n * nb);
   for (std::size_t k = 0; k < n && rank == n; k += nb) {
     const std::size_t kb = std::min(nb, n - k);
+    for (std::size_t i = k; i < n; ++i) lab[i] = i;
+    std::fill(pc.begin(), pc.end(), 0.0);
+    std::size_t jend = k + kb;  // columns of this panel written
     for (std::size_t j = k; j < k + kb; ++j) {
       std::size_t piv = j;
       for (std::size_t i = j + 1; i < n; ++i)
@@ -433,40 +576,98 @@ static Factor factor_gram(Mat g, std::size_t rows, double tol) {
       if (piv != j) {  // :211-218
         std::swap(out.order[j], out.order[piv]);
         std::swap(d[j], d[piv]);
-        for (std::size_t c = 0; c < j; ++c) std::swap(f(j, c), f(piv, c));
-        for (std::size_t c = 0; c < n; ++c) std::swap(g(j, c), g(piv, c));
-        for (std::size_t r = 0; r < n; ++r) std::swap(g(r, j), g(r, piv));
+        for (std::size_t c = 0; c < k; ++c) std::swap(f(j, c), f(piv, c));
+        for (std::size_t c = 0; c < j - k; ++c) std::swap(pc[j * nb + c], pc[piv * nb + c]);
+        std::swap(lab[j], lab[piv]);  // G row and column swap
       }
       const double rjj = d[j] > 0.0 ? std::sqrt(d[j]) : 0.0;
       if (rjj <= cut) {  // :219-223
         rank = j;
+        jend = j;
         break;
       }
-      f(j, j) = rjj;
-      for (std::size_t i = j + 1; i < n; ++i) {  // :225-235
-        double v = g(i, j);
-        if (j > k) {
-          double s = 0.0;
-          for (std::size_t c = k; c < j; ++c) s = s + f(i, c) * f(j, c);
-          v = v - s;
-        }
+      pc[j * nb + (j - k)] = rjj;  // f(j, j)
+      // :225-235 -- col = (G[i,j] - F[i,k:j] F[j,k:j]^T) / rjj, d -= col^2
+      const double* fj = &pc[j * nb] - k;
+      const double* grow = &g.v[lab[j] * n];
+      auto finish = [&](std::size_t i, double s) {
+        double v = grow[lab[i]];
+        if (j > k) v = v - s;
         v = v / rjj;
-        f(i, j) = v;
+        pc[i * nb + (j - k)] = v;
         d[i] = d[i] - v * v;
-      }
-    }
-    const std::size_t t0 = k + kb;  // :237-244 trailing rank-kb update, lower then mirror
-    if (rank == n && t0 < n) {
-      parallel_for(n - t0, (n - t0) > 256, [&](std::size_t ii) {
-        const std::size_t i = t0 + ii;
-        for (std::size_t jj = t0; jj <= i; ++jj) {
-          double acc = 0.0;
-          for (std::size_t c = k; c < k + kb; ++c) acc = acc + f(i, c) * f(jj, c);
-          g(i, jj) = g(i, jj) - acc;
+      };
+      constexpr std::size_t kRows = 512;  // rows per work item (one item per thread wake-up)
+      const std::size_t nrow = n - (j + 1);
+      parallel_for((nrow + kRows - 1) / kRows, nrow * (j - k) > 262144, [&](std::size_t item) {
+        std::size_t i = j + 1 + item * kRows;
+        const std::size_t iend = std::min(n, i + kRows);
+        for (; i + 4 <= iend; i += 4) {
+          const double* f0 = &pc[i * nb] - k;
+          const double* f1 = f0 + nb;
+          const double* f2 = f1 + nb;
+          const double* f3 = f2 + nb;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+          for (std::size_t c = k; c < j; ++c) {
+            s0 = s0 + f0[c] * fj[c];
+            s1 = s1 + f1[c] * fj[c];
+            s2 = s2 + f2[c] * fj[c];
+            s3 = s3 + f3[c] * fj[c];
+          }
+          finish(i, s0);
+          finish(i + 1, s1);
+          finish(i + 2, s2);
+          finish(i + 3, s3);
+        }
+        for (; i < iend; ++i) {
+          const double* fi = &pc[i * nb] - k;
+          double s = 0.0;
+          for (std::size_t c = k; c < j; ++c) s = s + fi[c] * fj[c];
+          finish(i, s);
         }
       });
-      for (std::size_t i = t0; i < n; ++i)
-        for (std::size_t jj = i + 1; jj < n; ++jj) g(i, jj) = g(jj, i);
+    }
+    parallel_for(n - k, n - k > 256, [&](std::size_t ii) {
+      const std::size_t i = k + ii;
+      for (std::size_t c = k; c < jend; ++c) f(i, c) = pc[i * nb + (c - k)];
+    });
+    const std::size_t t0 = k + kb;  // :237-244 trailing rank-kb update, lower then mirror
+    if (rank == n && t0 < n) {
+      const std::size_t nt = n - t0, nbk = (nt + 3) / 4;
+      pk.assign(nbk * kb * 4, 0.0);
+      parallel_for(nbk, nt > 256, [&](std::size_t bi) {
+        for (std::size_t t = 0; t < 4; ++t) {
+          const std::size_t i = t0 + 4 * bi + t;
+          if (i >= n) break;
+          for (std::size_t c = 0; c < kb; ++c) pk[(bi * kb + c) * 4 + t] = pc[i * nb + c];
+        }
+      });
+      parallel_for(nbk, nt > 256, [&](std::size_t rev) {
+        const std::size_t bi = nbk - 1 - rev;
+        for (std::size_t bj = 0; bj <= bi; ++bj) {
+          __m128d r[4][2];
+          for (int x = 0; x < 4; ++x) r[x][0] = r[x][1] = _mm_setzero_pd();
+          mk44(&pk[bi * kb * 4], &pk[bj * kb * 4], kb, r);
+          double acc[4][4];
+          for (int x = 0; x < 4; ++x) {
+            _mm_storeu_pd(&acc[x][0], r[x][0]);
+            _mm_storeu_pd(&acc[x][2], r[x][1]);
+          }
+          for (std::size_t x = 0; x < 4; ++x) {
+            const std::size_t ii = t0 + 4 * bi + x;
+            if (ii >= n) break;
+            const double* gr = &g.v[lab[ii] * n];
+            for (std::size_t y = 0; y < 4; ++y) {
+              const std::size_t jj = t0 + 4 * bj + y;
+              if (jj > ii) break;
+              const double v = gr[lab[jj]] - acc[x][y];
+              g2(ii, jj) = v;
+              g2(jj, ii) = v;
+            }
+          }
+        }
+      });
+      std::swap(g.v, g2.v);
     }
   }
   out.rank = rank;
@@ -637,6 +838,52 @@ static double accuracy(const Mat& pred, const Mat& y) {  // elm.cpp:286-300
     if (ap == ay) ++hits;
   }
   return static_cast<double>(hits) / static_cast<double>(pred.r);
+}
+
+// ---- synthetic BASELINE inputs; the same generator definition as the product's
+// rbpg_synth_classification, restated here so that the CPU legs of bench.py never load the product
+// library.  X iid U[0,1] from mt19937_64 per 65536-row block (seed ^ golden * (block + 1)); one-hot
+// T = argmax(X V + eps), V ~ N(0,1) (d x m, teacher_seed), eps ~ N(0, sigma) drawn after each row's
+// features; Gaussians by Box-Muller (cosine branch, u1 in (0, 1]); ties go to the lowest index.
+static double unit53(std::mt19937_64& g) { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
+static double normal01(std::mt19937_64& g) {
+  const double u1 = (static_cast<double>(g() >> 11) + 1.0) * 0x1.0p-53;
+  const double u2 = unit53(g);
+  return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+}
+static void synth_classification(std::size_t row0, std::size_t n, std::size_t d, std::size_t m, std::uint64_t seed,
+                                 std::uint64_t teacher_seed, double sigma, double* x, double* t) {
+  constexpr std::size_t kBlockRows = 65536;
+  std::vector<double> v(d * m);
+  {
+    std::mt19937_64 tg(teacher_seed);
+    for (auto& e : v) e = normal01(tg);
+  }
+  const std::size_t end = row0 + n;
+  const std::size_t b0 = row0 / kBlockRows, b1 = n ? (end - 1) / kBlockRows + 1 : b0;
+  // blocks are independent streams: generate them on the worker threads
+  parallel_for(b1 - b0, b1 - b0 > 1, [&](std::size_t bi) {
+    const std::size_t blk = b0 + bi;
+    std::mt19937_64 gen(seed ^ (0x9E3779B97F4A7C15ull * static_cast<std::uint64_t>(blk + 1)));
+    std::vector<double> xr(d), logits(m);
+    const std::size_t bstart = blk * kBlockRows, bend = std::min(end, bstart + kBlockRows);
+    for (std::size_t r = bstart; r < bend; ++r) {
+      for (std::size_t k = 0; k < d; ++k) xr[k] = unit53(gen);
+      for (std::size_t c = 0; c < m; ++c) logits[c] = sigma * normal01(gen);
+      if (r < row0) continue;
+      for (std::size_t c = 0; c < m; ++c) {
+        double s = 0.0;
+        for (std::size_t k = 0; k < d; ++k) s += xr[k] * v[k * m + c];
+        logits[c] += s;
+      }
+      std::size_t am = 0;
+      for (std::size_t c = 1; c < m; ++c)
+        if (logits[c] > logits[am]) am = c;
+      const std::size_t o = r - row0;
+      std::memcpy(x + o * d, xr.data(), sizeof(double) * d);
+      for (std::size_t c = 0; c < m; ++c) t[o * m + c] = (c == am) ? 1.0 : 0.0;
+    }
+  });
 }
 
 }  // namespace oracle
@@ -948,6 +1195,64 @@ int oracle_predict(const double* w, const double* b, std::size_t d, std::size_t 
 int oracle_accuracy(const double* pred, std::size_t pr, std::size_t pc, const double* y, std::size_t yr,
                     std::size_t yc, double* out, oracle_error* err) {
   return guarded(err, [&] { *out = accuracy(from_ptr(pred, pr, pc), from_ptr(y, yr, yc)); });
+}
+
+int oracle_synth_classification(std::size_t row0, std::size_t n, std::size_t d, std::size_t m, std::uint64_t seed,
+                                std::uint64_t teacher_seed, double sigma, double* x, double* t, oracle_error* err) {
+  return guarded(err, [&] {
+    if (d < 1 || m < 1) throw std::invalid_argument("synth: d and m must be >= 1");
+    synth_classification(row0, n, d, m, seed, teacher_seed, sigma, x, t);
+  });
+}
+
+// Phase timings of train(rank) on a row sample, for bench.py's CPU legs (a bounded sample of a
+// workload too large for the CPU): times[0] hidden_matrix of the sample rows, [1] their Gram and
+// H^T T, [2] the rank-revealing factorisation of an L x L Gram, [3] the full-rank solve
+// (gather, two triangular solves, scatter), [4] the training-accuracy pass over the sample.
+// Phases 0, 1 and 4 are linear in the row count; 2 and 3 do not depend on it.  When the sample has
+// fewer rows than L its Gram is rank-deficient, so the factorisation is timed on the sample Gram
+// plus ridge * max(diag) * I (full rank; the pivoted Cholesky's work does not depend on the values
+// once no pivot stops early).  out_rank receives the factorisation's rank.
+int oracle_train_phase_times(std::size_t inputs, std::size_t hidden, std::size_t outputs, std::uint64_t seed,
+                             const double* x, std::size_t rows, const double* y, double ridge, double* times,
+                             std::size_t* out_rank, oracle_error* err) {
+  return guarded(err, [&] {
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto sec = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+    Mat W, Bv;
+    init_hidden(inputs, hidden, outputs, seed, W, Bv);
+    Mat X = from_ptr(x, rows, inputs), Y = from_ptr(y, rows, outputs);
+    auto t0 = now();
+    Mat H = hidden_matrix(W, Bv, X);
+    auto t1 = now();
+    Mat G = gram(H);
+    Mat hty = matmul_at(H, Y);
+    auto t2 = now();
+    if (rows < hidden) {
+      double dmax = 0.0;
+      for (std::size_t i = 0; i < hidden; ++i) dmax = std::max(dmax, G(i, i));
+      for (std::size_t i = 0; i < hidden; ++i) G(i, i) = G(i, i) + ridge * dmax;
+    }
+    Factor fac = factor_gram(std::move(G), std::max(rows, hidden), 0.0);
+    auto t3 = now();
+    *out_rank = fac.rank;
+    Mat beta_m(hidden, outputs, 0.0);
+    if (fac.rank == hidden) {
+      Mat htyp(hidden, outputs);
+      for (std::size_t i = 0; i < hidden; ++i)
+        for (std::size_t j = 0; j < outputs; ++j) htyp(i, j) = hty(fac.order[i], j);
+      beta_m = invert_permutation_rows(solve_factored_gram(fac, htyp), fac.order);
+    }
+    auto t4 = now();
+    volatile double acc = accuracy(matmul(H, beta_m), Y);
+    (void)acc;
+    auto t5 = now();
+    times[0] = sec(t0, t1);
+    times[1] = sec(t1, t2);
+    times[2] = sec(t2, t3);
+    times[3] = sec(t3, t4);
+    times[4] = sec(t4, t5);
+  });
 }
 
 }  // extern "C"

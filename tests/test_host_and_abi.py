@@ -5,6 +5,7 @@ import ctypes
 import os
 import re
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -146,3 +147,36 @@ def test_golden_oracle_fixtures():
     assert r["diag"]["rank"] == gold["rank"]
     assert r["diag"]["training_accuracy"] == gold["training_accuracy"]
     assert np.linalg.norm(r["beta"] - np.array(gold["beta"])) / np.linalg.norm(gold["beta"]) < 1e-12
+
+
+def test_oracle_bitwise_digests():
+    """The blocked / threaded oracle reproduces the round-1 scalar-loop oracle bitwise
+    (tests/golden/make_digests.py; digests written by the scalar version) at 1 and 4 threads."""
+    import json
+
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    import make_digests
+
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "oracle_digests.json")))
+    try:
+        for th in (1, 4):
+            oracle.set_threads(th)
+            assert make_digests.compute() == gold
+    finally:
+        oracle.set_threads(os.cpu_count() or 1)
+
+
+@pytest.mark.parametrize("n,d,m,row0", [(1000, 16, 2, 0), (70000, 64, 10, 0), (5000, 32, 5, 131000),
+                                        (3, 7, 100, 65535)])
+def test_oracle_generator_bit_identical(n, d, m, row0):
+    """bench.py's CPU legs generate inputs with the oracle's restated generator (no product library in
+    that process); it must equal the product generator bit for bit, row shards included."""
+    x, t = oracle.synth_classification(n, d, m, 1234, 5678, row0=row0)
+    x2, t2 = rb.synth_classification(n, d, m, 1234, 5678, row0=row0)
+    assert np.array_equal(x, x2) and np.array_equal(t, t2)
+
+
+def test_oracle_phase_times():
+    x, t = oracle.synth_classification(300, 8, 3, 1, 2)
+    ph = oracle.train_phase_times(8, 500, 3, 3, x, t)
+    assert ph["rank"] == 500 and all(ph[k] >= 0 for k in oracle.PHASES)
