@@ -1,19 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the B200 RBP-ELM training hot path (BASELINE.json metric).
 
-One "step" = one full train() with the rank strategy on the workload:
-H build (K1) -> Gram/H^T T (K2) -> pivoted Cholesky (K3 + trailing SYRK) ->
-triangular solves (K4) -> training-accuracy pass, inputs resident in HBM.
+One "step" = one full train() with the rank strategy on the workload: H build (K1) ->
+Gram/H^T T (K2) -> pivoted Cholesky (K3 + trailing SYRK) -> triangular solves (K4) ->
+training-accuracy pass, inputs resident in HBM.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--scaling weak|strong]
+                  [--impl ours|reference]
 
-N > 1 runs under torchrun: rows are sharded (weak scaling, config rows per GPU),
-each rank builds its local Gram/H^T T, NCCL all-reduces them, every rank runs the
-replicated solve, hit counts are all-reduced.  Rank 0 prints one JSON line.
+Default workload: BASELINE config 5 ("C5", d=256, L=8192, m=100), 500k rows per GPU -- the
+largest single-GPU configuration (one shard of C5; the whole 4M-row C5 at 8 GPUs).  `--scaling
+weak` (C5's default) keeps the rows per GPU fixed; `--scaling strong` (the C2/C4 default) keeps
+the config's total row count and splits it over the ranks.  N > 1 runs under torchrun: each rank
+builds the augmented Gram [H T]^T [H T] of its contiguous row shard, NCCL all-reduces its packed
+lower triangle, every rank runs the replicated solve, hit counts are all-reduced.  Rank 0 prints
+one JSON line.
 
-`--impl reference` times the reference algorithm on the host CPU (the oracle
-restatement, all host threads; the reference itself cannot be built here -- no
-Eigen) on a bounded row sample of the same workload.
+`--impl reference` times the reference algorithm on the host CPU: the oracle restatement (the
+reference itself cannot be built: no Eigen), all host threads, on a bounded sample of
+the same workload (see reference_sample); that process never loads the product library.
 """
 from __future__ import annotations
 
@@ -26,29 +31,52 @@ import sys
 import threading
 import time
 
-import numpy as np
-
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
 
-# (N rows per GPU, d, L, m) -- BASELINE.json configs
+# name: (rows, d, L, m, default scaling).  rows are per GPU for weak scaling (C5: "H rows sharded
+# 500k per GPU") and the job total for strong scaling (C2: N=50000, C4: N=100000).
 CONFIGS = {
-    "c1": (2000, 16, 200, 2),
-    "c2": (50000, 64, 1000, 10),
-    "c4_250": (100000, 128, 250, 10),
-    "c4_500": (100000, 128, 500, 10),
-    "c4_1000": (100000, 128, 1000, 10),
-    "c4_2000": (100000, 128, 2000, 10),
-    "c4_4000": (100000, 128, 4000, 10),
-    "c4_8000": (100000, 128, 8000, 10),
-    "c5": (500000, 256, 8192, 100),
+    "c1": (2000, 16, 200, 2, "strong"),
+    "c2": (50000, 64, 1000, 10, "strong"),
+    "c4_250": (100000, 128, 250, 10, "strong"),
+    "c4_500": (100000, 128, 500, 10, "strong"),
+    "c4_1000": (100000, 128, 1000, 10, "strong"),
+    "c4_2000": (100000, 128, 2000, 10, "strong"),
+    "c4_4000": (100000, 128, 4000, 10, "strong"),
+    "c4_8000": (100000, 128, 8000, 10, "strong"),
+    "c5": (500000, 256, 8192, 100, "weak"),
 }
+DEFAULT_CONFIG = "c5"
 SEED_X, SEED_TEACHER, SEED_W = 1002, 2002, 3002
+METRIC = ("ELM train FP64 TFLOP/s (alg. flops of H build + Gram + pivoted Cholesky + solves + accuracy "
+          "/ train time)")
+DATA = "synthetic (seeded mt19937_64 generators, SURVEY 8(d)); random-init W, b from init_hidden"
 
 
 def alg_flops(n, d, L, m):
     """2NdL + N L(L+1) + 2NLm + L^3/3 + 2L^2 m + 2NLm."""
     return 2 * n * d * L + n * L * (L + 1) + 2 * n * L * m + L ** 3 / 3 + 2 * L * L * m + 2 * n * L * m
+
+
+def row_flops(d, L, m):
+    """Per-row part of alg_flops (hidden build, Gram, H^T T, accuracy pass)."""
+    return 2 * d * L + L * (L + 1) + 4 * L * m
+
+
+def workload(args, world):
+    """(config dict, rows of this rank, total rows, d, L, m).  The dict is printed identically by both
+    arms (the driver compares them)."""
+    rows, d, L, m, default_scaling = CONFIGS[args.config]
+    scaling = args.scaling or default_scaling
+    n_total = rows * world if scaling == "weak" else rows
+    n_rank = n_total // world  # rank r owns rows [r * n_rank, (r + 1) * n_rank) (+ remainder on the last)
+    desc = (f"{args.config}: N_total={n_total} ({n_total // world}/GPU) d={d} L={L} m={m}, rank strategy "
+            f"(default tol), full train() incl. training-accuracy pass")
+    cfg = {"workload": desc, "N_total": n_total, "d": d, "L": L, "m": m, "scaling": scaling,
+           "l2": "inputs > L2 (126 MB) and a 256 MB L2 flush write between timed steps, outside the events",
+           "parallelism": f"row-sharded dp{world} (NCCL all-reduce of the packed Gram)" if world > 1 else "single GPU"}
+    return cfg, n_rank, n_total, d, L, m
 
 
 def fp64_peak():
@@ -59,6 +87,14 @@ def fp64_peak():
             return float(json.load(f)["cublas_dgemm_8192_tflops"]), "measured cuBLAS DGEMM 8192^3 (profiles/fp64_peak_r01.json)"
     except Exception:
         return 37.0, "fallback datasheet-class FP64 figure"
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(HERE, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6518.0, "fallback (round-1 MEASURED_PEAKS.json figure)"
 
 
 class ClockSampler:
@@ -82,7 +118,7 @@ class ClockSampler:
                     self.rows.append([c.strip() for c in line.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -104,53 +140,72 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def cpu_oracle_sample(n, d, L, m, threads, rows):
-    """Time the oracle's train() on the first `rows` rows of the workload (TFLOP/s)."""
+# ---------------------------------------------------------------------------------------------
+# CPU legs (oracle restatement only; this code path never imports the product package)
+# ---------------------------------------------------------------------------------------------
+def reference_sample(n_total, d, L, m, threads, rows=None):
+    """Time the oracle's train(rank) on a bounded sample of the workload and extrapolate to N_total rows.
+
+    Phases that are linear in the row count (hidden build, Gram + H^T T, accuracy pass) run on the
+    first R rows of the workload (R sized for ~1.5e11 flops of row work, all rows when the whole
+    workload is that small); the row-count-independent phases (pivoted Cholesky of the L x L Gram,
+    triangular solves) run at full L.  time = row phases * N_total / R + factor + solve.
+    Returns (TFLOP/s, seconds, R, phases)."""
     import oracle
-    import paper_2011_02436_b200 as rb  # data generator only
 
-    rows = min(rows, n)
-    x, t = rb.synth_classification(rows, d, m, SEED_X, SEED_TEACHER)
+    if rows is None:
+        rows = int(1.5e11 // row_flops(d, L, m))
+        rows = max(256, (rows // 256) * 256)
+    rows = min(rows, n_total)
+    x, t = oracle.synth_classification(rows, d, m, SEED_X, SEED_TEACHER)
     oracle.set_threads(threads)
-    t0 = time.perf_counter()
-    oracle.train(d, L, m, SEED_W, x, t, "rank")
-    dt = time.perf_counter() - t0
-    return alg_flops(rows, d, L, m) / dt / 1e12, dt
+    ph = oracle.train_phase_times(d, L, m, SEED_W, x, t)
+    per_rows = ph["hidden"] + ph["gram"] + ph["accuracy"]
+    sec = per_rows * (n_total / rows) + ph["factor"] + ph["solve"]
+    return alg_flops(n_total, d, L, m) / sec / 1e12, sec, rows, ph
 
 
-def reference_arm(args, n, d, L, m, rank, world):
+def sample_text(cfg_name, rows, n_total, L, threads, ph):
+    how = ("whole workload" if rows >= n_total else
+           f"hidden build, Gram + H^T T and accuracy pass timed on the first {rows} of {n_total} rows and scaled "
+           f"linearly to N_total; pivoted Cholesky + triangular solves timed at full L={L}"
+           + (" on the sample Gram + 1e-2 max(diag) I (full rank)" if rows < L else ""))
+    return (f"oracle restatement of train(rank) (reference not buildable: no Eigen), {threads} host threads, "
+            f"{cfg_name}: {how}; phases {', '.join(f'{k} {v:.2f}s' for k, v in ph.items() if k != 'rank')}")
+
+
+def reference_arm(args, rank, world):
     if rank != 0:
         return
+    cfg, _, n_total, d, L, m = workload(args, world)
     threads = os.cpu_count() or 1
-    rows = int(os.environ.get("RBPG_REF_ROWS", str(n)))
     samples = []
     for i in range(args.warmup + args.steps):
-        v, dt = cpu_oracle_sample(n, d, L, m, threads, rows)
+        v, sec, rows, ph = reference_sample(n_total, d, L, m, threads)
         if i >= args.warmup:
-            samples.append((v, dt))
-    value = statistics.mean(v for v, _ in samples)
-    sec = statistics.mean(dt for _, dt in samples)
+            samples.append((v, sec, rows, ph))
+    value = statistics.mean(s[0] for s in samples)
+    sec = statistics.mean(s[1] for s in samples)
+    rows, ph = samples[-1][2], samples[-1][3]
     line = {
-        "impl": "reference",
-        "metric": "ELM train FP64 TFLOP/s (alg. flops of H build + Gram + pivoted Cholesky + solves + accuracy / train time)",
-        "value": value, "unit": "TFLOP/s", "higher_is_better": True, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": sec * 1e3, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded mt19937_64, SURVEY 8(d))",
-        "config": {"workload": f"{args.config}: N={n}/GPU d={d} L={L} m={m}, rank strategy", "sample_rows": min(rows, n)},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOP/s", "higher_is_better": True,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "scaling": cfg["scaling"], "vs_baseline": None, "dtype": "f64", "data": DATA, "config": cfg,
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "port",
-                         "sample": f"oracle restatement train() on the first {min(rows, n)} rows of {args.config} "
-                                   f"(L={L}, d={d}, m={m}), {threads} threads; reference not buildable (no Eigen)"},
+                         "sample": sample_text(args.config, rows, n_total, L, threads, ph)},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -158,16 +213,21 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    n, d, L, m = CONFIGS[args.config]
 
     if args.impl == "reference":
-        reference_arm(args, n, d, L, m, rank, world)
+        reference_arm(args, rank, world)
         return
 
     import torch
     import torch.distributed as dist
 
     import paper_2011_02436_b200 as rb
+    from paper_2011_02436_b200 import sharded
+
+    cfg, n, N_total, d, L, m = workload(args, world)
+    row0 = rank * n
+    if rank == world - 1:
+        n = N_total - row0  # the remainder rows go to the last rank
 
     # RBPG_DIST_BACKEND=gloo + more ranks than GPUs: a functional check of the sharded orchestration
     # on one GPU (host-staged all-reduce; not a scaling measurement)
@@ -182,7 +242,7 @@ def main():
             dist.init_process_group(backend)
 
     # ---- inputs: this rank's contiguous row shard of the global matrix, resident in HBM
-    xh, th = rb.synth_classification(n, d, m, SEED_X, SEED_TEACHER, row0=rank * n)
+    xh, th = rb.synth_classification(n, d, m, SEED_X, SEED_TEACHER, row0=row0)
     X = torch.from_numpy(xh).to(dev)
     T = torch.from_numpy(th).to(dev)
     params = rb.ElmParams(d, L, m, SEED_W)
@@ -191,26 +251,15 @@ def main():
     B = torch.from_numpy(hidden.biases.reshape(-1)).to(dev)
     ctx = rb.context(local_dev)
     strat = rb.SolverStrategy.rank_based()
-    N_total = n * world
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
-
-    Gaug = torch.empty((L + m, L + m), dtype=torch.float64, device=dev)
+    stages = sharded.DeviceStages(ctx) if world > 1 else None
 
     def step():
         if world == 1:
             beta, diag, _ = rb.train_device(X, T, params, strat, hidden=hidden, ctx=ctx)
             return diag
-        # row shard -> augmented Gram [H T]^T [H T] -> ONE all-reduce -> replicated solve
-        rb.gram_stage_device_aug(X, T, W, B, Gaug, ctx=ctx)
-        if backend != "nccl":
-            torch.cuda.synchronize()  # host-staged backends do not order against the stream
-        dist.all_reduce(Gaug)
-        beta, diag = rb.solve_stage_device_aug(Gaug, L, m, N_total, strat, ctx=ctx)
-        hits = torch.tensor([rb.accuracy_stage_device(X, T, W, B, beta, ctx=ctx)], dtype=torch.int64, device=dev)
-        if backend != "nccl":
-            torch.cuda.synchronize()
-        dist.all_reduce(hits)
-        diag.training_accuracy = hits.item() / N_total
+        # row shard -> augmented Gram -> ONE all-reduce of its packed lower triangle -> replicated solve
+        beta, diag, _ = sharded.train_shard_device(X, T, W, B, params, strat, N_total, stages=stages)
         return diag
 
     for _ in range(args.warmup):
@@ -241,114 +290,114 @@ def main():
         flush.zero_()
         step()
     torch.cuda.synchronize()
-    syrk_ms, syrk_n = ctx.profile("syrk_kernel")
-    hid_ms, hid_n = ctx.profile("hidden_kernel")
-    panel_ms, panel_n = ctx.profile("panel_kernel")
-    trail_ms, trail_n = ctx.profile("syrk_trailing")
-    trsm_ms, trsm_n = ctx.profile("trsm_pair_kernel")
+    prof = {k: ctx.profile(k) for k in ("hidden_kernel", "syrk_kernel", "syrk_finish", "panel_kernel",
+                                        "syrk_trailing", "trsm_pair_kernel", "scores_kernel")}
     ctx.set_profiling(False)
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
-    ms_step = ms_max / args.steps
+    ms_step = float(t_max.item()) / args.steps
     flops = alg_flops(N_total, d, L, m)
     value = flops / (ms_step * 1e-3) / 1e12
 
-    # ---- e2e: the reference-facing C-ABI call with host (pinned) buffers, copies inside the timed region
-    e2e = None
+    # ---- e2e: the reference-facing call with HOST buffers, host<->device copies inside the timed region
+    xp = torch.empty((n, d), dtype=torch.float64).pin_memory()
+    tp = torch.empty((n, m), dtype=torch.float64).pin_memory()
+    xp.copy_(torch.from_numpy(xh))
+    tp.copy_(torch.from_numpy(th))
     if world > 1:
-        # the sharded train() through the Python API from this rank's pinned host shard: H2D of the
-        # shard, augmented Gram, all-reduce, replicated solve, hit-count all-reduce, beta back to host
-        from paper_2011_02436_b200 import sharded
-
-        xp = torch.empty((n, d), dtype=torch.float64).pin_memory()
-        tp = torch.empty((n, m), dtype=torch.float64).pin_memory()
-        xp.copy_(torch.from_numpy(xh))
-        tp.copy_(torch.from_numpy(th))
-        stages = sharded.DeviceStages(ctx)
-
-        def e2e_step():
+        def e2e_step():  # pinned host shard -> device -> sharded train -> beta back to the host
             xd = xp.to(dev, non_blocking=True)
             td = tp.to(dev, non_blocking=True)
             beta, dg, _, _ = sharded.train_sharded(xd, td, params, strat, N_total, stages=stages, hidden=hidden)
             return beta.cpu()
-
-        e2e_step()
-        t_e = []
-        for _ in range(max(3, args.steps)):
-            flush.zero_()
-            torch.cuda.synchronize()
-            dist.barrier()
-            t0 = time.perf_counter()
-            e2e_step()
-            torch.cuda.synchronize()
-            te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            t_e.append(float(te.item()))
-        e2e_s = statistics.median(t_e)
-        e2e = {"value": flops / e2e_s / 1e12, "unit": "TFLOP/s", "seconds": e2e_s,
-               "h2d_bytes_per_step": int(n * d * 8 + n * m * 8), "d2h_bytes_per_step": int(L * m * 8),
-               "api": "sharded.train_sharded (Python API, pinned host shard per rank; max over ranks)"}
-    if world == 1:
-        xp = torch.empty((n, d), dtype=torch.float64).pin_memory()
-        tp = torch.empty((n, m), dtype=torch.float64).pin_memory()
-        xp.copy_(torch.from_numpy(xh))
-        tp.copy_(torch.from_numpy(th))
+        api = "sharded.train_sharded (Python API, pinned host shard per rank; max over ranks)"
+    else:
         xpn, tpn = xp.numpy(), tp.numpy()
         ctx.set_stream(0)
-        rb.train(params, xpn, tpn, strat, ctx=ctx)  # warm
-        t_e = []
-        for _ in range(max(3, args.steps)):
+
+        def e2e_step():
+            return rb.train(params, xpn, tpn, strat, ctx=ctx)
+        api = "rbpg_train (C ABI, host buffers)"
+    e2e_step()
+    t_e = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_step()
+        torch.cuda.synchronize()
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        t_e.append(float(te.item()))
+    e2e_s = statistics.median(t_e)
+    e2e = {"value": flops / e2e_s / 1e12, "unit": "TFLOP/s", "seconds": e2e_s,
+           "h2d_bytes_per_step": int(n * d * 8 + n * m * 8), "d2h_bytes_per_step": int(L * m * 8), "api": api}
+
+    # ---- batched prediction (elm.cpp:282-284) on this rank's rows: device-resident X, labels out
+    pred = None
+    try:
+        model = rb.ElmModel(params, hidden, torch.zeros(1).numpy())
+        beta_d, _, _ = rb.train_device(X, T, params, strat, hidden=hidden, ctx=ctx)
+        pr = min(n, 200000)
+        Xp = X[:pr]
+        labels = torch.empty(pr, dtype=torch.int32, device=dev)
+        rb.predict_labels_device(Xp, W, B, beta_d, labels, ctx=ctx)
+        torch.cuda.synchronize()
+        pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+        for a, b in pe:
             flush.zero_()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            model, dg = rb.train(params, xpn, tpn, strat, ctx=ctx)
-            t_e.append(time.perf_counter() - t0)
-        e2e_s = statistics.median(t_e)
-        e2e = {"value": flops / e2e_s / 1e12, "unit": "TFLOP/s", "seconds": e2e_s,
-               "h2d_bytes_per_step": int(n * d * 8 + n * m * 8),
-               "d2h_bytes_per_step": int(L * m * 8),  # beta (W, b are generated on the host)
-               "api": "rbpg_train (C ABI, host buffers)"}
+            a.record(stream)
+            rb.predict_labels_device(Xp, W, B, beta_d, labels, ctx=ctx)
+            b.record(stream)
+        torch.cuda.synchronize()
+        pms = statistics.median(a.elapsed_time(b) for a, b in pe)
+        pflops = 2 * pr * L * (d + m)
+        peak, _ = fp64_peak()
+        pred = {"rows": pr, "ms": pms, "TFLOP/s": pflops / (pms * 1e-3) / 1e12,
+                "frac_fp64_peak": pflops / (pms * 1e-3) / 1e12 / peak,
+                "kernel": "predict_kernel (fused sigma(XW+b) beta + arg-max; H never stored)"}
+        del model
+    except AttributeError:
+        pred = None
 
     if rank == 0:
         peak, peak_src = fp64_peak()
-        syrk_flops = N_total // world * L * (L + 1) + 2 * (N_total // world) * L * m
-        syrk_per_launch_ms = syrk_ms / max(syrk_n, 1)
-        achieved = syrk_flops / (syrk_per_launch_ms * 1e-3) / 1e12 if syrk_n else None
+        n_local = n
+        gram_flops = n_local * (L + m) * (L + m + 1)  # augmented lower-triangle Gram of [H T] (K2)
+        syrk_ms, syrk_n = prof["syrk_kernel"]
+        fin_ms, _ = prof["syrk_finish"]
+        gram_ms_per = (syrk_ms + fin_ms) / max(syrk_n, 1)
+        achieved = gram_flops / (gram_ms_per * 1e-3) / 1e12 if syrk_n else None
         traffic = None
-        tpath = os.path.join(HERE, "profiles", "traffic_r01.json")
+        tpath = os.path.join(HERE, "profiles", "traffic_r02.json")
         if os.path.exists(tpath):
             try:
-                traffic = json.load(open(tpath)).get(args.config, {}).get("syrk_kernel")
+                traffic = json.load(open(tpath)).get(args.config, {}).get("gram")
             except Exception:
                 traffic = None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            rows = int(os.environ.get("RBPG_CPU_ROWS", str(n)))
-            v, dt = cpu_oracle_sample(n, d, L, m, 1, rows)
-            cpu = {"value": v, "unit": "TFLOP/s", "cores": 1, "kind": "port",
-                   "sample": f"oracle restatement train() (single thread, as the reference build) on the first "
-                             f"{min(rows, n)} rows of {args.config} (L={L}, d={d}, m={m}); {dt:.1f} s; host has "
-                             f"{os.cpu_count()} cores"}
+            threads = os.cpu_count() or 1
+            v, sec, rows, ph = reference_sample(N_total, d, L, m, threads)
+            cpu = {"value": v, "unit": "TFLOP/s", "cores": threads, "kind": "port",
+                   "sample": sample_text(args.config, rows, N_total, L, threads, ph)}
         line = {
-            "metric": "ELM train FP64 TFLOP/s (alg. flops of H build + Gram + pivoted Cholesky + solves + accuracy / train time)",
-            "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded mt19937_64 generators, SURVEY 8(d)); random-init W, b from init_hidden",
-            "config": {"workload": f"{args.config}: N={n}/GPU (N_total={N_total}) d={d} L={L} m={m}, rank strategy, "
-                                   f"full train() incl. accuracy pass",
-                       "l2": "flushed between timed steps (256 MB write outside the events)",
-                       "parallelism": f"row-sharded dp{world}" if world > 1 else "single GPU"},
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": cfg["scaling"],
+            "vs_baseline": None, "dtype": "f64", "data": DATA, "config": cfg,
             "train_ms": ms_step, "rank": diag.rank, "training_accuracy": diag.training_accuracy,
-            "kernel_ms_per_step": {"hidden_kernel": hid_ms / args.steps, "syrk_kernel": syrk_ms / args.steps,
-                                   "panel_kernel": panel_ms / args.steps, "syrk_trailing": trail_ms / args.steps,
-                                   "trsm_pair_kernel": trsm_ms / args.steps},
-            "roofline": {"kernel": "syrk_kernel (K2 Gram H^T H + H^T T, DMMA)", "bound": "tensor",
+            "kernel_ms_per_step": {k: v[0] / args.steps for k, v in prof.items()},
+            "roofline": {"kernel": "K2 Gram of [H T] (syrk_kernel + syrk_diag_kernel grids + syrk_finish split "
+                                   "reduction), DMMA", "bound": "tensor",
                          "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "peak_source": peak_src,
-                         "alg_flops_per_launch": syrk_flops, "launches": syrk_n},
+                         "peak_source": peak_src, "alg_flops_per_launch": gram_flops, "launches": syrk_n,
+                         "alg_bytes_per_launch": n_local * (d + m) * 8 + (L + m) * (L + m) * 8},
+            "predict": pred,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

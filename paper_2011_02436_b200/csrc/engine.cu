@@ -29,7 +29,26 @@
 #include <vector>
 
 namespace rbpg {
-void trsm_trace_dump();
+cudaError_t ensure_attrs(const void* fn, size_t smem, bool nonportable_cluster) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, std::pair<size_t, bool>> done;  // (device, kernel) -> set
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  auto& cur = done[{dev, fn}];
+  if (smem > cur.first || (smem > 0 && cur.first == 0)) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    cur.first = smem;
+  }
+  if (nonportable_cluster && !cur.second) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    cur.second = true;
+  }
+  return cudaSuccess;
+}
 cudaError_t launch_hidden(const CUtensorMap&, const CUtensorMap&, const HiddenParams&, int, cudaStream_t);
 cudaError_t launch_syrk(const CUtensorMap&, const CUtensorMap&, const SyrkParams&, int, int, cudaStream_t, bool = false);
 cudaError_t launch_syrk_finish(const SyrkParams&, int, int, int, cudaStream_t);
@@ -249,7 +268,7 @@ void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_
                 size_t m = 0) {
   if (N == 0) return;
   CUtensorMap tmX = make_map(ctx, dX, d, N, ldx, 16, kTile, true);
-  static const int bn = std::getenv("RBPG_HIDDEN_BN") ? std::atoi(std::getenv("RBPG_HIDDEN_BN")) : 32;
+  constexpr int bn = 32;  // 128 x 32 tiles, three CTAs per SM (k_gemm.cu)
   CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, bn + 4, kBK, false);  // padded smem rows
   HiddenParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), db, dH, static_cast<long long>(ldh),
                  0, m > 0 ? dT : nullptr, static_cast<long long>(ldt), static_cast<int>(m)};
@@ -319,7 +338,6 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
   p.nbT = m > 0 ? static_cast<int>((m + kTile - 1) / kTile) : 0;
   const int tiles = p.nGram + p.nbI * p.nbT;
   int splits = gram_splits(ctx, N, L, m, tiles, p.nbI);
-  if (const char* e = std::getenv("RBPG_GRAM_SPLITS")) splits = std::max(1, std::atoi(e));  // tuning experiments
   long long per = static_cast<long long>(round_up((N + splits - 1) / splits, kBK));
   if (per == 0) per = kBK;
   splits = static_cast<int>((N + per - 1) / per);
@@ -450,26 +468,20 @@ void trsm_blocked_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X,
     ck(cudaMemcpy2DAsync(X, ldx * 8, src, lds * 8, m * 8, n, cudaMemcpyDeviceToDevice, ctx->stream), "trsm copy");
 }
 
-// X (n x m, ld ldx) <- (F F^T)^{-1} X, column chunks of <= 128 right-hand sides
+// X (n x m, ld ldx) <- (F F^T)^{-1} X: the cluster kernel for m <= 32 when its rows fit in shared
+// memory, the blocked step kernels otherwise
 void trsm_pair_dev(rbpg_context* ctx, const double* F, size_t ldf, double* X, size_t ldx, size_t n, size_t m,
                    bool fwd = true, bool bwd = true) {
-  static const bool legacy = std::getenv("RBPG_TRSM_LEGACY") != nullptr;  // the cooperative sweep for every m
-  if (n > 0 && m > 0 && (fwd || bwd) && !legacy &&
-      !trsm_cluster_fits(static_cast<int>(n), static_cast<int>(std::min<size_t>(m, 128)))) {
+  if (n == 0 || m == 0 || !(fwd || bwd)) return;
+  if (!trsm_cluster_fits(static_cast<int>(n), static_cast<int>(m))) {
     trsm_blocked_dev(ctx, F, ldf, X, ldx, n, m, fwd, bwd);
     return;
   }
-  static const bool tr = std::getenv("RBPG_TRSM_TRACE") != nullptr;
-  if (tr) { cudaStreamSynchronize(ctx->stream); trsm_trace_dump(); }
-  struct Dump { bool on; cudaStream_t s; ~Dump() { if (on) { cudaStreamSynchronize(s); trsm_trace_dump(); } } } dump{tr, ctx->stream};
-  for (size_t c0 = 0; c0 < m; c0 += 128) {
-    const int mc = static_cast<int>(std::min<size_t>(128, m - c0));
-    double* dinv = ctx->dbuf("trsm.dinv", ((n + 63) / 64) * 64 * 64);
-    ctx->run("trsm_pair_kernel", [&] {
-      return launch_trsm_pair(F, static_cast<long long>(ldf), X + c0, static_cast<long long>(ldx), static_cast<int>(n),
-                              mc, fwd ? 1 : 0, bwd ? 1 : 0, ctx->num_sms, dinv, ctx->stream);
-    });
-  }
+  double* dinv = ctx->dbuf("trsm.dinv", ((n + 63) / 64) * 64 * 64);
+  ctx->run("trsm_pair_kernel", [&] {
+    return launch_trsm_pair(F, static_cast<long long>(ldf), X, static_cast<long long>(ldx), static_cast<int>(n),
+                            static_cast<int>(m), fwd ? 1 : 0, bwd ? 1 : 0, ctx->num_sms, dinv, ctx->stream);
+  });
 }
 
 struct FactorResult {
@@ -572,13 +584,10 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     if (t0 < neligible) {  // another panel follows
       const size_t nrem = n - t0;
       // 32-wide tiles while they fit in three waves (the late, small updates: their DMMA work per
-      // SM is what bounds the update), 64-wide beyond.  The 128-wide trailing SYRK (RBPG_TRAIL_TILE
-      // = 128) gathers G_old element by element in its epilogue (no registers to stage them) and
-      // measured 1.5x slower at L = 8000 (C4: 21.5 -> 14.7 ms of trailing updates per train).
+      // SM is what bounds the update), 64-wide beyond.  (A 128-wide trailing SYRK, which gathers
+      // G_old element by element in its epilogue, measured 1.5x slower at L = 8000.)
       const size_t nb32 = (nrem + 31) / 32;
-      static const int force_tile = std::getenv("RBPG_TRAIL_TILE") ? std::atoi(std::getenv("RBPG_TRAIL_TILE")) : 0;
-      int ttile = (nb32 * (nb32 + 1) / 2 <= size_t(3 * ctx->num_sms)) ? 32 : 64;
-      if (force_tile == 128 && ttile == 64) ttile = kTile;
+      const int ttile = (nb32 * (nb32 + 1) / 2 <= size_t(3 * ctx->num_sms)) ? 32 : 64;
       CUtensorMap tm = make_map(ctx, PcT, nrem, static_cast<uint64_t>(kb), ldp, ttile + 4, kBK, false);
       SyrkParams sp{};
       sp.M = static_cast<int>(nrem);
@@ -601,11 +610,7 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
         sp.tl_slot = tl_n++;
         tl_kind.push_back('T');
       }
-      if (ttile == kTile) {
-        ctx->run("syrk_trailing", [&] { return launch_syrk(tm, tm, sp, 1, ttile, s, true); });
-      } else {
-        ctx->run("syrk_trailing", [&] { return launch_trail(tm, sp, ttile, s); });
-      }
+      ctx->run("syrk_trailing", [&] { return launch_trail(tm, sp, ttile, s); });
       double* written = gnext;
       gnext = (written == Ga) ? Gb : Ga;
       gcur = written;
@@ -938,7 +943,7 @@ void solve_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   if (sg.kind != RBPG_RANK_BASED) fail(RBPG_RUNTIME_ERROR, "solve_beta: unknown strategy");
   if (sg.rank_tol < 0.0 || !std::isfinite(sg.rank_tol))
     fail(RBPG_INVALID_ARGUMENT, "rank_revealing_permutation: tolerance must be >= 0");
-  const bool aug = gaug && m > 0 && m <= 32 && !std::getenv("RBPG_NO_AUG");
+  const bool aug = gaug && m > 0 && m <= 32;
   FactorResult f = factor_dev(ctx, dG, ldg, aug ? L + m : L, rows, sg.rank_tol, 1, "rrf", false, L);
   // speculate the full-rank solve (elm.cpp:202-214) before the one host readback of the rank;
   // with rank < L its result is discarded
@@ -1072,24 +1077,12 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
   // the main stream; part q > 0 starts once the aux stream has built its last block.
   // Default cuts (measured on one B200, PCIe ~40 GB/s): after block 2 when the Gram + hidden work
   // outlasts the upload (C2: 3.83 -> 3.74 ms e2e), every 2 blocks when the upload dominates
-  // (C4 L = 250: 3.32 -> 2.96 ms).  RBPG_E2E_PARTS overrides: the upload-block counts at which
-  // parts end, e.g. "2" or "1,3" (the last part always ends at N; "0" = one Gram after all blocks).
+  // (C4 L = 250: 3.32 -> 2.96 ms).  Parts end after these upload-block counts (the last part
+  // always ends at N).
   const double upload_s = double(N) * double(d + m) * 8.0 / 40e9;
   const double compute_s = (2.0 * N * d * L + double(N) * M * M) / 30e12;
-  const char* parts_env = std::getenv("RBPG_E2E_PARTS");
-  const std::vector<size_t> part_cuts = [&] {
-    std::vector<size_t> v;
-    std::string str = parts_env ? parts_env : (upload_s > compute_s ? "2,4,6,8,10,12,14" : "2");
-    size_t pos = 0;
-    while (pos < str.size()) {
-      const size_t c = str.find(',', pos);
-      const int x = std::atoi(str.substr(pos, c == std::string::npos ? std::string::npos : c - pos).c_str());
-      if (x > 0 && (v.empty() || size_t(x) > v.back()) && v.size() < 6) v.push_back(size_t(x));
-      if (c == std::string::npos) break;
-      pos = c + 1;
-    }
-    return v;
-  }();
+  const std::vector<size_t> part_cuts =
+      upload_s > compute_s ? std::vector<size_t>{2, 4, 6} : std::vector<size_t>{2};
   std::vector<size_t> cuts;  // block counts ending parts 0 .. P-2
   if (ready && chunk >= N && M >= 2 * kTile)
     for (size_t c : part_cuts)
@@ -1673,9 +1666,6 @@ int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, 
     if (strategy->kind == RBPG_DF_SPLIT && (strategy->split_index < 1 || strategy->split_index >= hidden))
       fail(RBPG_INVALID_ARGUMENT, "train: df split index must be in (0, " + std::to_string(hidden) + "), got " +
                                       std::to_string(strategy->split_index));
-    static const bool htrace = std::getenv("RBPG_HOST_TRACE") != nullptr;
-    auto now = [] { return std::chrono::steady_clock::now(); };
-    const auto h0 = now();
     // X and T go up in row blocks on the copy stream; the hidden build of each block waits only for
     // its own upload, and W, b are generated on the host meanwhile
     const size_t ldx = even(xcols), ldy = even(ycols);
@@ -1683,8 +1673,7 @@ int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, 
     double* dY = ctx->dbuf("T.in", std::max<size_t>(1, n) * ldy);
     std::vector<RowReady> ready;
     {
-      static const size_t max_blk =
-          std::getenv("RBPG_E2E_BLOCKS") ? std::min(15, std::max(1, std::atoi(std::getenv("RBPG_E2E_BLOCKS")))) : 7;
+      constexpr size_t max_blk = 7;  // upload blocks (10 or 14 measured slower at C2)
       const size_t nblk = std::min<size_t>(max_blk, std::max<size_t>(1, n / 4096));
       const size_t per = round_up((n + nblk - 1) / nblk, kTile);
       ck(cudaEventRecord(ctx->chunk_ev[15], ctx->stream), "event");  // buffers free (prior work done)
@@ -1711,20 +1700,11 @@ int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, 
       rbpg_status s2;
       if (rbpg_init_hidden(inputs, hidden, outputs, seed, w, b, &s2)) fail(s2.code, s2.message);
     }
-    const auto h1 = now();
-    const auto h2 = now();
     const size_t lb = even(outputs);
     double* B = ctx->dbuf("beta", hidden * lb);
     train_core(ctx, dX, ldx, dY, ldy, n, inputs, hidden, outputs, w, b, *strategy, B, lb, order, diag, &ready,
                !ready.empty());
-    const auto h3 = now();
     download(ctx, beta, B, lb, hidden, outputs);
-    const auto h4 = now();
-    if (htrace) {
-      auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
-      std::fprintf(stderr, "[train host] init %.3f upload %.3f core %.3f download %.3f ms\n", ms(h0, h1), ms(h1, h2),
-                   ms(h2, h3), ms(h3, h4));
-    }
   });
 }
 

@@ -2,9 +2,9 @@
 //   K1 hidden_kernel : H = sigmoid(X W + b)      -- reference elm.cpp:93-106 (matmul at
 //                      matrix.cpp:69-77, bias added after the dot at elm.cpp:102, sigmoid elm.cpp:27)
 //   K2 syrk_kernel   : lower-tile G = H^T H (+ H^T T tiles), split-K with a fixed-order
-//                      reduction; also the rank-kb trailing update of the pivoted Cholesky
-//                      -- reference linalg.cpp:179-184 (Gram), 237-244 (trailing update),
-//                      matrix.cpp:79-87 (matmul_at for H^T T)
+//                      reduction -- reference linalg.cpp:179-184 (Gram), matrix.cpp:79-87
+//                      (matmul_at for H^T T); trail_kernel: the rank-kb trailing update of the
+//                      pivoted Cholesky (linalg.cpp:237-244)
 //   gemm_kernel      : generic C = alpha op(A) op(B) + beta C for the small solve-side products
 //
 // Data layout: every matrix is row-major fp64 with an even leading dimension
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
   }
   tl_mark(p.tl, p.tl_slot, 0);
   pdl_trigger();  // PART 1: the diagonal-tile grid (this grid's dependent) may start launching
-  if (PART == 0) pdl_wait();  // trailing mode: the panel that wrote PcT / lab may still be finishing
+  if (PART == 0) pdl_wait();  // launched programmatic-dependent: the producer of A may still be finishing
   tl_mark(p.tl, p.tl_slot, 1);
   __syncthreads();
   if (tid == 0) {
@@ -315,33 +315,6 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
   // ---- epilogue.  Thread holds rows r, r+1 (r even) x cols c..c+3 per (mt, pp).
   const int split = p.split0 + blockIdx.y;
 
-  // trailing mode: every G_old gather is issued before the first store (the stores could alias
-  // the loads as far as the compiler knows, which would serialise one L2 round trip per element)
-  // (64-wide tiles only: the 128-wide kernel has no registers to spare for the staging)
-  constexpr bool kStageGold = TILE == 64;
-  double gold[kStageGold ? MT : 1][2][2][4];
-  if (kStageGold && p.mode == kSyrkTrailing && !isT) {
-    const int off = p.off;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int pp = 0; pp < 2; ++pp) {
-        const int r0 = i0 + wm + mt * 16 + 2 * g;
-        const int c0 = j0 + wn + pp * 16 + 4 * t;
-        int sc[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) sc[q] = (c0 + q < p.M) ? __ldg(p.lab + off + c0 + q) : 0;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = r0 + h;
-          const int sr = r < p.M ? __ldg(p.lab + off + r) : 0;
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            gold[mt][pp][h][q] =
-                (r < p.M && c0 + q < p.M && c0 + q <= r) ? __ldg(p.Gold + (long long)sr * p.ldgo + sc[q]) : 0.0;
-        }
-      }
-  }
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
 #pragma unroll
@@ -386,8 +359,7 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
         }
         continue;
       }
-      // direct / trailing: lower element (r >= c) written at (r, c) and mirrored to (c, r)
-      const int off = (p.mode == kSyrkTrailing) ? p.off : 0;
+      // direct: lower element (r >= c) written at (r, c) and mirrored to (c, r)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int r = r0 + h;
@@ -396,17 +368,8 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
         for (int q = 0; q < 4; ++q) {
           const int c = c0 + q;
           if (c >= p.M || c > r) continue;
-          double val = v[h][q];
-          if (p.mode == kSyrkTrailing) {
-            if constexpr (kStageGold) {
-              val = sub_rn(gold[mt][pp][h][q], val);
-            } else {
-              const int sr = p.lab[off + r], sc = p.lab[off + c];
-              val = sub_rn(p.Gold[(long long)sr * p.ldgo + sc], val);
-            }
-          }
-          p.G[(long long)(off + r) * p.ldg + off + c] = val;
-          p.G[(long long)(off + c) * p.ldg + off + r] = val;
+          p.G[(long long)r * p.ldg + c] = v[h][q];
+          p.G[(long long)c * p.ldg + r] = v[h][q];
         }
       }
     }
@@ -828,57 +791,43 @@ __global__ void __launch_bounds__(128) gemm_kernel(GemmParams p) {
 // ============================================================================
 // launchers
 // ============================================================================
-// bn = 64 (sigmoid build, two CTAs per SM) or 128 (plain transposed product); tmW's box is {bn + 4, kBK}
+// bn = 32 (sigmoid build: 128 x 32 tiles, three CTAs per SM) or 128 (plain transposed product of the
+// pseudo-inverse); tmW's box is {bn + 4, kBK}
 cudaError_t launch_hidden(const CUtensorMap& tmX, const CUtensorMap& tmW, const HiddenParams& p, int bn,
                           cudaStream_t s) {
-  static bool attr = false;
-  constexpr size_t kSmem64 = size_t(kStages) * (kTile + 68) * kBK * sizeof(double) + 1024 + 256;
-  constexpr size_t kSmem128 = size_t(kStages) * (kTile + 132) * kBK * sizeof(double) + 1024 + 256;
-  if (!attr) {
-    cudaFuncSetAttribute(hidden_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem128);
-    cudaFuncSetAttribute(hidden_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem64);
-    attr = true;
-  }
   dim3 grid((p.L + bn - 1) / bn, (p.N + kTile - 1) / kTile);
   if (bn == 32) {
     constexpr size_t kSmem32 = size_t(3) * (kTile + 36) * kBK * sizeof(double) + 1024 + 256;
-    static bool a32 = false;
-    if (!a32) {
-      cudaFuncSetAttribute(hidden_kernel<32, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem32);
-      a32 = true;
-    }
+    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(hidden_kernel<32, 3>), kSmem32);
+    if (e != cudaSuccess) return e;
     hidden_kernel<32, 3><<<grid, kGemmThreads, kSmem32, s>>>(tmX, tmW, p);
-  } else if (bn == 64)
-    hidden_kernel<64><<<grid, kGemmThreads, kSmem64, s>>>(tmX, tmW, p);
-  else
+  } else if (bn == 128) {
+    constexpr size_t kSmem128 = size_t(kStages) * (kTile + 132) * kBK * sizeof(double) + 1024 + 256;
+    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(hidden_kernel<128>), kSmem128);
+    if (e != cudaSuccess) return e;
     hidden_kernel<128><<<grid, kGemmThreads, kSmem128, s>>>(tmX, tmW, p);
+  } else {
+    return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
-// tile = 128 (256 threads, 1 CTA/SM: the Gram) or 64 (128 threads, several CTAs/SM: small
-// trailing updates, where 128-wide tiles would leave most SMs idle).  The tensor maps' boxes
-// must be {tile, kBK}.
-// pdl: launch as a programmatic dependent of the preceding kernel in the stream (trailing updates
-// behind a panel)
+// The Gram (tile 128, 256 threads, one CTA per SM).  With two or more tile rows the diagonal tiles
+// go to syrk_diag_kernel and the rest to syrk_kernel<128, 1>; a single tile row runs
+// syrk_kernel<128>.  The tensor maps' boxes must be {tile + 4, kBK} (padded shared-memory rows).
 constexpr size_t kSyrkSmem128 = size_t(kStages) * 2 * 132 * kBK * sizeof(double) + 1024 + 256;
-constexpr size_t kSyrkSmem64 = size_t(kStages) * 2 * 68 * kBK * sizeof(double) + 1024 + 256;
 
-// tensor-map boxes must be {tile + 4, kBK} (padded shared-memory rows)
 cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const SyrkParams& p, int splits, int tile,
                         cudaStream_t s, bool pdl) {
-  if (tile == 128 && p.mode != kSyrkTrailing && p.nbI >= 2) {
-    // Gram: diagonal tiles by syrk_diag_kernel, the rest by syrk_kernel<128, 1> as its
-    // programmatic dependent (the two grids share the machine)
-    static bool dattr = false;
-    if (!dattr) {
-      cudaFuncSetAttribute(syrk_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem128);
-      cudaFuncSetAttribute(syrk_kernel<128, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem128);
-      dattr = true;
-    }
+  if (tile != 128 || p.mode == kSyrkTrailing) return cudaErrorInvalidValue;
+  if (p.nbI >= 2) {
+    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(syrk_diag_kernel), kSyrkSmem128);
+    if (e == cudaSuccess) e = ensure_attrs(reinterpret_cast<const void*>(syrk_kernel<128, 1>), kSyrkSmem128);
+    if (e != cudaSuccess) return e;
     // off-diagonal (long) CTAs first, the diagonal (short) ones as its programmatic dependent:
     // they fill the SMs the last off-diagonal wave leaves idle
     syrk_kernel<128, 1><<<dim3(p.nbI * (p.nbI - 1) / 2 + p.nbI * p.nbT, splits), 256, kSyrkSmem128, s>>>(tmA, tmB, p);
-    cudaError_t e = cudaGetLastError();
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t c2 = {};
     c2.gridDim = dim3(p.nbI, splits);
@@ -892,6 +841,8 @@ cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const Sy
     c2.numAttrs = 1;
     return cudaLaunchKernelEx(&c2, syrk_diag_kernel, tmA, p);
   }
+  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(syrk_kernel<128>), kSyrkSmem128);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.nGram + p.nbI * p.nbT, splits);
   cfg.stream = s;
@@ -900,28 +851,9 @@ cudaError_t launch_syrk(const CUtensorMap& tmA, const CUtensorMap& tmB, const Sy
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl ? 1 : 0;
-  if (tile == 128) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(syrk_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem128);
-      attr = true;
-    }
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = kSyrkSmem128;
-    return cudaLaunchKernelEx(&cfg, syrk_kernel<128>, tmA, tmB, p);
-  }
-  if (tile == 64) {
-    constexpr size_t smem = kSyrkSmem64;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(syrk_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = smem;
-    return cudaLaunchKernelEx(&cfg, syrk_kernel<64>, tmA, tmB, p);
-  }
-  return cudaErrorInvalidValue;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = kSyrkSmem128;
+  return cudaLaunchKernelEx(&cfg, syrk_kernel<128>, tmA, tmB, p);
 }
 
 template <int TILE, int KS = kStages>
@@ -930,7 +862,9 @@ constexpr size_t trail_smem() {
          1024 + 256;
 }
 
-// Trailing update (tile 32 or 64); the tensor map covers PcT with box {tile + 4, 16}.
+// Trailing update (tile 32 or 64); the tensor map covers PcT with box {tile + 4, 16}.  64-wide tiles
+// stream the rank-64 panel through one 16-deep stage reloaded four times (four CTAs per SM; C4
+// L=8000: 9.1 ms of trailing updates, against 11.4 / 9.5 ms with the whole panel / halves resident).
 cudaError_t launch_trail(const CUtensorMap& tmP, const SyrkParams& p, int tile, cudaStream_t s) {
   if (p.kRows > kStages * kBK) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
@@ -942,36 +876,15 @@ cudaError_t launch_trail(const CUtensorMap& tmP, const SyrkParams& p, int tile, 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (tile == 64) {
-    // RBPG_TRAIL_KS: k-stages resident -- 4 = the whole panel (two CTAs per SM), 2 = halves (three),
-    // default 1 = one 16-deep stage reloaded four times (four CTAs per SM; C4 L=8000: 11.4 / 9.5 / 9.1 ms)
-    static const int ks = std::getenv("RBPG_TRAIL_KS") ? std::atoi(std::getenv("RBPG_TRAIL_KS")) : 1;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(trail_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trail_smem<64>());
-      cudaFuncSetAttribute(trail_kernel<64, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)trail_smem<64, 2>());
-      cudaFuncSetAttribute(trail_kernel<64, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)trail_smem<64, 1>());
-      attr = true;
-    }
+    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(trail_kernel<64, 1>), trail_smem<64, 1>());
+    if (e != cudaSuccess) return e;
     cfg.blockDim = dim3(128);
-    if (ks == 1) {
-      cfg.dynamicSmemBytes = trail_smem<64, 1>();
-      return cudaLaunchKernelEx(&cfg, trail_kernel<64, 1>, tmP, p);
-    }
-    if (ks == 2) {
-      cfg.dynamicSmemBytes = trail_smem<64, 2>();
-      return cudaLaunchKernelEx(&cfg, trail_kernel<64, 2>, tmP, p);
-    }
-    cfg.dynamicSmemBytes = trail_smem<64>();
-    return cudaLaunchKernelEx(&cfg, trail_kernel<64>, tmP, p);
+    cfg.dynamicSmemBytes = trail_smem<64, 1>();
+    return cudaLaunchKernelEx(&cfg, trail_kernel<64, 1>, tmP, p);
   }
   if (tile == 32) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(trail_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trail_smem<32>());
-      attr = true;
-    }
+    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(trail_kernel<32>), trail_smem<32>());
+    if (e != cudaSuccess) return e;
     cfg.blockDim = dim3(64);
     cfg.dynamicSmemBytes = trail_smem<32>();
     return cudaLaunchKernelEx(&cfg, trail_kernel<32>, tmP, p);
@@ -1097,7 +1010,7 @@ cudaError_t launch_scores(const CUtensorMap& tmH, const CUtensorMap& tmB, const 
     const size_t pipe = size_t(4) * (kTile * kBK + kBK * (bn + 4)) * sizeof(double) + 64;
     const size_t scb = size_t(kTile) * (bn + 1) * sizeof(double);
     const size_t smem = (pipe > scb ? pipe : scb) + 1024;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(kern), smem);
     if (e != cudaSuccess) return e;
     kern<<<grid, kGemmThreads, smem, s>>>(tmH, tmB, p);
     return cudaGetLastError();

@@ -844,18 +844,13 @@ int panel_cluster_size(int nl) {
   return 0;
 }
 
-// Labels per quad of panel_reg_kernel for a panel of nl labels (0: another variant).  Up to 4
-// labels per quad (256 per CTA, 4096 per 16-CTA cluster); RBPG_PANEL_REG_LPQ caps it (1 = the
-// round-1 limit of 1024 labels) and RBPG_PANEL_SMEM disables the variant.
+// Labels per quad of panel_reg_kernel for a panel of nl labels (0: the grid variant).  Up to 4
+// labels per quad: 256 per CTA, 4096 per 16-CTA cluster.
 int panel_reg_lpq(int nl) {
-  static const int cap = std::getenv("RBPG_PANEL_SMEM") ? 0
-                         : std::getenv("RBPG_PANEL_REG_LPQ") ? std::atoi(std::getenv("RBPG_PANEL_REG_LPQ"))
-                                                               : 4;
   const int CL = panel_cluster_size(nl);
   if (CL <= 0) return 0;
   const int R = (nl + CL - 1) / CL;
-  const int lpq = R <= kRegLabels ? 1 : (R <= 2 * kRegLabels ? 2 : (R <= 4 * kRegLabels ? 4 : 0));
-  return lpq <= cap ? lpq : 0;
+  return R <= kRegLabels ? 1 : (R <= 2 * kRegLabels ? 2 : (R <= 4 * kRegLabels ? 4 : 0));
 }
 
 // Whether a panel of nl labels runs panel_reg_kernel (which reads G through its lower triangle).
@@ -871,16 +866,8 @@ cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cuda
     auto kern = lpq == 1 ? (p.trace ? panel_reg_kernel<true, 1> : panel_reg_kernel<false, 1>)
                 : lpq == 2 ? (p.trace ? panel_reg_kernel<true, 2> : panel_reg_kernel<false, 2>)
                            : (p.trace ? panel_reg_kernel<true, 4> : panel_reg_kernel<false, 4>);
-    static size_t attr[6] = {0, 0, 0, 0, 0, 0};
-    size_t& a = attr[(p.trace ? 1 : 0) + 2 * (lpq == 1 ? 0 : (lpq == 2 ? 1 : 2))];
-    if (smem > a || a == 0) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)(smem > 0 ? smem : 16));
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-      a = smem > 0 ? smem : 16;
-    }
+    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(kern), smem > 0 ? smem : 16, true);
+    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(CL);
     cfg.blockDim = dim3(kPThreads);
@@ -898,49 +885,15 @@ cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cuda
     if (ctas_used) *ctas_used = CL;
     return cudaLaunchKernelEx(&cfg, kern, pp);
   }
-  if (CL > 0) {
-    pp.rows_per_cta = (nl + CL - 1) / CL;
-    const size_t smem = panel_smem_bytes(nl, pp.rows_per_cta);
-    static size_t attr = 0;
-    if (smem > attr) {
-      cudaError_t e = cudaFuncSetAttribute(panel_kernel_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem);
-      if (e != cudaSuccess) return e;
-      e = cudaFuncSetAttribute(panel_kernel_t<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-      attr = smem;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CL);
-    cfg.blockDim = dim3(kPThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CL;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    if (ctas_used) *ctas_used = CL;
-    return cudaLaunchKernelEx(&cfg, panel_kernel_t<true>, pp);
-  }
   // grid variant: ~ceil(nl / num_sms) labels per CTA, every CTA co-resident (cooperative launch)
   int R = (nl + num_sms - 1) / num_sms;
   if (R < 32) R = 32;
-  static const int min_r = std::getenv("RBPG_PANEL_GRID_R") ? std::atoi(std::getenv("RBPG_PANEL_GRID_R")) : 0;
-  if (R < min_r) R = std::min(min_r, kMaxLabelsPerCta);
   if (R > kMaxLabelsPerCta) return cudaErrorInvalidValue;  // n > 256 * num_sms unsupported
   const int C = (nl + R - 1) / R;
   pp.rows_per_cta = R;
   const size_t smem = panel_smem_bytes(nl, R);
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(panel_kernel_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = smem;
-  }
+  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(panel_kernel_t<false>), smem);
+  if (e != cudaSuccess) return e;
   if (ctas_used) *ctas_used = C;
   void* args[] = {&pp};
   return cudaLaunchCooperativeKernel((void*)panel_kernel_t<false>, dim3(C), dim3(kPThreads), args, smem, s);

@@ -6,11 +6,9 @@
 //   tri_inv_kernel   : the 64x64 diagonal blocks of F are inverted once, all blocks
 //                      in parallel (one CTA each), so a block step is a small product
 //                      instead of 64 dependent substitution steps.
-//   trsm_sweep_kernel: cooperative; per block step every CTA forms the block solution
-//                      Y_b = D_b^{-1} R_b (forward) or D_b^{-T} R_b (backward) in shared
-//                      memory, CTA (b mod C) stores it, and all CTAs update their share of
-//                      the remaining rows from 32-row F tiles staged in shared memory
-//                      (coalesced 512-byte row segments); one grid barrier per block.
+//   trsm_cluster_kernel: m <= 32 right-hand sides, one thread-block cluster, block solutions
+//                      pushed between CTAs over distributed shared memory (below);
+//   trsm_step_kernel : any m, one launch per 64-row block step (engine trsm_blocked_dev).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -25,7 +23,6 @@ namespace cg = cooperative_groups;
 namespace rbpg {
 
 constexpr int kTB = 64;    // diagonal block
-constexpr int kTR = 32;    // update row tile
 
 __global__ void __launch_bounds__(64) tri_inv_kernel(const double* F, long long ldf, int n, double* Dinv) {
   extern __shared__ __align__(16) double tsm[];
@@ -50,94 +47,6 @@ __global__ void __launch_bounds__(64) tri_inv_kernel(const double* F, long long 
   __syncthreads();
   double* D = Dinv + (long long)b * kTB * kTB;
   for (int r = 0; r < kTB; ++r) D[r * kTB + j] = Zs[r][j];
-}
-
-__global__ void __launch_bounds__(256) trsm_sweep_kernel(const double* F, long long ldf, const double* Dinv, double* X,
-                                                         long long ldx, int n, int m, int backward) {
-  extern __shared__ __align__(16) double sm[];
-  double* Rb = sm;                      // [64][m]      right-hand side block
-  double* Yb = Rb + kTB * m;            // [64][m]      block solution
-  double* Ds = Yb + kTB * m;            // [64][65]     diagonal-block inverse
-  double* Ft = Ds + kTB * (kTB + 1);    // [32][65]     F tile of the row update
-  cg::grid_group grid = cg::this_grid();
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int nblk = (n + kTB - 1) / kTB;
-
-  auto load_tile = [&](int i0, int nb, int r0, int nr) {
-    if (!backward) {
-      for (int e = tid; e < kTR * kTB; e += nt) {
-        const int rr = e / kTB, q = e % kTB;
-        Ft[rr * (kTB + 1) + q] = (rr < nr && q < nb) ? __ldg(F + (long long)(r0 + rr) * ldf + i0 + q) : 0.0;
-      }
-    } else {
-      for (int e = tid; e < kTR * kTB; e += nt) {
-        const int q = e / kTR, rr = e % kTR;
-        Ft[rr * (kTB + 1) + q] = (rr < nr && q < nb) ? __ldg(F + (long long)(i0 + q) * ldf + r0 + rr) : 0.0;
-      }
-    }
-  };
-
-  // The owner stores block b's solution only after the step's grid barrier (deferred to the
-  // start of step s+1): every CTA reads block b's right-hand side from X during step s.
-  auto store_solution = [&](int bb) {
-    const int j0 = bb * kTB, jb = min(kTB, n - j0);
-    for (int e = tid; e < jb * m; e += nt) X[(long long)(j0 + e / m) * ldx + e % m] = Yb[e];
-  };
-  for (int s = 0; s < nblk; ++s) {
-    const int b = backward ? nblk - 1 - s : s;
-    if (s > 0) {
-      const int bp = backward ? b + 1 : b - 1;
-      if (blockIdx.x == bp % gridDim.x) store_solution(bp);
-    }
-    const int i0 = b * kTB, nb = min(kTB, n - i0);
-    const int rlo = backward ? 0 : i0 + nb;  // rows updated by this block: forward [i0+nb, n), backward [0, i0)
-    const int rhi = backward ? i0 : n;
-    const int ntiles = (rhi - rlo + kTR - 1) / kTR;
-    // all loads of the step issued together: D_b, R_b and the first F tile
-    const double* D = Dinv + (long long)b * kTB * kTB;
-    for (int e = tid; e < kTB * kTB; e += nt) Ds[(e / kTB) * (kTB + 1) + e % kTB] = __ldg(D + e);
-    for (int e = tid; e < kTB * m; e += nt) {
-      const int q = e / m, c = e - q * m;
-      Rb[e] = q < nb ? __ldcg(X + (long long)(i0 + q) * ldx + c) : 0.0;
-    }
-    if (blockIdx.x < ntiles) load_tile(i0, nb, rlo + blockIdx.x * kTR, min(kTR, rhi - (rlo + blockIdx.x * kTR)));
-    __syncthreads();
-    for (int e = tid; e < nb * m; e += nt) {
-      const int i = e / m, c = e - i * m;
-      double acc = 0.0;
-      if (!backward) {
-        for (int q = 0; q <= i; ++q) acc = fma(Ds[i * (kTB + 1) + q], Rb[q * m + c], acc);
-      } else {
-        for (int q = i; q < nb; ++q) acc = fma(Ds[q * (kTB + 1) + i], Rb[q * m + c], acc);
-      }
-      Yb[e] = acc;
-    }
-    __syncthreads();
-
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-      const int r0 = rlo + t * kTR, nr = min(kTR, rhi - r0);
-      if (t != blockIdx.x) {
-        __syncthreads();
-        load_tile(i0, nb, r0, nr);
-        __syncthreads();
-      }
-      for (int e = tid; e < nr * m; e += nt) {
-        const int rr = e / m, c = e - rr * m;
-        const double* fr = Ft + rr * (kTB + 1);
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll 8
-        for (int q = 0; q < kTB; q += 2) {
-          a0 = fma(fr[q], Yb[q * m + c], a0);
-          a1 = fma(fr[q + 1], Yb[(q + 1) * m + c], a1);
-        }
-        double* xp = X + (long long)(r0 + rr) * ldx + c;
-        *xp = __ldcg(xp) - (a0 + a1);
-      }
-    }
-    grid.sync();
-  }
-  const int blast = backward ? 0 : nblk - 1;
-  if (nblk > 0 && blockIdx.x == blast % gridDim.x) store_solution(blast);
 }
 
 // ---------------------------------------------------------------------------
@@ -172,7 +81,6 @@ __device__ __forceinline__ void load_tile_async(double* T, const double* F, long
   }
 }
 
-__device__ long long* g_trsm_trace = nullptr;
 // C[64][m] = A * B  (or C -= A * B), A 64x64 with A(r, k) = aT ? A[k*lda + r] : A[r*lda + k],
 // B 64 x m row-major (ld m), on FP64 tensor cores: one (m16, n8) output tile per warp pass,
 // two interleaved accumulator chains over K = 64.
@@ -286,11 +194,8 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
     double* Rb = Rown + (size_t)(b / C) * kTB * m;
     const int slot = (s - s_begin) % kRing;
     double* Y = Ring + slot * kTB * m;
-    const long long q0 = clock64();
     mma64(D, kPadT, bwd, Rb, m, Y, false, tid);
-    const long long q1 = clock64();
     __syncthreads();
-    const long long q2 = clock64();
     const uint32_t yl = smem_u32(Y), bl = smem_u32(&rbar[slot]);
     if (tid < C - 1) {
       // one bulk DSMEM copy per destination (TMA engine), issued by C - 1 threads in parallel and
@@ -303,14 +208,7 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
     }
     if (tid == 32)  // the own copy was written in place
       asm volatile("mbarrier.complete_tx.shared::cta.b64 [%0], %1;\n" ::"r"(bl), "r"(ybytes) : "memory");
-    const long long q3 = clock64();
     for (int e = tid; e < kTB * m; e += nt) Rb[e] = Y[e];  // the block's solution
-    if (tid == 0 && g_trsm_trace) {
-      atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[8]), static_cast<unsigned long long>(q1 - q0));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[9]), static_cast<unsigned long long>(q2 - q1));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[10]), static_cast<unsigned long long>(q3 - q2));
-      atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[11]), 1ull);
-    }
   };
   // R_bp -= F-tile * Y (forward: tile = F[bp rows][b cols]; backward: tile = F[b rows][bp cols]^T)
   auto update = [&](int bp, const double* T, bool bwd, const double* Yb) {
@@ -340,7 +238,6 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
   __syncthreads();
   if (owns(block_of(s_begin))) solve_and_push(s_begin, Ds);
 
-  long long tw = 0, tc = 0, to = 0;
   for (int s = s_begin; s < s_end; ++s) {
     const int u = s - s_begin;
     const bool bwd = s >= nblk;
@@ -366,25 +263,15 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
     cp_async_commit();
     if (!last && tid == 0) mbar_arrive_expect_tx(&rbar[(u + 1) % kRing], ybytes);
     if ((u + 1) % kSyncEvery == 0) cl.sync();  // skew < kRing steps
-    long long t1 = clock64();
     mbar_wait(&rbar[slot], (u / kRing) & 1);
     const double* Yb = Ring + slot * kTB * m;
     cp_async_wait_all();
     __syncthreads();
-    long long t2 = clock64(); tw += t2 - t1;
     if (!last && owns(bn)) {  // critical path: update the next block, solve it, push
       if (crit) update(bn, Tc, bwd, Yb);
       __syncthreads();
-      const long long ta = clock64();
       solve_and_push(s + 1, Ds + ((u + 1) & 1) * kTB * kPadT);
-      if (tid == 0 && g_trsm_trace) {
-        atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[4]), static_cast<unsigned long long>(ta - t2));
-        atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[5]),
-                  static_cast<unsigned long long>(clock64() - ta));
-        atomicAdd(reinterpret_cast<unsigned long long*>(&g_trsm_trace[6]), 1ull);
-      }
     }
-    long long t3 = clock64(); tc += t3 - t2;
     for (int ob = 0; ob < nown; ++ob) {  // remaining updates off the critical path
 
       const int bp = cta + ob * C;
@@ -400,9 +287,7 @@ __global__ void __launch_bounds__(256, 1) trsm_cluster_kernel(const double* F, l
       update(bp, To, bwd, Yb);
     }
     __syncthreads();
-    to += clock64() - t3;
   }
-  if (cta == 0 && tid == 0 && g_trsm_trace) { g_trsm_trace[0] += tw; g_trsm_trace[1] += tc; g_trsm_trace[2] += to; g_trsm_trace[3] += s_end - s_begin; }
   cl.sync();  // no CTA exits while remote stores may still target it
   for (int e = tid; e < nown * kTB * m; e += nt) {
     const int ob = e / (kTB * m), rem = e % (kTB * m), q = rem / m, c = rem % m;
@@ -547,127 +432,58 @@ __global__ void __launch_bounds__(256) trsm_step_kernel(const double* __restrict
 cudaError_t launch_trsm_step(const double* F, long long ldf, const double* Db, double* src, long long lds,
                              double* dst, long long ldd, int n, int m, int r0, int nb, int bwd, cudaStream_t s) {
   const int rows = bwd ? r0 : n - r0 - nb;
-  auto go = [&](auto kern, int nc) -> cudaError_t {
-    const size_t smem = (size_t(128) * (nc + 2) + size_t(128) * 66) * sizeof(double);
-    static size_t attr[2] = {0, 0};
-    size_t& a = attr[nc == 128 ? 1 : 0];  // (per instantiation: the lambda is a template)
-    if (a < smem) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      a = smem;
-    }
-    dim3 grid((m + nc - 1) / nc, 1 + (rows + 63) / 64);
-    kern<<<grid, 256, smem, s>>>(F, ldf, Db, src, lds, dst, ldd, n, m, r0, nb, bwd);
-    return cudaGetLastError();
-  };
-  static const int nc = std::getenv("RBPG_TRSM_NC") ? std::atoi(std::getenv("RBPG_TRSM_NC")) : 32;
-  if (nc == 128) return go(trsm_step_kernel<128>, 128);
-  if (nc == 64) return go(trsm_step_kernel<64>, 64);
-  return go(trsm_step_kernel<32>, 32);
+  constexpr int kNC = 32;  // columns per CTA (measured best at C5's m = 100 against 64 / 128)
+  const size_t smem = (size_t(128) * (kNC + 2) + size_t(128) * 66) * sizeof(double);
+  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(trsm_step_kernel<kNC>), smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((m + kNC - 1) / kNC, 1 + (rows + 63) / 64);
+  trsm_step_kernel<kNC><<<grid, 256, smem, s>>>(F, ldf, Db, src, lds, dst, ldd, n, m, r0, nb, bwd);
+  return cudaGetLastError();
 }
 
 // The 64 x 64 diagonal-block inverses of F (blocked TRSM path of the engine).
 cudaError_t launch_tri_inv(const double* F, long long ldf, int n, double* dinv, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   constexpr size_t kInvSmem = size_t(2) * kTB * (kTB + 1) * sizeof(double);
-  static bool inv_attr = false;
-  if (!inv_attr) {
-    cudaError_t e = cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kInvSmem);
-    if (e != cudaSuccess) return e;
-    inv_attr = true;
-  }
+  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(tri_inv_kernel), kInvSmem);
+  if (e != cudaSuccess) return e;
   tri_inv_kernel<<<(n + kTB - 1) / kTB, kTB, kInvSmem, s>>>(F, ldf, n, dinv);
   return cudaGetLastError();
 }
 
-// Whether launch_trsm_pair runs its cluster kernel for n rows and m (<= 128) right-hand sides.
+// Whether launch_trsm_pair runs its cluster kernel for n rows and m right-hand sides.
 bool trsm_cluster_fits(int n, int m) {
-  if (m > kClusterMaxM || std::getenv("RBPG_TRSM_GRID")) return false;
+  if (m > kClusterMaxM) return false;
   const int nblk = (n + kTB - 1) / kTB;
   return trsm_cluster_smem(n, m, std::min(16, nblk)) <= 220 * 1024;
 }
 
+// Cluster TRSM pair (the caller checks trsm_cluster_fits; larger problems go through the blocked
+// step kernels).  The cluster kernel inverts its diagonal blocks itself into dinv_ws.
 cudaError_t launch_trsm_pair(const double* F, long long ldf, double* X, long long ldx, int n, int m, int fwd, int bwd,
                              int num_sms, double* dinv_ws, cudaStream_t s) {
-  if (n <= 0 || m <= 0) return cudaSuccess;
+  (void)num_sms;
+  if (n <= 0 || m <= 0 || !(fwd || bwd)) return cudaSuccess;
+  if (!trsm_cluster_fits(n, m)) return cudaErrorInvalidValue;
   const int nblk = (n + kTB - 1) / kTB;
-  constexpr size_t kInvSmem = size_t(2) * kTB * (kTB + 1) * sizeof(double);
-  static bool inv_attr = false;
-  if (!inv_attr) {
-    cudaFuncSetAttribute(tri_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kInvSmem);
-    inv_attr = true;
-  }
-  cudaError_t e = cudaSuccess;
-  const size_t smem = (size_t(2) * kTB * m + size_t(kTB + kTR) * (kTB + 1)) * sizeof(double);
-  static size_t attr_smem = 0;
-  if (smem > attr_smem) {
-    e = cudaFuncSetAttribute(trsm_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_smem = smem;
-  }
-  if ((fwd || bwd) && m <= kClusterMaxM && !std::getenv("RBPG_TRSM_GRID")) {
-    const int C = std::min(16, nblk);
-    const size_t csmem = trsm_cluster_smem(n, m, C);
-    if (csmem <= 220 * 1024) {
-      static size_t cattr = 0;
-      if (csmem > cattr) {
-        e = cudaFuncSetAttribute(trsm_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem);
-        if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(trsm_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return e;
-        cattr = csmem;
-      }
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(C);
-      cfg.blockDim = dim3(256);
-      cfg.dynamicSmemBytes = csmem;
-      cfg.stream = s;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = C;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      const int s_begin = fwd ? 0 : nblk, s_end = bwd ? 2 * nblk : nblk;
-      return cudaLaunchKernelEx(&cfg, trsm_cluster_kernel, F, ldf, dinv_ws, X, ldx, n, m, s_begin,
-                                s_end);  // inverts its diagonal blocks in-kernel
-    }
-  }
-  tri_inv_kernel<<<nblk, kTB, kInvSmem, s>>>(F, ldf, n, dinv_ws);
-  e = cudaGetLastError();
+  const int C = std::min(16, nblk);
+  const size_t csmem = trsm_cluster_smem(n, m, C);
+  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(trsm_cluster_kernel), csmem, true);
   if (e != cudaSuccess) return e;
-  int blocks = std::min(num_sms, std::max(1, (n + kTB - 1) / kTB));
-  const double* Dc = dinv_ws;
-  for (int dir = 0; dir < 2; ++dir) {
-    if ((dir == 0 && !fwd) || (dir == 1 && !bwd)) continue;
-    int backward = dir;
-    void* args[] = {(void*)&F, (void*)&ldf, (void*)&Dc, (void*)&X, (void*)&ldx, (void*)&n, (void*)&m, (void*)&backward};
-    e = cudaLaunchCooperativeKernel((void*)trsm_sweep_kernel, dim3(blocks), dim3(256), args, smem, s);
-    if (e != cudaSuccess) return e;
-  }
-  return cudaSuccess;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = csmem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const int s_begin = fwd ? 0 : nblk, s_end = bwd ? 2 * nblk : nblk;
+  return cudaLaunchKernelEx(&cfg, trsm_cluster_kernel, F, ldf, dinv_ws, X, ldx, n, m, s_begin, s_end);
 }
 
-}  // namespace rbpg
-namespace rbpg {
-void trsm_trace_dump() {
-  static long long* buf = nullptr;
-  if (!buf) {
-    cudaMalloc(&buf, 128);
-    cudaMemset(buf, 0, 128);
-    cudaMemcpyToSymbol(g_trsm_trace, &buf, sizeof(buf));
-    return;
-  }
-  long long h[12];
-  cudaMemcpy(h, buf, 96, cudaMemcpyDeviceToHost);
-  std::fprintf(stderr, "[trsm trace] solve_and_push x%lld: mma %.0f sync %.0f push-issue %.0f cycles\n", h[11],
-               double(h[8]) / (h[11] ? h[11] : 1), double(h[9]) / (h[11] ? h[11] : 1),
-               double(h[10]) / (h[11] ? h[11] : 1));
-  std::fprintf(stderr, "[trsm trace] steps %lld wait %.0f crit %.0f other %.0f cycles/step; owner steps %lld: "
-               "update %.0f solve+push %.0f cycles\n", h[3],
-               double(h[0]) / (h[3] ? h[3] : 1), double(h[1]) / (h[3] ? h[3] : 1), double(h[2]) / (h[3] ? h[3] : 1),
-               h[6], double(h[4]) / (h[6] ? h[6] : 1), double(h[5]) / (h[6] ? h[6] : 1));
-  cudaMemset(buf, 0, 128);
-}
 }  // namespace rbpg

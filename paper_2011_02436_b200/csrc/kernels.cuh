@@ -8,6 +8,11 @@
 
 namespace rbpg {
 
+// Opt kernel `fn` into `smem` bytes of dynamic shared memory (and, with nonportable_cluster,
+// cluster sizes above 8) on the CURRENT device.  Function attributes are per device, so the setting
+// is remembered per (device, kernel): contexts on several GPUs in one process each get it.
+cudaError_t ensure_attrs(const void* fn, size_t smem, bool nonportable_cluster = false);
+
 // CTA tile for the TMA-fed DMMA kernels (K1 hidden build, K2 Gram/trailing SYRK)
 constexpr int kTile = 128;   // rows x cols of the output tile
 constexpr int kBK = 16;      // reduction rows per pipeline stage

@@ -95,6 +95,29 @@ def train_sharded(x_local, t_local, params: api.ElmParams, strategy: api.SolverS
     return beta, diag, hidden, order
 
 
+def train_shard_device(x_local, t_local, w, b, params: api.ElmParams, strategy: api.SolverStrategy, n_total: int,
+                       stages: Optional[DeviceStages] = None, group=None):
+    """train() step of one rank on device-resident inputs (bench.py's timed step at N > 1): local
+    augmented Gram, ONE all-reduce, replicated solve, hit-count all-reduce.  w, b are the
+    replicated hidden layer as device tensors.  Returns (beta, SolveDiagnostics, order)."""
+    import torch
+    import torch.distributed as dist
+
+    stages = stages or DeviceStages()
+    gaug = stages.gram_aug(x_local, t_local, w, b)
+    if dist.get_backend(group) != "nccl":
+        torch.cuda.synchronize(gaug.device)
+    dist.all_reduce(gaug, group=group)
+    L, m = w.shape[1], t_local.shape[1]
+    beta, diag, order = stages.solve_aug(gaug, L, m, n_total, strategy)
+    hits = torch.tensor([stages.hits(x_local, t_local, w, b, beta)], dtype=torch.int64, device=gaug.device)
+    if dist.get_backend(group) != "nccl":
+        torch.cuda.synchronize(hits.device)
+    dist.all_reduce(hits, group=group)
+    diag.training_accuracy = float(hits.item()) / float(n_total)
+    return beta, diag, order
+
+
 def pseudo_inverse_sharded(h_local, n_total: int, tol: float = 0.0, stages=None, group=None):
     """Row-sharded rank-path pseudo-inverse: each rank holds a contiguous
     row block H_p of H; one all-reduce of the local Grams H_p^T H_p, then every rank factors the
