@@ -144,6 +144,27 @@ int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, 
 int rbpg_predict(rbpg_context* ctx, const double* w, const double* b, size_t d, size_t l, const double* beta,
                  size_t m, const double* x, size_t n, size_t xcols, double* scores, rbpg_status* st);
 
+/* solve_block_split (elm.cpp:124-156, elm.hpp:86-93): beta1 (c1 x m), beta2 (c2 x m) of the block solve
+ * of [H1 H2] against Y through the Gram of H2 and the Schur complement, one relative ridge retry per
+ * block (ridge, elm.cpp:30-49; 1e-8 in the reference's callers).  Row-count mismatch or n < c1 + c2:
+ * RBPG_SHAPE_ERROR; a block still singular after the retry: RBPG_SINGULAR_SPLIT (block 0 = A, 1 = D).
+ * diag->ridge_applied reports the retry. */
+int rbpg_solve_block_split(rbpg_context* ctx, const double* h1, size_t n, size_t c1, const double* h2, size_t n2,
+                           size_t c2, const double* y, size_t yrows, size_t m, double ridge, double* beta1,
+                           double* beta2, rbpg_diagnostics* diag, rbpg_status* st);
+/* SpdFactor (linalg.cpp:99-151, linalg.hpp:45-60): the Cholesky factor of m stays on the device and is
+ * reused by every solve.  create fails with RBPG_SINGULAR_MATRIX (pivot index / value in st) like the
+ * reference constructor; solve checks the right-hand-side row count (RBPG_SHAPE_ERROR). */
+typedef struct rbpg_spd rbpg_spd;
+int rbpg_spd_create(rbpg_context* ctx, const double* m, size_t mrows, size_t mcols, rbpg_spd** out, rbpg_status* st);
+int rbpg_spd_solve(const rbpg_spd* f, const double* rhs, size_t rrows, size_t rcols, double* out, rbpg_status* st);
+size_t rbpg_spd_dim(const rbpg_spd* f);
+void rbpg_spd_destroy(rbpg_spd* f);
+/* matmul (matrix.cpp:69-77; trans_a = 0) and matmul_at (matrix.cpp:79-87; trans_a = 1): out = op(a) b on
+ * the DMMA GEMM; the shape errors of the reference's matmul / matmul_at */
+int rbpg_matmul(rbpg_context* ctx, const double* a, size_t ar, size_t ac, int trans_a, const double* b, size_t br,
+                size_t bc, double* out, rbpg_status* st);
+
 /* ---- device-pointer stage API (torch plumbing, row-sharded multi-GPU)
  * Stage 1 (per shard): G (L x L, ld ldg) and HtT (L x m, ld ldt) of the local rows.  If keep_h,
  * H stays resident in the context for stage 3.  accumulate != 0 adds into G/HtT. */
@@ -180,6 +201,22 @@ int rbpg_gram_device(rbpg_context* ctx, const double* da, size_t lda, size_t row
 int rbpg_pseudo_inverse_stage_device(rbpg_context* ctx, const double* dg, size_t ldg, size_t n_total,
                                      const double* dh, size_t ldh, size_t n_local, size_t l, double tol, double* dout,
                                      size_t ldo, size_t* order, size_t* rank, rbpg_status* st);
+/* Batched predict (elm.cpp:282-284) on device X (n x d): fused sigma(X W + b) beta (H never stored),
+ * optional scores (n x m, ld lds) and/or arg-max labels (int32, strict '>' with the lowest index on
+ * ties, elm.cpp:291-296).  m <= 128 (RBPG_NOT_SUPPORTED otherwise; rbpg_predict handles any m). */
+int rbpg_predict_device(rbpg_context* ctx, const double* dx, size_t ldx, size_t n, size_t d, const double* dw,
+                        size_t ldw, const double* db, size_t l, const double* dbeta, size_t ldb, size_t m,
+                        double* dscores, size_t lds, int* dlabels, rbpg_status* st);
+/* Row-sharded exchange helpers: the all-reduce carries the packed lower triangle of the
+ * (augmented) Gram, n(n+1)/2 doubles (element (i, j <= i) at i(i+1)/2 + j); unpack rebuilds the
+ * exactly symmetric matrix.  sum_parts: out[e] = ((p_0[e] + p_1[e]) + p_2[e]) + ... over nparts
+ * partials stride apart (an all-gather plus this fixed-order sum keeps exact twin ties, C3). */
+int rbpg_pack_lower_device(rbpg_context* ctx, const double* dg, size_t ldg, size_t n, double* dpacked,
+                           rbpg_status* st);
+int rbpg_unpack_lower_device(rbpg_context* ctx, const double* dpacked, size_t n, double* dg, size_t ldg,
+                             rbpg_status* st);
+int rbpg_sum_parts_device(rbpg_context* ctx, const double* dparts, size_t stride, size_t nparts, size_t count,
+                          double* dout, rbpg_status* st);
 /* Whole train() on device-resident X, T (W, b host arrays from init_hidden). */
 int rbpg_train_device(rbpg_context* ctx, const double* dx, size_t ldx, const double* dt, size_t ldt_in, size_t n,
                       size_t d, size_t l, size_t m, const double* w, const double* b, const rbpg_strategy* strategy,

@@ -170,6 +170,9 @@ class SingularSplit : public std::runtime_error {
 HiddenLayer init_hidden(const ElmParams& params);
 DenseMatrix hidden_matrix(const HiddenLayer& hidden, const DenseMatrix& x);
 DenseMatrix solve_direct(const DenseMatrix& h, const DenseMatrix& y, SolveDiagnostics* diag = nullptr);
+std::pair<DenseMatrix, DenseMatrix> solve_block_split(const DenseMatrix& h1, const DenseMatrix& h2,
+                                                      const DenseMatrix& y, double ridge = 1e-8,
+                                                      SolveDiagnostics* diag = nullptr);
 DenseMatrix solve_beta(const DenseMatrix& h, const DenseMatrix& y, const SolverStrategy& strategy,
                        SolveDiagnostics& diag);
 std::pair<ElmModel, SolveDiagnostics> train(const ElmParams& params, const DenseMatrix& x, const DenseMatrix& y,

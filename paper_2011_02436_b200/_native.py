@@ -85,6 +85,18 @@ SIGNATURES = {
                                         P, c_size_t, P, POINTER(rbpg_diagnostics), ST]),
     "rbpg_accuracy_stage_device": (c_int, [P, P, c_size_t, P, c_size_t, c_size_t, c_size_t, c_size_t, c_size_t, P,
                                            c_size_t, P, P, c_size_t, POINTER(c_uint64), ST]),
+    "rbpg_solve_block_split": (c_int, [P, P, c_size_t, c_size_t, P, c_size_t, c_size_t, P, c_size_t, c_size_t,
+                                       c_double, P, P, POINTER(rbpg_diagnostics), ST]),
+    "rbpg_spd_create": (c_int, [P, P, c_size_t, c_size_t, POINTER(c_void_p), ST]),
+    "rbpg_spd_solve": (c_int, [P, P, c_size_t, c_size_t, P, ST]),
+    "rbpg_spd_dim": (c_size_t, [P]),
+    "rbpg_spd_destroy": (None, [P]),
+    "rbpg_matmul": (c_int, [P, P, c_size_t, c_size_t, c_int, P, c_size_t, c_size_t, P, ST]),
+    "rbpg_predict_device": (c_int, [P, P, c_size_t, c_size_t, c_size_t, P, c_size_t, P, c_size_t, P, c_size_t,
+                                    c_size_t, P, c_size_t, P, ST]),
+    "rbpg_pack_lower_device": (c_int, [P, P, c_size_t, c_size_t, P, ST]),
+    "rbpg_unpack_lower_device": (c_int, [P, P, c_size_t, P, c_size_t, ST]),
+    "rbpg_sum_parts_device": (c_int, [P, P, c_size_t, c_size_t, c_size_t, P, ST]),
     "rbpg_train_device": (c_int, [P, P, c_size_t, P, c_size_t, c_size_t, c_size_t, c_size_t, c_size_t, P, P,
                                   POINTER(rbpg_strategy), P, c_size_t, P, POINTER(rbpg_diagnostics), ST]),
 }

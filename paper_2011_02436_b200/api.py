@@ -404,6 +404,83 @@ def solve_spd(m, rhs, ctx: Optional[Context] = None) -> np.ndarray:
     return out
 
 
+class SpdFactor:
+    """linalg.hpp:45-60: Cholesky factor of a symmetric positive definite matrix, computed once on the
+    device (SingularMatrix at construction, as the reference) and reused by every solve()."""
+
+    def __init__(self, m, ctx: Optional[Context] = None):
+        self.ctx = ctx or context()
+        m = _f64(m)
+        h = ctypes.c_void_p()
+        st = rbpg_status()
+        self.ctx.lib.rbpg_spd_create(self.ctx.handle, _ptr(m), m.shape[0], m.shape[1], ctypes.byref(h),
+                                     ctypes.byref(st))
+        _raise(st)
+        self._h = h
+
+    def dim(self) -> int:
+        return int(self.ctx.lib.rbpg_spd_dim(self._h))
+
+    def solve(self, rhs) -> np.ndarray:
+        rhs = _f64(rhs)
+        out = np.empty_like(rhs)
+        st = rbpg_status()
+        self.ctx.lib.rbpg_spd_solve(self._h, _ptr(rhs), rhs.shape[0], rhs.shape[1], _ptr(out), ctypes.byref(st))
+        _raise(st)
+        return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self.ctx.lib.rbpg_spd_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def solve_block_split(h1, h2, y, ridge: float = 1e-8, diag: Optional[SolveDiagnostics] = None,
+                      ctx: Optional[Context] = None) -> Tuple[np.ndarray, np.ndarray]:
+    """elm.cpp:124-156: (beta1, beta2) of the block solve of [H1 H2] against Y (Gram of H2 + Schur
+    complement, one ridge retry per block).  Raises ShapeError / SingularSplit like the reference."""
+    ctx = ctx or context()
+    h1, h2, y = _f64(h1), _f64(h2), _f64(y)
+    b1 = np.empty((h1.shape[1], y.shape[1]))
+    b2 = np.empty((h2.shape[1], y.shape[1]))
+    d = rbpg_diagnostics()
+    st = rbpg_status()
+    ctx.lib.rbpg_solve_block_split(ctx.handle, _ptr(h1), h1.shape[0], h1.shape[1], _ptr(h2), h2.shape[0],
+                                   h2.shape[1], _ptr(y), y.shape[0], y.shape[1], float(ridge), _ptr(b1), _ptr(b2),
+                                   ctypes.byref(d), ctypes.byref(st))
+    _raise(st)
+    if diag is not None and d.ridge_applied:
+        diag.ridge_applied = True
+    return b1, b2
+
+
+def _matmul(a, b, trans_a: bool, ctx: Optional[Context]) -> np.ndarray:
+    ctx = ctx or context()
+    a, b = _f64(a), _f64(b)
+    out = np.empty((a.shape[1] if trans_a else a.shape[0], b.shape[1]))
+    st = rbpg_status()
+    ctx.lib.rbpg_matmul(ctx.handle, _ptr(a), a.shape[0], a.shape[1], int(trans_a), _ptr(b), b.shape[0], b.shape[1],
+                        _ptr(out), ctypes.byref(st))
+    _raise(st)
+    return out
+
+
+def matmul(a, b, ctx: Optional[Context] = None) -> np.ndarray:
+    """matrix.cpp:69-77 on the DMMA GEMM."""
+    return _matmul(a, b, False, ctx)
+
+
+def matmul_at(a, b, ctx: Optional[Context] = None) -> np.ndarray:
+    """matrix.cpp:79-87 (a^T b) on the DMMA GEMM."""
+    return _matmul(a, b, True, ctx)
+
+
 def solve_beta(h, y, strategy: SolverStrategy, diag: Optional[SolveDiagnostics] = None,
                ctx: Optional[Context] = None) -> np.ndarray:
     """elm.cpp:158-229 on a host H."""
@@ -704,3 +781,49 @@ def pseudo_inverse_stage_device(g, h, n_total: int, tol: float = 0.0, ctx: Optio
                                              ctypes.byref(st))
     _raise(st)
     return out[:, :n_local], [int(v) for v in order], int(rank.value)
+
+
+def predict_device(x, w, b, beta, scores=None, labels=None, ctx: Optional[Context] = None) -> None:
+    """Batched predict (elm.cpp:282-284, arg-max rule elm.cpp:291-296) on device tensors: the fused
+    sigma(X W + b) beta kernel writes scores (n x m float64) and/or labels (n int32); H is never stored."""
+    ctx = ctx or context(x.device.index or 0)
+    ctx.set_stream(_torch_stream(x.device))
+    m = beta.shape[1]
+    st = rbpg_status()
+    ctx.lib.rbpg_predict_device(ctx.handle, _tptr(x), _ld(x), x.shape[0], x.shape[1], _tptr(w), _ld(w), _tptr(b),
+                                w.shape[1], _tptr(beta), _ld(beta), m, _tptr(scores) if scores is not None else None,
+                                _ld(scores) if scores is not None else 0,
+                                _tptr(labels) if labels is not None else None, ctypes.byref(st))
+    _raise(st)
+
+
+def predict_labels_device(x, w, b, beta, labels, ctx: Optional[Context] = None) -> None:
+    predict_device(x, w, b, beta, labels=labels, ctx=ctx)
+
+
+def pack_lower_device(g, packed, ctx: Optional[Context] = None) -> None:
+    """packed (n(n+1)/2 float64) <- lower triangle of the square device tensor g (row-major order)."""
+    ctx = ctx or context(g.device.index or 0)
+    ctx.set_stream(_torch_stream(g.device))
+    st = rbpg_status()
+    ctx.lib.rbpg_pack_lower_device(ctx.handle, _tptr(g), _ld(g), g.shape[0], _tptr(packed), ctypes.byref(st))
+    _raise(st)
+
+
+def unpack_lower_device(packed, g, ctx: Optional[Context] = None) -> None:
+    """g (n x n, exactly symmetric) <- the packed lower triangle."""
+    ctx = ctx or context(g.device.index or 0)
+    ctx.set_stream(_torch_stream(g.device))
+    st = rbpg_status()
+    ctx.lib.rbpg_unpack_lower_device(ctx.handle, _tptr(packed), g.shape[0], _tptr(g), _ld(g), ctypes.byref(st))
+    _raise(st)
+
+
+def sum_parts_device(parts, out, ctx: Optional[Context] = None) -> None:
+    """out = ((parts[0] + parts[1]) + parts[2]) + ... (parts: nparts x count, contiguous rows)."""
+    ctx = ctx or context(parts.device.index or 0)
+    ctx.set_stream(_torch_stream(parts.device))
+    st = rbpg_status()
+    ctx.lib.rbpg_sum_parts_device(ctx.handle, _tptr(parts), parts.stride(0), parts.shape[0], parts.shape[1],
+                                  _tptr(out), ctypes.byref(st))
+    _raise(st)

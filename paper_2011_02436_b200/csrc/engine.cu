@@ -87,6 +87,11 @@ cudaError_t launch_transpose(const double*, long long, long long, long long, dou
                              cudaStream_t);
 cudaError_t launch_axpy_rows(const double*, long long, const double*, long long, int, int, double*, long long,
                              cudaStream_t);
+cudaError_t launch_predict(const CUtensorMap&, const CUtensorMap&, const CUtensorMap&, const PredictParams&, cudaStream_t);
+int predict_mp(int m);
+cudaError_t launch_pack_lower(const double*, long long, int, double*, cudaStream_t);
+cudaError_t launch_unpack_lower(const double*, int, double*, long long, cudaStream_t);
+cudaError_t launch_sum_parts(const double*, long long, int, long long, double*, cudaStream_t);
 }  // namespace rbpg
 
 using namespace rbpg;
@@ -128,9 +133,27 @@ struct rbpg_context {
   uint64_t launches = 0;
   EncodeTiledFn encode = nullptr;
   cudaEvent_t ev[8] = {};
-  // H kept resident by the gram stage for the accuracy stage
+  // H kept resident by the gram stage for the accuracy stage, valid only for the exact inputs that
+  // built it (X, W, b pointers and leading dimensions, row and node counts)
   const double* kept_h = nullptr;
   size_t kept_n = 0, kept_l = 0, kept_ldh = 0;
+  struct KeptKey {
+    const double *x = nullptr, *w = nullptr, *b = nullptr;
+    size_t ldx = 0, ldw = 0, d = 0;
+    bool operator==(const KeptKey& o) const {
+      return x == o.x && w == o.w && b == o.b && ldx == o.ldx && ldw == o.ldw && d == o.d;
+    }
+  } kept_key;
+  void keep_h(const double* h, size_t n, size_t l, size_t ldh, const KeptKey& key) {
+    kept_h = h;
+    kept_n = n;
+    kept_l = l;
+    kept_ldh = ldh;
+    kept_key = key;
+  }
+  bool kept_for(const KeptKey& key, size_t n, size_t l) const {
+    return kept_h && kept_n == n && kept_l == l && kept_key == key;
+  }
   size_t h_budget_bytes = size_t(48) << 30;
   // hidden matrix + targets of the current solve when resident (train / solve_beta): the SVD
   // pseudo-inverse branch of solve_direct needs H itself, not only its Gram
@@ -862,7 +885,8 @@ struct SourceScope {
 // Schur block solve (elm.cpp:124-156) on Gram sub-blocks.  ord: device position -> original
 // column; the first `split` positions form H1, the rest H2.  Writes beta in ORIGINAL order.
 void block_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dHtT, size_t ldt, size_t L, size_t m,
-               size_t rows, const int* ord, size_t split, double* dBeta, size_t ldb, rbpg_diagnostics* diag) {
+               size_t rows, const int* ord, size_t split, double* dBeta, size_t ldb, rbpg_diagnostics* diag,
+               double ridge_rel = 1e-8) {
   const size_t n1 = split, n2 = L - split;
   if (rows < L) fail(RBPG_SHAPE_ERROR, "solve_block_split: needs at least as many samples as columns");
   cudaStream_t s = ctx->stream;
@@ -883,13 +907,13 @@ void block_dev(rbpg_context* ctx, const double* dG, size_t ldg, const double* dH
   ctx->run("gather H2tT", [&] { return launch_gather_rows(dHtT, ldt, P2, n2, m, Bm, lm, s); });
   ctx->run("gather H1tT", [&] { return launch_gather_rows(dHtT, ldt, P1, n1, m, R1, lm, s); });
   bool ridge = false;
-  FactorResult fa = spd_with_ridge(ctx, A, l2, n2, 1e-8, ridge, 0, "fa");
+  FactorResult fa = spd_with_ridge(ctx, A, l2, n2, ridge_rel, ridge, 0, "fa");
   trsm_pair_dev(ctx, fa.F, fa.ldF, Bm, lm, n2, m);                                  // B = A^-1 H2^T T
   ck(cudaMemcpy2DAsync(X, l1 * 8, G21, l1 * 8, n1 * 8, n2, cudaMemcpyDeviceToDevice, s), "copy G21");
   trsm_pair_dev(ctx, fa.F, fa.ldF, X, l1, n2, n1);                                  // A^-1 G21
   gemm_dev(ctx, n1, n1, n2, G21, l1, true, X, l1, false, D, l1, -1.0, 1.0);         // D = G11 - G21^T A^-1 G21
   ctx->run("symmetrize", [&] { return launch_symmetrize(D, l1, n1, s); });                          // (D + D^T)/2
-  FactorResult fd = spd_with_ridge(ctx, D, l1, n1, 1e-8, ridge, 1, "fd");
+  FactorResult fd = spd_with_ridge(ctx, D, l1, n1, ridge_rel, ridge, 1, "fd");
   gemm_dev(ctx, n1, m, n2, G21, l1, true, Bm, lm, false, R1, lm, -1.0, 1.0);        // H1^T(T - H2 B)
   trsm_pair_dev(ctx, fd.F, fd.ldF, R1, lm, n1, m);                                  // beta1
   gemm_dev(ctx, n2, m, n1, G21, l1, false, R1, lm, false, T2, lm, 1.0, 0.0);        // G21 beta1
@@ -1066,6 +1090,8 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
   const size_t M = L + m;
   const size_t ldh = even(M);
   const size_t chunk = std::max<size_t>(1, h_chunk_rows(ctx, std::max<size_t>(N, 1), ldh));
+  const rbpg_context::KeptKey key{dX, dW, db, ldx, ldw, d};
+  ctx->kept_h = nullptr;  // the H buffer is rewritten below
   double* dH = ctx->dbuf("H", chunk * ldh);
   float hidden_ms = 0.f;
   if (N == 0) {
@@ -1120,10 +1146,7 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
     gram_parts_launch(ctx, gp, static_cast<int>(cuts.size()), dH, ldh);
     gram_parts_finish(ctx, gp, accumulate);
     if (keep_h) {
-      ctx->kept_h = dH;
-      ctx->kept_n = N;
-      ctx->kept_l = L;
-      ctx->kept_ldh = ldh;
+      ctx->keep_h(dH, N, L, ldh, key);
     } else {
       ctx->kept_h = nullptr;
     }
@@ -1143,10 +1166,7 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
     // quantisation costs more than the hidden upload tail)
     gram_dev(ctx, dH, ldh, N, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate);
     if (keep_h) {
-      ctx->kept_h = dH;
-      ctx->kept_n = N;
-      ctx->kept_l = L;
-      ctx->kept_ldh = ldh;
+      ctx->keep_h(dH, N, L, ldh, key);
     } else {
       ctx->kept_h = nullptr;
     }
@@ -1171,10 +1191,7 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
     gram_dev(ctx, dH, ldh, nr, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate || r0 > 0);
   }
   if (keep_h && chunk >= N) {
-    ctx->kept_h = dH;
-    ctx->kept_n = N;
-    ctx->kept_l = L;
-    ctx->kept_ldh = ldh;
+    ctx->keep_h(dH, N, L, ldh, key);
   } else {
     ctx->kept_h = nullptr;
   }
@@ -1195,6 +1212,25 @@ void scores_dev(rbpg_context* ctx, const double* H, size_t ldh, size_t N, size_t
   ctx->run("scores_kernel", [&] { return launch_scores(tmH, tmB, p, ctx->stream); });
 }
 
+// K6b: fused sigma(X W + b) beta with the arg-max epilogue (m <= 128): optional scores S, labels,
+// and hits += #rows whose arg-max equals argmax(T).  H is never written.
+void predict_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_t d, const double* dW, size_t ldw,
+                 const double* db, size_t L, const double* dBeta, size_t ldb, size_t m, double* S, size_t lds,
+                 int* labels, const double* T, size_t ldt, unsigned long long* hits) {
+  if (N == 0) return;
+  const int mp = predict_mp(static_cast<int>(m));
+  if (mp == 0) fail(RBPG_INVALID_ARGUMENT, "predict_dev: more than 128 classes");
+  Padded X = pad_device(ctx, "pred.x", dX, ldx, N, d);
+  Padded W = pad_device(ctx, "pred.w", dW, ldw, d, L);
+  Padded B = pad_device(ctx, "beta.pad", dBeta, ldb, L, m);
+  CUtensorMap tmX = make_map(ctx, X.p, d, N, X.ld, 16, kTile, true);
+  CUtensorMap tmW = make_map(ctx, W.p, L, d, W.ld, 36, kBK, false);
+  CUtensorMap tmB = make_map(ctx, B.p, m, L, B.ld, static_cast<uint32_t>(mp + 4), 32, false);
+  PredictParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), static_cast<int>(m), db,
+                  S, static_cast<long long>(lds), labels, T, static_cast<long long>(ldt), hits};
+  ctx->run("predict_kernel", [&] { return launch_predict(tmX, tmW, tmB, p, ctx->stream); });
+}
+
 uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* dT, size_t ldt_in, size_t N,
                         size_t d, size_t L, size_t m, const double* dW, size_t ldw, const double* db,
                         const double* dBeta, size_t ldb, unsigned long long** deferred = nullptr) {
@@ -1202,29 +1238,34 @@ uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const d
   ck(cudaMemsetAsync(hits, 0, 8, ctx->stream), "memset hits");
   if (N > 0) {
     const size_t ldh = even(L);
-    const bool kept = ctx->kept_h && ctx->kept_n == N && ctx->kept_l == L;
-    const size_t chunk = kept ? N : h_chunk_rows(ctx, N, ldh);
-    const size_t lm = even(m);
-    double* S = ctx->dbuf("scores", chunk * lm);
-    for (size_t r0 = 0; r0 < N; r0 += chunk) {
-      const size_t nr = std::min(chunk, N - r0);
-      const double* H = ctx->kept_h;
-      size_t hld = ctx->kept_ldh;
-      if (!kept) {
-        double* dH = ctx->dbuf("H", chunk * ldh);
-        hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh);
-        H = dH;
-        hld = ldh;
-      }
-      if (m <= 128) {  // K6: skinny DMMA GEMM with the fused arg-max / hit count, scores never stored
-        scores_dev(ctx, H, hld, nr, L, dBeta, ldb, m, nullptr, 0, dT + r0 * ldt_in, ldt_in, hits);
-      } else {
-        gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(L), H, hld, false, dBeta, ldb,
-                 false, S, lm, 1.0, 0.0);
-        ctx->run("accuracy", [&] {
-          return launch_accuracy(S, static_cast<long long>(lm), dT + r0 * ldt_in, static_cast<long long>(ldt_in),
-                                 static_cast<long long>(nr), static_cast<int>(m), hits, ctx->num_sms, ctx->stream);
-        });
+    const bool kept = ctx->kept_for(rbpg_context::KeptKey{dX, dW, db, ldx, ldw, d}, N, L);
+    if (!kept && m <= 128) {  // no resident H for these inputs: the fused predict kernel recomputes it
+      predict_dev(ctx, dX, ldx, N, d, dW, ldw, db, L, dBeta, ldb, m, nullptr, 0, nullptr, dT, ldt_in, hits);
+    } else {
+      if (!kept) ctx->kept_h = nullptr;  // the H buffer is rebuilt from these inputs below
+      const size_t chunk = kept ? N : h_chunk_rows(ctx, N, ldh);
+      const size_t lm = even(m);
+      double* S = ctx->dbuf("scores", chunk * lm);
+      for (size_t r0 = 0; r0 < N; r0 += chunk) {
+        const size_t nr = std::min(chunk, N - r0);
+        const double* H = ctx->kept_h;
+        size_t hld = ctx->kept_ldh;
+        if (!kept) {
+          double* dH = ctx->dbuf("H", chunk * ldh);
+          hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh);
+          H = dH;
+          hld = ldh;
+        }
+        if (m <= 128) {  // K6: skinny DMMA GEMM with the fused arg-max / hit count, scores never stored
+          scores_dev(ctx, H, hld, nr, L, dBeta, ldb, m, nullptr, 0, dT + r0 * ldt_in, ldt_in, hits);
+        } else {
+          gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(L), H, hld, false, dBeta, ldb,
+                   false, S, lm, 1.0, 0.0);
+          ctx->run("accuracy", [&] {
+            return launch_accuracy(S, static_cast<long long>(lm), dT + r0 * ldt_in, static_cast<long long>(ldt_in),
+                                   static_cast<long long>(nr), static_cast<int>(m), hits, ctx->num_sms, ctx->stream);
+          });
+        }
       }
     }
   }
@@ -1263,7 +1304,7 @@ void train_core(rbpg_context* ctx, const double* dX, size_t ldx, const double* d
   float hidden_ms = gram_stage(ctx, X.p, X.ld, T.p, T.ld, N, d, L, m, W.p, W.ld, db, G, ldg, false, true, true, ready);
   {
     // [H T] stays resident (unless H exceeded the memory budget) for solve_direct's SVD branch
-    const bool kept = ctx->kept_h && ctx->kept_n == N;
+    const bool kept = ctx->kept_for(rbpg_context::KeptKey{X.p, W.p, db, X.ld, W.ld, d}, N, L);
     SourceScope src(ctx, kept ? ctx->kept_h : nullptr, ctx->kept_ldh, kept ? ctx->kept_h + L : nullptr,
                     ctx->kept_ldh, kept ? N : 0);
     // finiteness check and accuracy pass enqueued behind the (speculative) solve: one
@@ -1431,8 +1472,10 @@ void rbpg_context_destroy(rbpg_context* ctx) {
   for (auto& e : ctx->ev) cudaEventDestroy(e);
   for (auto& e : ctx->chunk_ev) cudaEventDestroy(e);
   for (auto& e : ctx->aux_ev) cudaEventDestroy(e);
+  cudaStreamSynchronize(ctx->aux);
   cudaStreamDestroy(ctx->own);
   cudaStreamDestroy(ctx->copy);
+  cudaStreamDestroy(ctx->aux);
   delete ctx;
 }
 
@@ -1719,21 +1762,177 @@ int rbpg_predict(rbpg_context* ctx, const double* w, const double* b, size_t d, 
     Padded Bt = upload(ctx, "beta.in", beta, l, m);
     double* db = ctx->dbuf("b", l);
     ck(cudaMemcpyAsync(db, b, l * 8, cudaMemcpyHostToDevice, ctx->stream), "upload b");
-    const size_t ldh = even(l), lm = even(m);
-    const size_t chunk = h_chunk_rows(ctx, std::max<size_t>(n, 1), ldh);
-    double* H = ctx->dbuf("H", chunk * ldh);
-    ctx->kept_h = nullptr;
+    const size_t lm = even(m);
     double* S = ctx->dbuf("scores", std::max<size_t>(n, 1) * lm);
-    for (size_t r0 = 0; r0 < n; r0 += chunk) {
-      const size_t nr = std::min(chunk, n - r0);
-      hidden_dev(ctx, X.p + r0 * X.ld, X.ld, nr, d, W.p, W.ld, db, l, H, ldh);
-      if (m <= 128)
-        scores_dev(ctx, H, ldh, nr, l, Bt.p, Bt.ld, m, S + r0 * lm, lm, nullptr, 0, nullptr);
-      else
+    if (m <= 128) {  // K6b: fused, H never stored
+      predict_dev(ctx, X.p, X.ld, n, d, W.p, W.ld, db, l, Bt.p, Bt.ld, m, S, lm, nullptr, nullptr, 0, nullptr);
+    } else {  // K1 into row chunks of H, then the DMMA GEMM
+      const size_t ldh = even(l);
+      const size_t chunk = h_chunk_rows(ctx, std::max<size_t>(n, 1), ldh);
+      double* H = ctx->dbuf("H", chunk * ldh);
+      ctx->kept_h = nullptr;
+      for (size_t r0 = 0; r0 < n; r0 += chunk) {
+        const size_t nr = std::min(chunk, n - r0);
+        hidden_dev(ctx, X.p + r0 * X.ld, X.ld, nr, d, W.p, W.ld, db, l, H, ldh);
         gemm_dev(ctx, static_cast<int>(nr), static_cast<int>(m), static_cast<int>(l), H, ldh, false, Bt.p, Bt.ld,
                  false, S + r0 * lm, lm, 1.0, 0.0);
+      }
     }
     download(ctx, scores, S, lm, n, m);
+  });
+}
+
+int rbpg_predict_device(rbpg_context* ctx, const double* dx, size_t ldx, size_t n, size_t d, const double* dw,
+                        size_t ldw, const double* db, size_t l, const double* dbeta, size_t ldb, size_t m,
+                        double* dscores, size_t lds, int* dlabels, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (m > 128) fail(RBPG_NOT_SUPPORTED, "predict_device: at most 128 classes (use rbpg_predict)");
+    if (n == 0 || l == 0 || m == 0) return;
+    predict_dev(ctx, dx, ldx, n, d, dw, ldw, db, l, dbeta, ldb, m, dscores, lds, dlabels, nullptr, 0, nullptr);
+  });
+}
+
+int rbpg_solve_block_split(rbpg_context* ctx, const double* h1, size_t n, size_t c1, const double* h2, size_t n2,
+                           size_t c2, const double* y, size_t yrows, size_t m, double ridge, double* beta1,
+                           double* beta2, rbpg_diagnostics* diag, rbpg_status* st) {
+  rbpg_diagnostics local;
+  if (!diag) diag = &local;
+  zero_diag(diag);
+  return guarded(ctx, st, [&] {
+    if (n2 != n || yrows != n)  // elm.cpp:128-131
+      fail(RBPG_SHAPE_ERROR, "solve_block_split: row counts differ (" + shp(n, c1) + ", " + shp(n2, c2) + ", " +
+                                 shp(yrows, m) + ")");
+    if (n < c1 + c2) fail(RBPG_SHAPE_ERROR, "solve_block_split: needs at least as many samples as columns");
+    if (c1 == 0 || c2 == 0 || m == 0) fail(RBPG_SHAPE_ERROR, "solve_block_split: empty block");
+    // [H1 H2 Y] in one buffer: one SYRK gives every Gram block the Schur solve needs
+    const size_t L = c1 + c2, lda = even(L + m);
+    double* A = ctx->dbuf("A.in", n * lda);
+    ck(cudaMemcpy2DAsync(A, lda * 8, h1, c1 * 8, c1 * 8, n, cudaMemcpyHostToDevice, ctx->stream), "upload H1");
+    ck(cudaMemcpy2DAsync(A + c1, lda * 8, h2, c2 * 8, c2 * 8, n, cudaMemcpyHostToDevice, ctx->stream), "upload H2");
+    ck(cudaMemcpy2DAsync(A + L, lda * 8, y, m * 8, m * 8, n, cudaMemcpyHostToDevice, ctx->stream), "upload Y");
+    const size_t ldg = round_up(L + m, 8), lb = even(m);
+    double* G = ctx->dbuf("G0", (L + m) * ldg);
+    gram_dev(ctx, A, lda, n, L + m, nullptr, 0, 0, G, ldg, nullptr, 0, false);
+    std::vector<int> id(L);
+    for (size_t i = 0; i < L; ++i) id[i] = static_cast<int>(i);
+    int* dord = static_cast<int*>(ctx->buf("bs.ord", L * 4));
+    ck(cudaMemcpyAsync(dord, id.data(), L * 4, cudaMemcpyHostToDevice, ctx->stream), "upload identity");
+    double* B = ctx->dbuf("beta", L * lb);
+    block_dev(ctx, G, ldg, G + L, ldg, L, m, n, dord, c1, B, lb, diag, ridge);
+    download(ctx, beta1, B, lb, c1, m);
+    download(ctx, beta2, B + c1 * lb, lb, c2, m);
+  });
+}
+
+// SpdFactor (linalg.cpp:99-151) kept on the device: factor once, solve many right-hand sides
+struct rbpg_spd {
+  rbpg_context* ctx;
+  double* F = nullptr;  // lower factor (n x ldF), owned
+  size_t n = 0, ldF = 0;
+};
+
+int rbpg_spd_create(rbpg_context* ctx, const double* mat, size_t mrows, size_t mcols, rbpg_spd** out,
+                    rbpg_status* st) {
+  *out = nullptr;
+  return guarded(ctx, st, [&] {
+    if (mrows != mcols) fail(RBPG_SHAPE_ERROR, "solve_spd: matrix is not square, " + shp(mrows, mcols));
+    const size_t n = mrows;
+    double scale = 0.0, asym = 0.0;  // linalg.cpp:104-107 (host validation)
+    for (size_t i = 0; i < n * n; ++i) scale = std::max(scale, std::fabs(mat[i]));
+    for (size_t i = 0; i < n; ++i)
+      for (size_t j = 0; j < n; ++j) asym = std::max(asym, std::fabs(mat[i * n + j] - mat[j * n + i]));
+    if (asym > 1e-12 * std::max(scale, 1.0))
+      fail(RBPG_INVALID_ARGUMENT, "solve_spd: matrix is not symmetric within 1e-12 relative");
+    Padded M = upload(ctx, "M.in", mat, n, n);
+    FactorResult f = factor_dev(ctx, M.p, M.ld, n, n, 0.0, 0, "spd");
+    if (f.st.fail) {
+      Fail e{RBPG_SINGULAR_MATRIX, "non-positive pivot " + std::to_string(f.st.fail_value) + " at index " +
+                                       std::to_string(f.st.fail_index) + " in symmetric factorization"};
+      e.pivot_index = static_cast<size_t>(f.st.fail_index);
+      e.pivot_value = f.st.fail_value;
+      throw e;
+    }
+    auto* h = new rbpg_spd{ctx};
+    h->n = n;
+    h->ldF = f.ldF;
+    if (cudaMalloc(&h->F, sizeof(double) * std::max<size_t>(1, n * f.ldF)) != cudaSuccess) {
+      delete h;
+      fail(RBPG_CUDA_ERROR, "cudaMalloc SpdFactor");
+    }
+    ck(cudaMemcpyAsync(h->F, f.F, sizeof(double) * n * f.ldF, cudaMemcpyDeviceToDevice, ctx->stream), "copy F");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    *out = h;
+  });
+}
+
+int rbpg_spd_solve(const rbpg_spd* f, const double* rhs, size_t rrows, size_t rcols, double* out, rbpg_status* st) {
+  return guarded(f->ctx, st, [&] {
+    if (rrows != f->n)
+      fail(RBPG_SHAPE_ERROR, "solve_spd: rhs has " + std::to_string(rrows) + " rows, expected " + std::to_string(f->n));
+    if (rcols == 0) return;
+    Padded X = upload(f->ctx, "rhs.in", rhs, f->n, rcols);
+    trsm_pair_dev(f->ctx, f->F, f->ldF, const_cast<double*>(X.p), X.ld, f->n, rcols);
+    download(f->ctx, out, X.p, X.ld, f->n, rcols);
+  });
+}
+
+size_t rbpg_spd_dim(const rbpg_spd* f) { return f ? f->n : 0; }
+
+void rbpg_spd_destroy(rbpg_spd* f) {
+  if (!f) return;
+  cudaSetDevice(f->ctx->device);
+  cudaStreamSynchronize(f->ctx->stream);
+  cudaFree(f->F);
+  delete f;
+}
+
+// matmul (matrix.cpp:69-77) / matmul_at (matrix.cpp:79-87) on the DMMA GEMM
+int rbpg_matmul(rbpg_context* ctx, const double* a, size_t ar, size_t ac, int trans_a, const double* b, size_t br,
+                size_t bc, double* out, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    const size_t M = trans_a ? ac : ar, K = trans_a ? ar : ac;
+    if (K != br) {
+      if (trans_a)
+        fail(RBPG_SHAPE_ERROR, "matmul_at: row counts differ, " + shp(ar, ac) + "^T times " + shp(br, bc));
+      fail(RBPG_SHAPE_ERROR, "matmul: inner dimensions differ, " + shp(ar, ac) + " times " + shp(br, bc));
+    }
+    if (M == 0 || bc == 0) return;
+    Padded A = upload(ctx, "mm.a", a, ar, ac);
+    Padded B = upload(ctx, "mm.b", b, br, bc);
+    const size_t ldc = even(bc);
+    double* C = ctx->dbuf("mm.c", M * ldc);
+    gemm_dev(ctx, static_cast<int>(M), static_cast<int>(bc), static_cast<int>(K), A.p, A.ld, trans_a != 0, B.p, B.ld,
+             false, C, ldc, 1.0, 0.0);
+    download(ctx, out, C, ldc, M, bc);
+  });
+}
+
+int rbpg_pack_lower_device(rbpg_context* ctx, const double* dg, size_t ldg, size_t n, double* dpacked,
+                           rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    ctx->run("pack_lower", [&] {
+      return launch_pack_lower(dg, static_cast<long long>(ldg), static_cast<int>(n), dpacked, ctx->stream);
+    });
+  });
+}
+
+int rbpg_unpack_lower_device(rbpg_context* ctx, const double* dpacked, size_t n, double* dg, size_t ldg,
+                             rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    ctx->run("unpack_lower", [&] {
+      return launch_unpack_lower(dpacked, static_cast<int>(n), dg, static_cast<long long>(ldg), ctx->stream);
+    });
+  });
+}
+
+int rbpg_sum_parts_device(rbpg_context* ctx, const double* dparts, size_t stride, size_t nparts, size_t count,
+                          double* dout, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (nparts == 0) fail(RBPG_INVALID_ARGUMENT, "sum_parts: no parts");
+    ctx->run("sum_parts", [&] {
+      return launch_sum_parts(dparts, static_cast<long long>(stride), static_cast<int>(nparts),
+                              static_cast<long long>(count), dout, ctx->stream);
+    });
   });
 }
 

@@ -259,3 +259,75 @@ cudaError_t launch_add_block(double* out, long long ldo, const double* in, long 
   return cudaGetLastError();
 }
 }  // namespace rbpg
+
+// ---------------------------------------------------------------------------
+// Row-sharded exchange helpers: the all-reduce moves the packed lower triangle of the
+// (augmented) Gram, n(n+1)/2 doubles, instead of the full n x n buffer.
+// ---------------------------------------------------------------------------
+namespace rbpg {
+// packed[i(i+1)/2 + j] = G[i][j], j <= i; one CTA per row (coalesced on both sides)
+__global__ void pack_lower_kernel(const double* G, long long ldg, int n, double* packed) {
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const double* gr = G + (long long)i * ldg;
+    double* pr = packed + (long long)i * (i + 1) / 2;
+    for (int j = threadIdx.x; j <= i; j += blockDim.x) pr[j] = gr[j];
+  }
+}
+// G[i][j] = G[j][i] = packed[i(i+1)/2 + j]: one CTA per 32 x 32 block of the lower triangle, the
+// mirrored block written as a transpose through shared memory (coalesced rows both ways)
+__global__ void __launch_bounds__(256) unpack_lower_kernel(const double* packed, int n, double* G, long long ldg) {
+  __shared__ double blk[32][33];
+  const int nb = (n + 31) / 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (long long b = blockIdx.x; b < (long long)nb * (nb + 1) / 2; b += gridDim.x) {
+    int bi = static_cast<int>((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+    while ((long long)bi * (bi + 1) / 2 > b) --bi;
+    while ((long long)(bi + 1) * (bi + 2) / 2 <= b) ++bi;
+    const int bj = static_cast<int>(b - (long long)bi * (bi + 1) / 2);
+    const int i0 = bi * 32, j0 = bj * 32;
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+      const int i = i0 + r, j = j0 + tx;
+      double v = 0.0;
+      if (i < n && j <= i) {
+        v = packed[(long long)i * (i + 1) / 2 + j];
+        G[(long long)i * ldg + j] = v;
+      }
+      blk[r][tx] = v;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {  // G[j0 + r][i0 + tx] = blk[tx][r] (strictly upper part)
+      const int j = j0 + r, i = i0 + tx;
+      if (i < n && j < n && j < i) G[(long long)j * ldg + i] = blk[tx][r];
+    }
+  }
+}
+// out[e] = ((parts[0][e] + parts[1][e]) + parts[2][e]) + ... : a fixed-order sum of row-shard partials
+// (all-gathered), so the reduction order -- and exact ties between twin Gram columns -- does not
+// depend on the collective's internal order
+__global__ void sum_parts_kernel(const double* parts, long long stride, int nparts, long long count, double* out) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < count;
+       e += (long long)gridDim.x * blockDim.x) {
+    double v = parts[e];
+    for (int p = 1; p < nparts; ++p) v = add_rn(v, parts[p * stride + e]);
+    out[e] = v;
+  }
+}
+cudaError_t launch_pack_lower(const double* G, long long ldg, int n, double* packed, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  pack_lower_kernel<<<n < 4096 ? n : 4096, 256, 0, s>>>(G, ldg, n, packed);
+  return cudaGetLastError();
+}
+cudaError_t launch_unpack_lower(const double* packed, int n, double* G, long long ldg, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const long long nb = (n + 31) / 32, blocks = nb * (nb + 1) / 2;
+  unpack_lower_kernel<<<static_cast<unsigned>(blocks < 65535 ? blocks : 65535), 256, 0, s>>>(packed, n, G, ldg);
+  return cudaGetLastError();
+}
+cudaError_t launch_sum_parts(const double* parts, long long stride, int nparts, long long count, double* out,
+                             cudaStream_t s) {
+  if (count <= 0) return cudaSuccess;
+  sum_parts_kernel<<<1184, 256, 0, s>>>(parts, stride, nparts, count, out);
+  return cudaGetLastError();
+}
+}  // namespace rbpg

@@ -82,6 +82,16 @@ struct ScoresParams {
   unsigned long long* hits;
 };
 
+// ---- K6b: fused predict, scores = sigmoid(X W + b) beta with the arg-max epilogue (k_predict.cu)
+struct PredictParams {
+  int N, d, L, m;
+  const double* bias;
+  double* S; long long lds;            // optional scores (N x m)
+  int* labels;                         // optional arg-max labels (N)
+  const double* T; long long ldt;      // optional one-hot targets for the hit count
+  unsigned long long* hits;
+};
+
 // ---- K3: pivoted-Cholesky panel (reference linalg.cpp:186-247)
 struct FactorState {
   int rank;          // L until the stop rule fires

@@ -102,11 +102,21 @@ bool DenseMatrix::all_finite() const {
 }
 std::string DenseMatrix::shape_str() const { return std::to_string(r_) + "x" + std::to_string(c_); }
 
-// Host utilities of the dense-matrix layer (not on the training path).
+// Dense products: host loops for small operands, the DMMA GEMM above kDeviceFlops (the reference's
+// acceptance test predicts through matmul(hidden_matrix(...), beta), acceptance.cpp:152-153).
+namespace {
+constexpr double kDeviceFlops = 2e6;
+}
 DenseMatrix matmul(const DenseMatrix& a, const DenseMatrix& b) {
   if (a.cols() != b.rows())
     throw ShapeError("matmul: inner dimensions differ, " + a.shape_str() + " times " + b.shape_str());
   DenseMatrix o(a.rows(), b.cols(), 0.0);
+  if (2.0 * a.rows() * a.cols() * b.cols() >= kDeviceFlops) {
+    rbpg_status st;
+    rbpg_matmul(ctx(), a.data(), a.rows(), a.cols(), 0, b.data(), b.rows(), b.cols(), o.data(), &st);
+    raise(st);
+    return o;
+  }
   for (std::size_t i = 0; i < a.rows(); ++i)
     for (std::size_t k = 0; k < a.cols(); ++k) {
       const double s = a(i, k);
@@ -118,6 +128,12 @@ DenseMatrix matmul_at(const DenseMatrix& a, const DenseMatrix& b) {
   if (a.rows() != b.rows())
     throw ShapeError("matmul_at: row counts differ, " + a.shape_str() + "^T times " + b.shape_str());
   DenseMatrix o(a.cols(), b.cols(), 0.0);
+  if (2.0 * a.rows() * a.cols() * b.cols() >= kDeviceFlops) {
+    rbpg_status st;
+    rbpg_matmul(ctx(), a.data(), a.rows(), a.cols(), 1, b.data(), b.rows(), b.cols(), o.data(), &st);
+    raise(st);
+    return o;
+  }
   for (std::size_t n = 0; n < a.rows(); ++n)
     for (std::size_t i = 0; i < a.cols(); ++i) {
       const double s = a(n, i);
@@ -226,28 +242,27 @@ DenseMatrix invert_permutation_rows(const DenseMatrix& b, const ColumnPermutatio
   return o;
 }
 
+// The factor lives on the device (rbpg_spd): factored once at construction -- SingularMatrix is
+// raised there, as by the reference constructor (linalg.cpp:99-139) -- and reused by every solve.
 struct SpdFactor::Impl {
-  DenseMatrix m;
+  rbpg_spd* f = nullptr;
+  ~Impl() { rbpg_spd_destroy(f); }
 };
-SpdFactor::SpdFactor(const DenseMatrix& m) : impl_(new Impl{m}) {
-  // factor once now so a singular matrix raises at construction, as the reference does
-  DenseMatrix probe(m.rows(), 1, 0.0), out(m.rows(), 1, 0.0);
+SpdFactor::SpdFactor(const DenseMatrix& m) : impl_(new Impl) {
   rbpg_status st;
-  rbpg_solve_spd(ctx(), m.data(), m.rows(), m.cols(), probe.data(), probe.rows(), 1, out.data(), &st);
+  rbpg_spd_create(ctx(), m.data(), m.rows(), m.cols(), &impl_->f, &st);
   raise(st);
 }
 SpdFactor::~SpdFactor() = default;
 SpdFactor::SpdFactor(SpdFactor&&) noexcept = default;
 SpdFactor& SpdFactor::operator=(SpdFactor&&) noexcept = default;
-std::size_t SpdFactor::dim() const { return impl_->m.rows(); }
+std::size_t SpdFactor::dim() const { return rbpg_spd_dim(impl_->f); }
 DenseMatrix SpdFactor::solve(const DenseMatrix& rhs) const {
-  if (rhs.rows() != impl_->m.rows())
-    throw ShapeError("solve_spd: rhs has " + std::to_string(rhs.rows()) + " rows, expected " +
-                     std::to_string(impl_->m.rows()));
+  if (rhs.rows() != dim())
+    throw ShapeError("solve_spd: rhs has " + std::to_string(rhs.rows()) + " rows, expected " + std::to_string(dim()));
   DenseMatrix out(rhs.rows(), rhs.cols(), 0.0);
   rbpg_status st;
-  rbpg_solve_spd(ctx(), impl_->m.data(), impl_->m.rows(), impl_->m.cols(), rhs.data(), rhs.rows(), rhs.cols(),
-                 out.data(), &st);
+  rbpg_spd_solve(impl_->f, rhs.data(), rhs.rows(), rhs.cols(), out.data(), &st);
   raise(st);
   return out;
 }
@@ -359,6 +374,19 @@ DenseMatrix solve_beta(const DenseMatrix& h, const DenseMatrix& y, const SolverS
   diag.training_accuracy = keep_acc;
   diag.solve_seconds = diag.hidden_seconds = 0.0;
   return beta;
+}
+
+std::pair<DenseMatrix, DenseMatrix> solve_block_split(const DenseMatrix& h1, const DenseMatrix& h2,
+                                                      const DenseMatrix& y, double ridge, SolveDiagnostics* diag) {
+  DenseMatrix b1(std::max<std::size_t>(h1.cols(), 1), std::max<std::size_t>(y.cols(), 1), 0.0);
+  DenseMatrix b2(std::max<std::size_t>(h2.cols(), 1), std::max<std::size_t>(y.cols(), 1), 0.0);
+  rbpg_diagnostics d;
+  rbpg_status st;
+  rbpg_solve_block_split(ctx(), h1.data(), h1.rows(), h1.cols(), h2.data(), h2.rows(), h2.cols(), y.data(), y.rows(),
+                         y.cols(), ridge, b1.data(), b2.data(), &d, &st);
+  raise(st);
+  if (diag && d.ridge_applied) diag->ridge_applied = true;
+  return {std::move(b1), std::move(b2)};
 }
 
 DenseMatrix solve_direct(const DenseMatrix& h, const DenseMatrix& y, SolveDiagnostics* diag) {

@@ -2,10 +2,16 @@
 
 The hot path shards naturally by rows: each rank builds H for its
 contiguous block of rows and its local augmented Gram [H_p T_p]^T [H_p T_p]
-((L+m) x (L+m): G_p and (H^T T)_p in one buffer); ONE all-reduce (sum); every
-rank then runs the identical pivoted-Cholesky + triangular solve, so beta is
-bitwise identical on all ranks; training-accuracy hits are a local count plus an
-all-reduce.
+((L+m) x (L+m): G_p and (H^T T)_p in one buffer); ONE all-reduce (sum) of its packed
+lower triangle ((L+m)(L+m+1)/2 doubles: G and H^T T, half the bytes of the full
+buffer); every rank then runs the identical pivoted-Cholesky + triangular solve, so
+beta is bitwise identical on all ranks; training-accuracy hits are a local count
+plus an all-reduce.
+
+``fixed_order=True`` replaces the all-reduce by an all-gather of the packed partials
+and a sum in rank order on every rank: the Gram then no longer depends on the
+collective's internal reduction order, so exact ties between duplicated hidden
+nodes (config 3) survive sharding.
 
 ``train_sharded`` is the orchestration; the per-rank numerical stages are a
 pluggable object.  ``DeviceStages`` (the product) runs them through the C ABI on
@@ -33,6 +39,22 @@ class DeviceStages:
 
     def __init__(self, ctx: Optional[api.Context] = None):
         self.ctx = ctx
+        self._packed = None
+
+    def pack(self, g):
+        import torch
+
+        n = g.shape[0]
+        if self._packed is None or self._packed.numel() != n * (n + 1) // 2 or self._packed.device != g.device:
+            self._packed = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device=g.device)
+        api.pack_lower_device(g, self._packed, ctx=self.ctx)
+        return self._packed
+
+    def unpack(self, packed, g) -> None:
+        api.unpack_lower_device(packed, g, ctx=self.ctx)
+
+    def sum_parts(self, parts, out) -> None:
+        api.sum_parts_device(parts, out, ctx=self.ctx)
 
     def gram_aug(self, x, t, w, b):
         import torch
@@ -64,8 +86,33 @@ class DeviceStages:
         return api.pseudo_inverse_stage_device(g, h, n_total, tol, ctx=self.ctx)
 
 
+def _host_staged(t, group) -> bool:
+    import torch.distributed as dist
+
+    return t.is_cuda and dist.get_backend(group) != "nccl"
+
+
+def exchange_gram(gaug, stages, group=None, fixed_order: bool = False) -> None:
+    """The path's one exchange step, in place on gaug (square, symmetric): pack the lower triangle,
+    all-reduce it (or all-gather + fixed-order sum), unpack to the summed symmetric Gram."""
+    import torch
+    import torch.distributed as dist
+
+    packed = stages.pack(gaug)
+    if _host_staged(packed, group):
+        torch.cuda.synchronize(packed.device)  # host-staged backends (gloo) do not order against the stream
+    if fixed_order:
+        world = dist.get_world_size(group)
+        parts = torch.empty((world, packed.numel()), dtype=packed.dtype, device=packed.device)
+        dist.all_gather(list(parts.unbind(0)), packed, group=group)
+        stages.sum_parts(parts, packed)
+    else:
+        dist.all_reduce(packed, group=group)
+    stages.unpack(packed, gaug)
+
+
 def train_sharded(x_local, t_local, params: api.ElmParams, strategy: api.SolverStrategy, n_total: int,
-                  stages=None, group=None, hidden: Optional[api.HiddenLayer] = None):
+                  stages=None, group=None, hidden: Optional[api.HiddenLayer] = None, fixed_order: bool = False):
     """Row-sharded train(): returns (beta, SolveDiagnostics, HiddenLayer, order).
 
     x_local / t_local are this rank's contiguous row block (``shard_rows``) as tensors on the
@@ -81,9 +128,7 @@ def train_sharded(x_local, t_local, params: api.ElmParams, strategy: api.SolverS
     gaug = stages.gram_aug(x_local, t_local, w, b)
     distributed = dist.is_available() and dist.is_initialized()
     if distributed:
-        if gaug.is_cuda and dist.get_backend(group) != "nccl":
-            torch.cuda.synchronize(gaug.device)  # host-staged backends (gloo) do not order against the stream
-        dist.all_reduce(gaug, group=group)  # the one exchange step of the path
+        exchange_gram(gaug, stages, group, fixed_order)  # the one exchange step of the path
     L, m = w.shape[1], t_local.shape[1]
     beta, diag, order = stages.solve_aug(gaug, L, m, n_total, strategy)
     hits = torch.tensor([stages.hits(x_local, t_local, w, b, beta)], dtype=torch.int64, device=gaug.device)
@@ -96,7 +141,7 @@ def train_sharded(x_local, t_local, params: api.ElmParams, strategy: api.SolverS
 
 
 def train_shard_device(x_local, t_local, w, b, params: api.ElmParams, strategy: api.SolverStrategy, n_total: int,
-                       stages: Optional[DeviceStages] = None, group=None):
+                       stages: Optional[DeviceStages] = None, group=None, fixed_order: bool = False):
     """train() step of one rank on device-resident inputs (bench.py's timed step at N > 1): local
     augmented Gram, ONE all-reduce, replicated solve, hit-count all-reduce.  w, b are the
     replicated hidden layer as device tensors.  Returns (beta, SolveDiagnostics, order)."""
@@ -105,13 +150,11 @@ def train_shard_device(x_local, t_local, w, b, params: api.ElmParams, strategy: 
 
     stages = stages or DeviceStages()
     gaug = stages.gram_aug(x_local, t_local, w, b)
-    if dist.get_backend(group) != "nccl":
-        torch.cuda.synchronize(gaug.device)
-    dist.all_reduce(gaug, group=group)
+    exchange_gram(gaug, stages, group, fixed_order)
     L, m = w.shape[1], t_local.shape[1]
     beta, diag, order = stages.solve_aug(gaug, L, m, n_total, strategy)
     hits = torch.tensor([stages.hits(x_local, t_local, w, b, beta)], dtype=torch.int64, device=gaug.device)
-    if dist.get_backend(group) != "nccl":
+    if _host_staged(hits, group):
         torch.cuda.synchronize(hits.device)
     dist.all_reduce(hits, group=group)
     diag.training_accuracy = float(hits.item()) / float(n_total)
