@@ -8,6 +8,9 @@
 // rbpelm::b200::set_device); status records are rethrown as the reference's
 // exceptions.  pinv_svd runs the device block one-sided Jacobi SVD (the same SVD
 // serves solve_direct's pseudo-inverse branch) -- see INTEGRATION.md.
+//
+// Reference callers include "rbpelm/matrix.hpp", "rbpelm/elm.hpp", ... : the forwarding headers in
+// include/rbpelm/ map each of them onto this file, so they compile unedited with -I include.
 #pragma once
 
 #include <cstddef>
@@ -272,6 +275,29 @@ void emit_report(const BenchmarkReport& report, const std::string& format, const
 std::vector<std::string> emit_plot_data(const BenchmarkReport& report, const std::string& path_prefix);
 std::string report_to_json(const BenchmarkReport& report);
 BenchmarkReport report_from_json(const std::string& text);
+
+// ---- checks.hpp (test-scale algebra cross-checks; reference checks.hpp:12-41) ----------
+/// C = I - H2 (H2^T H2)^{-1} H2^T (N x N): the projector the production block solve never forms.
+DenseMatrix materialize_projector(const DenseMatrix& h2);
+/// D = H1^T C H1 through the explicit projector.
+DenseMatrix materialize_schur(const DenseMatrix& h1, const DenseMatrix& h2);
+/// Beta from the explicitly assembled 2 x 2 block inverse of [H1 H2]^T [H1 H2], applied to
+/// [H1^T Y; H2^T Y] (L x m, [H1 H2] column order).
+DenseMatrix u_block_beta(const DenseMatrix& h1, const DenseMatrix& h2, const DenseMatrix& y);
+
+struct PropertyResult {
+  std::string name;
+  double max_error = 0.0;
+  double tolerance = 0.0;
+  bool pass = true;
+  std::uint64_t failing_seed = 0;  // seed of the first failing instance
+};
+
+/// Randomized property suite over the solver algebra (block vs SVD equivalence, U-block route,
+/// projector / Schur structure, Penrose conditions, rank vs SVD count, permutation round trip, df vs
+/// rank label equality), `cases` instances seeded from `seed`; inject_fault perturbs one result so a
+/// harness can prove it detects failures.
+std::vector<PropertyResult> run_verification(std::uint64_t seed, std::size_t cases, bool inject_fault = false);
 
 // ---- B200 extras ----------------------------------------------------------
 namespace b200 {

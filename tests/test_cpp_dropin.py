@@ -43,3 +43,39 @@ def test_cpp_bench_protocol_on_device(tmp_path):
                          capture_output=True, text=True, timeout=600)
     print(out.stdout)
     assert out.returncode == 0, out.stdout + out.stderr
+
+
+REF_ACCEPTANCE = "/root/reference/proj/tests/acceptance.cpp"
+REF_BIN = os.path.join(ROOT, "oracle", "_ref", "acceptance_b200")
+
+
+@pytest.mark.skipif(not os.path.exists(REF_ACCEPTANCE), reason="reference tree not present (GPU box)")
+def test_reference_acceptance_compiles_unedited(tmp_path):
+    """The reference's own caller (proj/tests/acceptance.cpp: includes rbpelm/{bench,checks,data,elm}.hpp)
+    compiles UNEDITED against include/ and links to librbpelm_b200.so."""
+    exe = os.path.join(str(tmp_path), "acceptance_b200")
+    subprocess.run(["g++", "-std=c++20", "-O2", "-I", os.path.join(ROOT, "include"), REF_ACCEPTANCE, "-L", LIBDIR,
+                    "-lrbpelm_b200", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+    assert os.path.exists(exe)
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_suite_on_device():
+    """The reference's acceptance criteria 1-7 (proj/tests/acceptance.cpp, built by build() into
+    oracle/_ref/) run on the B200 build: block/rank vs SVD oracle over 200 instances, rank-deficient
+    fits, U-block / projector algebra, df-vs-rank label equality on the GINA-shaped synthetic,
+    timing stability, degenerate inputs."""
+    if not os.path.exists(REF_BIN):
+        pytest.skip("oracle/_ref/acceptance_b200 not built (needs /root/reference at build time)")
+    out = subprocess.run([REF_BIN], capture_output=True, text=True, timeout=900)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "acceptance: all criteria passed" in out.stdout
+
+
+@pytest.mark.gpu
+def test_property_suite_on_device(tmp_path):
+    out = subprocess.run([build(tmp_path, os.path.join(ROOT, "tests", "cpp", "verify_suite.cpp"))],
+                         capture_output=True, text=True, timeout=600)
+    print(out.stdout)
+    assert out.returncode == 0, out.stdout + out.stderr
