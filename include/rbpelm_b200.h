@@ -140,6 +140,19 @@ int rbpg_solve_beta(rbpg_context* ctx, const double* h, size_t n, size_t l, cons
 int rbpg_train(rbpg_context* ctx, size_t inputs, size_t hidden, size_t outputs, uint64_t seed, const double* x,
                size_t n, size_t xcols, const double* y, size_t yrows, size_t ycols, const rbpg_strategy* strategy,
                double* w, double* b, double* beta, size_t* order, rbpg_diagnostics* diag, rbpg_status* st);
+/* Multi-GPU train() in ONE process ("the multi-GPU variant takes a device count";
+ * §8(e)): contexts on ndev distinct devices; rows [r0_i, r0_i + n_i) go to device i (contiguous
+ * shards, the first n % ndev shards one row longer); each device builds its augmented Gram
+ * [H T]^T [H T]; ONE NCCL all-reduce (ncclCommInitAll over the devices, libnccl.so.2 resolved at run
+ * time) of its packed lower triangle, or with fixed_order != 0 an all-gather plus a rank-order sum
+ * (exact twin ties survive sharding); every device runs the identical solve (default tolerance with
+ * the GLOBAL n, linalg.cpp:171); hits are summed.  Outputs as rbpg_train (beta and order from
+ * device 0); diag->hidden_seconds = upload + H build + Gram, solve_seconds = exchange + solve +
+ * accuracy (host wall clock). */
+int rbpg_train_multi(rbpg_context* const* ctxs, size_t ndev, size_t inputs, size_t hidden, size_t outputs,
+                     uint64_t seed, const double* x, size_t n, size_t xcols, const double* y, size_t yrows,
+                     size_t ycols, const rbpg_strategy* strategy, int fixed_order, double* w, double* b,
+                     double* beta, size_t* order, rbpg_diagnostics* diag, rbpg_status* st);
 /* predict (elm.cpp:282-284): scores (n x m) = sigmoid(X W + b) beta */
 int rbpg_predict(rbpg_context* ctx, const double* w, const double* b, size_t d, size_t l, const double* beta,
                  size_t m, const double* x, size_t n, size_t xcols, double* scores, rbpg_status* st);

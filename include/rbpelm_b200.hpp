@@ -303,6 +303,11 @@ std::vector<PropertyResult> run_verification(std::uint64_t seed, std::size_t cas
 namespace b200 {
 /// Select the CUDA device used by the calls above (default 0).
 void set_device(int device);
+/// train() row-sharded over several GPUs of this process (rbpg_train_multi): one NCCL all-reduce of
+/// the packed augmented Gram, replicated solve; fixed_order: all-gather + rank-order sum instead.
+std::pair<ElmModel, SolveDiagnostics> train_multi(const ElmParams& params, const DenseMatrix& x, const DenseMatrix& y,
+                                                  const SolverStrategy& strategy, const std::vector<int>& devices,
+                                                  bool fixed_order = false);
 }  // namespace b200
 
 }  // namespace rbpelm

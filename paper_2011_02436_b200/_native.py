@@ -74,6 +74,9 @@ SIGNATURES = {
     "rbpg_solve_beta": (c_int, [P, P, c_size_t, c_size_t, P, c_size_t, c_size_t, POINTER(rbpg_strategy), P, POINTER(rbpg_diagnostics), ST]),
     "rbpg_train": (c_int, [P, c_size_t, c_size_t, c_size_t, c_uint64, P, c_size_t, c_size_t, P, c_size_t, c_size_t,
                            POINTER(rbpg_strategy), P, P, P, P, POINTER(rbpg_diagnostics), ST]),
+    "rbpg_train_multi": (c_int, [P, c_size_t, c_size_t, c_size_t, c_size_t, c_uint64, P, c_size_t, c_size_t, P,
+                                 c_size_t, c_size_t, POINTER(rbpg_strategy), c_int, P, P, P, P,
+                                 POINTER(rbpg_diagnostics), ST]),
     "rbpg_predict": (c_int, [P, P, P, c_size_t, c_size_t, P, c_size_t, P, c_size_t, c_size_t, P, ST]),
     "rbpg_gram_stage_device": (c_int, [P, P, c_size_t, P, c_size_t, c_size_t, c_size_t, c_size_t, c_size_t, P, c_size_t,
                                        P, P, c_size_t, P, c_size_t, c_int, c_int, ST]),

@@ -532,6 +532,36 @@ def train(params: ElmParams, x, y, strategy: SolverStrategy, ctx: Optional[Conte
     return model, diag
 
 
+def train_multi(params: ElmParams, x, y, strategy: SolverStrategy, devices=(0,), fixed_order: bool = False,
+                return_order: bool = False):
+    """Single-process multi-GPU train() (rbpg_train_multi): contiguous row shards over `devices`, one
+    NCCL all-reduce of the packed augmented Gram (or all-gather + rank-order sum with fixed_order),
+    replicated solve.  Returns (ElmModel, SolveDiagnostics) [, order]."""
+    ctxs = [context(int(dv)) for dv in devices]
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.handle.value for c in ctxs])
+    lib = ctxs[0].lib
+    x = _f64(x)
+    y = _f64(y)
+    L = max(params.hidden_nodes, 1)
+    w = np.empty((max(params.inputs, 1), L))
+    b = np.empty((1, L))
+    beta = np.empty((L, max(params.outputs, 1)))
+    order = np.zeros(L, dtype=np.uint64)
+    s = strategy._c()
+    d = rbpg_diagnostics()
+    st = rbpg_status()
+    lib.rbpg_train_multi(ctypes.cast(arr, ctypes.c_void_p), len(ctxs), params.inputs, params.hidden_nodes,
+                         params.outputs, params.seed, _ptr(x), x.shape[0], x.shape[1], _ptr(y), y.shape[0],
+                         y.shape[1], ctypes.byref(s), int(fixed_order), _ptr(w), _ptr(b), _ptr(beta), _ptr(order),
+                         ctypes.byref(d), ctypes.byref(st))
+    _raise(st)
+    diag = SolveDiagnostics(strategy=strategy.describe())._fill(d)
+    model = ElmModel(params, HiddenLayer(w, b), beta)
+    if return_order:
+        return model, diag, [int(v) for v in order]
+    return model, diag
+
+
 def predict(model: ElmModel, x, ctx: Optional[Context] = None) -> np.ndarray:
     """elm.cpp:282-284: sigmoid(X W + b) beta."""
     ctx = ctx or context()

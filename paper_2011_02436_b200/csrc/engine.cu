@@ -15,6 +15,9 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -26,6 +29,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace rbpg {
@@ -2030,6 +2034,215 @@ int rbpg_train_device(rbpg_context* ctx, const double* dx, size_t ldx, const dou
       fail(RBPG_INVALID_ARGUMENT, "train: block strategies need at least as many samples as hidden nodes (" +
                                       std::to_string(n) + " < " + std::to_string(l) + "); use the direct strategy");
     train_core(ctx, dx, ldx, dt, ldt_in, n, d, l, m, w, b, *strategy, dbeta, ldb, order_out, diag);
+  });
+}
+
+// ============================================================================
+// Single-process multi-device train() (SURVEY §8(b) "the multi-GPU variant takes a device count",
+// §8(e)): contiguous row shards, per-device augmented Gram, ONE NCCL all-reduce of its packed lower
+// triangle, replicated solve.  NCCL is resolved at run time (dlopen of libnccl.so.2: the same library
+// object torch may already have loaded), so the C ABI has no link-time NCCL dependency.
+// ============================================================================
+}  // extern "C"
+
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*ErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!h) return;
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    api.CommInitAll = reinterpret_cast<decltype(api.CommInitAll)>(sym("ncclCommInitAll"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.ErrorString = reinterpret_cast<decltype(api.ErrorString)>(sym("ncclGetErrorString"));
+    if (api.CommInitAll && api.AllReduce && api.AllGather && api.GroupStart && api.GroupEnd && api.ErrorString)
+      api.h = h;
+  });
+  return api;
+}
+
+void nck(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) fail(RBPG_CUDA_ERROR, std::string(what) + ": " + nccl().ErrorString(r));
+}
+
+// one communicator clique per device list, created once per process
+const std::vector<ncclComm_t>& comms_for(const std::vector<int>& devs) {
+  static std::mutex mu;
+  static std::map<std::vector<int>, std::vector<ncclComm_t>> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(devs);
+  if (it != cache.end()) return it->second;
+  std::vector<ncclComm_t> c(devs.size());
+  nck(nccl().CommInitAll(c.data(), static_cast<int>(devs.size()), devs.data()), "ncclCommInitAll");
+  return cache.emplace(devs, std::move(c)).first->second;
+}
+
+// run fn(i) for every device on its own host thread; the first failure is rethrown
+void per_device(size_t ndev, const std::function<void(size_t)>& fn) {
+  std::vector<Fail> fails(ndev);
+  std::vector<char> failed(ndev, 0);
+  std::vector<std::thread> th;
+  for (size_t i = 0; i < ndev; ++i)
+    th.emplace_back([&, i] {
+      try {
+        fn(i);
+      } catch (const Fail& e) {
+        fails[i] = e;
+        failed[i] = 1;
+      } catch (const std::exception& e) {
+        fails[i] = Fail{RBPG_RUNTIME_ERROR, e.what()};
+        failed[i] = 1;
+      }
+    });
+  for (auto& t : th) t.join();
+  for (size_t i = 0; i < ndev; ++i)
+    if (failed[i]) throw fails[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+int rbpg_train_multi(rbpg_context* const* ctxs, size_t ndev, size_t inputs, size_t hidden, size_t outputs,
+                     uint64_t seed, const double* x, size_t n, size_t xcols, const double* y, size_t yrows,
+                     size_t ycols, const rbpg_strategy* strategy, int fixed_order, double* w, double* b,
+                     double* beta, size_t* order, rbpg_diagnostics* diag, rbpg_status* st) {
+  rbpg_diagnostics local;
+  if (!diag) diag = &local;
+  zero_diag(diag);
+  return guarded(nullptr, st, [&] {
+    if (ndev == 0 || !ctxs) fail(RBPG_INVALID_ARGUMENT, "train_multi: no device contexts");
+    std::vector<int> devs(ndev);
+    for (size_t i = 0; i < ndev; ++i) {
+      if (!ctxs[i]) fail(RBPG_INVALID_ARGUMENT, "train_multi: null context");
+      devs[i] = ctxs[i]->device;
+      for (size_t j = 0; j < i; ++j)
+        if (devs[j] == devs[i]) fail(RBPG_INVALID_ARGUMENT, "train_multi: one context per device (NCCL ranks)");
+    }
+    // validation order of elm.cpp:234-258
+    if (n != yrows) fail(RBPG_SHAPE_ERROR, "train: X is " + shp(n, xcols) + " but Y is " + shp(yrows, ycols));
+    if (xcols != inputs)
+      fail(RBPG_SHAPE_ERROR, "train: X has " + std::to_string(xcols) + " features but params.inputs is " +
+                                 std::to_string(inputs));
+    if (ycols != outputs)
+      fail(RBPG_SHAPE_ERROR, "train: Y has " + std::to_string(ycols) + " columns but params.outputs is " +
+                                 std::to_string(outputs));
+    if (strategy->kind != RBPG_DIRECT && n < hidden)
+      fail(RBPG_INVALID_ARGUMENT, "train: block strategies need at least as many samples as hidden nodes (" +
+                                      std::to_string(n) + " < " + std::to_string(hidden) + "); use the direct strategy");
+    if (strategy->kind == RBPG_DF_SPLIT && (strategy->split_index < 1 || strategy->split_index >= hidden))
+      fail(RBPG_INVALID_ARGUMENT, "train: df split index must be in (0, " + std::to_string(hidden) + "), got " +
+                                      std::to_string(strategy->split_index));
+    if (ndev > 1 && !nccl().h) fail(RBPG_NOT_SUPPORTED, "train_multi: libnccl.so.2 not found");
+    rbpg_status s2;
+    if (rbpg_init_hidden(inputs, hidden, outputs, seed, w, b, &s2)) fail(s2.code, s2.message);
+    const size_t L = hidden, m = outputs, d = inputs, M = L + m, ldga = round_up(M, 8);
+    const size_t count = M * (M + 1) / 2;
+    const size_t ldx = even(d), ldy = even(m), ldw = even(L), lb = even(m);
+    std::vector<size_t> row0(ndev), rows(ndev);
+    for (size_t i = 0, r = 0; i < ndev; ++i) {  // sharded.shard_rows: the first n % ndev shards get one more row
+      rows[i] = n / ndev + (i < n % ndev ? 1 : 0);
+      row0[i] = r;
+      r += rows[i];
+    }
+    std::vector<double*> G(ndev), packed(ndev), parts(ndev), B(ndev);
+    std::vector<const double*> X(ndev), T(ndev), W(ndev), bb(ndev);
+    const auto t0 = std::chrono::steady_clock::now();
+    // phase 1: every device uploads its rows and builds its augmented Gram, packed
+    per_device(ndev, [&](size_t i) {
+      rbpg_context* c = ctxs[i];
+      std::lock_guard<std::mutex> lk(c->mu);
+      ck(cudaSetDevice(c->device), "cudaSetDevice");
+      double* dx = c->dbuf("multi.X", std::max<size_t>(1, rows[i]) * ldx);
+      double* dy = c->dbuf("multi.T", std::max<size_t>(1, rows[i]) * ldy);
+      double* dw = c->dbuf("multi.W", std::max<size_t>(1, d) * ldw);
+      double* db = c->dbuf("multi.b", L);
+      copy_rows(dx, ldx * 8, x + row0[i] * xcols, xcols * 8, xcols * 8, rows[i], cudaMemcpyHostToDevice, c->stream,
+                "upload X");
+      copy_rows(dy, ldy * 8, y + row0[i] * ycols, ycols * 8, ycols * 8, rows[i], cudaMemcpyHostToDevice, c->stream,
+                "upload Y");
+      copy_rows(dw, ldw * 8, w, L * 8, L * 8, d, cudaMemcpyHostToDevice, c->stream, "upload W");
+      ck(cudaMemcpyAsync(db, b, L * 8, cudaMemcpyHostToDevice, c->stream), "upload b");
+      X[i] = dx;
+      T[i] = dy;
+      W[i] = dw;
+      bb[i] = db;
+      G[i] = c->dbuf("multi.G", M * ldga);
+      gram_stage(c, dx, ldx, dy, ldy, rows[i], d, L, m, dw, ldw, db, G[i], ldga, false, true, false);
+      packed[i] = c->dbuf("multi.packed", count);
+      if (fixed_order) parts[i] = c->dbuf("multi.parts", count * ndev);
+      c->run("pack_lower", [&] { return launch_pack_lower(G[i], static_cast<long long>(ldga), static_cast<int>(M),
+                                                          packed[i], c->stream); });
+      ck(cudaStreamSynchronize(c->stream), "gram sync");
+    });
+    const auto t1 = std::chrono::steady_clock::now();
+    // phase 2: the one exchange step
+    if (ndev > 1) {
+      const std::vector<ncclComm_t>& comms = comms_for(devs);
+      nck(nccl().GroupStart(), "ncclGroupStart");
+      for (size_t i = 0; i < ndev; ++i) {
+        ck(cudaSetDevice(devs[i]), "cudaSetDevice");
+        if (fixed_order)
+          nck(nccl().AllGather(packed[i], parts[i], count, ncclDouble, comms[i], ctxs[i]->stream), "ncclAllGather");
+        else
+          nck(nccl().AllReduce(packed[i], packed[i], count, ncclDouble, ncclSum, comms[i], ctxs[i]->stream),
+              "ncclAllReduce");
+      }
+      nck(nccl().GroupEnd(), "ncclGroupEnd");
+    }
+    // phase 3: replicated solve and the local hit counts
+    std::vector<unsigned long long> hits(ndev, 0);
+    std::vector<rbpg_diagnostics> dg(ndev);
+    std::vector<std::vector<size_t>> ord(ndev, std::vector<size_t>(L));
+    per_device(ndev, [&](size_t i) {
+      rbpg_context* c = ctxs[i];
+      std::lock_guard<std::mutex> lk(c->mu);
+      ck(cudaSetDevice(c->device), "cudaSetDevice");
+      if (ndev > 1 && fixed_order)
+        c->run("sum_parts", [&] { return launch_sum_parts(parts[i], static_cast<long long>(count),
+                                                          static_cast<int>(ndev), static_cast<long long>(count),
+                                                          packed[i], c->stream); });
+      c->run("unpack_lower", [&] { return launch_unpack_lower(packed[i], static_cast<int>(M), G[i],
+                                                              static_cast<long long>(ldga), c->stream); });
+      B[i] = c->dbuf("multi.beta", L * lb);
+      zero_diag(&dg[i]);
+      // the SVD branch of solve_direct needs all of H on one device: only with one device
+      SourceScope src(c, ndev == 1 && c->kept_h ? c->kept_h : nullptr, c->kept_ldh,
+                      ndev == 1 && c->kept_h ? c->kept_h + L : nullptr, c->kept_ldh, ndev == 1 ? n : 0);
+      solve_dev(c, G[i], ldga, G[i] + L, ldga, L, m, n, *strategy, B[i], lb, ord[i].data(), &dg[i], true);
+      check_finite(c, B[i], lb, L, m);
+      hits[i] = accuracy_stage(c, X[i], ldx, T[i], ldy, rows[i], d, L, m, W[i], ldw, bb[i], B[i], lb);
+    });
+    const auto t2 = std::chrono::steady_clock::now();
+    {
+      rbpg_context* c = ctxs[0];
+      std::lock_guard<std::mutex> lk(c->mu);
+      ck(cudaSetDevice(c->device), "cudaSetDevice");
+      download(c, beta, B[0], lb, L, m);
+    }
+    if (order) std::copy(ord[0].begin(), ord[0].end(), order);
+    unsigned long long tot = 0;
+    for (auto h : hits) tot += h;
+    *diag = dg[0];
+    diag->training_accuracy = n ? static_cast<double>(tot) / static_cast<double>(n) : 0.0;
+    diag->hidden_seconds = std::chrono::duration<double>(t1 - t0).count();  // upload + H build + Gram
+    diag->solve_seconds = std::chrono::duration<double>(t2 - t1).count();   // exchange + solve + accuracy
   });
 }
 

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <mutex>
 #include <sstream>
 
@@ -77,6 +78,44 @@ void set_device(int device) {
     g_ctx = nullptr;
   }
   g_device = device;
+}
+
+std::pair<ElmModel, SolveDiagnostics> train_multi(const ElmParams& params, const DenseMatrix& x, const DenseMatrix& y,
+                                                  const SolverStrategy& strategy, const std::vector<int>& devices,
+                                                  bool fixed_order) {
+  static std::mutex mu;
+  static std::map<int, rbpg_context*> ctxs;  // one context per device, process lifetime
+  std::vector<rbpg_context*> list;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (int dv : devices) {
+      auto it = ctxs.find(dv);
+      if (it == ctxs.end()) {
+        rbpg_context* c = nullptr;
+        rbpg_status st;
+        if (rbpg_context_create(dv, &c, &st) != RBPG_OK) throw std::runtime_error(st.message);
+        it = ctxs.emplace(dv, c).first;
+      }
+      list.push_back(it->second);
+    }
+  }
+  ElmModel model;
+  model.params = params;
+  SolveDiagnostics diag;
+  diag.strategy = strategy.describe();
+  const std::size_t L = std::max<std::size_t>(params.hidden_nodes, 1);
+  model.hidden.weights = DenseMatrix(std::max<std::size_t>(params.inputs, 1), L, 0.0);
+  model.hidden.biases = DenseMatrix(1, L, 0.0);
+  model.beta = DenseMatrix(L, std::max<std::size_t>(params.outputs, 1), 0.0);
+  rbpg_strategy s = to_c(strategy);
+  rbpg_diagnostics d;
+  rbpg_status st;
+  rbpg_train_multi(list.data(), list.size(), params.inputs, params.hidden_nodes, params.outputs, params.seed, x.data(),
+                   x.rows(), x.cols(), y.data(), y.rows(), y.cols(), &s, fixed_order ? 1 : 0,
+                   model.hidden.weights.data(), model.hidden.biases.data(), model.beta.data(), nullptr, &d, &st);
+  raise(st);
+  from_c(d, diag);
+  return {std::move(model), std::move(diag)};
 }
 }  // namespace b200
 

@@ -96,3 +96,24 @@ def test_device_stage_odd_leading_dimension(L, m):
     gh = torch.empty((L, L), dtype=torch.float64, device="cuda")
     rb.gram_device(h, gh)
     assert torch.allclose(gh, g_even[:L, :L], rtol=1e-12, atol=1e-9)
+
+
+@pytest.mark.parametrize("fixed_order", [False, True])
+def test_train_multi_native_entry(fixed_order):
+    """rbpg_train_multi (single-process multi-device C entry) on the one GPU here: upload of the shard,
+    augmented Gram, packed-triangle exchange (NCCL path taken only with > 1 device), replicated solve.
+    With one device its Gram is the device-resident train()'s, so beta is bitwise equal."""
+    import paper_2011_02436_b200 as rb
+
+    n, d, L, m = 20000, 32, 700, 6
+    x, t = rb.synth_classification(n, d, m, 81, 82)
+    params = rb.ElmParams(d, L, m, 83)
+    model, diag, order = rb.train_multi(params, x, t, rb.SolverStrategy.rank_based(), devices=[0],
+                                        fixed_order=fixed_order, return_order=True)
+    X, T = torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda()
+    beta_d, diag_d, _, order_d = rb.train_device(X, T, params, rb.SolverStrategy.rank_based(), return_order=True)
+    assert order == order_d and diag.rank == diag_d.rank == L
+    assert np.array_equal(model.beta, beta_d.cpu().numpy())
+    assert diag.training_accuracy == diag_d.training_accuracy
+    with pytest.raises(ValueError, match="one context per device"):
+        rb.train_multi(params, x, t, rb.SolverStrategy.rank_based(), devices=[0, 0])
