@@ -143,14 +143,15 @@ def test_pack_unpack_and_fixed_order_sum_device(n):
 
     rng = np.random.default_rng(n)
     a = rng.standard_normal((n, n))
-    g = torch.from_numpy(a + a.T).cuda()
+    sym = a + a.T
+    g = torch.from_numpy(sym).cuda()
     packed = torch.empty(n * (n + 1) // 2, dtype=torch.float64, device="cuda")
     rb.pack_lower_device(g, packed)
-    ref = np.concatenate([(a + a.T)[i, :i + 1] for i in range(n)])
+    ref = sym[np.tril_indices(n)]  # row-major lower triangle: (i, j <= i) at i(i+1)/2 + j
     assert np.array_equal(packed.cpu().numpy(), ref)
     out = torch.full((n, n), np.nan, dtype=torch.float64, device="cuda")
     rb.unpack_lower_device(packed, out)
-    assert np.array_equal(out.cpu().numpy(), (a + a.T))
+    assert np.array_equal(out.cpu().numpy(), sym)
     parts = torch.from_numpy(rng.standard_normal((5, 1000))).cuda()
     s = torch.empty(1000, dtype=torch.float64, device="cuda")
     rb.sum_parts_device(parts, s)
