@@ -278,9 +278,16 @@ def test_grid_panel_rank_deficient(L, ndup):
     assert [cls[i] for i in order[:r]] == [cls[i] for i in o_ord[:r]]
     h = oracle.hidden_matrix(hid.weights, hid.biases, x)
     beta_o, diag_o, _ = oracle.solve_beta(h, t, "rank", 0, 1e-6)
+    beta_o8, _, _ = oracle.solve_beta(h, t, "rank", 0, 1e-6, 8)
     assert diag_o["rank"] == r
+    # rank 22 of >= 5000 columns: the Schur block path solves a ~5000-wide ridge-rescued block, so
+    # fitted values are only as reproducible as the oracle's own 1-vs-8-shard floor
     fit, fit_o = h @ beta.cpu().numpy(), h @ beta_o
-    assert rel_fro(fit, fit_o) < 1e-7
+    floor = rel_fro(h @ beta_o8, fit_o)
+    err = rel_fro(fit, fit_o)
+    print(f"  fitted rel {err:.3e} (oracle floor {floor:.3e}); ridge {diag.ridge_applied} / {diag_o['ridge_applied']}")
+    assert diag.ridge_applied == bool(diag_o["ridge_applied"])
+    assert err <= max(1e-7, 4 * floor)
 
 
 def test_sharded_stages_equal_single_pass():

@@ -15,7 +15,7 @@ dev = torch.device("cuda", int(os.environ["LOCAL_RANK"]) % torch.cuda.device_cou
 torch.cuda.set_device(dev)
 dist.init_process_group(os.environ.get("RBPG_DIST_BACKEND", "nccl"))
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-n, d, L, m = bench.CONFIGS[cfg]
+n, d, L, m, _ = bench.CONFIGS[cfg]
 xh, th = rb.synth_classification(n, d, m, bench.SEED_X, bench.SEED_TEACHER, row0=rank * n)
 X, T = torch.from_numpy(xh).to(dev), torch.from_numpy(th).to(dev)
 p = rb.ElmParams(d, L, m, bench.SEED_W)

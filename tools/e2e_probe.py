@@ -11,7 +11,7 @@ import bench  # noqa: E402
 import paper_2011_02436_b200 as rb  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
-n, d, L, m = bench.CONFIGS[cfg]
+n, d, L, m, _ = bench.CONFIGS[cfg]
 xh, th = rb.synth_classification(n, d, m, bench.SEED_X, bench.SEED_TEACHER)
 xp = torch.from_numpy(xh).pin_memory()
 tp = torch.from_numpy(th).pin_memory()

@@ -9,7 +9,7 @@ import paper_2011_02436_b200 as rb  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-n, d, L, m = bench.CONFIGS[cfg]
+n, d, L, m, _ = bench.CONFIGS[cfg]
 x, t = rb.synth_classification(n, d, m, bench.SEED_X, bench.SEED_TEACHER)
 X = torch.from_numpy(x).cuda()
 T = torch.from_numpy(t).cuda()
