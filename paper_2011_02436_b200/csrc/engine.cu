@@ -62,6 +62,7 @@ cudaError_t launch_factor_setup(const double*, long long, int, int, long long, d
                                 FactorState*, cudaStream_t);
 cudaError_t launch_panel(const PanelParams&, int, int*, cudaStream_t);
 bool panel_is_reg(int nl);
+int panel_width(int n, int k);
 cudaError_t launch_trail(const CUtensorMap&, const SyrkParams&, int, cudaStream_t);
 cudaError_t launch_gather_factor(const double*, long long, const int*, int, double*, long long, const FactorState*,
                                  int, cudaStream_t);
@@ -577,8 +578,10 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
   size_t ldcur = ldg;
   double* gnext = Ga;
   int cur = 0;
-  for (size_t k = 0; k < neligible; k += 64) {
-    const int kb = static_cast<int>(std::min<size_t>(64, neligible - k));
+  for (size_t k = 0, kb = 0; k < neligible; k += kb) {
+    // 64-wide panels, 32-wide while more than 4096 labels remain (k_panel.cu, wide variant)
+    kb = std::min<size_t>(static_cast<size_t>(panel_width(static_cast<int>(n), static_cast<int>(k))),
+                          neligible - k);
     PanelParams pp{};
     pp.G = gcur;
     pp.ldg = static_cast<long long>(ldcur);
@@ -587,7 +590,7 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     pp.ord_in = ov[cur];
     pp.ord_out = ov[1 - cur];
     pp.k = static_cast<int>(k);
-    pp.kb = kb;
+    pp.kb = static_cast<int>(kb);
     pp.n = static_cast<int>(n);
     pp.st = st;
     pp.Pg = Pg;
@@ -621,7 +624,7 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
       sp.nbI = static_cast<int>((nrem + ttile - 1) / ttile);
       sp.nGram = sp.nbI * (sp.nbI + 1) / 2;
       sp.nbT = 0;
-      sp.kRows = kb;
+      sp.kRows = static_cast<long long>(kb);
       sp.kPerSplit = static_cast<long long>(round_up(kb, kBK));
       sp.mode = kSyrkTrailing;
       sp.G = gnext;

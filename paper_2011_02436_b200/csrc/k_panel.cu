@@ -433,40 +433,52 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel_t(PanelParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// Quad-per-label cluster variant (nl <= 16 * 64): one label per quad (4 lanes); lane q of the
-// quad owns its label's panel columns q, q+4, ..., q+60, kept in the CTA's shared memory in the
-// padded "lane-major" order (row[q*kRowQ + i] = P[label][q + 4i]) in which candidate rows also
-// travel and are consumed.  The owner lane stores each new column with one 8-byte store (a
-// register copy would need a select over all 16 slots, the slot being a run-time value), the
-// label's row is re-read (8 x 16 B per lane, issued before the exchange wait) for the dot product,
-// and the CTA's candidate row is pushed straight from this array.
+// Quad-per-label cluster variant (nl <= 16 * 64 * LPQ): one label per quad (4 lanes) and layer; lane
+// q of the quad owns its label's panel columns q, q+4, ..., kept in the CTA's shared memory in the
+// padded "lane-major" order (row[q*kRQ + i] = P[label][q + 4i]) in which candidate rows also travel
+// and are consumed.  The owner lane stores each new column with one 8-byte store (a register copy
+// would need a select over all slots, the slot being a run-time value), the label's row is re-read
+// (issued before the exchange wait) for the dot product, and the CTA's candidate row is pushed
+// straight from this array.
 // Arithmetic is identical in the 4 lanes of a quad (xor-shuffle sums), so every lane holds the
 // same col and d; the reduction order is fixed and label-independent (exact twin ties persist).
+// Template: LPQ labels per quad, NT threads, PW panel width (64; 32 for the wide panels of more
+// than 4096 labels, whose rows would not fit in shared memory at 64), MapT the type of the
+// replicated position maps (short when n < 32768 keeps 8192 labels' maps within shared memory).
 // ---------------------------------------------------------------------------
-constexpr int kRegLabels = kPThreads / 4;  // 64 labels per CTA
-constexpr int kRowQ = 18;                   // padded quarter of a lane-major row (16 used)
-constexpr int kRowLen = 4 * kRowQ;
-constexpr size_t kQrowBytes = size_t(kRegLabels) * kRowLen * sizeof(double);
+template <int NT, int PW>
+struct RegPanel {
+  static constexpr int kWarps = NT / 32;
+  static constexpr int kQuads = NT / 4;          // labels per layer (one per quad)
+  static constexpr int kQ = PW / 4;              // panel columns per lane and label
+  static constexpr int kRQ = kQ + 2;             // padded quarter of a lane-major row
+  static constexpr int kRL = 4 * kRQ;            // padded row
+  static constexpr int kCPQ = kQ / 2;            // 16-byte chunks per quarter
+  static constexpr size_t kLayerBytes = size_t(kQuads) * kRL * sizeof(double);
+};
 
 // kTrace: per-phase cycle counters (RBPG_PANEL_TRACE), compiled out of the production variant
-template <bool kTrace, int LPQ>
-__global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) {
-  constexpr int kLabels = kRegLabels * LPQ;  // labels per CTA: LPQ per quad
+template <bool kTrace, int LPQ, int NT = kPThreads, int PW = kPanelW, typename MapT = int>
+__global__ void __launch_bounds__(NT, 1) panel_reg_kernel(PanelParams p) {
+  using RP = RegPanel<NT, PW>;
+  constexpr int kWarps = RP::kWarps, kQuads = RP::kQuads, kQ = RP::kQ, kRQ = RP::kRQ, kRL = RP::kRL;
+  constexpr int kCPQ = RP::kCPQ;
+  constexpr int kLabels = kQuads * LPQ;  // labels per CTA
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int n = p.n, k = p.k, kb = p.kb, nl = n - k;
   const int R = p.rows_per_cta;  // <= kLabels
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   cg::cluster_group cl = cg::this_cluster();
   const int C = static_cast<int>(cl.num_blocks()), cta = static_cast<int>(cl.block_rank());
-  double (*qrow)[kRowLen] = reinterpret_cast<double (*)[kRowLen]>(smem_raw);  // [kRegLabels] own rows
-  int* lab_at = reinterpret_cast<int*>(smem_raw + kQrowBytes * LPQ);  // [nl]
-  int* pos_of = lab_at + nl;                                     // [nl]
+  double (*qrow)[kRL] = reinterpret_cast<double (*)[kRL]>(smem_raw);       // [kLabels] own rows
+  MapT* lab_at = reinterpret_cast<MapT*>(smem_raw + RP::kLayerBytes * LPQ);  // [nl]
+  MapT* pos_of = lab_at + nl;                                                 // [nl]
   __shared__ Cand cand_all[2][kMaxCluster];
-  // candidate rows, lane-major with a padded quarter stride (row[q*kRowQ + i] = P[label][q + 4i]):
-  // the 4 distinct 128-byte quarters a warp reads per step land on different banks
-  __shared__ __align__(16) double rows_all[2][kMaxCluster][kRowLen];
+  // candidate rows, lane-major with a padded quarter stride (row[q*kRQ + i] = P[label][q + 4i]):
+  // the 4 distinct quarters a warp reads per step land on different banks
+  __shared__ __align__(16) double rows_all[2][kMaxCluster][kRL];
   __shared__ __align__(8) uint64_t cand_full[2];
-  __shared__ Cand wbest[kPWarps];
+  __shared__ Cand wbest[kWarps];
   __shared__ int s_stop;
 
   tl_mark(p.tl, p.tl_slot, 0);
@@ -483,23 +495,23 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   const int lbeg = k + cta * R;
   const int nown = max(0, min(n, lbeg + R) - lbeg);
   const int qi = tid >> 2, q = tid & 3;
-  // quad qi holds labels lbeg + qi + 64 l (l < LPQ): consecutive quads, consecutive labels
+  // quad qi holds labels lbeg + qi + kQuads * l (l < LPQ): consecutive quads, consecutive labels
   int x[LPQ];
   bool mine[LPQ];
-  double* myrow[LPQ];  // this lane's 16 slots of each of its labels' rows
+  double* myrow[LPQ];  // this lane's kQ slots of each of its labels' rows
   double dl[LPQ];
 #pragma unroll
   for (int l = 0; l < LPQ; ++l) {
-    const int li = qi + kRegLabels * l;
+    const int li = qi + kQuads * l;
     x[l] = lbeg + li;
     mine[l] = li < nown;
-    myrow[l] = &qrow[li][q * kRowQ];
+    myrow[l] = &qrow[li][q * kRQ];
     dl[l] = mine[l] ? p.d_in[x[l]] : -DBL_MAX;
   }
 
   for (int i = tid; i < nl; i += blockDim.x) {
-    lab_at[i] = k + i;
-    pos_of[i] = k + i;
+    lab_at[i] = static_cast<MapT>(k + i);
+    pos_of[i] = static_cast<MapT>(k + i);
   }
   if (tid == 0) {
     s_stop = 0;
@@ -510,8 +522,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   cl.sync();
   const double cut = st->cut;
   const double thresh = st->thresh;
-  for (int i = tid; i < 2 * kMaxCluster * kRowLen; i += blockDim.x) (&rows_all[0][0][0])[i] = 0.0;
-  for (int i = tid; i < kLabels * kRowLen; i += blockDim.x) (&qrow[0][0])[i] = 0.0;
+  for (int i = tid; i < 2 * kMaxCluster * kRL; i += blockDim.x) (&rows_all[0][0][0])[i] = 0.0;
+  for (int i = tid; i < kLabels * kRL; i += blockDim.x) (&qrow[0][0])[i] = 0.0;
   __syncthreads();
 
   // the CTA row index (label - lbeg) of this warp's best candidate (any valid row when none)
@@ -523,7 +535,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     } else {
       const int src = who ? __ffs(who) - 1 : 0;
       const int bl = __shfl_sync(0xffffffffu, myl, src);
-      return who ? warp * 8 + (src >> 2) + kRegLabels * bl : 0;
+      return who ? warp * 8 + (src >> 2) + kQuads * bl : 0;
     }
   };
   // the lane's best candidate over its LPQ labels: larger key, then smaller position
@@ -539,20 +551,22 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   auto combine_publish = [&](int j, int nch) {
     unsigned long long key = 0, k0 = 0;
     int pos = INT_MAX, p0 = INT_MAX;
-    if (lane < kPWarps) {
+    if (lane < kWarps) {
       k0 = key = wbest[lane].key;
       p0 = pos = wbest[lane].pos;
     }
     warp_argmax(key, pos);
-    const int wsrc = __ffs(__ballot_sync(0xffffffffu, lane < kPWarps && k0 == key && p0 == pos)) - 1;
+    const int wsrc = __ffs(__ballot_sync(0xffffffffu, lane < kWarps && k0 == key && p0 == pos)) - 1;
     const int par = (j - k) & 1;
-    const int roff = (lane >> 3) * kRowQ + 2 * (lane & 7);  // lane's 16-byte chunk of the padded row
+    // lane's 16-byte chunk of the padded row (4 quarters x kCPQ chunks; lanes beyond push nothing)
+    const bool row_lane = lane < 4 * kCPQ;
+    const int roff = row_lane ? (lane / kCPQ) * kRQ + 2 * (lane % kCPQ) : 0;
     const double2 rv = *reinterpret_cast<const double2*>(&qrow[wbest[wsrc].pad][roff]);
     const uint32_t row_l = smem_u32(&rows_all[par][cta][roff]);
     const uint32_t cand_l = smem_u32(&cand_all[par][cta]);
     const uint32_t bar_l = smem_u32(&cand_full[par]);
-    const bool push_row = ((lane & 7) >> 1) < nch;
-    for (int d = warp; d < C; d += kPWarps) {
+    const bool push_row = row_lane && ((lane % kCPQ) >> 1) < nch;
+    for (int d = warp; d < C; d += kWarps) {
       const uint32_t rbar = mapa_u32(bar_l, d);
       if (push_row) st_async_v2f64(mapa_u32(row_l, d), rv.x, rv.y, rbar);
       if (lane == 0) st_async_v2b64(mapa_u32(cand_l, d), key, static_cast<unsigned long long>(pos), rbar);
@@ -601,16 +615,16 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
   // The position swap of step c is written by tid 0 after step c's barrier, so a warp reading the
   // maps during step c + 1 applies that last swap itself (pivp <-> jp, labels xpp / ypp).
   int pivp = -1, xpp = -1, ypp = -1;
-  // Steps run in 4 groups of 16 (the outer loop is unrolled, so the group ch is a compile-time
+  // Steps run in PW/16 groups of 16 (the outer loop is unrolled, so the group ch is a compile-time
   // constant): group ch writes only slot chunk ch of the rows, so the label's own row stays in
   // registers and only that chunk (plus, on entry, the previous one) is re-read per step.
-  double2 own[LPQ][8];
+  double2 own[LPQ][kQ / 2];
 #pragma unroll
   for (int l = 0; l < LPQ; ++l)
 #pragma unroll
-    for (int i = 0; i < 8; ++i) own[l][i] = make_double2(0.0, 0.0);
+    for (int i = 0; i < kQ / 2; ++i) own[l][i] = make_double2(0.0, 0.0);
 #pragma unroll
-  for (int ch = 0; ch < 4; ++ch) {
+  for (int ch = 0; ch < PW / 16; ++ch) {
 #pragma unroll 1
   for (int u = 0; u < 16; ++u) {
     const int c = 16 * ch + u;
@@ -618,8 +632,8 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     const int j = k + c;
     PANEL_TS(0);
     const int jp = j - 1;
-    auto lab_eff = [&](int ps) { return ps == jp ? xpp : (ps == pivp ? ypp : lab_at[ps - k]); };
-    auto pos_eff = [&](int lb) { return lb == xpp ? jp : (lb == ypp ? pivp : pos_of[lb - k]); };
+    auto lab_eff = [&](int ps) { return ps == jp ? xpp : (ps == pivp ? ypp : static_cast<int>(lab_at[ps - k])); };
+    auto pos_eff = [&](int lb) { return lb == xpp ? jp : (lb == ypp ? pivp : static_cast<int>(pos_of[lb - k])); };
     int mypos[LPQ];
 #pragma unroll
     for (int l = 0; l < LPQ; ++l) mypos[l] = mine[l] ? pos_eff(x[l]) : -1;  // before the exchange wait
@@ -667,21 +681,21 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
     }
     // the dot product and sqrt(dj) go before the stop test: one basic block, so their latency
     // chains interleave (dj <= 0 or NaN always stops; rjj is then unused)
-    const double* prow = rows_all[c & 1][src];  // lane-major: prow[q*16 + i] = P[xp][q + 4i]
+    const double* prow = rows_all[c & 1][src];  // lane-major: prow[q*kRQ + i] = P[xp][q + 4i]
     // ---- update: dot over columns cc = q + 4i < c from registers.  Entries at and beyond c are
     // zero in both operands, so whole 16-column chunks are summed unpredicated; a chunk is skipped
     // (warp-uniform) once c <= its first column.
     double a0[LPQ], a1[LPQ], a2[LPQ], a3[LPQ];
 #pragma unroll
     for (int l = 0; l < LPQ; ++l) a0[l] = a1[l] = a2[l] = a3[l] = 0.0;
-    const double2* pv = reinterpret_cast<const double2*>(prow + q * kRowQ);
+    const double2* pv = reinterpret_cast<const double2*>(prow + q * kRQ);
     if (kTrace) {  // diagnostic split of the dot phase: first row chunk landed
       const double2 t = pv[0];
       PANEL_FORCE(t.x + t.y);
       PANEL_TS(10);
     }
 #pragma unroll
-    for (int i = 0; i < 16; i += 4) {
+    for (int i = 0; i < kQ; i += 4) {
       if (i / 4 < ch || (i / 4 == ch && u > 0)) {  // == (c > 4 * i)
         const double2 v0 = pv[i / 2], v1 = pv[i / 2 + 1];
 #pragma unroll
@@ -714,10 +728,10 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
       __syncthreads();
       if (tid == 0) {
         if (piv != j) {
-          lab_at[j - k] = xp;
-          lab_at[piv - k] = y;
-          pos_of[xp - k] = j;
-          pos_of[y - k] = piv;
+          lab_at[j - k] = static_cast<MapT>(xp);
+          lab_at[piv - k] = static_cast<MapT>(y);
+          pos_of[xp - k] = static_cast<MapT>(j);
+          pos_of[y - k] = static_cast<MapT>(piv);
         }
         s_stop = p.pivoting ? 1 : 2;
         if (cta == 0) {
@@ -780,10 +794,10 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_reg_kernel(PanelParams p) 
       tacc[10] += ts[10] - ts[2];
     }
     if (tid == 0 && piv != j) {
-      lab_at[j - k] = xp;
-      lab_at[piv - k] = y;
-      pos_of[xp - k] = j;
-      pos_of[y - k] = piv;
+      lab_at[j - k] = static_cast<MapT>(xp);
+      lab_at[piv - k] = static_cast<MapT>(y);
+      pos_of[xp - k] = static_cast<MapT>(j);
+      pos_of[y - k] = static_cast<MapT>(piv);
     }
     pivp = piv;
     xpp = xp;
@@ -802,7 +816,7 @@ panel_done:
     if (!mine[l]) continue;
     const int orig = p.ord_in[x[l]];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < kQ; ++i) {
       const int cc = q + 4 * i;
       if (cc < kb) p.Fo[(long long)orig * p.ldf + k + cc] = myrow[l][i];
     }
@@ -811,7 +825,7 @@ panel_done:
       const int ps = pos_of[x[l] - k];
       if (ps >= t0) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i = 0; i < kQ; ++i) {
           const int cc = q + 4 * i;
           if (cc < kb) p.PcT[(long long)cc * p.ldp + (ps - t0)] = myrow[l][i];
         }
@@ -844,17 +858,49 @@ int panel_cluster_size(int nl) {
   return 0;
 }
 
-// Labels per quad of panel_reg_kernel for a panel of nl labels (0: the grid variant).  Up to 4
-// labels per quad: 256 per CTA, 4096 per 16-CTA cluster.
+// Labels per quad of panel_reg_kernel (256 threads, 64-wide) for a panel of nl labels (0: another
+// variant).  Up to 4 labels per quad: 256 per CTA, 4096 per 16-CTA cluster.
 int panel_reg_lpq(int nl) {
   const int CL = panel_cluster_size(nl);
   if (CL <= 0) return 0;
   const int R = (nl + CL - 1) / CL;
-  return R <= kRegLabels ? 1 : (R <= 2 * kRegLabels ? 2 : (R <= 4 * kRegLabels ? 4 : 0));
+  constexpr int kQuads = RegPanel<kPThreads, kPanelW>::kQuads;
+  return R <= kQuads ? 1 : (R <= 2 * kQuads ? 2 : (R <= 4 * kQuads ? 4 : 0));
 }
 
-// Whether a panel of nl labels runs panel_reg_kernel (which reads G through its lower triangle).
-bool panel_is_reg(int nl) { return panel_reg_lpq(nl) > 0; }
+// Wide panels (4096 < nl <= 8192 labels): a 16-CTA cluster of 512-thread CTAs, 4 labels per quad
+// (512 per CTA), 32 panel columns (the rows of 512 labels at 64 columns would not fit in shared
+// memory), 16-bit position maps.  Replaces the cooperative-grid panel there (about 6 us per pivot
+// step through global-memory exchange slots).
+constexpr int kWideThreads = 512, kWideWidth = 32, kWideLabels = kMaxCluster * (kWideThreads / 4) * 4;
+bool panel_is_wide(int n, int k) { return n - k > kMaxCluster * kMaxLabelsPerCta && n - k <= kWideLabels && n < 32768; }
+// Panel width the factorisation uses at panel start k of an n-label factorisation.
+int panel_width(int n, int k) { return panel_is_wide(n, k) ? kWideWidth : kPanelW; }
+
+// Whether a panel of nl labels runs a register variant (which reads G through its lower triangle).
+bool panel_is_reg(int nl) { return panel_reg_lpq(nl) > 0 || (nl > kMaxCluster * kMaxLabelsPerCta && nl <= kWideLabels); }
+
+template <typename K>
+static cudaError_t launch_cluster_panel(K kern, const PanelParams& pp, int CL, int threads, size_t smem,
+                                        cudaStream_t s) {
+  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(kern), smem > 0 ? smem : 16, true);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CL);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, pp);
+}
 
 cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cudaStream_t s) {
   const int nl = p.n - p.k;
@@ -862,28 +908,21 @@ cudaError_t launch_panel(const PanelParams& p, int num_sms, int* ctas_used, cuda
   const int CL = panel_cluster_size(nl);
   if (const int lpq = panel_reg_lpq(nl)) {
     pp.rows_per_cta = (nl + CL - 1) / CL;
-    const size_t smem = kQrowBytes * lpq + size_t(2) * nl * sizeof(int);
+    const size_t smem = RegPanel<kPThreads, kPanelW>::kLayerBytes * lpq + size_t(2) * nl * sizeof(int);
     auto kern = lpq == 1 ? (p.trace ? panel_reg_kernel<true, 1> : panel_reg_kernel<false, 1>)
                 : lpq == 2 ? (p.trace ? panel_reg_kernel<true, 2> : panel_reg_kernel<false, 2>)
                            : (p.trace ? panel_reg_kernel<true, 4> : panel_reg_kernel<false, 4>);
-    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(kern), smem > 0 ? smem : 16, true);
-    if (e != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(CL);
-    cfg.blockDim = dim3(kPThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = CL;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
     if (ctas_used) *ctas_used = CL;
-    return cudaLaunchKernelEx(&cfg, kern, pp);
+    return launch_cluster_panel(kern, pp, CL, kPThreads, smem, s);
+  }
+  if (panel_is_wide(p.n, p.k)) {
+    if (p.kb > kWideWidth) return cudaErrorInvalidValue;
+    pp.rows_per_cta = (nl + kMaxCluster - 1) / kMaxCluster;
+    const size_t smem = RegPanel<kWideThreads, kWideWidth>::kLayerBytes * 4 + size_t(2) * nl * sizeof(short);
+    auto kern = p.trace ? panel_reg_kernel<true, 4, kWideThreads, kWideWidth, short>
+                        : panel_reg_kernel<false, 4, kWideThreads, kWideWidth, short>;
+    if (ctas_used) *ctas_used = kMaxCluster;
+    return launch_cluster_panel(kern, pp, kMaxCluster, kWideThreads, smem, s);
   }
   // grid variant: ~ceil(nl / num_sms) labels per CTA, every CTA co-resident (cooperative launch)
   int R = (nl + num_sms - 1) / num_sms;

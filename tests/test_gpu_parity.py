@@ -248,10 +248,11 @@ def test_c5_standin_pivots_vs_oracle():
     assert bwd < 1e-12
 
 
-@pytest.mark.parametrize("L,ndup", [(5000, 0), (6000, 400)])
+@pytest.mark.parametrize("L,ndup", [(5000, 0), (6000, 400), (9000, 300)])
 def test_grid_panel_rank_deficient(L, ndup):
-    """Rank stop inside the >4096-label grid panel: d = 2 features make H numerically low-rank, so
-    at tol 1e-6 the factorisation stops after a few dozen pivots with > 4096 labels live; with
+    """Rank stop inside a wide panel: d = 2 features make H numerically low-rank, so at tol 1e-6 the
+    factorisation stops after a few dozen pivots with > 4096 labels live -- in the 32-wide 512-thread
+    cluster panel (4096 < labels <= 8192) or, at L = 9000, the cooperative-grid panel (> 8192); with
     duplicated nodes the stop rule and the final swap also see exact twins.  Rank and pivots equal
     the oracle's factorisation of the device's own Gram (modulo twin classes); the rank-deficient
     solve (Schur block path) fits like the oracle's."""
