@@ -308,9 +308,12 @@ void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_
 // sees the same arithmetic): greedy list scheduling of the tile x split CTAs on the SMs --
 // off-diagonal and H^T T tiles first, then the diagonal ones at ~0.56 of their work (72 of 128
 // fragments) -- plus the fixed-order reduction of the S partials
+// Large Grams (thousands of tiles, e.g. C5's 2145) are split too: with one split the tiles fill
+// 14.05 waves and the last wave leaves most SMs idle (~5 %); two or three splits level it for one
+// fixed-order reduction pass (~0.2 ms at L + m = 8292).
 int gram_splits(rbpg_context* ctx, size_t N, size_t L, size_t m, int tiles, int nbI) {
   int splits = 1;
-  if (tiles < 4 * ctx->num_sms) {
+  {
     const int P = ctx->num_sms;
     const int nfull = tiles - (nbI >= 2 ? nbI : 0), ndiag = nbI >= 2 ? nbI : 0;
     const double us_per_row = 2.0 * kTile * kTile / (35.7e12 / P) * 1e6;
@@ -318,7 +321,8 @@ int gram_splits(rbpg_context* ctx, size_t N, size_t L, size_t m, int tiles, int 
     const double finish_us_per_split = double(L + m) * double(L + m) / (1010.0 * 1010.0);
     const double ws_bytes_per_split = double(L + m) * double(L + m) * 8.0;
     std::vector<std::pair<double, int>> cand;  // (modelled time, S)
-    for (int sp = 1; sp <= 40; ++sp) {
+    const int max_sp = tiles < 4 * P ? 40 : 4;
+    for (int sp = 1; sp <= max_sp; ++sp) {
       if (sp > 1 && N / static_cast<size_t>(sp) < 768) break;
       if (sp > 1 && sp * ws_bytes_per_split > 2.0e9) break;  // split workspace <= 2 GB
       const double dur = double(N) / sp * us_per_row + 2.0;  // + per-CTA prologue / partial store
