@@ -1215,7 +1215,7 @@ void scores_dev(rbpg_context* ctx, const double* H, size_t ldh, size_t N, size_t
                 size_t m, double* S, size_t lds, const double* T, size_t ldt, unsigned long long* hits) {
   if (N == 0) return;
   Padded B = pad_device(ctx, "beta.pad", dBeta, ldb, L, m);
-  const uint32_t bn = m <= 16 ? 16 : m <= 32 ? 32 : m <= 64 ? 64 : 128;
+  const uint32_t bn = static_cast<uint32_t>((m + 15) / 16 * 16);  // scores_kernel<BN>, BN = m rounded up to 16
   CUtensorMap tmH = make_map(ctx, H, L, N, ldh, 16, kTile, true);
   CUtensorMap tmB = make_map(ctx, B.p, m, L, B.ld, bn + 4, kBK, false);  // padded smem rows
   ScoresParams p{static_cast<int>(N), static_cast<int>(L), static_cast<int>(m), S, static_cast<long long>(lds), T,

@@ -1015,11 +1015,18 @@ cudaError_t launch_scores(const CUtensorMap& tmH, const CUtensorMap& tmB, const 
     kern<<<grid, kGemmThreads, smem, s>>>(tmH, tmB, p);
     return cudaGetLastError();
   };
-  if (p.m <= 16) return go(scores_kernel<16>, 16);
-  if (p.m <= 32) return go(scores_kernel<32>, 32);
-  if (p.m <= 64) return go(scores_kernel<64>, 64);
-  if (p.m <= 128) return go(scores_kernel<128>, 128);
-  return cudaErrorInvalidValue;
+  // BN = m rounded up to 16 (pairs of n8 fragments): C5's m = 100 computes 112 columns, not 128
+  switch ((p.m + 15) / 16) {
+    case 1: return go(scores_kernel<16>, 16);
+    case 2: return go(scores_kernel<32>, 32);
+    case 3: return go(scores_kernel<48>, 48);
+    case 4: return go(scores_kernel<64>, 64);
+    case 5: return go(scores_kernel<80>, 80);
+    case 6: return go(scores_kernel<96>, 96);
+    case 7: return go(scores_kernel<112>, 112);
+    case 8: return go(scores_kernel<128>, 128);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_gemm(const GemmParams& p, cudaStream_t s) {

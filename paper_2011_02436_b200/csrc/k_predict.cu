@@ -54,7 +54,7 @@ constexpr size_t predict_smem() {
 }
 
 template <int MP>
-__global__ void __launch_bounds__(kGemmThreads, MP <= 32 ? 2 : 1)
+__global__ void __launch_bounds__(kGemmThreads, MP <= 48 ? 2 : 1)
     predict_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                    const __grid_constant__ CUtensorMap tmB, PredictParams p) {
   extern __shared__ unsigned char smem_raw[];
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kGemmThreads, MP <= 32 ? 2 : 1)
 
 // tmX: X (N x d) box {16, 128} 128B-swizzled; tmW: W (d x L) box {36, 16}; tmB: beta (L x m) box
 // {MP + 4, 32} (out-of-bounds columns / rows read as zero)
-int predict_mp(int m) { return m <= 16 ? 16 : m <= 32 ? 32 : m <= 64 ? 64 : m <= 128 ? 128 : 0; }
+int predict_mp(int m) { return m >= 1 && m <= 128 ? (m + 15) / 16 * 16 : 0; }  // pairs of n8 fragments
 
 cudaError_t launch_predict(const CUtensorMap& tmX, const CUtensorMap& tmW, const CUtensorMap& tmB,
                            const PredictParams& p, cudaStream_t s) {
@@ -232,7 +232,11 @@ cudaError_t launch_predict(const CUtensorMap& tmX, const CUtensorMap& tmW, const
   switch (predict_mp(p.m)) {
     case 16: return go(predict_kernel<16>, predict_smem<16>());
     case 32: return go(predict_kernel<32>, predict_smem<32>());
+    case 48: return go(predict_kernel<48>, predict_smem<48>());
     case 64: return go(predict_kernel<64>, predict_smem<64>());
+    case 80: return go(predict_kernel<80>, predict_smem<80>());
+    case 96: return go(predict_kernel<96>, predict_smem<96>());
+    case 112: return go(predict_kernel<112>, predict_smem<112>());
     case 128: return go(predict_kernel<128>, predict_smem<128>());
     default: return cudaErrorInvalidValue;
   }
