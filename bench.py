@@ -338,31 +338,26 @@ def main():
            "h2d_bytes_per_step": int(n * d * 8 + n * m * 8), "d2h_bytes_per_step": int(L * m * 8), "api": api}
 
     # ---- batched prediction (elm.cpp:282-284) on this rank's rows: device-resident X, labels out
-    pred = None
-    try:
-        model = rb.ElmModel(params, hidden, torch.zeros(1).numpy())
-        beta_d, _, _ = rb.train_device(X, T, params, strat, hidden=hidden, ctx=ctx)
-        pr = min(n, 200000)
-        Xp = X[:pr]
-        labels = torch.empty(pr, dtype=torch.int32, device=dev)
+    ctx.set_stream(rb.api._torch_stream(dev))
+    beta_d, _, _ = rb.train_device(X, T, params, strat, hidden=hidden, ctx=ctx)
+    pr = min(n, 200000)
+    Xp = X[:pr]
+    labels = torch.empty(pr, dtype=torch.int32, device=dev)
+    rb.predict_labels_device(Xp, W, B, beta_d, labels, ctx=ctx)
+    torch.cuda.synchronize()
+    pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+    for a, b in pe:
+        flush.zero_()
+        a.record(stream)
         rb.predict_labels_device(Xp, W, B, beta_d, labels, ctx=ctx)
-        torch.cuda.synchronize()
-        pe = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
-        for a, b in pe:
-            flush.zero_()
-            a.record(stream)
-            rb.predict_labels_device(Xp, W, B, beta_d, labels, ctx=ctx)
-            b.record(stream)
-        torch.cuda.synchronize()
-        pms = statistics.median(a.elapsed_time(b) for a, b in pe)
-        pflops = 2 * pr * L * (d + m)
-        peak, _ = fp64_peak()
-        pred = {"rows": pr, "ms": pms, "TFLOP/s": pflops / (pms * 1e-3) / 1e12,
-                "frac_fp64_peak": pflops / (pms * 1e-3) / 1e12 / peak,
-                "kernel": "predict_kernel (fused sigma(XW+b) beta + arg-max; H never stored)"}
-        del model
-    except AttributeError:
-        pred = None
+        b.record(stream)
+    torch.cuda.synchronize()
+    pms = statistics.median(a.elapsed_time(b) for a, b in pe)
+    pflops = 2 * pr * L * (d + m)
+    pred = {"rows": pr, "ms": pms, "TFLOP/s": pflops / (pms * 1e-3) / 1e12,
+            "frac_fp64_peak": pflops / (pms * 1e-3) / 1e12 / fp64_peak()[0],
+            "alg_flops": pflops, "hbm_bytes": pr * d * 8 + pr * 4,
+            "kernel": "predict_kernel (K6b: fused sigma(XW+b) beta + arg-max labels; H never stored)"}
 
     if rank == 0:
         peak, peak_src = fp64_peak()
