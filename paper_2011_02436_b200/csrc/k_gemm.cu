@@ -377,33 +377,43 @@ __global__ void __launch_bounds__(TILE == 128 ? 256 : 128, 1)
   tl_mark(p.tl, p.tl_slot, 2);
 }
 
-// One 16-deep k-slab of a diagonal 128-wide Gram tile for warp (DS, DH): its 9 lower-triangle
-// (m16, n8) fragments -- row groups DS and 7 - DS of SMSP DS, split 9 / 9 between the SMSP's two
-// warps -- accumulate into acc[i].
+// Fragment pairs of a diagonal 128-wide Gram tile: row group mt (16 rows) x column pair pp (two n8
+// fragments, 16 columns) with pp <= mt, i.e. the 72 of 128 (m16, n8) fragments that touch the lower
+// triangle.  SMSP s = warp & 3 owns row groups s and 7 - s: 9 pairs (18 fragments, equal tensor-pipe
+// work per SMSP), 5 pairs for warp s and 4 for warp s + 4 (the SMSP's pipe is shared, so the split
+// within it does not matter).  Whole pairs per warp let every B fragment load be one 16-byte load
+// feeding two DMMAs (split pairs compiled to 8-byte loads with 4-way bank conflicts).
 template <int DS, int DH>
-__device__ __forceinline__ void diag_step(double (&acc)[9][4], const double* as, const double* bs, int g, int t) {
+struct DiagPairs {
+  static constexpr int kFirst = DS + 1;  // pairs of row group DS
+  static constexpr int kP0 = DH == 0 ? 0 : 5, kNP = DH == 0 ? 5 : 4;
+  static __device__ __forceinline__ int mt(int P) { return P < kFirst ? DS : 7 - DS; }
+  static __device__ __forceinline__ int pp(int P) { return P < kFirst ? P : P - kFirst; }
+};
+
+// One 16-deep k-slab for warp (DS, DH): its kNP pairs accumulate into acc[2i], acc[2i + 1].
+template <int DS, int DH>
+__device__ __forceinline__ void diag_step(double (&acc)[10][4], const double* as, const double* bs, int g, int t) {
+  using DP = DiagPairs<DS, DH>;
 #pragma unroll
   for (int ks = 0; ks < kBK / 4; ++ks) {
     const int kc = ks * 4 + t;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) {
-      constexpr int kFirst = 2 * DS + 2;
-      const int q = 9 * DH + i;
-      const int mt = q < kFirst ? DS : 7 - DS;
-      const int nt = q < kFirst ? q : q - kFirst;
-      const double2 a = *reinterpret_cast<const double2*>(as + kc * 132 + mt * 16 + 2 * g);
-      const double2 bw = *reinterpret_cast<const double2*>(bs + kc * 132 + (nt >> 1) * 16 + 2 * g);
-      dmma_16x8x4(acc[i], a.x, a.y, (nt & 1) ? bw.y : bw.x);
+    for (int i = 0; i < DP::kNP; ++i) {
+      const int P = DP::kP0 + i;
+      const double2 a = *reinterpret_cast<const double2*>(as + kc * 132 + DP::mt(P) * 16 + 2 * g);
+      const double2 bw = *reinterpret_cast<const double2*>(bs + kc * 132 + DP::pp(P) * 16 + 2 * g);
+      dmma_16x8x4(acc[2 * i], a.x, a.y, bw.x);
+      dmma_16x8x4(acc[2 * i + 1], a.x, a.y, bw.y);
     }
   }
 }
 
-// Diagonal 128 x 128 Gram tiles (direct or split-K partial): only the 72 of 128 (m16, n8) fragments
-// that touch the lower triangle are computed.  SMSP s = warp & 3 owns row groups s and 7 - s
-// (18 fragments each: equal tensor-pipe work per SMSP), split 9 / 9 between its two warps.  Every
-// element sees the same DMMA k-sequence as in a full tile (exact twin ties survive).
+// Diagonal 128 x 128 Gram tiles (direct or split-K partial): only the lower-triangle fragment pairs
+// are computed.  Every element sees the same DMMA k-sequence as in a full tile (exact twin ties
+// survive).
 template <int DS, int DH>
-__device__ __forceinline__ void diag_tile_loop(double (&acc)[9][4], double* As, double* Bs,
+__device__ __forceinline__ void diag_tile_loop(double (&acc)[10][4], double* As, double* Bs,
                                                uint64_t* full, const CUtensorMap* tmA, int i0, long long kbeg,
                                                int ktiles, int tid, int g, int t) {
   constexpr uint32_t kStageBytes = 2u * 132 * kBK * sizeof(double);
@@ -417,6 +427,30 @@ __device__ __forceinline__ void diag_tile_loop(double (&acc)[9][4], double* As, 
       mbar_arrive_expect_tx(&full[s], kStageBytes);
       tma_load_2d(As + s * kBK * 132, tmA, &full[s], i0, kr);
       tma_load_2d(Bs + s * kBK * 132, tmA, &full[s], i0, kr);
+    }
+  }
+}
+
+template <int DS, int DH>
+__device__ __forceinline__ void diag_store(const double (&acc)[10][4], double* out, const SyrkParams& p, int i0,
+                                           int g, int t) {
+  using DP = DiagPairs<DS, DH>;
+#pragma unroll
+  for (int i = 0; i < DP::kNP; ++i) {
+    const int P = DP::kP0 + i, mt = DP::mt(P), pp = DP::pp(P);
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int nt = 2 * pp + f;
+      // fragment (mt, nt): MMA row g / g+8 <-> tile row mt*16 + 2g / +1; MMA col j <-> tile col
+      // (nt >> 1) * 16 + 2j + (nt & 1); lower elements only (mirrored in direct mode)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = i0 + mt * 16 + 2 * g + (e >> 1);
+        const int c = i0 + (nt >> 1) * 16 + 2 * (2 * t + (e & 1)) + (nt & 1);
+        if (r >= p.M || c > r) continue;
+        out[(long long)r * p.ldg + c] = acc[2 * i + f][e];
+        if (p.mode != kSyrkPartial) out[(long long)c * p.ldg + r] = acc[2 * i + f][e];
+      }
     }
   }
 }
@@ -449,9 +483,9 @@ __global__ void __launch_bounds__(256, 1)
       tma_load_2d(Bs + s * kBK * 132, &tmA, &full[s], i0, kr);
     }
   }
-  double acc[9][4];
+  double acc[10][4];
 #pragma unroll
-  for (int i = 0; i < 9; ++i)
+  for (int i = 0; i < 10; ++i)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[i][q] = 0.0;
   switch (warp) {  // compile-time fragment lists per warp
@@ -465,24 +499,16 @@ __global__ void __launch_bounds__(256, 1)
     default: diag_tile_loop<3, 1>(acc, As, Bs, full, &tmA, i0, kbeg, ktiles, tid, g, t); break;
   }
   pdl_wait();  // completes only after the off-diagonal grid (its primary): the reduction follows
-  // fragment (mt, nt): MMA row g / g+8 <-> tile row mt*16 + 2g / +1; MMA col j <-> tile col
-  // (nt >> 1) * 16 + 2j + (nt & 1); lower elements only (mirrored in direct mode)
-  const int ds = warp & 3, dh = warp >> 2;
   double* out = (p.mode == kSyrkPartial) ? p.ws + (p.split0 + blockIdx.y) * p.wsStride : p.G;
-#pragma unroll
-  for (int i = 0; i < 9; ++i) {
-    const int q = 9 * dh + i;
-    const bool first = q < 2 * ds + 2;
-    const int mt = first ? ds : 7 - ds;
-    const int nt = first ? q : q - (2 * ds + 2);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int r = i0 + mt * 16 + 2 * g + (e >> 1);
-      const int c = i0 + (nt >> 1) * 16 + 2 * (2 * t + (e & 1)) + (nt & 1);
-      if (r >= p.M || c > r) continue;
-      out[(long long)r * p.ldg + c] = acc[i][e];
-      if (p.mode != kSyrkPartial) out[(long long)c * p.ldg + r] = acc[i][e];
-    }
+  switch (warp) {
+    case 0: diag_store<0, 0>(acc, out, p, i0, g, t); break;
+    case 1: diag_store<1, 0>(acc, out, p, i0, g, t); break;
+    case 2: diag_store<2, 0>(acc, out, p, i0, g, t); break;
+    case 3: diag_store<3, 0>(acc, out, p, i0, g, t); break;
+    case 4: diag_store<0, 1>(acc, out, p, i0, g, t); break;
+    case 5: diag_store<1, 1>(acc, out, p, i0, g, t); break;
+    case 6: diag_store<2, 1>(acc, out, p, i0, g, t); break;
+    default: diag_store<3, 1>(acc, out, p, i0, g, t); break;
   }
 }
 

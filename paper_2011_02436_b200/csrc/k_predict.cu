@@ -42,6 +42,8 @@ constexpr int kPBN = 32;          // hidden nodes per chunk
 constexpr int kPNS = 3;           // GEMM1 ring stages
 constexpr int kPWP = kPBN + 4;    // padded W tile rows
 constexpr int kPHP = kTile + 4;   // padded H^T rows (k-major)
+// row swizzle of the H^T chunk: rows XOR 0 / 4 / 8 / 12 by column group of 4
+__device__ __forceinline__ int hsw(int col) { return ((col >> 2) & 3) << 2; }
 
 template <int MP>
 constexpr size_t predict_smem() {
@@ -139,24 +141,29 @@ __global__ void __launch_bounds__(kGemmThreads, MP <= 48 ? 2 : 1)
       __syncthreads();
       if (tid == 0 && step + kPNS < total) issue_step(step + kPNS);
     }
-    // epilogue 1: h = sigmoid(z + b) into Hs[col][row] (this warp's rows); nodes >= L give 0
+    // epilogue 1: h = sigmoid(z + b) into Hs[col][row] (this warp's rows, rows 2g and 2g+1 as one
+    // 16-byte store); nodes >= L give 0.  Rows are XOR-swizzled per column group (hsw), which keeps
+    // the row pairs together and makes both these stores and GEMM2's fragment loads conflict-free.
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
       const int cb = pp * 16 + 4 * t;  // chunk column of acc1[2pp][*] / acc1[2pp+1][*]
 #pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        const double v[4] = {acc1[2 * pp][2 * half], acc1[2 * pp + 1][2 * half], acc1[2 * pp][2 * half + 1],
-                             acc1[2 * pp + 1][2 * half + 1]};
+      for (int q = 0; q < 4; ++q) {
+        // acc1[2pp + (q & 1)][2 * half + (q >> 1)] holds (row 2g + half, column cb + q)
+        double h2[2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int half = 0; half < 2; ++half) {
           const int col = c * kPBN + cb + q;
+          const double v = acc1[2 * pp + (q & 1)][2 * half + (q >> 1)];
           double h = 0.0;
           if (col < p.L) {
-            const double z = add_rn(v[q], p.bias[col]);
+            const double z = add_rn(v, p.bias[col]);
             h = recip_ge1p(1.0 + exp(-z));
           }
-          Hs[(cb + q) * kPHP + wm + 2 * g + half] = h;
+          h2[half] = h;
         }
+        const int kc = cb + q;
+        *reinterpret_cast<double2*>(Hs + kc * kPHP + ((wm + 2 * g) ^ hsw(kc))) = make_double2(h2[0], h2[1]);
       }
     }
     __syncwarp();
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(kGemmThreads, MP <= 48 ? 2 : 1)
 #pragma unroll
     for (int kk = 0; kk < kPBN; kk += 4) {
       const int kc = kk + t;
-      const double2 a = *reinterpret_cast<const double2*>(Hs + kc * kPHP + wm + 2 * g);
+      const double2 a = *reinterpret_cast<const double2*>(Hs + kc * kPHP + ((wm + 2 * g) ^ hsw(kc)));
 #pragma unroll
       for (int pp = 0; pp < NT2 / 2; ++pp) {
         const double2 w = *reinterpret_cast<const double2*>(bs + kc * BP + pp * 16 + 2 * g);
