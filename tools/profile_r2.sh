@@ -31,9 +31,9 @@ cap predict_c5 "predict_kernel" 0 c5 --predict
 cap panel_c2 "panel_reg_kernel" 3 c2
 # 4. compute-sanitizer on the cluster / st.async kernels (small shapes)
 for tool in racecheck synccheck memcheck; do
-  timeout 900 compute-sanitizer --tool $tool python tools/sanitize_case.py 3000 16 600 3 > $O/sanitize_${tool}_reg.log 2>&1
+  timeout 900 compute-sanitizer --tool $tool python tools/case_train.py 3000 16 600 3 > $O/sanitize_${tool}_reg.log 2>&1
   echo "rc=$?" >> $O/sanitize_${tool}_reg.log
-  timeout 1200 compute-sanitizer --tool $tool python tools/sanitize_case.py 5000 8 4300 2 > $O/sanitize_${tool}_grid.log 2>&1
+  timeout 1200 compute-sanitizer --tool $tool python tools/case_train.py 5000 8 4300 2 > $O/sanitize_${tool}_grid.log 2>&1
   echo "rc=$?" >> $O/sanitize_${tool}_grid.log
 done
 echo profile-done
