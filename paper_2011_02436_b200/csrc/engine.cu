@@ -622,8 +622,6 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
       // G_old element by element in its epilogue, measured 1.5x slower at L = 8000.)
       const size_t nb32 = (nrem + 31) / 32;
       const int ttile = (nb32 * (nb32 + 1) / 2 <= size_t(3 * ctx->num_sms)) ? 32 : 64;
-      static const int tv = std::getenv("RBPG_TRAIL_VARIANT") ? std::atoi(std::getenv("RBPG_TRAIL_VARIANT")) : 0;
-      const int tcode = (ttile == 64 && tv) ? tv : ttile;  // TEMP experiment knob
       CUtensorMap tm = make_map(ctx, PcT, nrem, static_cast<uint64_t>(kb), ldp, ttile + 4, kBK, false);
       SyrkParams sp{};
       sp.M = static_cast<int>(nrem);
@@ -646,7 +644,7 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
         sp.tl_slot = tl_n++;
         tl_kind.push_back('T');
       }
-      ctx->run("syrk_trailing", [&] { return launch_trail(tm, sp, tcode, s); });
+      ctx->run("syrk_trailing", [&] { return launch_trail(tm, sp, ttile, s); });
       double* written = gnext;
       gnext = (written == Ga) ? Gb : Ga;
       gcur = written;

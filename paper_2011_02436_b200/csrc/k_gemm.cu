@@ -681,125 +681,6 @@ __global__ void __launch_bounds__(2 * TILE, 1)
   tl_mark(p.tl, p.tl_slot, 2);
 }
 
-// Trailing update, 64 x 64 tiles on 256 threads (8 warps of 16 x 32): the whole rank-kb panel
-// (kb <= 64) is loaded by TMA in one batch on one barrier, and every G_old gather (label, then
-// entry, through the lower triangle) is issued into registers before the DMMAs, so a tile costs one
-// TMA round trip plus the gathers' latency under its 16 DMMA k-steps -- instead of up to four
-// dependent 16-row stage reloads.  The per-element arithmetic (DMMA k-steps in increasing k, then
-// one rounded subtraction) is that of trail_kernel: results are bitwise identical.
-constexpr size_t kTrailWideSmem = size_t(2) * kStages * kBK * 68 * sizeof(double) + 1024 + 64;
-
-template <int MINB>
-__global__ void __launch_bounds__(256, MINB) trail_wide_kernel(const __grid_constant__ CUtensorMap tmP, SyrkParams p) {
-  constexpr int TP = 68;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = align1024(smem_raw);
-  double* As = reinterpret_cast<double*>(smem);   // [kt][16][68]
-  double* Bs = As + kStages * kBK * TP;            // [kt][16][68]
-  uint64_t* full = reinterpret_cast<uint64_t*>(Bs + kStages * kBK * TP);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  int I, J;
-  {
-    const int bx = blockIdx.x;
-    int i = static_cast<int>((sqrtf(8.0f * bx + 1.0f) - 1.0f) * 0.5f);
-    while (i * (i + 1) / 2 > bx) --i;
-    while ((i + 1) * (i + 2) / 2 <= bx) ++i;
-    I = i;
-    J = bx - i * (i + 1) / 2;
-  }
-  const int i0 = I * 64, j0 = J * 64;
-  const bool diag = I == J;
-  const int ktiles = static_cast<int>((p.kRows + kBK - 1) / kBK);  // <= kStages (launcher checks)
-  if (tid == 0) {
-    tma_prefetch_desc(&tmP);
-    mbar_init(full, 1);
-    fence_mbar_init();
-  }
-  tl_mark(p.tl, p.tl_slot, 0);
-  pdl_trigger();
-  pdl_wait();  // the panel that wrote PcT / lab may still be finishing
-  tl_mark(p.tl, p.tl_slot, 1);
-  __syncthreads();
-  if (tid == 0) {
-    mbar_arrive_expect_tx(full, static_cast<uint32_t>(ktiles * (diag ? 1 : 2) * TP * kBK * sizeof(double)));
-    for (int s = 0; s < ktiles; ++s) {
-      tma_load_2d(As + s * kBK * TP, &tmP, full, i0, s * kBK);
-      if (!diag) tma_load_2d(Bs + s * kBK * TP, &tmP, full, j0, s * kBK);
-    }
-  }
-  const int wm = (warp & 3) * 16, wn = (warp >> 2) * 32;
-  const int M = p.M, off = p.off;
-  // G_old gathers into registers (consumed by the epilogue)
-  double gold[2][2][4];
-  {
-    int sr[2], sc[2][4];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = i0 + wm + 2 * g + h;
-      sr[h] = r < M ? __ldg(p.lab + off + r) : 0;
-    }
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = j0 + wn + pp * 16 + 4 * t + q;
-        sc[pp][q] = c < M ? __ldg(p.lab + off + c) : 0;
-      }
-#pragma unroll
-    for (int pp = 0; pp < 2; ++pp)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int r = i0 + wm + 2 * g + h, c = j0 + wn + pp * 16 + 4 * t + q;
-          const int a = max(sr[h], sc[pp][q]), b = min(sr[h], sc[pp][q]);
-          gold[pp][h][q] = (r < M && c <= r) ? __ldg(p.Gold + (long long)a * p.ldgo + b) : 0.0;
-        }
-  }
-  double acc[4][4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) acc[j][q] = 0.0;
-  mbar_wait(full, 0);
-  const double* bsrc = diag ? As : Bs;
-  for (int kt = 0; kt < ktiles; ++kt) {
-    const double* as = As + kt * kBK * TP;
-    const double* bs = bsrc + kt * kBK * TP;
-#pragma unroll
-    for (int ks = 0; ks < kBK / 4; ++ks) {
-      const int kc = ks * 4 + t;
-      const double2 a = *reinterpret_cast<const double2*>(as + kc * TP + wm + 2 * g);
-#pragma unroll
-      for (int pp = 0; pp < 2; ++pp) {
-        const double2 w = *reinterpret_cast<const double2*>(bs + kc * TP + wn + pp * 16 + 2 * g);
-        dmma_16x8x4(acc[2 * pp], a.x, a.y, w.x);
-        dmma_16x8x4(acc[2 * pp + 1], a.x, a.y, w.y);
-      }
-    }
-  }
-#pragma unroll
-  for (int pp = 0; pp < 2; ++pp)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = i0 + wm + 2 * g + h, c0 = j0 + wn + pp * 16 + 4 * t;
-      if (r >= M || c0 > r) continue;
-      double v[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = sub_rn(gold[pp][h][q], acc[2 * pp + (q & 1)][2 * h + (q >> 1)]);
-      double* dst = p.G + (long long)(off + r) * p.ldg + off + c0;
-      if (c0 + 3 <= r) {
-        reinterpret_cast<double2*>(dst)[0] = make_double2(v[0], v[1]);
-        reinterpret_cast<double2*>(dst)[1] = make_double2(v[2], v[3]);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (c0 + q <= r) dst[q] = v[q];
-      }
-    }
-  tl_mark(p.tl, p.tl_slot, 2);
-}
-
 // Fixed-order split reduction: G[i][j] = G[j][i] = (acc ? G[i][j] : 0) + sum_s ws[s][i][j] over the
 // lower triangle (i >= j), plus the H^T T partials.  One CTA per 32 x 32 block of the lower
 // triangle: the summed block is staged in shared memory and written both ways with coalesced rows
@@ -1020,14 +901,6 @@ cudaError_t launch_trail(const CUtensorMap& tmP, const SyrkParams& p, int tile, 
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (tile == 65 || tile == 66) {  // experiment: 64-wide tiles on 256 threads, whole panel up front
-    auto kern = tile == 65 ? trail_wide_kernel<3> : trail_wide_kernel<2>;
-    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(kern), kTrailWideSmem);
-    if (e != cudaSuccess) return e;
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = kTrailWideSmem;
-    return cudaLaunchKernelEx(&cfg, kern, tmP, p);
-  }
   if (tile == 64) {
     cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(trail_kernel<64, 1>), trail_smem<64, 1>());
     if (e != cudaSuccess) return e;
