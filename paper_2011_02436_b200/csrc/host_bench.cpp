@@ -1,16 +1,17 @@
 // Trial protocol and report formats of the reference's benchmark layer (proj/src/bench.cpp,
 // include/rbpelm/bench.hpp), so GPU timings come out in the reference's own
 // report schema.  Behaviour restated:
-//   * run_trials (bench.cpp:110-150): one discarded warm-up trial at the template seed, then
+//   * one trial (bench.cpp:19-37): total_seconds is the host wall time around train().
+//   * run_trials (bench.cpp:93-130): one discarded warm-up trial at the template seed, then
 //     `trials` trainings with seed = base + t; min / max / mean / sample stddev of the wall time,
 //     mean solve time and mean training accuracy.
-//   * sweep_df_splits (:152-174): one TrialStats per split (each in (0, L)), best / worst by mean.
-//   * sweep_nodes (:176-201): node counts x strategies; node counts may not exceed the samples.
-//   * JSON schema 1 (:203-256): {"schema":1, machine, dataset{name,samples,features,classes},
+//   * sweep_df_splits (:132-153): one TrialStats per split (each in (0, L)), best / worst by mean.
+//   * sweep_nodes (:155-181): node counts x strategies; node counts may not exceed the samples.
+//   * JSON schema 1 (:183-215): {"schema":1, machine, dataset{name,samples,features,classes},
 //     node_counts, split_points, stats[...]} with per-trial records.  The writer here emits
 //     sorted keys and two-space indentation; report_from_json(report_to_json(r)) is lossless
 //     (doubles are written with 17 significant digits).
-//   * CSV and per-strategy TSV plot series (:258-290).
+//   * emit_report CSV (:217-238) and per-strategy TSV plot series (:240-266).
 #include "../../include/rbpelm_b200.hpp"
 
 #include <algorithm>
