@@ -208,6 +208,11 @@ int rbpg_accuracy_stage_device(rbpg_context* ctx, const double* dx, size_t ldx, 
 /* gram on a device matrix: G (cols x cols, ld ldg) (+)= A^T A, exactly symmetric (matrix.cpp:152-161) */
 int rbpg_gram_device(rbpg_context* ctx, const double* da, size_t lda, size_t rows, size_t cols, double* dg, size_t ldg,
                      int accumulate, rbpg_status* st);
+/* The train path's Gram kernel on an arbitrary device matrix: G (cols x cols, ld ldg) (+)= A^T A on the
+ * INT8 tensor cores (exact digit planes, fp64 combination; lower triangle + mirror, exactly symmetric).
+ * Same contract as rbpg_gram_device; accuracy: |G - exact| <= ~2^-53 sqrt(G_aa G_bb) (tests/test_ozaki_gpu.py). */
+int rbpg_gram_int8_device(rbpg_context* ctx, const double* da, size_t lda, size_t rows, size_t cols, double* dg,
+                          size_t ldg, int accumulate, rbpg_status* st);
 /* Row-sharded pseudo-inverse: from the (all-reduced) Gram of all n_total rows, writes this shard's
  * column block dout (l x n_local, ld ldo) = H^+[:, local rows] for the local rows dh (n_local x l).
  * order/rank (host) optional. */

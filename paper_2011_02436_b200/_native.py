@@ -68,6 +68,7 @@ SIGNATURES = {
     "rbpg_pseudo_inverse": (c_int, [P, P, c_size_t, c_size_t, c_double, P, P, P, ST]),
     "rbpg_pinv_svd": (c_int, [P, P, c_size_t, c_size_t, c_double, P, ST]),
     "rbpg_gram_device": (c_int, [P, P, c_size_t, c_size_t, c_size_t, P, c_size_t, c_int, ST]),
+    "rbpg_gram_int8_device": (c_int, [P, P, c_size_t, c_size_t, c_size_t, P, c_size_t, c_int, ST]),
     "rbpg_pseudo_inverse_stage_device": (c_int, [P, P, c_size_t, c_size_t, P, c_size_t, c_size_t, c_size_t,
                                                  c_double, P, c_size_t, P, P, ST]),
     "rbpg_solve_spd": (c_int, [P, P, c_size_t, c_size_t, P, c_size_t, c_size_t, P, ST]),

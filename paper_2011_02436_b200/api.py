@@ -792,6 +792,16 @@ def gram_device(a, g, accumulate: bool = False, ctx: Optional[Context] = None) -
     _raise(st)
 
 
+def gram_int8_device(a, g, accumulate: bool = False, ctx: Optional[Context] = None) -> None:
+    """g (+)= a^T a with the train path's INT8 digit-plane Gram kernel (k_ozaki.cu) on any device matrix."""
+    ctx = ctx or context(a.device.index or 0)
+    ctx.set_stream(_torch_stream(a.device))
+    st = rbpg_status()
+    ctx.lib.rbpg_gram_int8_device(ctx.handle, _tptr(a), _ld(a), a.shape[0], a.shape[1], _tptr(g), _ld(g),
+                                  int(accumulate), ctypes.byref(st))
+    _raise(st)
+
+
 def pseudo_inverse_stage_device(g, h, n_total: int, tol: float = 0.0, ctx: Optional[Context] = None):
     """Row-sharded H^+: from the all-reduced Gram g (L x L) of all n_total rows, this shard's column
     block H^+[:, local rows] (L x n_local torch tensor) for the local rows h (n_local x L).

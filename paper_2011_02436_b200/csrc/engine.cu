@@ -96,6 +96,11 @@ cudaError_t launch_predict(const CUtensorMap&, const CUtensorMap&, const CUtenso
 int predict_mp(int m);
 cudaError_t launch_pack_lower(const double*, long long, int, double*, cudaStream_t);
 cudaError_t launch_unpack_lower(const double*, int, double*, long long, cudaStream_t);
+cudaError_t launch_oz_colmax(const double*, long long, long long, int, unsigned long long*, int, cudaStream_t);
+cudaError_t launch_oz_slice(const double*, long long, long long, int, const unsigned long long*, int*, int, long long,
+                            int8_t*, cudaStream_t);
+cudaError_t launch_oz_gram(const CUtensorMap&, const OzParams&, cudaStream_t);
+void oz_tile_order(int nbI, int B, int2* out);
 cudaError_t launch_sum_parts(const double*, long long, int, long long, double*, cudaStream_t);
 }  // namespace rbpg
 
@@ -160,6 +165,9 @@ struct rbpg_context {
     return kept_h && kept_n == n && kept_l == l && kept_key == key;
   }
   size_t h_budget_bytes = size_t(48) << 30;
+  // train-path Gram on the INT8 tensor cores (k_ozaki.cu); RBPG_GRAM_DMMA=1: the FP64 DMMA Gram
+  bool gram_int8 = std::getenv("RBPG_GRAM_DMMA") == nullptr;
+  int oz_tiles_nbI = -1;  // tile grid whose launch order is in the "oz_tiles" buffer
   // hidden matrix + targets of the current solve when resident (train / solve_beta): the SVD
   // pseudo-inverse branch of solve_direct needs H itself, not only its Gram
   const double* src_h = nullptr;
@@ -404,6 +412,103 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
   if (!direct) ctx->run("syrk_finish", [&] { return launch_syrk_finish(p, splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
 }
 
+// ---- Gram on the INT8 tensor cores (k_ozaki.cu): exact digit planes, FP64-accurate result.
+// Splits: items of at most 1024 k-steps (32768 rows) keep the CTAs that share operand panels close
+// together in K (L2 reuse; C5: 667 -> 612 ms from 1 to 16 splits), and at least ~one wave of items;
+// the partial workspace (2 slots per split) stays below 16 GB.
+int oz_splits(rbpg_context* ctx, size_t rows, size_t M) {
+  const size_t nbI = (M + 127) / 128, tiles = nbI * (nbI + 1) / 2;
+  const size_t ksteps = (rows + 63) / 64 * 2;
+  size_t sp = std::max<size_t>((ksteps + 1023) / 1024, (size_t(ctx->num_sms) + 2 * tiles - 1) / (2 * tiles));
+  sp = std::min<size_t>(sp, std::max<size_t>(1, ksteps / 128));
+  const double slot_bytes = double(M) * double(even(M)) * 8.0;
+  while (sp > 1 && 2.0 * sp * slot_bytes > 16e9) --sp;
+  return static_cast<int>(std::max<size_t>(sp, 1));
+}
+// Partials of rows [0, rows) of A (rows x M, ld lda) into ws slots [0, 2 * splits) (each M x ldg).
+void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, size_t M, int splits, double* ws,
+                  size_t ldg) {
+  const int nbI = static_cast<int>((M + 127) / 128), Mpad = nbI * 128;
+  const long long Npad = static_cast<long long>((rows + 63) / 64 * 64);
+  auto* cmax = reinterpret_cast<unsigned long long*>(ctx->dbuf("oz_cmax", M));
+  auto* exps = reinterpret_cast<int*>(ctx->dbuf("oz_exps", (Mpad + 1) / 2));
+  auto* planes = reinterpret_cast<int8_t*>(ctx->buf("oz_planes", size_t(7) * Mpad * Npad));
+  ctx->run("oz_colmax", [&] {
+    return launch_oz_colmax(dA, static_cast<long long>(lda), static_cast<long long>(rows), static_cast<int>(M), cmax,
+                            ctx->num_sms, ctx->stream);
+  });
+  ctx->run("oz_slice", [&] {
+    return launch_oz_slice(dA, static_cast<long long>(lda), static_cast<long long>(rows), static_cast<int>(M), cmax,
+                           exps, Mpad, Npad, planes, ctx->stream);
+  });
+  CUtensorMap tm;
+  {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(Mpad), static_cast<cuuint64_t>(7) * Npad};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(Mpad)};
+    cuuint32_t box[2] = {128, 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = ctx->encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, planes, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(RBPG_CUDA_ERROR, "cuTensorMapEncodeTiled (digit planes) failed (" + std::to_string(int(r)) + ")");
+  }
+  if (ctx->oz_tiles_nbI != nbI) {  // tile launch order, uploaded once per tile-grid size
+    std::vector<int2> order(size_t(nbI) * (nbI + 1) / 2);
+    oz_tile_order(nbI, 6, order.data());  // 6 x 6 tile blocks: best of 6 / 12 / 24 / row-major (tools/oz_ab.sh)
+    int2* dt = reinterpret_cast<int2*>(ctx->buf("oz_tiles", order.size() * sizeof(int2)));
+    ck(cudaMemcpyAsync(dt, order.data(), order.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream),
+       "upload tile order");
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+    ctx->oz_tiles_nbI = nbI;
+  }
+  OzParams p{};
+  p.tiles = reinterpret_cast<const int2*>(ctx->buf("oz_tiles", 0));
+  p.M = static_cast<int>(M);
+  p.nbI = nbI;
+  p.nTiles = nbI * (nbI + 1) / 2;
+  p.Mpad = Mpad;
+  p.Npad = Npad;
+  p.ksteps = Npad / 32;
+  p.kPerSplit = (p.ksteps + splits - 1) / splits;
+  p.splits = static_cast<int>((p.ksteps + p.kPerSplit - 1) / p.kPerSplit);
+  p.exps = exps;
+  p.ws = ws;
+  p.wsStride = static_cast<long long>(M * ldg);
+  p.ldg = static_cast<long long>(ldg);
+  p.interleave = 0;  // measured: interleaving the two groups of a tile is ~6 % slower (tools/oz_ab.sh)
+  // fewer effective splits than planned (short parts): the unused slots are zeroed
+  if (p.splits < splits)
+    ck(cudaMemsetAsync(ws + size_t(2) * p.splits * M * ldg, 0, sizeof(double) * size_t(2) * (splits - p.splits) * M * ldg,
+                       ctx->stream),
+       "memset oz slots");
+  ctx->run("oz_gram_kernel", [&] { return launch_oz_gram(tm, p, ctx->stream); });
+}
+// G (+)= A^T A on the INT8 tensor cores (A: N x M); same contract as gram_dev with m = 0.
+void gram_oz_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t M, double* dG, size_t ldg,
+                 bool accumulate) {
+  if (N == 0) {
+    gram_dev(ctx, dA, lda, 0, M, nullptr, 0, 0, dG, ldg, nullptr, 0, accumulate);
+    return;
+  }
+  const int splits = oz_splits(ctx, N, M);
+  SyrkParams p{};
+  p.M = static_cast<int>(M);
+  p.G = dG;
+  p.ldg = static_cast<long long>(ldg);
+  p.ws = ctx->dbuf("syrk_ws", size_t(2) * splits * M * ldg);
+  p.wsStride = static_cast<long long>(M * ldg);
+  oz_gram_part(ctx, dA, lda, N, M, splits, p.ws, ldg);
+  ctx->run("syrk_finish", [&] { return launch_syrk_finish(p, 2 * splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
+}
+
+// The augmented Gram of the train path: INT8 digit-plane Gram unless RBPG_GRAM_DMMA=1 selects the
+// FP64 DMMA Gram (comparison / fallback for inputs whose exponents leave the fp64 normal range).
+void gram_aug_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t M, double* dG, size_t ldg,
+                  bool accumulate) {
+  if (ctx->gram_int8) gram_oz_dev(ctx, dA, lda, N, M, dG, ldg, accumulate);
+  else gram_dev(ctx, dA, lda, N, M, nullptr, 0, 0, dG, ldg, nullptr, 0, accumulate);
+}
+
 // Row-blocked Gram G = A^T A over rows [0, N) for the e2e path: part q covers rows
 // [ends[q-1], ends[q]) with its own uniform split count, every split writes its own partial slot
 // (split0 offset), and one fixed-order reduction sums all parts' partials.  Each part is launched
@@ -428,6 +533,15 @@ GramParts gram_parts_plan(rbpg_context* ctx, size_t L, const std::vector<size_t>
   size_t r0 = 0;
   for (size_t e : ends) {
     const size_t rows = e - r0;
+    if (ctx->gram_int8) {  // INT8 Gram: 2 partial slots per split
+      const int sp = oz_splits(ctx, rows, L);
+      gp.split0.push_back(gp.total);
+      gp.splits.push_back(sp);
+      gp.per.push_back(0);
+      gp.total += 2 * sp;
+      r0 = e;
+      continue;
+    }
     int sp = gram_splits(ctx, rows, L, 0, p.nGram, p.nbI);
     long long per = static_cast<long long>(round_up((rows + sp - 1) / sp, kBK));
     if (per == 0) per = kBK;
@@ -444,6 +558,11 @@ GramParts gram_parts_plan(rbpg_context* ctx, size_t L, const std::vector<size_t>
 }
 void gram_parts_launch(rbpg_context* ctx, GramParts& gp, int q, const double* dA, size_t lda) {
   const size_t r0 = q == 0 ? 0 : gp.ends[q - 1], rows = gp.ends[q] - r0;
+  if (ctx->gram_int8) {
+    oz_gram_part(ctx, dA + r0 * lda, lda, rows, gp.p.M, gp.splits[q], gp.p.ws + gp.split0[q] * gp.p.wsStride,
+                 gp.p.ldg);
+    return;
+  }
   SyrkParams p = gp.p;
   p.kRows = static_cast<long long>(rows);
   p.kPerSplit = gp.per[q];
@@ -1175,7 +1294,7 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
     if (timed) cudaEventRecord(ctx->ev[1], ctx->stream);
     // (a row-blocked Gram behind the uploads was measured slower: its per-block wave
     // quantisation costs more than the hidden upload tail)
-    gram_dev(ctx, dH, ldh, N, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate);
+    gram_aug_dev(ctx, dH, ldh, N, M, dGaug, ldga, accumulate);
     if (keep_h) {
       ctx->keep_h(dH, N, L, ldh, key);
     } else {
@@ -1199,7 +1318,7 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
         hidden_ms += ms;
       }
     }
-    gram_dev(ctx, dH, ldh, nr, M, nullptr, 0, 0, dGaug, ldga, nullptr, 0, accumulate || r0 > 0);
+    gram_aug_dev(ctx, dH, ldh, nr, M, dGaug, ldga, accumulate || r0 > 0);
   }
   if (keep_h && chunk >= N) {
     ctx->keep_h(dH, N, L, ldh, key);
@@ -1627,6 +1746,16 @@ int rbpg_gram_device(rbpg_context* ctx, const double* da, size_t lda, size_t row
       gram_dev(ctx, A.p, A.ld, rows, cols, nullptr, 0, 0, S, lds, nullptr, 0, accumulate != 0);
       ck(cudaMemcpy2DAsync(dg, ldg * 8, S, lds * 8, cols * 8, cols, cudaMemcpyDeviceToDevice, ctx->stream), "store");
     }
+    ck(cudaStreamSynchronize(ctx->stream), "sync");
+  });
+}
+
+int rbpg_gram_int8_device(rbpg_context* ctx, const double* da, size_t lda, size_t rows, size_t cols, double* dg,
+                          size_t ldg, int accumulate, rbpg_status* st) {
+  return guarded(ctx, st, [&] {
+    if (cols == 0) fail(RBPG_SHAPE_ERROR, "gram: empty matrix");
+    if (ldg < cols) fail(RBPG_SHAPE_ERROR, "gram: ldg < cols");
+    gram_oz_dev(ctx, da, lda, rows, cols, dg, ldg, accumulate != 0);
     ck(cudaStreamSynchronize(ctx->stream), "sync");
   });
 }

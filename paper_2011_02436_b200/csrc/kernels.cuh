@@ -65,6 +65,24 @@ struct SyrkParams {
   int mirror;            // trailing: also write the upper triangle (the next panel reads whole rows)
 };
 
+// ---- K2i: Gram on the INT8 tensor cores by exact digit planes (k_ozaki.cu)
+struct OzParams {
+  int M;              // columns of A
+  int nbI;            // 128-wide tile rows
+  int nTiles;         // nbI (nbI + 1) / 2
+  int splits;
+  int Mpad;           // nbI * 128 (plane row length)
+  long long Npad;     // plane rows (multiple of 64)
+  long long ksteps;   // Npad / 32
+  long long kPerSplit;  // k-steps per split
+  const int* exps;
+  const int2* tiles;  // lower-triangle tiles (I, J) in launch order (oz_tile_order)
+  double* ws;         // slot (split * 2 + group): ws + slot * wsStride, ld ldg
+  long long wsStride, ldg;
+  int interleave;     // item order: 1 = per tile (group 1, group 0) adjacent; 0 = all group-1 items first
+  int max_stages;     // 0: as many as fit
+};
+
 // ---- generic DMMA GEMM: C = alpha * op(A) op(B) + beta * C (row-major)
 struct GemmParams {
   int M, N, K;

