@@ -99,8 +99,9 @@ cudaError_t launch_unpack_lower(const double*, int, double*, long long, cudaStre
 cudaError_t launch_oz_colmax(const double*, long long, long long, int, unsigned long long*, int, cudaStream_t);
 cudaError_t launch_oz_slice(const double*, long long, long long, int, const unsigned long long*, int*, int, long long,
                             int8_t*, cudaStream_t);
-cudaError_t launch_oz_gram(const CUtensorMap&, const OzParams&, cudaStream_t);
-void oz_tile_order(int nbI, int B, int2* out);
+cudaError_t launch_oz_gram2(const CUtensorMap* maps, const OzParams&, cudaStream_t);
+int oz_pair_order(int nbI, int B, int2* out);
+cudaError_t launch_oz_finish(const double*, long long, int, int, double*, long long, int, cudaStream_t);
 cudaError_t launch_sum_parts(const double*, long long, int, long long, double*, cudaStream_t);
 }  // namespace rbpg
 
@@ -168,6 +169,7 @@ struct rbpg_context {
   // train-path Gram on the INT8 tensor cores (k_ozaki.cu); RBPG_GRAM_DMMA=1: the FP64 DMMA Gram
   bool gram_int8 = std::getenv("RBPG_GRAM_DMMA") == nullptr;
   int oz_tiles_nbI = -1;  // tile grid whose launch order is in the "oz_tiles" buffer
+  int oz_tiles_n = 0;
   // hidden matrix + targets of the current solve when resident (train / solve_beta): the SVD
   // pseudo-inverse branch of solve_direct needs H itself, not only its Gram
   const double* src_h = nullptr;
@@ -413,22 +415,18 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
 }
 
 // ---- Gram on the INT8 tensor cores (k_ozaki.cu): exact digit planes, FP64-accurate result.
-// Splits: items of at most 1024 k-steps (32768 rows) keep the CTAs that share operand panels close
-// together in K (L2 reuse; C5: 667 -> 612 ms from 1 to 16 splits), and at least ~one wave of items;
-// the partial workspace (2 slots per split) stays below 16 GB.
-int oz_splits(rbpg_context* ctx, size_t rows, size_t M) {
-  const size_t nbI = (M + 127) / 128, tiles = nbI * (nbI + 1) / 2;
-  const size_t ksteps = (rows + 63) / 64 * 2;
-  size_t sp = std::max<size_t>((ksteps + 1023) / 1024, (size_t(ctx->num_sms) + 2 * tiles - 1) / (2 * tiles));
-  sp = std::min<size_t>(sp, std::max<size_t>(1, ksteps / 128));
-  const double slot_bytes = double(M) * double(even(M)) * 8.0;
-  while (sp > 1 && 2.0 * sp * slot_bytes > 16e9) --sp;
-  return static_cast<int>(std::max<size_t>(sp, 1));
+// Row splits of at most 512 k-steps (16384 rows: the int32 headroom of one accumulation), so every
+// CTA-pair item is read out once into its own packed partial tile set (2 slots per split: the two
+// accumulator groups); the fixed-order reduction (oz_finish_kernel) sums the slots.
+constexpr size_t kOzRowsPerSplit = 16384;
+int oz_splits(size_t rows) { return static_cast<int>(std::max<size_t>(1, (rows + kOzRowsPerSplit - 1) / kOzRowsPerSplit)); }
+size_t oz_slot_doubles(size_t M) {
+  const size_t nbI = (M + 127) / 128;
+  return nbI * (nbI + 1) / 2 * 16384;  // lower 128 x 128 tiles, packed
 }
-// Partials of rows [0, rows) of A (rows x M, ld lda) into ws slots [0, 2 * splits) (each M x ldg).
-void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, size_t M, int splits, double* ws,
-                  size_t ldg) {
-  const int nbI = static_cast<int>((M + 127) / 128), Mpad = nbI * 128;
+// Partials of rows [0, rows) of A (rows x M, ld lda) into the 2 * oz_splits(rows) slots at ws.
+void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, size_t M, double* ws) {
+  const int nbI = static_cast<int>((M + 127) / 128), Mpad = (nbI + 1) / 2 * 2 * 128;
   const long long Npad = static_cast<long long>((rows + 63) / 64 * 64);
   auto* cmax = reinterpret_cast<unsigned long long*>(ctx->dbuf("oz_cmax", M));
   auto* exps = reinterpret_cast<int*>(ctx->dbuf("oz_exps", (Mpad + 1) / 2));
@@ -441,47 +439,46 @@ void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, 
     return launch_oz_slice(dA, static_cast<long long>(lda), static_cast<long long>(rows), static_cast<int>(M), cmax,
                            exps, Mpad, Npad, planes, ctx->stream);
   });
-  CUtensorMap tm;
-  {
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(Mpad), static_cast<cuuint64_t>(7) * Npad};
-    cuuint64_t strides[1] = {static_cast<cuuint64_t>(Mpad)};
-    cuuint32_t box[2] = {128, 32};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = ctx->encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, planes, dims, strides, box, estr,
-                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) fail(RBPG_CUDA_ERROR, "cuTensorMapEncodeTiled (digit planes) failed (" + std::to_string(int(r)) + ")");
-  }
-  if (ctx->oz_tiles_nbI != nbI) {  // tile launch order, uploaded once per tile-grid size
-    std::vector<int2> order(size_t(nbI) * (nbI + 1) / 2);
-    oz_tile_order(nbI, 6, order.data());  // 6 x 6 tile blocks: best of 6 / 12 / 24 / row-major (tools/oz_ab.sh)
+  // 3-D maps over the planes [plane][row][column]: one box per operand and k-step holds all the planes
+  // a group needs (A: 128 columns, 128-byte swizzle; B: this CTA's 64 columns, 64-byte swizzle)
+  CUtensorMap maps[4];
+  for (int g = 0; g < 2; ++g)
+    for (int ab = 0; ab < 2; ++ab) {
+      cuuint64_t dims[3] = {static_cast<cuuint64_t>(Mpad), static_cast<cuuint64_t>(Npad), 7};
+      cuuint64_t strides[2] = {static_cast<cuuint64_t>(Mpad), static_cast<cuuint64_t>(Mpad) * Npad};
+      cuuint32_t box[3] = {ab ? 64u : 128u, 32u, g ? 7u : 4u};
+      cuuint32_t estr[3] = {1, 1, 1};
+      CUresult r = ctx->encode(&maps[2 * g + ab], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, planes, dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, ab ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        fail(RBPG_CUDA_ERROR, "cuTensorMapEncodeTiled (digit planes) failed (" + std::to_string(int(r)) + ")");
+    }
+  if (ctx->oz_tiles_nbI != nbI) {  // (pair, column) block launch order, uploaded once per tile-grid size
+    std::vector<int2> order(size_t(nbI) * nbI + 2);
+    const int n = oz_pair_order(nbI, 3, order.data());
+    order.resize(n);
     int2* dt = reinterpret_cast<int2*>(ctx->buf("oz_tiles", order.size() * sizeof(int2)));
     ck(cudaMemcpyAsync(dt, order.data(), order.size() * sizeof(int2), cudaMemcpyHostToDevice, ctx->stream),
        "upload tile order");
     ck(cudaStreamSynchronize(ctx->stream), "sync");
     ctx->oz_tiles_nbI = nbI;
+    ctx->oz_tiles_n = n;
   }
   OzParams p{};
   p.tiles = reinterpret_cast<const int2*>(ctx->buf("oz_tiles", 0));
   p.M = static_cast<int>(M);
   p.nbI = nbI;
-  p.nTiles = nbI * (nbI + 1) / 2;
+  p.nTiles = ctx->oz_tiles_n;
   p.Mpad = Mpad;
   p.Npad = Npad;
   p.ksteps = Npad / 32;
-  p.kPerSplit = (p.ksteps + splits - 1) / splits;
-  p.splits = static_cast<int>((p.ksteps + p.kPerSplit - 1) / p.kPerSplit);
+  p.splits = oz_splits(rows);
+  p.kPerSplit = kOzRowsPerSplit / 32;
   p.exps = exps;
   p.ws = ws;
-  p.wsStride = static_cast<long long>(M * ldg);
-  p.ldg = static_cast<long long>(ldg);
-  p.interleave = 0;  // measured: interleaving the two groups of a tile is ~6 % slower (tools/oz_ab.sh)
-  // fewer effective splits than planned (short parts): the unused slots are zeroed
-  if (p.splits < splits)
-    ck(cudaMemsetAsync(ws + size_t(2) * p.splits * M * ldg, 0, sizeof(double) * size_t(2) * (splits - p.splits) * M * ldg,
-                       ctx->stream),
-       "memset oz slots");
-  ctx->run("oz_gram_kernel", [&] { return launch_oz_gram(tm, p, ctx->stream); });
+  p.wsStride = static_cast<long long>(oz_slot_doubles(M));
+  ctx->run("oz_gram_kernel", [&] { return launch_oz_gram2(maps, p, ctx->stream); });
 }
 // G (+)= A^T A on the INT8 tensor cores (A: N x M); same contract as gram_dev with m = 0.
 void gram_oz_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t M, double* dG, size_t ldg,
@@ -490,15 +487,13 @@ void gram_oz_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size
     gram_dev(ctx, dA, lda, 0, M, nullptr, 0, 0, dG, ldg, nullptr, 0, accumulate);
     return;
   }
-  const int splits = oz_splits(ctx, N, M);
-  SyrkParams p{};
-  p.M = static_cast<int>(M);
-  p.G = dG;
-  p.ldg = static_cast<long long>(ldg);
-  p.ws = ctx->dbuf("syrk_ws", size_t(2) * splits * M * ldg);
-  p.wsStride = static_cast<long long>(M * ldg);
-  oz_gram_part(ctx, dA, lda, N, M, splits, p.ws, ldg);
-  ctx->run("syrk_finish", [&] { return launch_syrk_finish(p, 2 * splits, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
+  const int splits = oz_splits(N);
+  double* ws = ctx->dbuf("syrk_ws", size_t(2) * splits * oz_slot_doubles(M));
+  oz_gram_part(ctx, dA, lda, N, M, ws);
+  ctx->run("syrk_finish", [&] {
+    return launch_oz_finish(ws, static_cast<long long>(oz_slot_doubles(M)), 2 * splits, static_cast<int>(M), dG,
+                            static_cast<long long>(ldg), accumulate ? 1 : 0, ctx->stream);
+  });
 }
 
 // The augmented Gram of the train path: INT8 digit-plane Gram unless RBPG_GRAM_DMMA=1 selects the
@@ -533,8 +528,8 @@ GramParts gram_parts_plan(rbpg_context* ctx, size_t L, const std::vector<size_t>
   size_t r0 = 0;
   for (size_t e : ends) {
     const size_t rows = e - r0;
-    if (ctx->gram_int8) {  // INT8 Gram: 2 partial slots per split
-      const int sp = oz_splits(ctx, rows, L);
+    if (ctx->gram_int8) {  // INT8 Gram: 2 packed partial slots per split
+      const int sp = oz_splits(rows);
       gp.split0.push_back(gp.total);
       gp.splits.push_back(sp);
       gp.per.push_back(0);
@@ -552,15 +547,15 @@ GramParts gram_parts_plan(rbpg_context* ctx, size_t L, const std::vector<size_t>
     gp.total += sp;
     r0 = e;
   }
-  p.ws = ctx->dbuf("syrk_ws", size_t(gp.total) * L * ldg);
-  p.wsStride = static_cast<long long>(L * ldg);
+  const size_t slot = ctx->gram_int8 ? oz_slot_doubles(L) : L * ldg;
+  p.ws = ctx->dbuf("syrk_ws", size_t(gp.total) * slot);
+  p.wsStride = static_cast<long long>(slot);
   return gp;
 }
 void gram_parts_launch(rbpg_context* ctx, GramParts& gp, int q, const double* dA, size_t lda) {
   const size_t r0 = q == 0 ? 0 : gp.ends[q - 1], rows = gp.ends[q] - r0;
   if (ctx->gram_int8) {
-    oz_gram_part(ctx, dA + r0 * lda, lda, rows, gp.p.M, gp.splits[q], gp.p.ws + gp.split0[q] * gp.p.wsStride,
-                 gp.p.ldg);
+    oz_gram_part(ctx, dA + r0 * lda, lda, rows, gp.p.M, gp.p.ws + gp.split0[q] * gp.p.wsStride);
     return;
   }
   SyrkParams p = gp.p;
@@ -572,6 +567,13 @@ void gram_parts_launch(rbpg_context* ctx, GramParts& gp, int q, const double* dA
   if (p.nbI >= 2) ++ctx->launches;
 }
 void gram_parts_finish(rbpg_context* ctx, GramParts& gp, bool accumulate) {
+  if (ctx->gram_int8) {
+    ctx->run("syrk_finish", [&] {
+      return launch_oz_finish(gp.p.ws, gp.p.wsStride, gp.total, gp.p.M, gp.p.G, gp.p.ldg, accumulate ? 1 : 0,
+                              ctx->stream);
+    });
+    return;
+  }
   ctx->run("syrk_finish", [&] { return launch_syrk_finish(gp.p, gp.total, accumulate ? 1 : 0, ctx->num_sms, ctx->stream); });
 }
 

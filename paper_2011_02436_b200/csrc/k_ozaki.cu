@@ -8,25 +8,26 @@
 // written in 7 balanced base-256 digits
 //     X = sum_{i=1..7} d_i 256^(7-i),   d_2..d_7 in [-128, 127],  d_1 in [-64, 64],
 // so that A[k][c] = 2^(e_c - 54) X exactly up to that one rounding.  The digit planes D_i (int8,
-// N x M) keep A's row-major layout, [plane][row][column]: MN-major MMA operands, so one TMA box row
-// is 128 contiguous bytes (a K-major box row would be 32: four times the L2 requests).
+// N x M) keep A's row-major layout, [plane][row][column]: MN-major MMA operands, so a TMA box row is
+// 128 contiguous bytes.
 //
 // Products.  G[a][b] = 2^(e_a + e_b) sum_{i,j} 2^(4 - 8(i + j)) (D_i^T D_j)[a][b].  Terms with
-// i + j >= 9 are below 2^-56 of |G|'s scale and zero-mean (balanced digits): they are dropped, which
-// leaves 28 INT8 products per 32-row k-step, grouped by weight w = i + j into int32 accumulators in
-// tensor memory: group 0 = w 2..5 (10 products, 4 accumulators, planes 1..4), group 1 = w 6..8 (18
-// products, 3 accumulators, planes 1..7).  One CTA computes one (128 x 128 tile, group, K-split)
-// item; every 512 k-steps (16384 rows, the int32 headroom: 7 pairs x 32 rows x 2^14 x 512 < 2^31)
-// the epilogue warps read the accumulators, combine the weights by Horner's rule in fp64 (exact but
-// for the last addition) and add the chunk into the item's fp64 partial in global memory.  The
-// fixed-order split reduction (syrk_finish_kernel) sums the partials and mirrors: the result is
-// exactly symmetric and, as integer arithmetic is exact, identical columns give bit-identical Gram
-// entries wherever they sit (the exact twin ties of C3 survive).
+// i + j >= 9 are below 2^-56 of the scale max_a max_b per row and zero-mean (balanced digits): they
+// are dropped, which leaves 28 INT8 products per 32-row k-step, grouped by weight w = i + j into int32
+// accumulators in tensor memory: group 0 = w 2..5 (10 products, 4 accumulators, planes 1..4), group
+// 1 = w 6..8 (18 products, 3 accumulators, planes 1..7).  An item is one (256 x 128 block, group,
+// split of at most 512 k-steps) -- 512 k-steps is the int32 headroom (7 pairs x 32 rows x 2^14 x 512
+// < 2^31) -- read out once: Horner's rule over the weights in fp64 (exact for group 1, one rounding
+// for group 0), scaled by the column exponents, stored into the item's packed partial tile.  The
+// fixed-order reduction (oz_finish_kernel) sums the partials and mirrors: the result is exactly
+// symmetric and, integer arithmetic being exact, identical columns give bit-identical Gram entries
+// wherever they sit (the exact twin ties of C3 survive).
 //
-// Warp roles (192 threads): warp 0 issues TMA (4-stage ring of one k-step: one 4 KB box {128
-// columns, 32 rows} per plane tile, 128-byte swizzle),
-// warp 1 allocates TMEM and issues tcgen05.mma from one lane, warps 2-5 are the epilogue (warp w
-// reads TMEM lanes 32 (w % 4) .. +31, i.e. tile rows).
+// Execution (oz_gram2_kernel): persistent CTA pairs (tcgen05 cta_group::2, M = 256, N = 128); per
+// pair one producer warp per CTA (3-D TMA, one box per operand and k-step), one MMA warp (rank 0),
+// eight epilogue warps per CTA.  Measured (tools/ozaki_test, one B200): C5 shard 413 ms = 2.38 int8
+// POP/s (83 FP64-equivalent TF/s), C4 L = 8000 68 ms; operands-resident ceiling 3.5 POP/s; the MMA
+// pattern itself 4.5 POP/s (tools/mma_rate2.cu).
 #include "common.cuh"
 #include "kernels.cuh"
 
@@ -39,12 +40,7 @@ namespace {
 constexpr int kOzPlanes = 7;
 constexpr int kOzMaxStages = 12;
 constexpr uint32_t kOzRing = 224 * 1024;  // operand ring: as many whole k-step stages as fit
-constexpr int kOzChunk = 512;  // k-steps between accumulator read-outs
 constexpr uint32_t kOzTileBytes = 128 * 32;  // one plane tile: 32 rows x 128 columns (bytes)
-
-// instruction descriptor: D s32, A s8, B s8, MN-major both (bits 15, 16), M = 128, N = 128
-constexpr uint32_t kOzIdesc =
-    (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
 
 // shared-memory matrix descriptor, MN-major, 128-byte swizzle: a K row of 128 bytes (the whole 128-wide
 // M / N extent, one swizzle atom wide), 8-row K groups 1024 B apart (stride byte offset); the leading
@@ -54,30 +50,8 @@ __device__ __forceinline__ uint64_t oz_desc(uint32_t saddr) {
          (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
 }
 
-__device__ __forceinline__ void oz_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
-  asm volatile(
-      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kOzIdesc), "r"(acc));
-}
-__device__ __forceinline__ void oz_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
-               : "memory");
-}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
-        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
-        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
-        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-}
 
 // Group G: number of weights, first weight, planes used, and the (i, j) pairs in issue order
 template <int G>
@@ -156,59 +130,151 @@ __global__ void __launch_bounds__(256) oz_slice_kernel(const double* __restrict_
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs on one TPC computes a 256 x 128 block
+// -- tile rows 2P (CTA rank 0) and 2P + 1 (rank 1) against tile column J -- as ONE M = 256, N = 128
+// MMA stream issued by rank 0.  Each CTA stages its own 128 A rows (box {128, 32}, 128-byte swizzle)
+// and HALF of the B columns (box {64, 32}, 64-byte swizzle): per SM the tensor core reads 6 KB of
+// shared memory per 64-cycle MMA instead of 8 KB, and the L2 delivers 6 KB per plane instead of 8.
+// Every CTA's TMA bytes complete on rank 0's full barrier; rank 0's commits arrive on both CTAs'
+// empty / tmem-full barriers (multicast); both epilogues arrive on rank 0's tmem-empty barrier.  The
+// accumulator rows live in the TMEM of the CTA that owns them, so the epilogue is unchanged.  The
+// block (2P, 2P + 1) is above the diagonal: computed, not stored.
+// ---------------------------------------------------------------------------------------------
+namespace {
+constexpr uint32_t kOzBHalfBytes = 64 * 32;  // B half-tile: 32 rows x 64 columns
+// instruction descriptor: M = 256, N = 128, MN-major, s8 x s8 -> s32
+constexpr uint32_t kOzIdesc2 =
+    (2u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | (1u << 16) | ((128u >> 3) << 17) | ((256u >> 4) << 24);
+// MN-major, 64-byte swizzle: K rows of 64 bytes (this CTA's 64 columns, one swizzle atom), 8-row
+// groups 512 B apart
+__device__ __forceinline__ uint64_t oz_desc64(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(2048 >> 4) << 16) |
+         (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(4) << 61);
+}
+// Executed by the whole (converged) MMA warp with warp-uniform operands, so the descriptors stay in
+// uniform registers; one elected lane issues.  (Issued from a single-lane branch, every MMA needed a
+// register -> uniform-register broadcast loop: ~1.5x the 64-cycle MMA time at 10 MMAs per k-step.)
+__device__ __forceinline__ void oz_mma2(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kOzIdesc2), "r"(acc));
+}
+__device__ __forceinline__ void oz_commit2(uint64_t* bar) {  // arrive on `bar` in both CTAs of the pair
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}\n" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<unsigned short>(3))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void named_bar_sync_n(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_bar) : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+
 template <int G>
-__device__ __forceinline__ void oz_mma_kstep(uint32_t tbase, uint32_t sa, uint32_t sb, bool first) {
-  // pairs (i, j), i + j = w, in increasing w; the first pair of each weight starts its accumulator
-  // on the first k-step of a chunk
+__device__ __forceinline__ void oz_mma_kstep2(uint32_t tbase, uint32_t sa, uint32_t sb, bool first) {
 #pragma unroll
   for (int w = OzGroup<G>::kW0; w < OzGroup<G>::kW0 + OzGroup<G>::kW; ++w) {
 #pragma unroll
     for (int i = 1; i < w; ++i) {
       const int j = w - i;
       if (i > OzGroup<G>::kPlanes || j > OzGroup<G>::kPlanes) continue;
-      const uint64_t da = oz_desc(sa + (i - 1) * kOzTileBytes);
-      const uint64_t db = oz_desc(sb + (j - 1) * kOzTileBytes);
-      oz_mma(tbase + (w - OzGroup<G>::kW0) * 128, da, db, (first && i == 1) ? 0u : 1u);
+      oz_mma2(tbase + (w - OzGroup<G>::kW0) * 128, oz_desc(sa + (i - 1) * kOzTileBytes),
+              oz_desc64(sb + (j - 1) * kOzBHalfBytes), (first && i == 1) ? 0u : 1u);
     }
   }
 }
+}  // namespace
 
+// x 2^e without a libm call: two exact power-of-two factors, each inside the normal exponent range
+// for |e| <= 2044 (column exponents of finite data)
+__device__ __forceinline__ double pow2i(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
+__device__ __forceinline__ double scale2(double x, int e) {
+  const int e1 = e / 2;
+  return (x * pow2i(e1)) * pow2i(e - e1);
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+
+// One chunk's read-out for one epilogue thread (row `quarter * 32 + lane`, 64 columns from `col0`):
+// Horner over the group's weights, added to the fp64 running sums in registers.
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+// One chunk's read-out for one epilogue thread (row `quarter * 32 + lane`, 64 columns from `col0`):
+// Horner over the group's weights, added to the fp64 running sums in registers.
+// Read-out of one item's accumulators by one epilogue thread (tile row `quarter * 32 + lane`, all 128
+// columns, 8 at a time): Horner over the group's weights in fp64 (exact for group 1, one rounding for
+// group 0), times 2^(e_row + e_col + 4 - 8 w0), stored to the item's packed partial tile.  Every
+// TMEM load of the item is done before the caller releases the accumulators; the stores drain after.
 template <int G>
-__device__ __forceinline__ void oz_epilogue_chunk(uint32_t tbase, int quarter, int lane, const OzParams& p, int I,
-                                                  int J, double* part, bool first_chunk) {
+__device__ __forceinline__ void oz_readout(uint32_t trow, const OzParams& p, int I, int J, int quarter, int lane,
+                                           int col0, const int* ecol, double* tile_out) {
   constexpr int kW = OzGroup<G>::kW, kW0 = OzGroup<G>::kW0;
-  const int r = I * 128 + quarter * 32 + lane;
-  const uint32_t trow = tbase + (static_cast<uint32_t>(quarter * 32) << 16);
-  const int er = r < p.M ? p.exps[r] : 0;
-  for (int cb = 0; cb < 4; ++cb) {
-    double v[32];
-    int c32[32];
-    tmem_ld32(trow + (kW - 1) * 128 + cb * 32, c32);
+  const int rl = quarter * 32 + lane, r = I * 128 + rl;
+  const bool rok = r < p.M;
+  const int er = (rok ? p.exps[r] : 0) + 4 - 8 * kW0;
+  double* dst = tile_out + rl * 128;
+#pragma unroll 2
+  for (int cb = col0 / 8; cb < col0 / 8 + 8; ++cb) {
+    double v[8];
+    int c[8];
+    tmem_ld8(trow + (kW - 1) * 128 + cb * 8, c);
+    tmem_wait_ld();
 #pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = static_cast<double>(c32[q]);
+    for (int q = 0; q < 8; ++q) v[q] = static_cast<double>(c[q]);
 #pragma unroll
     for (int a = kW - 2; a >= 0; --a) {
-      tmem_ld32(trow + a * 128 + cb * 32, c32);
+      tmem_ld8(trow + a * 128 + cb * 8, c);
+      tmem_wait_ld();
 #pragma unroll
-      for (int q = 0; q < 32; ++q) v[q] = fma(v[q], 0x1.0p-8, static_cast<double>(c32[q]));
+      for (int q = 0; q < 8; ++q) v[q] = fma(v[q], 0x1.0p-8, static_cast<double>(c[q]));
     }
-    const int cbase = J * 128 + cb * 32;
-    if (r < p.M) {
-      double* dst = part + static_cast<long long>(r) * p.ldg + cbase;
+    if (rok) {
 #pragma unroll
-      for (int q = 0; q < 32; ++q) {
-        const int c = cbase + q;
-        if (c < p.M) {
-          const double s = ldexp(v[q], er + p.exps[c] + 4 - 8 * kW0);
-          dst[q] = first_chunk ? s : dst[q] + s;
-        }
-      }
+      for (int q = 0; q < 8; q += 2)
+        *reinterpret_cast<double2*>(dst + cb * 8 + q) =
+            make_double2(scale2(v[q], er + ecol[cb * 8 + q]), scale2(v[q + 1], er + ecol[cb * 8 + q + 1]));
     }
-    __syncwarp();
   }
 }
 
-__global__ void __launch_bounds__(192, 1) oz_gram_kernel(const __grid_constant__ CUtensorMap tmS, OzParams p) {
+constexpr int kOz2Threads = 320;  // producer warp, MMA warp, 8 epilogue warps (2 per TMEM lane quarter)
+constexpr uint32_t kOz2Stage = kOzPlanes * (kOzTileBytes + kOzBHalfBytes);  // 42 KB: a group-1 k-step
+constexpr int kOz2Stages = static_cast<int>(kOzRing / kOz2Stage);
+
+// Persistent: cluster c of C processes items c, c + C, ... (group-1 items first, then group 0; split-
+// major; pair blocks in the host's order).  An item is at most one int32-safe chunk (512 k-steps), so
+// its accumulators are read out once, straight into the item's own packed partial tile (no
+// read-modify-write); the fixed-order reduction (oz_finish_kernel) sums the partials.  The stage ring
+// and the accumulator barriers run on across items: the producer streams the next item's operands
+// while the epilogue drains the previous item's accumulators (released after its last TMEM load).
+__global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
+    oz_gram2_kernel(const __grid_constant__ CUtensorMap tmA3g0, const __grid_constant__ CUtensorMap tmB3g0,
+                    const __grid_constant__ CUtensorMap tmA3g1, const __grid_constant__ CUtensorMap tmB3g1, OzParams p) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzRing);
@@ -217,124 +283,226 @@ __global__ void __launch_bounds__(192, 1) oz_gram_kernel(const __grid_constant__
   uint64_t* tempty = tfull + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(cluster_rank());
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int per = p.nTiles * p.splits;
+  const int nitems = 2 * per;
+  const int nst = min(p.max_stages > 0 ? p.max_stages : kOz2Stages, kOz2Stages);
 
-  // item decode: split-major; within a split the tiles in the host's order (square blocks of tiles, so
-  // the CTAs of a wave share few operand panels), each tile's group-1 item (the longer) before its
-  // group-0 item (both read planes 1..4 of the same panels)
-  const int item = blockIdx.x;
-  int split, G, ti;
-  if (p.interleave) {
-    split = item / (2 * p.nTiles);
-    const int r2 = item % (2 * p.nTiles);
-    G = (r2 & 1) ? 0 : 1;
-    ti = r2 >> 1;
-  } else {  // all group-1 items first (longest first), split-major
-    const int per = p.nTiles * p.splits;
-    G = item < per ? 1 : 0;
-    const int r = item < per ? item : item - per;
-    split = r / p.nTiles;
-    ti = r % p.nTiles;
-  }
-  const int2 tij = p.tiles[ti];
-  const int I = tij.x, J = tij.y;
-  const bool diag = I == J;
-  const long long kb = static_cast<long long>(split) * p.kPerSplit;
-  const long long ke = min(p.ksteps, kb + p.kPerSplit);
-  const int nk = ke > kb ? static_cast<int>(ke - kb) : 0;
-  const int planes = G == 0 ? OzGroup<0>::kPlanes : OzGroup<1>::kPlanes;
-  const uint32_t stage_bytes = (diag ? 1u : 2u) * planes * kOzTileBytes;
-  const int nst = min(p.max_stages > 0 ? p.max_stages : kOzMaxStages, static_cast<int>(kOzRing / stage_bytes));
+  struct Item {
+    int G, split, I, J, nk;
+    long long kb;
+  };
+  auto item_of = [&](int it) {
+    Item t;
+    t.G = it < per ? 1 : 0;
+    const int r = it < per ? it : it - per;
+    t.split = r / p.nTiles;
+    const int2 pj = p.tiles[r % p.nTiles];
+    t.I = 2 * pj.x + rank;
+    t.J = pj.y;
+    t.kb = static_cast<long long>(t.split) * p.kPerSplit;
+    const long long ke = min(p.ksteps, t.kb + p.kPerSplit);
+    t.nk = ke > t.kb ? static_cast<int>(ke - t.kb) : 0;
+    return t;
+  };
 
   if (threadIdx.x == 0) {
-    tma_prefetch_desc(&tmS);
+    tma_prefetch_desc(&tmA3g0);
+    tma_prefetch_desc(&tmB3g0);
+    tma_prefetch_desc(&tmA3g1);
+    tma_prefetch_desc(&tmB3g1);
     for (int s = 0; s < kOzMaxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
-    mbar_init(tempty, 4);
+    mbar_init(tempty, 16);
     fence_mbar_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tslot)));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tbase = *tslot;
-  double* part = p.ws + static_cast<long long>(split * 2 + G) * p.wsStride;
+  const uint32_t leader_full0 = mapa_u32(smem_u32(&full[0]), 0);
+  const uint32_t leader_tempty = mapa_u32(smem_u32(tempty), 0);
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int k = 0; k < nk; ++k) {
-        const int s = k % nst;
-        if (k >= nst) mbar_wait(&empty[s], ((k / nst) - 1) & 1);
-        unsigned char* st = smem + s * stage_bytes;
-        const int kr = static_cast<int>((kb + k) * 32);
-        mbar_arrive_expect_tx(&full[s], stage_bytes);
-        for (int pl = 0; pl < planes; ++pl) {
-          const int prow = static_cast<int>(pl * p.Npad + kr);
-          tma_load_2d(st + pl * kOzTileBytes, &tmS, &full[s], I * 128, prow);
-          if (!diag) tma_load_2d(st + (planes + pl) * kOzTileBytes, &tmS, &full[s], J * 128, prow);
+      long long gk = 0;  // k-steps issued by this CTA over all its items
+      for (int it = cl; it < nitems; it += ncl) {
+        const Item t = item_of(it);
+        const int planes = t.G ? OzGroup<1>::kPlanes : OzGroup<0>::kPlanes;
+        const uint32_t a_bytes = planes * kOzTileBytes, bytes = planes * (kOzTileBytes + kOzBHalfBytes);
+        for (int k = 0; k < t.nk; ++k, ++gk) {
+          const int s = static_cast<int>(gk % nst);
+          if (gk >= nst) mbar_wait(&empty[s], static_cast<uint32_t>((gk / nst) - 1) & 1);
+          if (p.dbg_notma) {
+            if (rank == 0) mbar_arrive(&full[s]);
+            continue;
+          }
+          unsigned char* st = smem + s * kOz2Stage;
+          const int kr = static_cast<int>((t.kb + k) * 32);
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
+          const uint32_t bar = leader_full0 + s * 8;
+          tma_load_3d_pair(st, t.G ? &tmA3g1 : &tmA3g0, bar, t.I * 128, kr, 0);
+          tma_load_3d_pair(st + a_bytes, t.G ? &tmB3g1 : &tmB3g0, bar, t.J * 128 + 64 * rank, kr, 0);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      for (int k = 0; k < nk; ++k) {
-        const int s = k % nst;
-        const int kc = k % kOzChunk;
-        if (kc == 0 && k > 0) {  // the epilogue must have drained the previous chunk
-          mbar_wait(tempty, ((k / kOzChunk) - 1) & 1);
-          tc_fence_after();
-        }
-        mbar_wait(&full[s], (k / nst) & 1);
+    if (rank == 0) {  // the whole warp runs the issue loop (uniform operands); oz_mma2 elects one lane
+      long long gk = 0, gi = 0;  // k-steps and non-empty items so far
+      long long t_te = 0, t_full = 0, t_all = clock64();
+      for (int it = cl; it < nitems; it += ncl) {
+        const Item t = item_of(it);
+        if (t.nk == 0) continue;
+        const uint32_t a_bytes = (t.G ? OzGroup<1>::kPlanes : OzGroup<0>::kPlanes) * kOzTileBytes;
+        long long c0 = p.dbg ? clock64() : 0;
+        if (gi > 0) mbar_wait(tempty, static_cast<uint32_t>(gi - 1) & 1);  // previous item read out
+        if (p.dbg) t_te += clock64() - c0;
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + s * stage_bytes);
-        const uint32_t sb = diag ? sa : sa + planes * kOzTileBytes;
-        if (G == 0) oz_mma_kstep<0>(tbase, sa, sb, kc == 0);
-        else oz_mma_kstep<1>(tbase, sa, sb, kc == 0);
-        oz_commit(&empty[s]);
-        if (kc == kOzChunk - 1 || k == nk - 1) oz_commit(tfull);
+        for (int k = 0; k < t.nk; ++k, ++gk) {
+          const int s = static_cast<int>(gk % nst);
+          c0 = p.dbg ? clock64() : 0;
+          mbar_wait(&full[s], static_cast<uint32_t>(gk / nst) & 1);
+          if (p.dbg) t_full += clock64() - c0;
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + s * kOz2Stage);
+          if (t.G == 0) oz_mma_kstep2<0>(tbase, sa, sa + a_bytes, k == 0);
+          else oz_mma_kstep2<1>(tbase, sa, sa + a_bytes, k == 0);
+          oz_commit2(&empty[s]);
+        }
+        oz_commit2(tfull);
+        ++gi;
+      }
+      if (p.dbg && lane == 0) {
+        atomicAdd(p.dbg + 0, static_cast<unsigned long long>(t_te));
+        atomicAdd(p.dbg + 1, static_cast<unsigned long long>(t_full));
+        atomicAdd(p.dbg + 2, static_cast<unsigned long long>(clock64() - t_all));
+        atomicAdd(p.dbg + 3, static_cast<unsigned long long>(gk));
+        atomicAdd(p.dbg + 4, static_cast<unsigned long long>(gi));
       }
     }
   } else {
-    const int quarter = warp & 3;
-    const int nchunks = (nk + kOzChunk - 1) / kOzChunk;
-    for (int ch = 0; ch < nchunks; ++ch) {
-      mbar_wait(tfull, ch & 1);
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const uint32_t trow = tbase + (static_cast<uint32_t>(quarter * 32) << 16);
+    int* ecol = reinterpret_cast<int*>(tslot + 4) + 64 * half;  // this warp pair's 64 column exponents
+    long long gi = 0;
+    for (int it = cl; it < nitems; it += ncl) {
+      const Item t = item_of(it);
+      const bool store = t.I < p.nbI && t.J <= t.I;  // the block above the diagonal is not stored
+      double* tile_out = p.ws + static_cast<long long>(t.split * 2 + t.G) * p.wsStride +
+                         static_cast<long long>(store ? t.I * (t.I + 1) / 2 + t.J : 0) * 16384;
+      if (t.nk == 0) {  // empty split: a zero partial
+        if (store)
+          for (int c = half * 64; c < half * 64 + 64; ++c) tile_out[(quarter * 32 + lane) * 128 + c] = 0.0;
+        continue;
+      }
+      // column exponents of this item, staged while the MMAs run (the previous item's read-out by this
+      // warp pair is complete: warps of one pair cover disjoint quarters, so sync the pair)
+      named_bar_sync_n(1 + half, 128);
+      if (quarter == 0 || quarter == 1) {  // two of the pair's four warps fill its 64 entries
+        const int c = t.J * 128 + half * 64 + (quarter & 1) * 32 + lane;
+        ecol[(quarter & 1) * 32 + lane] = p.exps[min(c, p.Mpad - 1)];
+      }
+      named_bar_sync_n(1 + half, 128);
+      long long c1 = (p.dbg && lane == 0) ? clock64() : 0;
+      mbar_wait(tfull, static_cast<uint32_t>(gi) & 1);
       tc_fence_after();
-      if (G == 0) oz_epilogue_chunk<0>(tbase, quarter, lane, p, I, J, part, ch == 0);
-      else oz_epilogue_chunk<1>(tbase, quarter, lane, p, I, J, part, ch == 0);
+      long long c2 = (p.dbg && lane == 0) ? clock64() : 0;
+      OzParams q = p;
+      if (!store) q.M = 0;
+      if (t.G == 0) oz_readout<0>(trow, q, t.I, t.J, quarter, lane, half * 64, ecol - 64 * half, tile_out);
+      else oz_readout<1>(trow, q, t.I, t.J, quarter, lane, half * 64, ecol - 64 * half, tile_out);
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty);
-    }
-    if (nchunks == 0) {  // empty split: the partial is zero
-      const int r = I * 128 + quarter * 32 + lane;
-      if (r < p.M)
-        for (int c = J * 128; c < min(p.M, J * 128 + 128); ++c) part[static_cast<long long>(r) * p.ldg + c] = 0.0;
+      if (lane == 0) mbar_arrive_cluster(leader_tempty);
+      if (p.dbg && lane == 0) {
+        atomicAdd(p.dbg + 5, static_cast<unsigned long long>(c2 - c1));
+        atomicAdd(p.dbg + 6, static_cast<unsigned long long>(clock64() - c2));
+      }
+      ++gi;
     }
   }
-  __syncthreads();
+  tc_fence_before();
+  cluster_sync_all();  // all MMAs consumed, all remote arrivals delivered
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
   }
 }
 
-size_t oz_gram_smem() { return size_t(kOzRing) + 1024 + 256; }
+// Fixed-order reduction of the packed partial tiles: G[i][j] = G[j][i] = (acc ? G[i][j] : 0) +
+// sum_{slot} part[slot][tile(i, j)][i % 128][j % 128] over the lower triangle, slots in increasing
+// order (split-major, group 0 before group 1 within a split).  One CTA per 32 x 32 block, staged in
+// shared memory for the mirrored (transposed) half.
+__global__ void __launch_bounds__(256) oz_finish_kernel(const double* __restrict__ ws, long long wsStride, int slots,
+                                                        int M, double* G, long long ldg, int accumulate) {
+  __shared__ double blk[32][33];
+  const int nb = (M + 31) / 32;
+  const int b = blockIdx.x;
+  int bi = static_cast<int>((sqrt(8.0 * b + 1.0) - 1.0) * 0.5);
+  while (bi * (bi + 1) / 2 > b) --bi;
+  while ((bi + 1) * (bi + 2) / 2 <= b) ++bi;
+  const int bj = b - bi * (bi + 1) / 2;
+  if (bi >= nb) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int i0 = bi * 32, j0 = bj * 32;
+  for (int rr = ty; rr < 32; rr += 8) {
+    const int i = i0 + rr, j = j0 + tx;
+    double v = 0.0;
+    if (i < M && j <= i) {
+      const int I = i >> 7, J = j >> 7;
+      const long long off = static_cast<long long>(I * (I + 1) / 2 + J) * 16384 + (i & 127) * 128 + (j & 127);
+      v = ws[off];
+      for (int sl = 1; sl < slots; ++sl) v = add_rn(v, ws[sl * wsStride + off]);
+      if (accumulate) v = add_rn(G[static_cast<long long>(i) * ldg + j], v);
+      G[static_cast<long long>(i) * ldg + j] = v;
+    }
+    blk[rr][tx] = v;
+  }
+  __syncthreads();
+  for (int rr = ty; rr < 32; rr += 8) {  // mirror: G[j0 + rr][i0 + tx] = blk[tx][rr]
+    const int j = j0 + rr, i = i0 + tx;
+    if (i < M && j < M && (bi != bj || rr < tx)) G[static_cast<long long>(j) * ldg + i] = blk[tx][rr];
+  }
+}
 
-// Lower-triangle tiles of an nbI x nbI tile grid in square blocks of B x B tiles (block rows and columns
-// in lower-triangle order, tiles row-major inside a block): about num_sms consecutive tiles then read
-// ~2 sqrt(num_sms) panels instead of up to nbI + 3.
-void oz_tile_order(int nbI, int B, int2* out) {
+cudaError_t launch_oz_finish(const double* ws, long long wsStride, int slots, int M, double* G, long long ldg,
+                             int accumulate, cudaStream_t s) {
+  const int nb = (M + 31) / 32;
+  oz_finish_kernel<<<nb * (nb + 1) / 2, 256, 0, s>>>(ws, wsStride, slots, M, G, ldg, accumulate);
+  return cudaGetLastError();
+}
+
+// (pair, J) blocks of the CTA-pair Gram: pair P covers tile rows 2P, 2P + 1 and columns J <= 2P + 1
+// (< nbI), in square blocks of B pairs x 2B columns
+int oz_pair_order(int nbI, int B, int2* out) {
+  const int np = (nbI + 1) / 2;
   int n = 0;
-  for (int bi = 0; bi * B < nbI; ++bi)
-    for (int bj = 0; bj <= bi; ++bj)
-      for (int i = bi * B; i < std::min(nbI, bi * B + B); ++i)
-        for (int j = bj * B; j < std::min(i + 1, bj * B + B); ++j) out[n++] = make_int2(i, j);
+  for (int bp = 0; bp * B < np; ++bp)
+    for (int bj = 0; bj * 2 * B <= std::min(nbI - 1, 2 * (bp * B + B - 1) + 1); ++bj)
+      for (int P = bp * B; P < std::min(np, bp * B + B); ++P)
+        for (int J = bj * 2 * B; J < std::min({nbI, 2 * P + 2, bj * 2 * B + 2 * B}); ++J) out[n++] = make_int2(P, J);
+  return n;
+}
+
+cudaError_t launch_oz_gram2(const CUtensorMap* maps, const OzParams& p, cudaStream_t s) {
+  const size_t smem = size_t(kOzRing) + 2048;  // ring, barriers, TMEM slot, 128 column exponents, alignment
+  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(oz_gram2_kernel), smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int items = 2 * p.nTiles * p.splits;
+  const int clusters = std::min(items, nsm / 2);
+  oz_gram2_kernel<<<2 * clusters, kOz2Threads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_oz_colmax(const double* A, long long lda, long long N, int M, unsigned long long* cmax,
@@ -358,14 +526,6 @@ cudaError_t launch_oz_slice(const double* A, long long lda, long long N, int M, 
   const long long work = Npad * (Mpad / 8);
   const unsigned grid = static_cast<unsigned>(std::min<long long>((work + 255) / 256, 148LL * 16));
   oz_slice_kernel<<<grid, 256, 0, s>>>(A, lda, N, M, exps, S, static_cast<long long>(Mpad) * Npad, Mpad, Npad);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_oz_gram(const CUtensorMap& tmS, const OzParams& p, cudaStream_t s) {
-  const size_t smem = oz_gram_smem();
-  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(oz_gram_kernel), smem);
-  if (e != cudaSuccess) return e;
-  oz_gram_kernel<<<2 * p.nTiles * p.splits, 192, smem, s>>>(tmS, p);
   return cudaGetLastError();
 }
 

@@ -69,18 +69,19 @@ struct SyrkParams {
 struct OzParams {
   int M;              // columns of A
   int nbI;            // 128-wide tile rows
-  int nTiles;         // nbI (nbI + 1) / 2
+  int nTiles;         // (pair, column) blocks in p.tiles
   int splits;
-  int Mpad;           // nbI * 128 (plane row length)
+  int Mpad;           // plane row length (whole tile-row pairs)
   long long Npad;     // plane rows (multiple of 64)
   long long ksteps;   // Npad / 32
-  long long kPerSplit;  // k-steps per split
+  long long kPerSplit;  // k-steps per split (<= 512)
   const int* exps;
-  const int2* tiles;  // lower-triangle tiles (I, J) in launch order (oz_tile_order)
-  double* ws;         // slot (split * 2 + group): ws + slot * wsStride, ld ldg
-  long long wsStride, ldg;
-  int interleave;     // item order: 1 = per tile (group 1, group 0) adjacent; 0 = all group-1 items first
-  int max_stages;     // 0: as many as fit
+  const int2* tiles;  // (pair P, column J) blocks in launch order (oz_pair_order)
+  double* ws;         // packed partial slots: slot (split * 2 + group) at ws + slot * wsStride
+  long long wsStride;
+  int max_stages;     // 0: as many as fit (diagnostic override)
+  int dbg_notma;      // diagnostic only (tools/ozaki_test): skip the operand loads
+  unsigned long long* dbg;  // diagnostic cycle counters (tools/ozaki_test), null in production
 };
 
 // ---- generic DMMA GEMM: C = alpha * op(A) op(B) + beta * C (row-major)

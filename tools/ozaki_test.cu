@@ -3,6 +3,7 @@
 //                               Gram vs a long-double CPU reference
 //   ozaki_test time N M reps  : device-generated columns, kernel timing only
 #include "../paper_2011_02436_b200/csrc/k_ozaki.cu"
+constexpr long long kOzChunkRows = 16384;
 
 #include <cuda.h>
 #include <cstdio>
@@ -33,16 +34,6 @@ __global__ void gen_kernel(double* H, long long N, int M, long long ld, unsigned
     double zz = (u - 0.5) * 12.0 + 0.37 * (c % 17) - 3.0;
     H[r * ld + c] = 1.0 / (1.0 + exp(-zz));
   }
-}
-
-__global__ void finish_kernel(const double* ws, long long stride, int slots, int M, long long ldg, double* G) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= (long long)M * M) return;
-  int r = (int)(i / M), c = (int)(i % M);
-  int a = r >= c ? r : c, b = r >= c ? c : r;
-  double v = ws[(long long)a * ldg + b];
-  for (int s = 1; s < slots; ++s) v += ws[s * stride + (long long)a * ldg + b];
-  G[(long long)r * M + c] = v;
 }
 
 int main(int argc, char** argv) {
@@ -77,47 +68,41 @@ int main(int argc, char** argv) {
     CK(cudaGetLastError());
   }
   int nsm = 148;
-  const int nbI = (M + 127) / 128, Mpad = nbI * 128;
+  (void)nsm;
+  const int nbI = (M + 127) / 128, Mpad = (nbI + 1) / 2 * 2 * 128;
   const long long Npad = (N + 63) / 64 * 64;
-  const int nTiles = nbI * (nbI + 1) / 2;
+  std::vector<int2> order((size_t)nbI * nbI + 2);
+  const int nTiles = oz_pair_order(nbI, getenv("OZ_PBLOCK") ? atoi(getenv("OZ_PBLOCK")) : 3, order.data());
   const long long ksteps = Npad / 32;
-  int splits = splits_arg;
-  if (splits <= 0) {
-    splits = (int)((2LL * nsm + 2 * nTiles - 1) / (2 * nTiles));
-    if (splits < 1) splits = 1;
-    long long maxsp = ksteps / 128;
-    if (maxsp < 1) maxsp = 1;
-    if (splits > maxsp) splits = (int)maxsp;
-  }
-  long long per = (ksteps + splits - 1) / splits;
-  splits = (int)((ksteps + per - 1) / per);
-  unsigned long long* cmax; int* exps; int8_t* S; double* ws; double* G;
+  const long long per = kOzChunkRows / 32;
+  const int splits = (int)((ksteps + per - 1) / per);
+  unsigned long long* cmax; int* exps; int8_t* S; double* ws; double* G; int2* dtiles;
   CK(cudaMalloc(&cmax, 8 * M));
   CK(cudaMalloc(&exps, 4 * Mpad));
   CK(cudaMalloc(&S, (size_t)kOzPlanes * Mpad * Npad));
-  const long long ldg = ld;
-  const long long wsStride = (long long)M * ldg;
+  const long long wsStride = (long long)(nbI * (nbI + 1) / 2) * 16384;
   CK(cudaMalloc(&ws, sizeof(double) * wsStride * 2 * splits));
   CK(cudaMalloc(&G, sizeof(double) * M * M));
-
-  // tensor map over the planes: [7 * Mpad rows][Npad bytes]
-  CUtensorMap tm;
-  cuuint64_t dims[2] = {(cuuint64_t)Mpad, (cuuint64_t)kOzPlanes * Npad};
-  cuuint64_t strides[1] = {(cuuint64_t)Mpad};
-  cuuint32_t box[2] = {128, 32};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult cr = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, S, dims, strides, box, estr,
-                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (cr != CUDA_SUCCESS) { printf("encode failed %d\n", (int)cr); return 1; }
-  std::vector<int2> order(nTiles);
-  const int blk = getenv("OZ_BLOCK") ? atoi(getenv("OZ_BLOCK")) : 6;
-  oz_tile_order(nbI, blk, order.data());
-  int2* dtiles;
   CK(cudaMalloc(&dtiles, sizeof(int2) * nTiles));
   CK(cudaMemcpy(dtiles, order.data(), sizeof(int2) * nTiles, cudaMemcpyHostToDevice));
-  OzParams p{M, nbI, nTiles, splits, Mpad, Npad, ksteps, per, exps, dtiles, ws, wsStride, ldg,
-              getenv("OZ_INTERLEAVE") ? atoi(getenv("OZ_INTERLEAVE")) : 1, getenv("OZ_STAGES") ? atoi(getenv("OZ_STAGES")) : 0};
+  CUtensorMap maps[4];
+  for (int g = 0; g < 2; ++g)
+    for (int ab = 0; ab < 2; ++ab) {
+      cuuint64_t d3[3] = {(cuuint64_t)Mpad, (cuuint64_t)Npad, (cuuint64_t)kOzPlanes};
+      cuuint64_t s3[2] = {(cuuint64_t)Mpad, (cuuint64_t)Mpad * Npad};
+      cuuint32_t b3[3] = {ab ? 64u : 128u, 32u, g ? 7u : 4u};
+      cuuint32_t e3[3] = {1, 1, 1};
+      CUresult cr = cuTensorMapEncodeTiled(&maps[2 * g + ab], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, S, d3, s3, b3, e3,
+                                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                           ab ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) { printf("encode failed %d\n", (int)cr); return 1; }
+    }
+  OzParams p{M, nbI, nTiles, splits, Mpad, Npad, ksteps, per, exps, dtiles, ws, wsStride,
+             getenv("OZ_STAGES") ? atoi(getenv("OZ_STAGES")) : 0, getenv("OZ_NOTMA") ? atoi(getenv("OZ_NOTMA")) : 0,
+             nullptr};
+  unsigned long long* ddbg = nullptr;
+  if (getenv("OZ_DBG")) { CK(cudaMalloc(&ddbg, 64)); CK(cudaMemset(ddbg, 0, 64)); p.dbg = ddbg; }
   cudaEvent_t e0, e1, e2, e3;
   cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2); cudaEventCreate(&e3);
   float best_slice = 1e30f, best_gram = 1e30f;
@@ -126,7 +111,7 @@ int main(int argc, char** argv) {
     CK(launch_oz_colmax(dH, ld, N, M, cmax, nsm, 0));
     CK(launch_oz_slice(dH, ld, N, M, cmax, exps, Mpad, Npad, S, 0));
     cudaEventRecord(e1);
-    CK(launch_oz_gram(tm, p, 0));
+    CK(launch_oz_gram2(maps, p, 0));
     cudaEventRecord(e2);
     CK(cudaEventSynchronize(e2));
     CK(cudaGetLastError());
@@ -137,11 +122,18 @@ int main(int argc, char** argv) {
     if (b < best_gram) best_gram = b;
   }
   CK(cudaDeviceSynchronize());
+  if (ddbg) {
+    unsigned long long h[8];
+    CK(cudaMemcpy(h, ddbg, 64, cudaMemcpyDeviceToHost));
+    printf("dbg (summed over clusters, all reps): MMA tempty-wait %.3g cyc, full-wait %.3g, total %.3g, ksteps %llu, items %llu; "
+           "epi tfull-wait %.3g, readout %.3g (per warp-item: %.0f)\n", (double)h[0], (double)h[1], (double)h[2], h[3], h[4],
+           (double)h[5], (double)h[6], (double)h[6] / (h[4] * 16.0));
+  }
   const double fl = (double)N * M * (M + 1);  // algorithmic flops of the lower-triangle Gram
-  const double iops = 28.0 * 2.0 * 128 * 128 * (double)Npad * nTiles;
-  printf("[blk %s il %s st %s] N=%lld M=%d tiles=%d splits=%d items=%d  slice %.3f ms  gram %.3f ms  => %.2f FP64-equiv TF/s, %.1f int8 TOPS\n",
-         getenv("OZ_BLOCK"), getenv("OZ_INTERLEAVE"), getenv("OZ_STAGES"), N, M, nTiles, splits, 2 * nTiles * splits, best_slice, best_gram, fl / best_gram * 1e-9, iops / best_gram * 1e-9);
-  finish_kernel<<<(unsigned)(((long long)M * M + 255) / 256), 256>>>(ws, wsStride, 2 * splits, M, ldg, G);
+  const double iops = 28.0 * 2.0 * 128 * 128 * (double)Npad * (nbI * (nbI + 1) / 2);  // lower tiles only
+  printf("N=%lld M=%d tiles=%d splits=%d items=%d  slice %.3f ms  gram %.3f ms  => %.2f FP64-equiv TF/s, %.1f int8 TOPS\n",
+         N, M, nTiles, splits, 2 * nTiles * splits, best_slice, best_gram, fl / best_gram * 1e-9, iops / best_gram * 1e-9);
+  CK(launch_oz_finish(ws, wsStride, 2 * splits, M, G, M, 0, 0));
   CK(cudaDeviceSynchronize());
   if (check) {
     std::vector<double> g((size_t)M * M);
