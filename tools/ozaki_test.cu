@@ -74,7 +74,7 @@ int main(int argc, char** argv) {
   std::vector<int2> order((size_t)nbI * nbI + 2);
   const int nTiles = oz_pair_order(nbI, getenv("OZ_PBLOCK") ? atoi(getenv("OZ_PBLOCK")) : 3, order.data());
   const long long ksteps = Npad / 32;
-  const long long per = kOzChunkRows / 32;
+  const long long per = getenv("OZ_KPER") ? atoll(getenv("OZ_KPER")) : kOzChunkRows / 32;
   const int splits = (int)((ksteps + per - 1) / per);
   unsigned long long* cmax; int* exps; int8_t* S; double* ws; double* G; int2* dtiles;
   CK(cudaMalloc(&cmax, 8 * M));
