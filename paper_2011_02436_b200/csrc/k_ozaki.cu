@@ -95,38 +95,62 @@ __global__ void oz_exps_kernel(const unsigned long long* cmax, int M, int Mpad, 
 
 // Digit planes, [plane][row][column] with the padded extents (rows >= N, columns >= M: zeros).
 // One thread per 8 consecutive columns of a row: 64 bytes of A in, 8 bytes per plane out.
+// Balanced digits without a digit loop: adding B = 0x808080808080 (128 in each of the six low bytes)
+// turns X = sum_i d_i 256^i (d_0..d_5 in [-128, 127]) into X + B = sum_{i<6} (d_i + 128) 256^i +
+// d_6 256^6 with every d_i + 128 in [0, 255] -- byte i of X + B is d_i + 128, i.e. d_i ^ 0x80 as a
+// signed byte, and (X + B) >> 48 is the top digit d_6.  So V = (X + B) ^ B holds all seven digit bytes
+// (byte i: plane 6 - i), and the 8 x 8 byte transpose of a thread's 8 values into its 8-byte plane
+// words takes four 4 x 4 PRMT transposes.
+// 2^e for a normal exponent (-1022 <= e <= 1023)
+__device__ __forceinline__ double pow2i(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
+
+__device__ __forceinline__ void byte_transpose4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t (&r)[4]) {
+  const uint32_t t0 = __byte_perm(a, b, 0x5140), t1 = __byte_perm(a, b, 0x7362);
+  const uint32_t t2 = __byte_perm(c, d, 0x5140), t3 = __byte_perm(c, d, 0x7362);
+  r[0] = __byte_perm(t0, t2, 0x5410);
+  r[1] = __byte_perm(t0, t2, 0x7632);
+  r[2] = __byte_perm(t1, t3, 0x5410);
+  r[3] = __byte_perm(t1, t3, 0x7632);
+}
+
 __global__ void __launch_bounds__(256) oz_slice_kernel(const double* __restrict__ A, long long lda, long long N, int M,
                                                        const int* __restrict__ exps, int8_t* __restrict__ S,
                                                        long long plane_stride, int Mpad, long long Npad) {
+  constexpr unsigned long long kBias = 0x808080808080ull;
   const int groups = Mpad / 8;
   const long long total = Npad * groups;
   for (long long it = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; it < total;
        it += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long r = it / groups;
     const int c0 = static_cast<int>(it - r * groups) * 8;
-    unsigned long long w[kOzPlanes];
+    uint32_t lo[8], hi[8];
 #pragma unroll
-    for (int p = 0; p < kOzPlanes; ++p) w[p] = 0;
-    if (r < N) {
-      const double* row = A + r * lda;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int c = c0 + q;
-        long long X = 0;
-        if (c < M) X = __double2ll_rn(ldexp(row[c], 54 - exps[c]));
-        // balanced base-256 digits from the least significant one
-#pragma unroll
-        for (int p = kOzPlanes - 1; p >= 1; --p) {
-          const long long dgt = ((X + 128) & 255) - 128;
-          X = (X - dgt) >> 8;
-          w[p] |= (static_cast<unsigned long long>(dgt) & 255ull) << (8 * q);
-        }
-        w[0] |= (static_cast<unsigned long long>(X) & 255ull) << (8 * q);
+    for (int q = 0; q < 8; ++q) {
+      const int c = c0 + q;
+      long long X = 0;
+      if (r < N && c < M) {
+        // A 2^(54 - e) exactly (|.| < 2^54): one power-of-two factor, two when 54 - e exceeds the
+        // normal exponent range (columns with max < 2^-969); a result below 2^-1022 rounds to 0 either way
+        const int k = 54 - exps[c];
+        double v = A[r * lda + c] * pow2i(min(k, 1023));
+        if (k > 1023) v *= pow2i(k - 1023);
+        X = __double2ll_rn(v);
       }
+      const unsigned long long V = (static_cast<unsigned long long>(X) + kBias) ^ kBias;
+      lo[q] = static_cast<uint32_t>(V);
+      hi[q] = static_cast<uint32_t>(V >> 32);
     }
+    uint32_t l0[4], l1[4], h0[4], h1[4];  // [byte] words of columns 0-3 / 4-7
+    byte_transpose4(lo[0], lo[1], lo[2], lo[3], l0);
+    byte_transpose4(lo[4], lo[5], lo[6], lo[7], l1);
+    byte_transpose4(hi[0], hi[1], hi[2], hi[3], h0);
+    byte_transpose4(hi[4], hi[5], hi[6], hi[7], h1);
+    int8_t* dst = S + r * Mpad + c0;
 #pragma unroll
-    for (int p = 0; p < kOzPlanes; ++p)
-      *reinterpret_cast<unsigned long long*>(S + p * plane_stride + r * Mpad + c0) = w[p];
+    for (int i = 0; i < 7; ++i) {  // byte i -> plane 6 - i
+      const uint32_t w0 = i < 4 ? l0[i & 3] : h0[i & 3], w1 = i < 4 ? l1[i & 3] : h1[i & 3];
+      *reinterpret_cast<uint2*>(dst + (kOzPlanes - 1 - i) * plane_stride) = make_uint2(w0, w1);
+    }
   }
 }
 
@@ -209,7 +233,6 @@ __device__ __forceinline__ void oz_mma_kstep2(uint32_t tbase, uint32_t sa, uint3
 
 // x 2^e without a libm call: two exact power-of-two factors, each inside the normal exponent range
 // for |e| <= 2044 (column exponents of finite data)
-__device__ __forceinline__ double pow2i(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
 __device__ __forceinline__ double scale2(double x, int e) {
   const int e1 = e / 2;
   return (x * pow2i(e1)) * pow2i(e - e1);
