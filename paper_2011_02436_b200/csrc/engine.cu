@@ -100,6 +100,7 @@ cudaError_t launch_oz_colmax(const double*, long long, long long, int, unsigned 
 cudaError_t launch_oz_slice(const double*, long long, long long, int, const unsigned long long*, int*, int, long long,
                             int8_t*, cudaStream_t);
 cudaError_t launch_oz_gram2(const CUtensorMap* maps, const OzParams&, cudaStream_t);
+cudaError_t launch_oz_hidden(const CUtensorMap* maps, const OzHidParams&, cudaStream_t);
 int oz_pair_order(int nbI, int B, int2* out);
 cudaError_t launch_oz_finish(const double*, long long, int, int, double*, long long, int, cudaStream_t);
 cudaError_t launch_sum_parts(const double*, long long, int, long long, double*, cudaStream_t);
@@ -301,10 +302,86 @@ CUtensorMap make_map(rbpg_context* ctx, const double* base, uint64_t cols, uint6
 // ---------------------------------------------------------------------------
 // device building blocks
 // ---------------------------------------------------------------------------
+// 3-D map over digit planes [7][rows][cols] (int8): boxes of {bc, 32, planes}, 128- or 64-byte swizzle
+CUtensorMap plane_map(rbpg_context* ctx, int8_t* planes, size_t cols, size_t rows, uint32_t bc, uint32_t nplanes) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows), 7};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(cols) * rows};
+  cuuint32_t box[3] = {bc, 32u, nplanes};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = ctx->encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, planes, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, bc == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(RBPG_CUDA_ERROR, "cuTensorMapEncodeTiled (digit planes) failed (" + std::to_string(int(r)) + ")");
+  return m;
+}
+
+// K1i (k_ozaki.cu): H = sigmoid(X W + b) on the INT8 tensor cores.  W (d x L) and X^T (d x N) are cut
+// into digit planes with one exponent per W column / X row (the Gram's column scan + slice, on the
+// transposed X), then one persistent CTA-pair kernel computes 256-node x 128-row blocks of H^T with the
+// fused epilogue.  Scratch buffers are per stream: the e2e path builds row blocks on two streams.
+constexpr size_t kOzHidMaxD = 16384;  // int32 headroom of one k range: 7 d 2^14 < 2^31
+void hidden_oz_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_t d, const double* dW, size_t ldw,
+                   const double* db, size_t L, double* dH, size_t ldh) {
+  const size_t Nr = (N + 127) / 128 * 128, Kpad = (d + 31) / 32 * 32, Lp = (L + 255) / 256 * 256;
+  const std::string sfx = "." + std::to_string(reinterpret_cast<uintptr_t>(ctx->stream));
+  double* xt = ctx->dbuf("ozh.xt" + sfx, d * Nr);
+  for (size_t r0 = 0; r0 < N; r0 += (size_t(1) << 20)) {  // X^T in row chunks (grid.y limit of the transpose)
+    const size_t nr = std::min(N - r0, size_t(1) << 20);
+    ctx->run("oz_hidden_prep", [&] {
+      return launch_transpose(dX + r0 * ldx, static_cast<long long>(ldx), static_cast<long long>(nr),
+                              static_cast<long long>(d), xt + r0, static_cast<long long>(Nr), static_cast<long long>(nr),
+                              ctx->stream);
+    });
+  }
+  auto* cmx = reinterpret_cast<unsigned long long*>(ctx->dbuf("ozh.cmx" + sfx, N));
+  auto* cmw = reinterpret_cast<unsigned long long*>(ctx->dbuf("ozh.cmw" + sfx, L));
+  int* ex = reinterpret_cast<int*>(ctx->buf("ozh.ex" + sfx, Nr * sizeof(int)));
+  int* ew = reinterpret_cast<int*>(ctx->buf("ozh.ew" + sfx, Lp * sizeof(int)));
+  auto* px = reinterpret_cast<int8_t*>(ctx->buf("ozh.px" + sfx, 7 * Kpad * Nr));
+  auto* pw = reinterpret_cast<int8_t*>(ctx->buf("ozh.pw" + sfx, 7 * Kpad * Lp));
+  ctx->run("oz_hidden_prep", [&] {
+    return launch_oz_colmax(xt, static_cast<long long>(Nr), static_cast<long long>(d), static_cast<int>(N), cmx,
+                            ctx->num_sms, ctx->stream);
+  });
+  ctx->run("oz_hidden_prep", [&] {
+    return launch_oz_slice(xt, static_cast<long long>(Nr), static_cast<long long>(d), static_cast<int>(N), cmx, ex,
+                           static_cast<int>(Nr), static_cast<long long>(Kpad), px, ctx->stream);
+  });
+  ctx->run("oz_hidden_prep", [&] {
+    return launch_oz_colmax(dW, static_cast<long long>(ldw), static_cast<long long>(d), static_cast<int>(L), cmw,
+                            ctx->num_sms, ctx->stream);
+  });
+  ctx->run("oz_hidden_prep", [&] {
+    return launch_oz_slice(dW, static_cast<long long>(ldw), static_cast<long long>(d), static_cast<int>(L), cmw, ew,
+                           static_cast<int>(Lp), static_cast<long long>(Kpad), pw, ctx->stream);
+  });
+  CUtensorMap maps[4] = {plane_map(ctx, pw, Lp, Kpad, 128, 4), plane_map(ctx, px, Nr, Kpad, 64, 4),
+                         plane_map(ctx, pw, Lp, Kpad, 128, 7), plane_map(ctx, px, Nr, Kpad, 64, 7)};
+  OzHidParams p{};
+  p.N = static_cast<int>(N);
+  p.L = static_cast<int>(L);
+  p.nP = static_cast<int>(Lp / 256);
+  p.nJ = static_cast<int>(Nr / 128);
+  p.ksteps = static_cast<int>(Kpad / 32);
+  p.rexp = ex;
+  p.cexp = ew;
+  p.bias = db;
+  p.H = dH;
+  p.ldh = static_cast<long long>(ldh);
+  ctx->run("hidden_kernel", [&] { return launch_oz_hidden(maps, p, ctx->stream); });
+}
+
 void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_t d, const double* dW, size_t ldw,
                 const double* db, size_t L, double* dH, size_t ldh, const double* dT = nullptr, size_t ldt = 0,
                 size_t m = 0) {
   if (N == 0) return;
+  if (ctx->gram_int8 && d <= kOzHidMaxD && N < (size_t(1) << 31)) {
+    hidden_oz_dev(ctx, dX, ldx, N, d, dW, ldw, db, L, dH, ldh);
+    if (m > 0 && dT)  // augmented rows [H T]
+      ck(cudaMemcpy2DAsync(dH + L, ldh * 8, dT, ldt * 8, m * 8, N, cudaMemcpyDeviceToDevice, ctx->stream), "append T");
+    return;
+  }
   CUtensorMap tmX = make_map(ctx, dX, d, N, ldx, 16, kTile, true);
   constexpr int bn = 32;  // 128 x 32 tiles, three CTAs per SM (k_gemm.cu)
   CUtensorMap tmW = make_map(ctx, dW, L, d, ldw, bn + 4, kBK, false);  // padded smem rows

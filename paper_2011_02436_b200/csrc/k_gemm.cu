@@ -39,21 +39,6 @@ __device__ __forceinline__ unsigned char* align1024(unsigned char* p) {
   return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
 
-// 1 / x for x >= 1 (x = 1 + exp(-z) in the sigmoid) without the XU pipe: an integer-subtraction
-// seed on the bit pattern (relative error < 5.1%), then four Newton-Raphson steps on DFMA
-// (error 5e-2 -> 2.6e-3 -> 6.5e-6 -> 4e-11 -> ~1e-21 before rounding), the last one giving the
-// correctly rounded quotient in all tested cases.  The DP reciprocal seed (MUFU.RCP64H) is the
-// bottleneck of the sigmoid epilogue on sm_100 (XU pipe ~90% busy), DFMA is not.
-__device__ __forceinline__ double recip_ge1(double x) {
-  double y = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(x));
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-  }
-  return x <= 1.7976931348623157e308 ? y : (x > 0.0 ? 0.0 : x);  // 1/inf = 0, NaN propagates
-}
-
 }  // namespace
 
 // ============================================================================

@@ -237,6 +237,47 @@ __device__ __forceinline__ double scale2(double x, int e) {
   const int e1 = e / 2;
   return (x * pow2i(e1)) * pow2i(e - e1);
 }
+// exact int64 -> fp64 for |t| < 2^51 on the integer and FP64 pipes (I2F.F64 runs on the XU pipe, which
+// the sigmoid epilogue would saturate): the bits of 1.5 * 2^52 plus t are the double 1.5 * 2^52 + t
+__device__ __forceinline__ double i51_to_f64(long long t) {
+  constexpr double kMagic = 0x1.8p52;
+  return __longlong_as_double(__double_as_longlong(kMagic) + t) - kMagic;
+}
+// e^t without branches for the sigmoid epilogue (~1 ulp, like exp): t = k ln2 + r with k = rint(t / ln2)
+// read from the bits of the magic-shifted product (no F2I), r by two FMAs (|r| <= ln2 / 2), e^r by its
+// degree-13 Taylor polynomial (truncation < 2^-57; coefficients in constant memory, so every DFMA takes
+// its operand from the constant bank), 2^k as two exact factors; t > 709.78 -> inf and t < -745.14 -> 0
+// by selects.  Branch-free, so the unrolled epilogue interleaves many of them.
+__constant__ double c_exp_taylor[14] = {1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0,
+                                        1.0 / 362880.0,     1.0 / 40320.0,     1.0 / 5040.0,     1.0 / 720.0,
+                                        1.0 / 120.0,        1.0 / 24.0,        1.0 / 6.0,        0.5,
+                                        1.0,                1.0};
+__device__ __forceinline__ double exp_sig(double t) {
+  const double kb = fma(t, 0x1.71547652b82fep0, 0x1.8p52);
+  const int k = __double2loint(kb);
+  const double kd = kb - 0x1.8p52;
+  double r = fma(-kd, 0x1.62e42fefa39efp-1, t);
+  r = fma(-kd, 0x1.abc9e3b39803fp-56, r);
+  double q = c_exp_taylor[0];
+#pragma unroll
+  for (int i = 1; i < 14; ++i) q = fma(q, r, c_exp_taylor[i]);
+  const int k1 = k >> 1;
+  const double v = (q * pow2i(k1)) * pow2i(k - k1);
+  return t > 709.782712893384 ? __longlong_as_double(0x7ff0000000000000LL) : (t < -745.1332191019412 ? 0.0 : v);
+}
+// mbarrier wait that suspends the thread (up to the hint) instead of spinning: the producer and MMA
+// warps of oz_hidden_kernel share the SM sub-partitions with the epilogue's FP64 math
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITS_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
+      "@!p bra WAITS_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 
 // One chunk's read-out for one epilogue thread (row `quarter * 32 + lane`, 64 columns from `col0`):
@@ -268,13 +309,13 @@ __device__ __forceinline__ void oz_readout(uint32_t trow, const OzParams& p, int
     tmem_ld8(trow + (kW - 1) * 128 + cb * 8, c);
     tmem_wait_ld();
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = static_cast<double>(c[q]);
+    for (int q = 0; q < 8; ++q) v[q] = i51_to_f64(c[q]);
 #pragma unroll
     for (int a = kW - 2; a >= 0; --a) {
       tmem_ld8(trow + a * 128 + cb * 8, c);
       tmem_wait_ld();
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = fma(v[q], 0x1.0p-8, static_cast<double>(c[q]));
+      for (int q = 0; q < 8; ++q) v[q] = fma(v[q], 0x1.0p-8, i51_to_f64(c[q]));
     }
     if (rok) {
 #pragma unroll
@@ -460,6 +501,212 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// K1i: the hidden build H = sigmoid(X W + b) on the INT8 tensor cores -- reference elm.cpp:93-106
+// (XW at matrix.cpp:69-77, bias added after the full dot product elm.cpp:102, sigmoid elm.cpp:27).
+// Same digit-plane product as the Gram with W's columns and X's rows as the scaled dimensions:
+// W[k][c] = 2^(f_c - 54) sum_i dw_i 256^(7-i), X[r][k] = 2^(e_r - 54) sum_j dx_j 256^(7-j), so
+// (XW)[r][c] = 2^(f_c + e_r - 60) sum_{w=2..8} a_w 256^(8-w), a_w = sum_{i+j=w} (DW_i^T DX_j^T)[c][r]
+// (int32, exact while 7 d 2^14 < 2^31: d <= 16384).  The combination is exact up to one rounding:
+// v0 = sum_{w<=5} a_w 256^(5-w) < 2^50 and v1 = sum_{w>=6} a_w 256^(8-w) < 2^41 are exact integers (int64
+// Horner, converted exactly without I2F),
+// z = fma(v0, 2^24, v1) rounds once, the power-of-two scale is exact.
+// The accumulator is H^T: TMEM lane = hidden node, column = sample row, so an epilogue warp holds 32
+// consecutive hidden nodes of one row per store (coalesced 256-byte rows of H) and keeps its node's
+// exponent and bias in registers.
+// Execution: persistent CTA pairs as oz_gram2_kernel (M = 256 hidden nodes, N = 128 rows per item);
+// an item runs group 1 (w 6..8, planes 1..7, 3 accumulators, 18 products) over the whole k range,
+// then group 0 (w 2..5, planes 1..4, 4 accumulators = all 512 TMEM columns, 10 products).  The
+// epilogue reads group 1 into registers (v1, 64 rows per thread), adds group 0, releases TMEM -- the
+// next item's group-1 MMAs start -- and runs bias, sigmoid and the stores while they execute.
+// Operands: A = planes of W ([plane][k][node], MN-major), B = planes of X^T ([plane][k][row]).
+// ---------------------------------------------------------------------------------------------
+constexpr int kOzHidThreads = 576;  // producer warp, MMA warp, 16 epilogue warps (4 per TMEM lane quarter)
+__global__ void __launch_bounds__(kOzHidThreads, 1) __cluster_dims__(2, 1, 1)
+    oz_hidden_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+                     const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+                     OzHidParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzRing);
+  uint64_t* empty = full + kOzMaxStages;
+  uint64_t* tfull = empty + kOzMaxStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+  double* s_frow = reinterpret_cast<double*>(tslot + 4);  // [128] 2^(row exponent) of this item's rows
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(cluster_rank());
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nitems = p.nP * p.nJ;
+  const int nst = kOz2Stages;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA0);
+    tma_prefetch_desc(&tmB0);
+    tma_prefetch_desc(&tmA1);
+    tma_prefetch_desc(&tmB1);
+    for (int s = 0; s < kOzMaxStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 32);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t leader_full0 = mapa_u32(smem_u32(&full[0]), 0);
+  const uint32_t leader_tempty = mapa_u32(smem_u32(tempty), 0);
+  // item it: row tile J = it / nP (consecutive items share the X rows), node pair P = it % nP
+
+  if (warp == 0) {
+    if (lane == 0) {
+      long long gk = 0;
+      for (int it = cl; it < nitems; it += ncl) {
+        const int J = it / p.nP, P = it - J * p.nP;
+        for (int ph = 0; ph < 2; ++ph) {
+          const int g = 1 - ph;  // group 1 (18 products) first: its MMAs overlap the previous item's math
+          const int planes = g ? OzGroup<1>::kPlanes : OzGroup<0>::kPlanes;
+          const uint32_t a_bytes = planes * kOzTileBytes, bytes = planes * (kOzTileBytes + kOzBHalfBytes);
+          for (int k = 0; k < p.ksteps; ++k, ++gk) {
+            const int s = static_cast<int>(gk % nst);
+            if (gk >= nst) mbar_wait_sleep(&empty[s], static_cast<uint32_t>((gk / nst) - 1) & 1);
+            unsigned char* st = smem + s * kOz2Stage;
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
+            const uint32_t bar = leader_full0 + s * 8;
+            tma_load_3d_pair(st, g ? &tmA1 : &tmA0, bar, (2 * P + rank) * 128, k * 32, 0);
+            tma_load_3d_pair(st + a_bytes, g ? &tmB1 : &tmB0, bar, J * 128 + 64 * rank, k * 32, 0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // whole warp: uniform descriptors, oz_mma2 elects the issuing lane
+      long long gk = 0, q = 0;  // k-steps, accumulator phases (two per item)
+      for (int it = cl; it < nitems; it += ncl) {
+        for (int ph = 0; ph < 2; ++ph, ++q) {
+          const int g = 1 - ph;
+          if (q > 0) mbar_wait_sleep(tempty, static_cast<uint32_t>(q - 1) & 1);  // previous phase read out
+          tc_fence_after();
+          const uint32_t a_bytes = (g ? OzGroup<1>::kPlanes : OzGroup<0>::kPlanes) * kOzTileBytes;
+          for (int k = 0; k < p.ksteps; ++k, ++gk) {
+            const int s = static_cast<int>(gk % nst);
+            mbar_wait_sleep(&full[s], static_cast<uint32_t>(gk / nst) & 1);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + s * kOz2Stage);
+            if (g == 0) oz_mma_kstep2<0>(tbase, sa, sa + a_bytes, k == 0);
+            else oz_mma_kstep2<1>(tbase, sa, sa + a_bytes, k == 0);
+            oz_commit2(&empty[s]);
+          }
+          oz_commit2(tfull);
+        }
+      }
+    }
+  } else {
+    // 16 epilogue warps: warp w reads TMEM lane quarter w % 4; part = (w - 2) / 4 picks 32 of the item's
+    // 128 rows, so a thread holds 32 partial sums (64 registers) and the math of four warps per SM
+    // sub-partition interleaves
+    const int quarter = warp & 3, part = (warp - 2) >> 2;
+    const uint32_t trow = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + part * 32;
+    long long q = 0;
+    for (int it = cl; it < nitems; it += ncl) {
+      const int J = it / p.nP, P = it - J * p.nP;
+      const int c = (2 * P + rank) * 128 + quarter * 32 + lane;  // this thread's hidden node
+      const int r0 = J * 128 + part * 32;                          // its 32 rows
+      // this part's 32 row scales (the previous item's stores by these four warps are done)
+      named_bar_sync_n(1 + part, 128);
+      if (quarter == 0) {
+        const int r = r0 + lane;
+        s_frow[part * 32 + lane] = pow2i(r < p.N ? min(max(p.rexp[r], -1022), 1023) : 0);
+      }
+      named_bar_sync_n(1 + part, 128);
+      double v[32];
+      // group 1 (first): v1 = (a6 256 + a7) 256 + a8, exact (< 2^41)
+      mbar_wait(tfull, static_cast<uint32_t>(q) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        int a6[8], a7[8], a8[8];
+        tmem_ld8(trow + 0 * 128 + cb * 8, a6);
+        tmem_ld8(trow + 1 * 128 + cb * 8, a7);
+        tmem_ld8(trow + 2 * 128 + cb * 8, a8);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          v[cb * 8 + i] = i51_to_f64(((static_cast<long long>(a6[i]) << 8) + a7[i]) * 256 + a8[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty);
+      ++q;
+      // group 0: v0 = ((a2 256 + a3) 256 + a4) 256 + a5, exact (< 2^50); z = v0 2^24 + v1 (one rounding)
+      mbar_wait(tfull, static_cast<uint32_t>(q) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int cb = 0; cb < 4; ++cb) {
+        int a2[8], a3[8], a4[8], a5[8];
+        tmem_ld8(trow + 0 * 128 + cb * 8, a2);
+        tmem_ld8(trow + 1 * 128 + cb * 8, a3);
+        tmem_ld8(trow + 2 * 128 + cb * 8, a4);
+        tmem_ld8(trow + 3 * 128 + cb * 8, a5);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const long long t = (((static_cast<long long>(a2[i]) << 8) + a3[i]) * 256 + a4[i]) * 256 + a5[i];
+          v[cb * 8 + i] = fma(i51_to_f64(t), 0x1.0p24, v[cb * 8 + i]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty);  // the next item's group-1 MMAs may start
+      ++q;
+      // scale, bias after the full dot product, sigmoid (elm.cpp:102, :27), store: the warp writes 32
+      // consecutive nodes of each row
+      if (c < p.L) {
+        // (XW)[r][c] = v 2^(f_c - 60) 2^(e_r): both factors exact powers of two (exponents clamped to the
+        // normal range: rows / columns whose maximum is below 2^-962 are outside the supported inputs);
+        // z = fma(v 2^(f_c - 60), 2^(e_r), b) rounds once, as the product then the bias addition would
+        const double sc = pow2i(min(max(p.cexp[c] - 60, -1022), 1023));
+        const double bc = p.bias[c];
+        const int nr = min(32, p.N - r0);
+        double* dst = p.H + static_cast<long long>(r0) * p.ldh + c;
+        const double* frow = s_frow + part * 32;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const double z = fma(v[i] * sc, frow[i], bc);
+          const double h = recip_ge1(1.0 + exp_sig(-z));
+          if (i < nr) dst[static_cast<long long>(i) * p.ldh] = h;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+  }
+}
+
+cudaError_t launch_oz_hidden(const CUtensorMap* maps, const OzHidParams& p, cudaStream_t s) {
+  const size_t smem = size_t(kOzRing) + 3072;  // ring, barriers, TMEM slot, row scales, alignment (227 KB)
+  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(oz_hidden_kernel), smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int items = p.nP * p.nJ;
+  const int clusters = std::min(items, nsm / 2);
+  oz_hidden_kernel<<<2 * clusters, kOzHidThreads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  return cudaGetLastError();
+}
+
 // Fixed-order reduction of the packed partial tiles: G[i][j] = G[j][i] = (acc ? G[i][j] : 0) +
 // sum_{slot} part[slot][tile(i, j)][i % 128][j % 128] over the lower triangle, slots in increasing
 // order (split-major, group 0 before group 1 within a split).  One CTA per 32 x 32 block, staged in
@@ -533,7 +780,7 @@ cudaError_t launch_oz_colmax(const double* A, long long lda, long long N, int M,
   cudaError_t e = cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * M, s);
   if (e != cudaSuccess) return e;
   const int cb = (M + 31) / 32;
-  long long ry = (2LL * num_sms + cb - 1) / cb;
+  long long ry = (8LL * num_sms) / cb;  // up to 8 CTAs of 8 warps per SM in one wave: enough loads in flight
   const long long rmax = (N + 255) / 256;
   if (ry > rmax) ry = rmax;
   if (ry < 1) ry = 1;

@@ -25,17 +25,6 @@ __device__ __forceinline__ int swz16p(int row, int col) {
 __device__ __forceinline__ unsigned char* align1024p(unsigned char* p) {
   return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
 }
-// 1 / x for x >= 1 without the XU pipe (identical to k_gemm.cu's recip_ge1: K1 and this kernel
-// produce the same H bits)
-__device__ __forceinline__ double recip_ge1p(double x) {
-  double y = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(x));
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-  }
-  return x <= 1.7976931348623157e308 ? y : (x > 0.0 ? 0.0 : x);
-}
 }  // namespace
 
 constexpr int kPBN = 32;          // hidden nodes per chunk
@@ -158,7 +147,7 @@ __global__ void __launch_bounds__(kGemmThreads, MP <= 48 ? 2 : 1)
           double h = 0.0;
           if (col < p.L) {
             const double z = add_rn(v, p.bias[col]);
-            h = recip_ge1p(1.0 + exp(-z));
+            h = recip_ge1(1.0 + exp(-z));
           }
           h2[half] = h;
         }

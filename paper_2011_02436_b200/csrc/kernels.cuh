@@ -84,6 +84,19 @@ struct OzParams {
   unsigned long long* dbg;  // diagnostic cycle counters (tools/ozaki_test), null in production
 };
 
+// ---- K1i: hidden build on the INT8 tensor cores (k_ozaki.cu): H = sigmoid(X W + b) from the digit
+// planes of W (column exponents) and X^T (row exponents of X), 28 exact int8 products per k-step
+struct OzHidParams {
+  int N, L;           // rows of X / H, hidden nodes
+  int nP, nJ;         // 256-node pair tiles of W's columns, 128-row tiles of X
+  int ksteps;         // padded d / 32
+  const int* rexp;    // exponent of each X row (max |X[r][:]| < 2^e)
+  const int* cexp;    // exponent of each W column
+  const double* bias;
+  double* H;
+  long long ldh;
+};
+
 // ---- generic DMMA GEMM: C = alpha * op(A) op(B) + beta * C (row-major)
 struct GemmParams {
   int M, N, K;

@@ -93,3 +93,26 @@ def test_int8_gram_matches_dmma_gram():
     # heavy-tailed sigmoid columns (max / rms ~ 30): the digit-plane error scales with max_a max_b / sqrt(N)
     # (dropped w >= 9 digit products), a blocked fp64 sum's with the rms -- measured 8.5e-16 vs 9.3e-16
     assert e8 <= 1e-15 and e8 <= e64 + 1e-17
+
+
+@pytest.mark.parametrize("n,d,L", [(2000, 16, 200), (1000, 33, 129), (3000, 256, 300), (257, 64, 1), (5, 3, 7),
+                                   (600, 130, 513)])
+def test_int8_hidden_vs_extended_precision(n, d, L):
+    """K1i (oz_hidden_kernel): H = sigmoid(X W + b) from 28 exact int8 digit-plane products, checked against
+    the same formula in long double (elm.cpp:93-106: bias after the full dot product) and against the
+    oracle's fp64 restatement."""
+    import oracle
+
+    x, _ = rb.synth_classification(n, d, 2, n + d, L + 1)
+    x[:, 0] *= -3.0e-7                                    # a small, negative feature column
+    hid = rb.init_hidden(rb.ElmParams(d, L, 2, n + L))
+    h = rb.hidden_matrix(hid, x)
+    xl, wl, bl = (a.astype(np.longdouble) for a in (x, hid.weights, hid.biases.reshape(1, -1)))
+    z = xl @ wl + bl
+    ref = 1.0 / (1.0 + np.exp(-z))
+    err = float(np.abs(h.astype(np.longdouble) - ref).max())
+    ho = oracle.hidden_matrix(hid.weights, hid.biases, x)
+    err_o = float(np.abs(ho.astype(np.longdouble) - ref).max())
+    print(f"n={n} d={d} L={L}: int8 H max err {err:.2e} (oracle fp64: {err_o:.2e})")
+    assert err <= max(4e-16, 2.0 * err_o)
+    assert np.abs(h - ho).max() < 1e-12
