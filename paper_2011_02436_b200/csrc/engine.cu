@@ -101,6 +101,9 @@ cudaError_t launch_oz_slice(const double*, long long, long long, int, const unsi
                             int8_t*, cudaStream_t);
 cudaError_t launch_oz_gram2(const CUtensorMap* maps, const OzParams&, cudaStream_t);
 cudaError_t launch_oz_hidden(const CUtensorMap* maps, const OzHidParams&, cudaStream_t);
+cudaError_t launch_oz_beta_planes(const double*, long long, int, int, const int*, int, int8_t*, double*, cudaStream_t);
+cudaError_t launch_oz_labels(const double*, long long, long long, int, int*, cudaStream_t);
+cudaError_t launch_oz_scores(const CUtensorMap* maps, const OzScoresParams&, cudaStream_t);
 int oz_pair_order(int nbI, int B, int2* out);
 cudaError_t launch_oz_finish(const double*, long long, int, int, double*, long long, int, cudaStream_t);
 cudaError_t launch_sum_parts(const double*, long long, int, long long, double*, cudaStream_t);
@@ -156,7 +159,18 @@ struct rbpg_context {
       return x == o.x && w == o.w && b == o.b && ldx == o.ldx && ldw == o.ldw && d == o.d;
     }
   } kept_key;
+  // digit planes of [H T] written by the INT8 Gram, one record per Gram part (row range, planes, column
+  // exponents); the records of the parts that built the kept H serve the INT8 accuracy pass
+  struct OzPart {
+    size_t r0 = 0, rows = 0, Mpad = 0, Npad = 0;
+    int8_t* planes = nullptr;
+    int* exps = nullptr;
+  };
+  std::vector<OzPart> oz_pending, oz_kept;
+  const double* oz_kept_h = nullptr;
   void keep_h(const double* h, size_t n, size_t l, size_t ldh, const KeptKey& key) {
+    oz_kept = oz_pending;
+    oz_kept_h = h;
     kept_h = h;
     kept_n = n;
     kept_l = l;
@@ -502,12 +516,17 @@ size_t oz_slot_doubles(size_t M) {
   return nbI * (nbI + 1) / 2 * 16384;  // lower 128 x 128 tiles, packed
 }
 // Partials of rows [0, rows) of A (rows x M, ld lda) into the 2 * oz_splits(rows) slots at ws.
-void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, size_t M, double* ws) {
+// Part `part` (rows [r0, r0 + rows) of the Gram operand) keeps its own planes and exponents, recorded in
+// ctx->oz_pending for the INT8 accuracy pass.
+void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, size_t M, double* ws, int part = 0,
+                  size_t r0 = 0) {
   const int nbI = static_cast<int>((M + 127) / 128), Mpad = (nbI + 1) / 2 * 2 * 128;
   const long long Npad = static_cast<long long>((rows + 63) / 64 * 64);
-  auto* cmax = reinterpret_cast<unsigned long long*>(ctx->dbuf("oz_cmax", M));
-  auto* exps = reinterpret_cast<int*>(ctx->dbuf("oz_exps", (Mpad + 1) / 2));
-  auto* planes = reinterpret_cast<int8_t*>(ctx->buf("oz_planes", size_t(7) * Mpad * Npad));
+  const std::string sfx = part ? "." + std::to_string(part) : std::string();
+  auto* cmax = reinterpret_cast<unsigned long long*>(ctx->dbuf("oz_cmax" + sfx, M));
+  auto* exps = reinterpret_cast<int*>(ctx->dbuf("oz_exps" + sfx, (Mpad + 1) / 2));
+  auto* planes = reinterpret_cast<int8_t*>(ctx->buf("oz_planes" + sfx, size_t(7) * Mpad * Npad));
+  ctx->oz_pending.push_back({r0, rows, static_cast<size_t>(Mpad), static_cast<size_t>(Npad), planes, exps});
   ctx->run("oz_colmax", [&] {
     return launch_oz_colmax(dA, static_cast<long long>(lda), static_cast<long long>(rows), static_cast<int>(M), cmax,
                             ctx->num_sms, ctx->stream);
@@ -566,6 +585,7 @@ void gram_oz_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size
   }
   const int splits = oz_splits(N);
   double* ws = ctx->dbuf("syrk_ws", size_t(2) * splits * oz_slot_doubles(M));
+  ctx->oz_pending.clear();
   oz_gram_part(ctx, dA, lda, N, M, ws);
   ctx->run("syrk_finish", [&] {
     return launch_oz_finish(ws, static_cast<long long>(oz_slot_doubles(M)), 2 * splits, static_cast<int>(M), dG,
@@ -632,7 +652,8 @@ GramParts gram_parts_plan(rbpg_context* ctx, size_t L, const std::vector<size_t>
 void gram_parts_launch(rbpg_context* ctx, GramParts& gp, int q, const double* dA, size_t lda) {
   const size_t r0 = q == 0 ? 0 : gp.ends[q - 1], rows = gp.ends[q] - r0;
   if (ctx->gram_int8) {
-    oz_gram_part(ctx, dA + r0 * lda, lda, rows, gp.p.M, gp.p.ws + gp.split0[q] * gp.p.wsStride);
+    if (q == 0) ctx->oz_pending.clear();
+    oz_gram_part(ctx, dA + r0 * lda, lda, rows, gp.p.M, gp.p.ws + gp.split0[q] * gp.p.wsStride, q, r0);
     return;
   }
   SyrkParams p = gp.p;
@@ -1421,6 +1442,60 @@ void scores_dev(rbpg_context* ctx, const double* H, size_t ldh, size_t N, size_t
   ctx->run("scores_kernel", [&] { return launch_scores(tmH, tmB, p, ctx->stream); });
 }
 
+// K6i (k_ozaki.cu): the training-accuracy pass on the INT8 tensor cores, from the digit planes the Gram
+// of the kept H wrote (one launch per Gram part: each part has its own column exponents, folded into
+// beta's planes).  Valid when those parts cover exactly the N kept rows and the plane rows (the columns
+// of [H T]) fit the int32 headroom.
+bool oz_scores_ready(rbpg_context* ctx, size_t N, size_t M) {
+  if (!ctx->gram_int8 || ctx->oz_kept.empty() || ctx->oz_kept_h != ctx->kept_h) return false;
+  size_t r = 0;
+  for (const auto& pt : ctx->oz_kept) {
+    if (pt.r0 != r || pt.Mpad > 16384 || pt.Mpad < M) return false;
+    r += pt.rows;
+  }
+  return r == N;
+}
+void oz_scores_dev(rbpg_context* ctx, size_t N, size_t L, size_t m, const double* dBeta, size_t ldb, const double* dT,
+                   size_t ldt, unsigned long long* hits) {
+  int* labels = reinterpret_cast<int*>(ctx->buf("ozs.labels", N * sizeof(int)));
+  ctx->run("scores_kernel", [&] {
+    return launch_oz_labels(dT, static_cast<long long>(ldt), static_cast<long long>(N), static_cast<int>(m), labels,
+                            ctx->stream);
+  });
+  for (const auto& pt : ctx->oz_kept) {
+    const size_t K = pt.Mpad;
+    auto* bp = reinterpret_cast<int8_t*>(ctx->buf("ozs.bplanes", 7 * 128 * K));
+    double* cs = ctx->dbuf("ozs.cscale", 128);
+    ctx->run("scores_kernel", [&] {
+      return launch_oz_beta_planes(dBeta, static_cast<long long>(ldb), static_cast<int>(L), static_cast<int>(m), pt.exps,
+                                   static_cast<int>(K), bp, cs, ctx->stream);
+    });
+    auto map = [&](int8_t* base, size_t rows, uint32_t box_rows, uint32_t np) {
+      CUtensorMap mp;
+      cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), 7};
+      cuuint64_t strides[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(K) * rows};
+      cuuint32_t box[3] = {32u, box_rows, np};
+      cuuint32_t estr[3] = {1, 1, 1};
+      CUresult r = ctx->encode(&mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) fail(RBPG_CUDA_ERROR, "cuTensorMapEncodeTiled (scores planes) failed (" + std::to_string(int(r)) + ")");
+      return mp;
+    };
+    CUtensorMap maps[4] = {map(pt.planes, pt.Npad, 128, 4), map(bp, 128, 64, 4), map(pt.planes, pt.Npad, 128, 7),
+                           map(bp, 128, 64, 7)};
+    OzScoresParams p{};
+    p.rows = static_cast<int>(pt.rows);
+    p.m = static_cast<int>(m);
+    p.nP = static_cast<int>((pt.rows + 255) / 256);
+    p.ksteps = static_cast<int>(K / 32);
+    p.cscale = cs;
+    p.labels = labels + pt.r0;
+    p.hits = hits;
+    ctx->run("scores_kernel", [&] { return launch_oz_scores(maps, p, ctx->stream); });
+  }
+}
+
 // K6b: fused sigma(X W + b) beta with the arg-max epilogue (m <= 128): optional scores S, labels,
 // and hits += #rows whose arg-max equals argmax(T).  H is never written.
 void predict_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_t d, const double* dW, size_t ldw,
@@ -1464,6 +1539,13 @@ uint64_t accuracy_stage(rbpg_context* ctx, const double* dX, size_t ldx, const d
           hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh);
           H = dH;
           hld = ldh;
+        }
+        // K6i on the Gram's digit planes for many classes: its cost (28 int8 products against the 128
+        // padded classes per row) undercuts the DMMA K6 once m > 48, where K6 turns FP64-bound (C5,
+        // m = 100: 31 -> 11 ms); below, K6 reads H once at HBM speed (C4, m = 10: 1.2 vs 2.7 ms)
+        if (kept && m > 48 && m <= 128 && oz_scores_ready(ctx, N, L + m)) {
+          oz_scores_dev(ctx, N, L, m, dBeta, ldb, dT, ldt_in, hits);
+          break;
         }
         if (m <= 128) {  // K6: skinny DMMA GEMM with the fused arg-max / hit count, scores never stored
           scores_dev(ctx, H, hld, nr, L, dBeta, ldb, m, nullptr, 0, dT + r0 * ldt_in, ldt_in, hits);

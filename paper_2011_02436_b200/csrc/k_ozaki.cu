@@ -707,6 +707,287 @@ cudaError_t launch_oz_hidden(const CUtensorMap* maps, const OzHidParams& p, cuda
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// K6i: the training-accuracy pass (elm.cpp:278, 286-300: hits = #rows with argmax(H beta) ==
+// argmax(T), strict '>' scans, lowest index on ties) on the INT8 tensor cores.  The Gram's digit
+// planes of [H T] (H[r][c] = 2^(e_c - 54) X_rc, column exponents e_c) are reused: folding 2^(e_c) into
+// beta, beta'[c][j] = beta[c][j] 2^(e_c) (exact) = 2^(f_j - 54) Y_cj with class exponents f_j, gives
+// scores[r][j] = 2^(f_j - 60) sum_{w=2..8} a_w 256^(8-w), a_w = sum_{i+j=w} (DX_i DY_j^T)[r][j]
+// (int32: columns of [H T] <= 16384).  Rows of T's columns meet zero beta' rows, so the contraction
+// runs over the whole plane row.  Both operands are K-major (the planes are [row][column] with the
+// contraction index contiguous): 32-byte TMA boxes at 32-byte swizzle, one MMA k-step per stage.
+// Execution: CTA pairs (M = 256 rows, N = 128 classes), an item per 256-row tile: group 1 (18 products)
+// then group 0 (10) over the whole contraction; 8 epilogue warps (64 classes per thread), the arg-max
+// of the two halves of a row combined through shared memory.
+// ---------------------------------------------------------------------------------------------
+namespace {
+// K-major, 32-byte swizzle: 8-row groups of 32-byte rows 256 B apart (stride byte offset), leading byte
+// offset unused (1)
+__device__ __forceinline__ uint64_t oz_desc_k32(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(256 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(6) << 61);
+}
+// instruction descriptor: M = 256, N = 128, K-major A and B, s8 x s8 -> s32
+constexpr uint32_t kOzIdescK = (2u << 4) | (1u << 7) | (1u << 10) | ((128u >> 3) << 17) | ((256u >> 4) << 24);
+__device__ __forceinline__ void oz_mma2k(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kOzIdescK), "r"(acc));
+}
+template <int G>
+__device__ __forceinline__ void oz_mma_kstep2k(uint32_t tbase, uint32_t sa, uint32_t sb, bool first) {
+#pragma unroll
+  for (int w = OzGroup<G>::kW0; w < OzGroup<G>::kW0 + OzGroup<G>::kW; ++w) {
+#pragma unroll
+    for (int i = 1; i < w; ++i) {
+      const int j = w - i;
+      if (i > OzGroup<G>::kPlanes || j > OzGroup<G>::kPlanes) continue;
+      oz_mma2k(tbase + (w - OzGroup<G>::kW0) * 128, oz_desc_k32(sa + (i - 1) * kOzTileBytes),
+               oz_desc_k32(sb + (j - 1) * kOzBHalfBytes), (first && i == 1) ? 0u : 1u);
+    }
+  }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
+    oz_scores_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+                     const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+                     OzScoresParams p) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOzRing);
+  uint64_t* empty = full + kOzMaxStages;
+  uint64_t* tfull = empty + kOzMaxStages;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
+  double* s_best = reinterpret_cast<double*>(tslot + 4);  // [128] half 1's best score per row
+  int* s_idx = reinterpret_cast<int*>(s_best + 128);       // [128] and its class
+  unsigned int& s_hits = *reinterpret_cast<unsigned int*>(s_idx + 128);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = static_cast<int>(cluster_rank());
+  const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int nitems = p.nP;
+  const int nst = kOz2Stages;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmA0);
+    tma_prefetch_desc(&tmB0);
+    tma_prefetch_desc(&tmA1);
+    tma_prefetch_desc(&tmB1);
+    for (int s = 0; s < kOzMaxStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 16);
+    fence_mbar_init();
+    s_hits = 0;
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t leader_full0 = mapa_u32(smem_u32(&full[0]), 0);
+  const uint32_t leader_tempty = mapa_u32(smem_u32(tempty), 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      long long gk = 0;
+      for (int it = cl; it < nitems; it += ncl) {
+        for (int ph = 0; ph < 2; ++ph) {
+          const int g = 1 - ph;
+          const int planes = g ? OzGroup<1>::kPlanes : OzGroup<0>::kPlanes;
+          const uint32_t a_bytes = planes * kOzTileBytes, bytes = planes * (kOzTileBytes + kOzBHalfBytes);
+          for (int k = 0; k < p.ksteps; ++k, ++gk) {
+            const int s = static_cast<int>(gk % nst);
+            if (gk >= nst) mbar_wait_sleep(&empty[s], static_cast<uint32_t>((gk / nst) - 1) & 1);
+            unsigned char* st = smem + s * kOz2Stage;
+            if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * bytes);
+            const uint32_t bar = leader_full0 + s * 8;
+            tma_load_3d_pair(st, g ? &tmA1 : &tmA0, bar, k * 32, (2 * it + rank) * 128, 0);
+            tma_load_3d_pair(st + a_bytes, g ? &tmB1 : &tmB0, bar, k * 32, 64 * rank, 0);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      long long gk = 0, q = 0;
+      for (int it = cl; it < nitems; it += ncl) {
+        for (int ph = 0; ph < 2; ++ph, ++q) {
+          const int g = 1 - ph;
+          if (q > 0) mbar_wait_sleep(tempty, static_cast<uint32_t>(q - 1) & 1);
+          tc_fence_after();
+          const uint32_t a_bytes = (g ? OzGroup<1>::kPlanes : OzGroup<0>::kPlanes) * kOzTileBytes;
+          for (int k = 0; k < p.ksteps; ++k, ++gk) {
+            const int s = static_cast<int>(gk % nst);
+            mbar_wait_sleep(&full[s], static_cast<uint32_t>(gk / nst) & 1);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + s * kOz2Stage);
+            if (g == 0) oz_mma_kstep2k<0>(tbase, sa, sa + a_bytes, k == 0);
+            else oz_mma_kstep2k<1>(tbase, sa, sa + a_bytes, k == 0);
+            oz_commit2(&empty[s]);
+          }
+          oz_commit2(tfull);
+        }
+      }
+    }
+  } else {
+    const int quarter = warp & 3, half = (warp - 2) >> 2;
+    const uint32_t trow = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + half * 64;
+    const int rl = quarter * 32 + lane;
+    unsigned int my_hits = 0;
+    long long q = 0;
+    for (int it = cl; it < nitems; it += ncl) {
+      const int r = (2 * it + rank) * 128 + rl;
+      double v[64];
+      mbar_wait(tfull, static_cast<uint32_t>(q) & 1);  // group 1: exact integers < 2^41
+      tc_fence_after();
+#pragma unroll
+      for (int cb = 0; cb < 8; ++cb) {
+        int a6[8], a7[8], a8[8];
+        tmem_ld8(trow + 0 * 128 + cb * 8, a6);
+        tmem_ld8(trow + 1 * 128 + cb * 8, a7);
+        tmem_ld8(trow + 2 * 128 + cb * 8, a8);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          v[cb * 8 + i] = i51_to_f64(((static_cast<long long>(a6[i]) << 8) + a7[i]) * 256 + a8[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty);
+      ++q;
+      mbar_wait(tfull, static_cast<uint32_t>(q) & 1);  // group 0: exact < 2^50; z = v0 2^24 + v1
+      tc_fence_after();
+#pragma unroll
+      for (int cb = 0; cb < 8; ++cb) {
+        int a2[8], a3[8], a4[8], a5[8];
+        tmem_ld8(trow + 0 * 128 + cb * 8, a2);
+        tmem_ld8(trow + 1 * 128 + cb * 8, a3);
+        tmem_ld8(trow + 2 * 128 + cb * 8, a4);
+        tmem_ld8(trow + 3 * 128 + cb * 8, a5);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const long long t = (((static_cast<long long>(a2[i]) << 8) + a3[i]) * 256 + a4[i]) * 256 + a5[i];
+          v[cb * 8 + i] = fma(i51_to_f64(t), 0x1.0p24, v[cb * 8 + i]);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty);
+      ++q;
+      // arg-max over this thread's classes (strict '>' in increasing class order)
+      double best = 0.0;
+      int bi = -1;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const int j = half * 64 + i;
+        const double sv = v[i] * __ldg(p.cscale + j);
+        if (j < p.m && (bi < 0 || sv > best)) {
+          best = sv;
+          bi = j;
+        }
+      }
+      // the two halves of row rl: half 1 posts, half 0 combines (ties stay with the lower classes)
+      named_bar_sync_n(1 + quarter, 64);
+      if (half == 1) {
+        s_best[rl] = best;
+        s_idx[rl] = bi;
+      }
+      named_bar_sync_n(1 + quarter, 64);
+      if (half == 0 && r < p.rows) {
+        const int b1 = s_idx[rl];
+        if (b1 >= 0 && (bi < 0 || s_best[rl] > best)) bi = b1;
+        my_hits += (bi == p.labels[r]) ? 1u : 0u;
+      }
+    }
+    if (half == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) my_hits += __shfl_xor_sync(0xffffffffu, my_hits, o);
+      if (lane == 0 && my_hits) atomicAdd(&s_hits, my_hits);
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+  }
+  if (threadIdx.x == 0 && s_hits) atomicAdd(p.hits, static_cast<unsigned long long>(s_hits));
+}
+
+// Digit planes of the folded beta (K-major, [plane][class][column], 128 class rows; rows >= m and
+// columns >= L zero) and the class scales 2^(f_j - 60).  One CTA per class row: the exact maximum of
+// |beta[c][j] 2^(e_c)|, then the 54-bit integers and their digits (as oz_slice_kernel).
+__global__ void __launch_bounds__(256) oz_beta_planes_kernel(const double* __restrict__ beta, long long ldb, int L, int m,
+                                                             const int* __restrict__ cexp, int Kpad, int8_t* S,
+                                                             double* cscale) {
+  const int j = blockIdx.x;
+  __shared__ double red[256];
+  double mx = 0.0;
+  if (j < m)
+    for (int c = threadIdx.x; c < L; c += 256) mx = fmax(mx, fabs(scale2(beta[static_cast<long long>(c) * ldb + j], cexp[c])));
+  red[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] = fmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  int f = 0;
+  if (red[0] > 0.0) frexp(red[0], &f);
+  if (threadIdx.x == 0) cscale[j] = pow2i(min(max(f - 60, -1022), 1023));
+  constexpr unsigned long long kBias = 0x808080808080ull;
+  const long long plane = 128LL * Kpad;
+  for (int c = threadIdx.x; c < Kpad; c += 256) {
+    long long X = 0;
+    if (j < m && c < L) X = __double2ll_rn(scale2(beta[static_cast<long long>(c) * ldb + j], cexp[c] + 54 - f));
+    const unsigned long long V = (static_cast<unsigned long long>(X) + kBias) ^ kBias;
+#pragma unroll
+    for (int i = 0; i < 7; ++i) S[(kOzPlanes - 1 - i) * plane + static_cast<long long>(j) * Kpad + c] = static_cast<int8_t>(V >> (8 * i));
+  }
+}
+
+// target labels: argmax of each T row (strict '>', lowest index on ties; elm.cpp:291-296)
+__global__ void oz_labels_kernel(const double* T, long long ldt, long long rows, int m, int* labels) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < rows;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const double* y = T + i * ldt;
+    int a = 0;
+    for (int j = 1; j < m; ++j)
+      if (y[j] > y[a]) a = j;
+    labels[i] = a;
+  }
+}
+
+cudaError_t launch_oz_beta_planes(const double* beta, long long ldb, int L, int m, const int* cexp, int Kpad, int8_t* S,
+                                  double* cscale, cudaStream_t s) {
+  oz_beta_planes_kernel<<<128, 256, 0, s>>>(beta, ldb, L, m, cexp, Kpad, S, cscale);
+  return cudaGetLastError();
+}
+cudaError_t launch_oz_labels(const double* T, long long ldt, long long rows, int m, int* labels, cudaStream_t s) {
+  const long long blocks = std::min<long long>((rows + 255) / 256, 148LL * 8);
+  oz_labels_kernel<<<static_cast<unsigned>(std::max<long long>(blocks, 1)), 256, 0, s>>>(T, ldt, rows, m, labels);
+  return cudaGetLastError();
+}
+cudaError_t launch_oz_scores(const CUtensorMap* maps, const OzScoresParams& p, cudaStream_t s) {
+  const size_t smem = size_t(kOzRing) + 3072;  // ring, barriers, TMEM slot, half-row arg-max exchange
+  cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(oz_scores_kernel), smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int clusters = std::min(p.nP, nsm / 2);
+  oz_scores_kernel<<<2 * clusters, kOz2Threads, smem, s>>>(maps[0], maps[1], maps[2], maps[3], p);
+  return cudaGetLastError();
+}
+
 // Fixed-order reduction of the packed partial tiles: G[i][j] = G[j][i] = (acc ? G[i][j] : 0) +
 // sum_{slot} part[slot][tile(i, j)][i % 128][j % 128] over the lower triangle, slots in increasing
 // order (split-major, group 0 before group 1 within a split).  One CTA per 32 x 32 block, staged in

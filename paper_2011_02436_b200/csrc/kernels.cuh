@@ -97,6 +97,19 @@ struct OzHidParams {
   long long ldh;
 };
 
+// ---- K6i: accuracy pass on the INT8 tensor cores (k_ozaki.cu): scores = H beta from the Gram's digit
+// planes of H (column exponents folded into beta) and the digit planes of the folded beta; the
+// arg-max of each row's scores compared with the row's target label, hits counted
+struct OzScoresParams {
+  int rows;            // rows of this Gram part
+  int m;               // classes (<= 128)
+  int nP;              // 256-row pair tiles
+  int ksteps;          // plane row length / 32 (the contraction over the columns of [H T])
+  const double* cscale;  // [128] 2^(f_j - 60): the class exponents of the folded beta
+  const int* labels;   // target label (arg-max of the T row) of each row of the part
+  unsigned long long* hits;
+};
+
 // ---- generic DMMA GEMM: C = alpha * op(A) op(B) + beta * C (row-major)
 struct GemmParams {
   int M, N, K;

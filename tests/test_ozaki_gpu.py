@@ -116,3 +116,24 @@ def test_int8_hidden_vs_extended_precision(n, d, L):
     print(f"n={n} d={d} L={L}: int8 H max err {err:.2e} (oracle fp64: {err_o:.2e})")
     assert err <= max(4e-16, 2.0 * err_o)
     assert np.abs(h - ho).max() < 1e-12
+
+
+@pytest.mark.parametrize("n,d,L,m", [(7000, 24, 400, 60), (3001, 20, 130, 128), (20000, 40, 700, 100)])
+def test_int8_accuracy_pass_vs_oracle(n, d, L, m):
+    """K6i (oz_scores_kernel, m > 48): the training-accuracy pass from the Gram's digit planes gives the
+    oracle's hit count (elm.cpp:278, 286-300) through the host-buffer train (two Gram parts, each with
+    its own column exponents) and the device-resident train (one part); the ragged row counts leave
+    partial 256-row tiles."""
+    import oracle
+    import torch
+
+    x, t = rb.synth_classification(n, d, m, n + 7, m + 11)
+    params = rb.ElmParams(d, L, m, L + 13)
+    ref = oracle.train(d, L, m, L + 13, x, t, "rank", 0, 0.0)
+    _, diag = rb.train(params, x, t, rb.SolverStrategy.rank_based())
+    _, diag_d, _ = rb.train_device(torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda(), params,
+                                   rb.SolverStrategy.rank_based())
+    print(f"n={n} L={L} m={m}: accuracy {diag.training_accuracy} / {diag_d.training_accuracy} "
+          f"(oracle {ref['diag']['training_accuracy']})")
+    assert diag.training_accuracy == ref["diag"]["training_accuracy"]
+    assert diag_d.training_accuracy == ref["diag"]["training_accuracy"]
