@@ -97,6 +97,7 @@ int predict_mp(int m);
 cudaError_t launch_pack_lower(const double*, long long, int, double*, cudaStream_t);
 cudaError_t launch_unpack_lower(const double*, int, double*, long long, cudaStream_t);
 cudaError_t launch_oz_colmax(const double*, long long, long long, int, unsigned long long*, int, cudaStream_t);
+cudaError_t launch_oz_colmax_acc(const double*, long long, long long, int, unsigned long long*, int, cudaStream_t);
 cudaError_t launch_oz_slice(const double*, long long, long long, int, const unsigned long long*, int*, int, long long,
                             int8_t*, cudaStream_t);
 cudaError_t launch_oz_gram2(const CUtensorMap* maps, const OzParams&, cudaStream_t);
@@ -336,7 +337,7 @@ CUtensorMap plane_map(rbpg_context* ctx, int8_t* planes, size_t cols, size_t row
 // fused epilogue.  Scratch buffers are per stream: the e2e path builds row blocks on two streams.
 constexpr size_t kOzHidMaxD = 16384;  // int32 headroom of one k range: 7 d 2^14 < 2^31
 void hidden_oz_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_t d, const double* dW, size_t ldw,
-                   const double* db, size_t L, double* dH, size_t ldh) {
+                   const double* db, size_t L, double* dH, size_t ldh, unsigned long long* cmax = nullptr) {
   const size_t Nr = (N + 127) / 128 * 128, Kpad = (d + 31) / 32 * 32, Lp = (L + 255) / 256 * 256;
   const std::string sfx = "." + std::to_string(reinterpret_cast<uintptr_t>(ctx->stream));
   double* xt = ctx->dbuf("ozh.xt" + sfx, d * Nr);
@@ -383,17 +384,25 @@ void hidden_oz_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, si
   p.bias = db;
   p.H = dH;
   p.ldh = static_cast<long long>(ldh);
+  p.cmax = cmax;
   ctx->run("hidden_kernel", [&] { return launch_oz_hidden(maps, p, ctx->stream); });
 }
 
+// cmax (optional, m > 0 with T): the column maxima of the built rows of [H T] accumulated for the INT8
+// Gram's scan (zeroed by the caller before the first block of a Gram part).
 void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_t d, const double* dW, size_t ldw,
                 const double* db, size_t L, double* dH, size_t ldh, const double* dT = nullptr, size_t ldt = 0,
-                size_t m = 0) {
+                size_t m = 0, unsigned long long* cmax = nullptr) {
   if (N == 0) return;
   if (ctx->gram_int8 && d <= kOzHidMaxD && N < (size_t(1) << 31)) {
-    hidden_oz_dev(ctx, dX, ldx, N, d, dW, ldw, db, L, dH, ldh);
+    hidden_oz_dev(ctx, dX, ldx, N, d, dW, ldw, db, L, dH, ldh, cmax);
     if (m > 0 && dT)  // augmented rows [H T]
       ck(cudaMemcpy2DAsync(dH + L, ldh * 8, dT, ldt * 8, m * 8, N, cudaMemcpyDeviceToDevice, ctx->stream), "append T");
+    if (cmax && m > 0)
+      ctx->run("oz_colmax", [&] {
+        return launch_oz_colmax_acc(dH + L, static_cast<long long>(ldh), static_cast<long long>(N), static_cast<int>(m),
+                                    cmax + L, ctx->num_sms, ctx->stream);
+      });
     return;
   }
   CUtensorMap tmX = make_map(ctx, dX, d, N, ldx, 16, kTile, true);
@@ -402,6 +411,11 @@ void hidden_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size_
   HiddenParams p{static_cast<int>(N), static_cast<int>(d), static_cast<int>(L), db, dH, static_cast<long long>(ldh),
                  0, m > 0 ? dT : nullptr, static_cast<long long>(ldt), static_cast<int>(m)};
   ctx->run("hidden_kernel", [&] { return launch_hidden(tmX, tmW, p, bn, ctx->stream); });
+  if (cmax)  // the DMMA build has no fused scan: scan its rows of [H T]
+    ctx->run("oz_colmax", [&] {
+      return launch_oz_colmax_acc(dH, static_cast<long long>(ldh), static_cast<long long>(N),
+                                  static_cast<int>(L + (dT ? m : 0)), cmax, ctx->num_sms, ctx->stream);
+    });
 }
 
 // G (+)= A^T A over rows [0, N) of A (N x L, ld lda); HtT (+)= A^T T when m > 0.
@@ -518,19 +532,22 @@ size_t oz_slot_doubles(size_t M) {
 // Partials of rows [0, rows) of A (rows x M, ld lda) into the 2 * oz_splits(rows) slots at ws.
 // Part `part` (rows [r0, r0 + rows) of the Gram operand) keeps its own planes and exponents, recorded in
 // ctx->oz_pending for the INT8 accuracy pass.
+// cmax_ready: the column maxima of these rows already accumulated by their hidden builds (fused scan).
 void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, size_t M, double* ws, int part = 0,
-                  size_t r0 = 0) {
+                  size_t r0 = 0, const unsigned long long* cmax_ready = nullptr) {
   const int nbI = static_cast<int>((M + 127) / 128), Mpad = (nbI + 1) / 2 * 2 * 128;
   const long long Npad = static_cast<long long>((rows + 63) / 64 * 64);
   const std::string sfx = part ? "." + std::to_string(part) : std::string();
-  auto* cmax = reinterpret_cast<unsigned long long*>(ctx->dbuf("oz_cmax" + sfx, M));
+  auto* cmax = cmax_ready ? const_cast<unsigned long long*>(cmax_ready)
+                          : reinterpret_cast<unsigned long long*>(ctx->dbuf("oz_cmax" + sfx, M));
   auto* exps = reinterpret_cast<int*>(ctx->dbuf("oz_exps" + sfx, (Mpad + 1) / 2));
   auto* planes = reinterpret_cast<int8_t*>(ctx->buf("oz_planes" + sfx, size_t(7) * Mpad * Npad));
   ctx->oz_pending.push_back({r0, rows, static_cast<size_t>(Mpad), static_cast<size_t>(Npad), planes, exps});
-  ctx->run("oz_colmax", [&] {
-    return launch_oz_colmax(dA, static_cast<long long>(lda), static_cast<long long>(rows), static_cast<int>(M), cmax,
-                            ctx->num_sms, ctx->stream);
-  });
+  if (!cmax_ready)
+    ctx->run("oz_colmax", [&] {
+      return launch_oz_colmax(dA, static_cast<long long>(lda), static_cast<long long>(rows), static_cast<int>(M), cmax,
+                              ctx->num_sms, ctx->stream);
+    });
   ctx->run("oz_slice", [&] {
     return launch_oz_slice(dA, static_cast<long long>(lda), static_cast<long long>(rows), static_cast<int>(M), cmax,
                            exps, Mpad, Npad, planes, ctx->stream);
@@ -578,7 +595,7 @@ void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, 
 }
 // G (+)= A^T A on the INT8 tensor cores (A: N x M); same contract as gram_dev with m = 0.
 void gram_oz_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t M, double* dG, size_t ldg,
-                 bool accumulate) {
+                 bool accumulate, const unsigned long long* cmax_ready = nullptr) {
   if (N == 0) {
     gram_dev(ctx, dA, lda, 0, M, nullptr, 0, 0, dG, ldg, nullptr, 0, accumulate);
     return;
@@ -586,7 +603,7 @@ void gram_oz_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size
   const int splits = oz_splits(N);
   double* ws = ctx->dbuf("syrk_ws", size_t(2) * splits * oz_slot_doubles(M));
   ctx->oz_pending.clear();
-  oz_gram_part(ctx, dA, lda, N, M, ws);
+  oz_gram_part(ctx, dA, lda, N, M, ws, 0, 0, cmax_ready);
   ctx->run("syrk_finish", [&] {
     return launch_oz_finish(ws, static_cast<long long>(oz_slot_doubles(M)), 2 * splits, static_cast<int>(M), dG,
                             static_cast<long long>(ldg), accumulate ? 1 : 0, ctx->stream);
@@ -596,8 +613,8 @@ void gram_oz_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size
 // The augmented Gram of the train path: INT8 digit-plane Gram unless RBPG_GRAM_DMMA=1 selects the
 // FP64 DMMA Gram (comparison / fallback for inputs whose exponents leave the fp64 normal range).
 void gram_aug_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t M, double* dG, size_t ldg,
-                  bool accumulate) {
-  if (ctx->gram_int8) gram_oz_dev(ctx, dA, lda, N, M, dG, ldg, accumulate);
+                  bool accumulate, const unsigned long long* cmax_ready = nullptr) {
+  if (ctx->gram_int8) gram_oz_dev(ctx, dA, lda, N, M, dG, ldg, accumulate, cmax_ready);
   else gram_dev(ctx, dA, lda, N, M, nullptr, 0, 0, dG, ldg, nullptr, 0, accumulate);
 }
 
@@ -649,11 +666,12 @@ GramParts gram_parts_plan(rbpg_context* ctx, size_t L, const std::vector<size_t>
   p.wsStride = static_cast<long long>(slot);
   return gp;
 }
-void gram_parts_launch(rbpg_context* ctx, GramParts& gp, int q, const double* dA, size_t lda) {
+void gram_parts_launch(rbpg_context* ctx, GramParts& gp, int q, const double* dA, size_t lda,
+                       const unsigned long long* cmax_ready = nullptr) {
   const size_t r0 = q == 0 ? 0 : gp.ends[q - 1], rows = gp.ends[q] - r0;
   if (ctx->gram_int8) {
     if (q == 0) ctx->oz_pending.clear();
-    oz_gram_part(ctx, dA + r0 * lda, lda, rows, gp.p.M, gp.p.ws + gp.split0[q] * gp.p.wsStride, q, r0);
+    oz_gram_part(ctx, dA + r0 * lda, lda, rows, gp.p.M, gp.p.ws + gp.split0[q] * gp.p.wsStride, q, r0, cmax_ready);
     return;
   }
   SyrkParams p = gp.p;
@@ -1351,14 +1369,22 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
     if (timed) cudaEventRecord(ctx->ev[0], ctx->stream);
     ck(cudaEventRecord(ctx->aux_ev[0], ctx->stream), "event");  // H rows free (earlier work done)
     ck(cudaStreamWaitEvent(ctx->aux, ctx->aux_ev[0], 0), "wait");
+    // column maxima of each part's rows of [H T], accumulated by the hidden builds (the INT8 Gram's scan)
+    std::vector<unsigned long long*> pcm(cuts.size() + 1, nullptr);
+    if (ctx->gram_int8)
+      for (size_t qq = 0; qq <= cuts.size(); ++qq)
+        pcm[qq] = reinterpret_cast<unsigned long long*>(ctx->dbuf("oz_hcmax." + std::to_string(qq), M));
     size_t r0 = 0, q = 0;
     for (size_t i = 0; i < ready->size(); ++i) {
       const RowReady& rr = (*ready)[i];
       const bool on_aux = i >= cuts[0];
+      const size_t part = static_cast<size_t>(std::upper_bound(cuts.begin(), cuts.end(), i) - cuts.begin());
       ck(cudaStreamWaitEvent(on_aux ? ctx->aux : ctx->stream, rr.ev, 0), "wait upload");
       if (on_aux) std::swap(ctx->stream, ctx->aux);
+      if (pcm[part] && i == (part == 0 ? 0 : cuts[part - 1]))  // first block of the part
+        ck(cudaMemsetAsync(pcm[part], 0, M * sizeof(unsigned long long), ctx->stream), "zero column maxima");
       hidden_dev(ctx, dX + r0 * ldx, ldx, rr.end - r0, d, dW, ldw, db, L, dH + r0 * ldh, ldh, dT + r0 * ldt_in,
-                 ldt_in, m);
+                 ldt_in, m, pcm[part]);
       if (on_aux) std::swap(ctx->stream, ctx->aux);
       r0 = rr.end;
       if (q < cuts.size() && i + 1 == cuts[q]) {  // part q's rows are built: launch it on the main stream
@@ -1366,14 +1392,14 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
           ck(cudaEventRecord(ctx->aux_ev[1 + q], ctx->aux), "event");
           ck(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1 + q], 0), "wait hidden");
         }
-        gram_parts_launch(ctx, gp, static_cast<int>(q), dH, ldh);
+        gram_parts_launch(ctx, gp, static_cast<int>(q), dH, ldh, pcm[q]);
         ++q;
       }
     }
     ck(cudaEventRecord(ctx->aux_ev[1], ctx->aux), "event");
     ck(cudaStreamWaitEvent(ctx->stream, ctx->aux_ev[1], 0), "wait hidden");
     if (timed) cudaEventRecord(ctx->ev[1], ctx->stream);
-    gram_parts_launch(ctx, gp, static_cast<int>(cuts.size()), dH, ldh);
+    gram_parts_launch(ctx, gp, static_cast<int>(cuts.size()), dH, ldh, pcm[cuts.size()]);
     gram_parts_finish(ctx, gp, accumulate);
     if (keep_h) {
       ctx->keep_h(dH, N, L, ldh, key);
@@ -1384,17 +1410,22 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
   }
   if (ready && chunk >= N) {
     if (timed) cudaEventRecord(ctx->ev[0], ctx->stream);
+    unsigned long long* cm = nullptr;
+    if (ctx->gram_int8) {
+      cm = reinterpret_cast<unsigned long long*>(ctx->dbuf("oz_hcmax.0", M));
+      ck(cudaMemsetAsync(cm, 0, M * sizeof(unsigned long long), ctx->stream), "zero column maxima");
+    }
     size_t r0 = 0;
     for (const RowReady& rr : *ready) {
       ck(cudaStreamWaitEvent(ctx->stream, rr.ev, 0), "wait upload");
       hidden_dev(ctx, dX + r0 * ldx, ldx, rr.end - r0, d, dW, ldw, db, L, dH + r0 * ldh, ldh, dT + r0 * ldt_in,
-                 ldt_in, m);
+                 ldt_in, m, cm);
       r0 = rr.end;
     }
     if (timed) cudaEventRecord(ctx->ev[1], ctx->stream);
     // (a row-blocked Gram behind the uploads was measured slower: its per-block wave
     // quantisation costs more than the hidden upload tail)
-    gram_aug_dev(ctx, dH, ldh, N, M, dGaug, ldga, accumulate);
+    gram_aug_dev(ctx, dH, ldh, N, M, dGaug, ldga, accumulate, cm);
     if (keep_h) {
       ctx->keep_h(dH, N, L, ldh, key);
     } else {
@@ -1408,7 +1439,12 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
     // further chunks (H larger than the budget) synchronise on ev[4]/ev[5]
     cudaEvent_t ea = r0 == 0 ? ctx->ev[0] : ctx->ev[4], eb = r0 == 0 ? ctx->ev[1] : ctx->ev[5];
     if (timed) cudaEventRecord(ea, ctx->stream);
-    hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh, dT + r0 * ldt_in, ldt_in, m);  // + T columns
+    unsigned long long* cm = nullptr;
+    if (ctx->gram_int8) {
+      cm = reinterpret_cast<unsigned long long*>(ctx->dbuf("oz_hcmax.0", M));
+      ck(cudaMemsetAsync(cm, 0, M * sizeof(unsigned long long), ctx->stream), "zero column maxima");
+    }
+    hidden_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh, dT + r0 * ldt_in, ldt_in, m, cm);  // + T columns
     if (timed) {
       cudaEventRecord(eb, ctx->stream);
       if (r0 > 0) {
@@ -1418,7 +1454,7 @@ float gram_stage(rbpg_context* ctx, const double* dX, size_t ldx, const double* 
         hidden_ms += ms;
       }
     }
-    gram_aug_dev(ctx, dH, ldh, nr, M, dGaug, ldga, accumulate || r0 > 0);
+    gram_aug_dev(ctx, dH, ldh, nr, M, dGaug, ldga, accumulate || r0 > 0, cm);
   }
   if (keep_h && chunk >= N) {
     ctx->keep_h(dH, N, L, ldh, key);

@@ -677,12 +677,18 @@ __global__ void __launch_bounds__(kOzHidThreads, 1) __cluster_dims__(2, 1, 1)
         const int nr = min(32, p.N - r0);
         double* dst = p.H + static_cast<long long>(r0) * p.ldh + c;
         const double* frow = s_frow + part * 32;
+        double hm = 0.0;  // column maximum of this thread's rows (h >= 0; fmax skips NaN like the scan)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           const double z = fma(v[i] * sc, frow[i], bc);
           const double h = recip_ge1(1.0 + exp_sig(-z));
-          if (i < nr) dst[static_cast<long long>(i) * p.ldh] = h;
+          if (i < nr) {
+            dst[static_cast<long long>(i) * p.ldh] = h;
+            hm = fmax(hm, h);
+          }
         }
+        // fused column scan of the Gram that follows (oz_colmax_kernel's result for these rows)
+        if (p.cmax) atomicMax(p.cmax + c, static_cast<unsigned long long>(__double_as_longlong(hm)));
       }
     }
   }
@@ -1062,6 +1068,20 @@ cudaError_t launch_oz_colmax(const double* A, long long lda, long long N, int M,
   if (e != cudaSuccess) return e;
   const int cb = (M + 31) / 32;
   long long ry = (8LL * num_sms) / cb;  // up to 8 CTAs of 8 warps per SM in one wave: enough loads in flight
+  const long long rmax = (N + 255) / 256;
+  if (ry > rmax) ry = rmax;
+  if (ry < 1) ry = 1;
+  oz_colmax_kernel<<<dim3(cb, static_cast<unsigned>(ry)), 256, 0, s>>>(A, lda, N, M, cmax);
+  return cudaGetLastError();
+}
+
+// column scan accumulated into cmax (no reset): the T columns of a hidden build whose H columns the
+// hidden kernel scanned, or the H of the DMMA hidden kernel
+cudaError_t launch_oz_colmax_acc(const double* A, long long lda, long long N, int M, unsigned long long* cmax,
+                                 int num_sms, cudaStream_t s) {
+  if (N <= 0 || M <= 0) return cudaSuccess;
+  const int cb = (M + 31) / 32;
+  long long ry = (8LL * num_sms) / cb;
   const long long rmax = (N + 255) / 256;
   if (ry > rmax) ry = rmax;
   if (ry < 1) ry = 1;

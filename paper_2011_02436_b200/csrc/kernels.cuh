@@ -95,6 +95,7 @@ struct OzHidParams {
   const double* bias;
   double* H;
   long long ldh;
+  unsigned long long* cmax;  // optional: atomic max of each H column (as ordered bits) for the Gram's scan
 };
 
 // ---- K6i: accuracy pass on the INT8 tensor cores (k_ozaki.cu): scores = H beta from the Gram's digit
