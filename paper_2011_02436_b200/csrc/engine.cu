@@ -559,7 +559,7 @@ void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, 
     for (int ab = 0; ab < 2; ++ab) {
       cuuint64_t dims[3] = {static_cast<cuuint64_t>(Mpad), static_cast<cuuint64_t>(Npad), 7};
       cuuint64_t strides[2] = {static_cast<cuuint64_t>(Mpad), static_cast<cuuint64_t>(Mpad) * Npad};
-      cuuint32_t box[3] = {ab ? 64u : 128u, 32u, g ? 7u : 4u};
+      cuuint32_t box[3] = {ab ? 64u : 128u, 32u, g ? 7u : static_cast<cuuint32_t>(kOzGramPlanesG0)};
       cuuint32_t estr[3] = {1, 1, 1};
       CUresult r = ctx->encode(&maps[2 * g + ab], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, planes, dims, strides, box, estr,
                                CU_TENSOR_MAP_INTERLEAVE_NONE, ab ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,

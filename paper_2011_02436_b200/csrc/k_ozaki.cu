@@ -60,6 +60,14 @@ struct OzGroup {
   static constexpr int kW0 = G == 0 ? 2 : 6;
   static constexpr int kPlanes = G == 0 ? 4 : 7;
 };
+// The Gram's weight split (kOzGramW0G1 = first weight of group 1, kernels.cuh): group 0 = weights
+// 2 .. kOzGramW0G1 - 1 on planes 1 .. kOzGramW0G1 - 2, group 1 = kOzGramW0G1 .. 8 on planes 1 .. 7
+template <int G>
+struct OzGramGroup {
+  static constexpr int kW = G == 0 ? kOzGramW0G1 - 2 : 9 - kOzGramW0G1;
+  static constexpr int kW0 = G == 0 ? 2 : kOzGramW0G1;
+  static constexpr int kPlanes = G == 0 ? kOzGramPlanesG0 : 7;
+};
 
 }  // namespace
 
@@ -216,15 +224,15 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   return r;
 }
 
-template <int G>
+template <class Grp>
 __device__ __forceinline__ void oz_mma_kstep2(uint32_t tbase, uint32_t sa, uint32_t sb, bool first) {
 #pragma unroll
-  for (int w = OzGroup<G>::kW0; w < OzGroup<G>::kW0 + OzGroup<G>::kW; ++w) {
+  for (int w = Grp::kW0; w < Grp::kW0 + Grp::kW; ++w) {
 #pragma unroll
     for (int i = 1; i < w; ++i) {
       const int j = w - i;
-      if (i > OzGroup<G>::kPlanes || j > OzGroup<G>::kPlanes) continue;
-      oz_mma2(tbase + (w - OzGroup<G>::kW0) * 128, oz_desc(sa + (i - 1) * kOzTileBytes),
+      if (i > Grp::kPlanes || j > Grp::kPlanes) continue;
+      oz_mma2(tbase + (w - Grp::kW0) * 128, oz_desc(sa + (i - 1) * kOzTileBytes),
               oz_desc64(sb + (j - 1) * kOzBHalfBytes), (first && i == 1) ? 0u : 1u);
     }
   }
@@ -297,7 +305,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&v)[8]) {
 template <int G>
 __device__ __forceinline__ void oz_readout(uint32_t trow, const OzParams& p, int I, int J, int quarter, int lane,
                                            int col0, const int* ecol, double* tile_out) {
-  constexpr int kW = OzGroup<G>::kW, kW0 = OzGroup<G>::kW0;
+  constexpr int kW = OzGramGroup<G>::kW, kW0 = OzGramGroup<G>::kW0;
   const int rl = quarter * 32 + lane, r = I * 128 + rl;
   const bool rok = r < p.M;
   const int er = (rok ? p.exps[r] : 0) + 4 - 8 * kW0;
@@ -400,7 +408,7 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
       long long gk = 0;  // k-steps issued by this CTA over all its items
       for (int it = cl; it < nitems; it += ncl) {
         const Item t = item_of(it);
-        const int planes = t.G ? OzGroup<1>::kPlanes : OzGroup<0>::kPlanes;
+        const int planes = t.G ? OzGramGroup<1>::kPlanes : OzGramGroup<0>::kPlanes;
         const uint32_t a_bytes = planes * kOzTileBytes, bytes = planes * (kOzTileBytes + kOzBHalfBytes);
         for (int k = 0; k < t.nk; ++k, ++gk) {
           const int s = static_cast<int>(gk % nst);
@@ -425,7 +433,7 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
       for (int it = cl; it < nitems; it += ncl) {
         const Item t = item_of(it);
         if (t.nk == 0) continue;
-        const uint32_t a_bytes = (t.G ? OzGroup<1>::kPlanes : OzGroup<0>::kPlanes) * kOzTileBytes;
+        const uint32_t a_bytes = (t.G ? OzGramGroup<1>::kPlanes : OzGramGroup<0>::kPlanes) * kOzTileBytes;
         long long c0 = p.dbg ? clock64() : 0;
         if (gi > 0) mbar_wait(tempty, static_cast<uint32_t>(gi - 1) & 1);  // previous item read out
         if (p.dbg) t_te += clock64() - c0;
@@ -437,8 +445,8 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
           if (p.dbg) t_full += clock64() - c0;
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + s * kOz2Stage);
-          if (t.G == 0) oz_mma_kstep2<0>(tbase, sa, sa + a_bytes, k == 0);
-          else oz_mma_kstep2<1>(tbase, sa, sa + a_bytes, k == 0);
+          if (t.G == 0) oz_mma_kstep2<OzGramGroup<0>>(tbase, sa, sa + a_bytes, k == 0);
+          else oz_mma_kstep2<OzGramGroup<1>>(tbase, sa, sa + a_bytes, k == 0);
           oz_commit2(&empty[s]);
         }
         oz_commit2(tfull);
@@ -600,8 +608,8 @@ __global__ void __launch_bounds__(kOzHidThreads, 1) __cluster_dims__(2, 1, 1)
             mbar_wait_sleep(&full[s], static_cast<uint32_t>(gk / nst) & 1);
             tc_fence_after();
             const uint32_t sa = smem_u32(smem + s * kOz2Stage);
-            if (g == 0) oz_mma_kstep2<0>(tbase, sa, sa + a_bytes, k == 0);
-            else oz_mma_kstep2<1>(tbase, sa, sa + a_bytes, k == 0);
+            if (g == 0) oz_mma_kstep2<OzGroup<0>>(tbase, sa, sa + a_bytes, k == 0);
+            else oz_mma_kstep2<OzGroup<1>>(tbase, sa, sa + a_bytes, k == 0);
             oz_commit2(&empty[s]);
           }
           oz_commit2(tfull);

@@ -66,6 +66,13 @@ struct SyrkParams {
 };
 
 // ---- K2i: Gram on the INT8 tensor cores by exact digit planes (k_ozaki.cu)
+// INT8 Gram accumulator groups (k_ozaki.cu): group 0 = weights 2 .. kOzGramW0G1 - 1, group 1 = the rest
+// up to 8 (at most 4 weights = 512 TMEM columns each); group 0 reads planes 1 .. kOzGramPlanesG0.
+// The 3 + 4 split (kOzGramW0G1 = 5: 9 % fewer plane bytes per k-step) measured no faster
+// (profiles/r02/oz_split_experiment.txt), so 4 + 3 it is.
+constexpr int kOzGramW0G1 = 6;
+constexpr int kOzGramPlanesG0 = kOzGramW0G1 - 2;
+
 struct OzParams {
   int M;              // columns of A
   int nbI;            // 128-wide tile rows

@@ -90,7 +90,7 @@ int main(int argc, char** argv) {
     for (int ab = 0; ab < 2; ++ab) {
       cuuint64_t d3[3] = {(cuuint64_t)Mpad, (cuuint64_t)Npad, (cuuint64_t)kOzPlanes};
       cuuint64_t s3[2] = {(cuuint64_t)Mpad, (cuuint64_t)Mpad * Npad};
-      cuuint32_t b3[3] = {ab ? 64u : 128u, 32u, g ? 7u : 4u};
+      cuuint32_t b3[3] = {ab ? 64u : 128u, 32u, g ? 7u : (cuuint32_t)kOzGramPlanesG0};
       cuuint32_t e3[3] = {1, 1, 1};
       CUresult cr = cuTensorMapEncodeTiled(&maps[2 * g + ab], CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, S, d3, s3, b3, e3,
                                            CU_TENSOR_MAP_INTERLEAVE_NONE,
