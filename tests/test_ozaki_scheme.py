@@ -70,3 +70,42 @@ def test_digit_reconstruction_exact():
         X = X * 256 + D[p]
     assert np.array_equal(X, np.rint(np.ldexp(a, 54 - e)).astype(np.int64))
     assert np.abs(np.ldexp(X.astype(np.float64), e - 54) - a).max() <= np.ldexp(1.0, e - 55).max()
+
+
+def test_scalar_arithmetic_restatement(tmp_path):
+    """tests/cpp/oz_arith.cpp: the INT8 path's branch-free exp (<= 1 ulp vs std::exp), the exact
+    int64 -> fp64 magic conversion and the bias-trick digit bytes (== the balanced-digit loop), restated
+    on the host."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "oz_arith")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-ffp-contract=off", os.path.join(root, "tests", "cpp", "oz_arith.cpp"),
+                    "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(out.stdout)
+    assert out.returncode == 0 and "PASS" in out.stdout
+
+
+def test_hidden_product_scheme():
+    """The hidden build's XW (csrc/k_ozaki.cu oz_hidden_kernel): X split per row, W per column, 28 digit
+    products summed exactly, v0 = sum_{w<=5} a_w 256^(5-w), v1 = sum_{w>=6} a_w 256^(8-w) exact, one
+    rounding in v0 2^24 + v1, exact power-of-two scale: within 2 ulp-of-scale of the exact product
+    (elm.cpp:93-106 computes the same XW in fp64)."""
+    rng = np.random.default_rng(5)
+    x = rng.uniform(0, 1, (300, 37))
+    x[:, 3] *= -1e-7
+    w = rng.uniform(-1, 1, (37, 50))
+    er, DX = digits(x.T.copy())        # per row of X (columns of X^T)
+    ec, DW = digits(w)                 # per column of W
+    a = {wt: sum(DX[i - 1].T @ DW[wt - i - 1] for i in range(1, wt) if i <= PLANES and wt - i <= PLANES)
+         for wt in range(2, 9)}
+    v0 = ((a[2] * 256 + a[3]) * 256 + a[4]) * 256 + a[5]
+    v1 = (a[6] * 256 + a[7]) * 256 + a[8]
+    assert np.abs(v0).max() < 2 ** 51 and np.abs(v1).max() < 2 ** 41
+    z = v0.astype(np.float64) * 2.0 ** 24 + v1.astype(np.float64)
+    xw = np.ldexp(z, er[:, None] + ec[None, :] - 60)
+    exact = x.astype(np.longdouble) @ w.astype(np.longdouble)
+    scale = np.ldexp(1.0, er[:, None] + ec[None, :]) * x.shape[1]
+    assert float((np.abs(xw.astype(np.longdouble) - exact) / scale).max()) <= 2.0 ** -52
