@@ -19,6 +19,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <tuple>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -523,8 +524,65 @@ void gram_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size_t 
 // Row splits of at most 512 k-steps (16384 rows: the int32 headroom of one accumulation), so every
 // CTA-pair item is read out once into its own packed partial tile set (2 slots per split: the two
 // accumulator groups); the fixed-order reduction (oz_finish_kernel) sums the slots.
-constexpr size_t kOzRowsPerSplit = 16384;
-int oz_splits(size_t rows) { return static_cast<int>(std::max<size_t>(1, (rows + kOzRowsPerSplit - 1) / kOzRowsPerSplit)); }
+// k-steps (32 rows) per split: at most 512 (the int32 headroom).  A small Gram gets shorter splits when
+// that shortens the persistent kernel: a list-scheduling model of the items (round robin over the CTA
+// pairs, group-1 items of 18 MMAs per k-step first, then group 0 with 10; ~34 ns per MMA and ~6 us of
+// read-out per item) plus the fixed-order reduction reading every partial slot (~5 TB/s).  (C4 L = 500:
+// 84 items on 74 pairs at 512 k-steps, 0.62 -> 0.38 ms; C4 L = 8000 / C5: unchanged.)
+long long oz_ksteps_per_split_model(size_t rows, size_t M, int num_sms);
+long long oz_ksteps_per_split(size_t rows, size_t M, int num_sms) {  // memoised: called several times per train
+  static std::mutex mu;
+  static std::map<std::tuple<size_t, size_t, int>, long long> memo;
+  const auto key = std::make_tuple((rows + 63) / 64, M, num_sms);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = memo.find(key);
+    if (it != memo.end()) return it->second;
+  }
+  const long long per = oz_ksteps_per_split_model(rows, M, num_sms);
+  std::lock_guard<std::mutex> lk(mu);
+  if (memo.size() > 4096) memo.clear();
+  memo[key] = per;
+  return per;
+}
+long long oz_ksteps_per_split_model(size_t rows, size_t M, int num_sms) {
+  const long long ksteps = static_cast<long long>((rows + 63) / 64 * 64 / 32);
+  const int nbI = static_cast<int>((M + 127) / 128), np = (nbI + 1) / 2;
+  long long tiles = 0;
+  for (int P = 0; P < np; ++P) tiles += std::min(nbI, 2 * P + 2);
+  const int pairs = std::max(1, num_sms / 2);
+  const long long base = std::max<long long>(1, (ksteps + 511) / 512);
+  long long best_per = (ksteps + base - 1) / base;  // uniform splits
+  if (2 * tiles * base >= 6LL * pairs) return std::min<long long>(best_per, 512);  // already >= 6 waves of items
+  const double slot_bytes = double(nbI) * (nbI + 1) / 2 * 16384 * 8;
+  double best = 1e30;
+  for (long long sp = base; sp <= base * 16; ++sp) {
+    const long long per = (ksteps + sp - 1) / sp;
+    if (per < 32 && sp > base) break;
+    const long long splits = (ksteps + per - 1) / per;
+    const long long items = 2 * tiles * splits;
+    if (items > 4 * 1024 * 1024) break;
+    std::vector<double> load(static_cast<size_t>(std::min<long long>(pairs, items)), 0.0);
+    for (long long it = 0; it < items; ++it) {  // the kernel's item order: group 1 first, split-major
+      const bool g1 = it < tiles * splits;
+      const long long r = g1 ? it : it - tiles * splits;
+      const long long split = r / tiles;
+      const long long nk = std::min(per, ksteps - split * per);
+      load[static_cast<size_t>(it % static_cast<long long>(load.size()))] += (g1 ? 18 : 10) * nk * 34e-9 + 6e-6;
+    }
+    const double t = *std::max_element(load.begin(), load.end()) + 2.0 * splits * slot_bytes / 5e12;
+    if (t < best * 0.98) {
+      best = t;
+      best_per = per;
+    }
+  }
+  return std::min<long long>(best_per, 512);
+}
+int oz_splits(size_t rows, size_t M, int num_sms) {
+  const long long per = oz_ksteps_per_split(rows, M, num_sms);
+  const long long ksteps = static_cast<long long>((rows + 63) / 64 * 64 / 32);
+  return static_cast<int>(std::max<long long>(1, (ksteps + per - 1) / per));
+}
 size_t oz_slot_doubles(size_t M) {
   const size_t nbI = (M + 127) / 128;
   return nbI * (nbI + 1) / 2 * 16384;  // lower 128 x 128 tiles, packed
@@ -586,8 +644,8 @@ void oz_gram_part(rbpg_context* ctx, const double* dA, size_t lda, size_t rows, 
   p.Mpad = Mpad;
   p.Npad = Npad;
   p.ksteps = Npad / 32;
-  p.splits = oz_splits(rows);
-  p.kPerSplit = kOzRowsPerSplit / 32;
+  p.splits = oz_splits(rows, M, ctx->num_sms);
+  p.kPerSplit = oz_ksteps_per_split(rows, M, ctx->num_sms);
   p.exps = exps;
   p.ws = ws;
   p.wsStride = static_cast<long long>(oz_slot_doubles(M));
@@ -600,7 +658,7 @@ void gram_oz_dev(rbpg_context* ctx, const double* dA, size_t lda, size_t N, size
     gram_dev(ctx, dA, lda, 0, M, nullptr, 0, 0, dG, ldg, nullptr, 0, accumulate);
     return;
   }
-  const int splits = oz_splits(N);
+  const int splits = oz_splits(N, M, ctx->num_sms);
   double* ws = ctx->dbuf("syrk_ws", size_t(2) * splits * oz_slot_doubles(M));
   ctx->oz_pending.clear();
   oz_gram_part(ctx, dA, lda, N, M, ws, 0, 0, cmax_ready);
@@ -643,7 +701,7 @@ GramParts gram_parts_plan(rbpg_context* ctx, size_t L, const std::vector<size_t>
   for (size_t e : ends) {
     const size_t rows = e - r0;
     if (ctx->gram_int8) {  // INT8 Gram: 2 packed partial slots per split
-      const int sp = oz_splits(rows);
+      const int sp = oz_splits(rows, L, ctx->num_sms);
       gp.split0.push_back(gp.total);
       gp.splits.push_back(sp);
       gp.per.push_back(0);

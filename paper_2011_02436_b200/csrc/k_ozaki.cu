@@ -121,29 +121,46 @@ __device__ __forceinline__ void byte_transpose4(uint32_t a, uint32_t b, uint32_t
   r[3] = __byte_perm(t1, t3, 0x7632);
 }
 
-__global__ void __launch_bounds__(256) oz_slice_kernel(const double* __restrict__ A, long long lda, long long N, int M,
+// Grid: x over 128-thread blocks of 8-column groups (a thread's 8 columns and their scales are fixed),
+// y strides the rows -- no index division in the loop; 16-byte loads when the row segment is aligned.
+__global__ void __launch_bounds__(128) oz_slice_kernel(const double* __restrict__ A, long long lda, long long N, int M,
                                                        const int* __restrict__ exps, int8_t* __restrict__ S,
                                                        long long plane_stride, int Mpad, long long Npad) {
   constexpr unsigned long long kBias = 0x808080808080ull;
-  const int groups = Mpad / 8;
-  const long long total = Npad * groups;
-  for (long long it = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; it < total;
-       it += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long r = it / groups;
-    const int c0 = static_cast<int>(it - r * groups) * 8;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= Mpad / 8) return;
+  const int c0 = g * 8;
+  // A 2^(54 - e) exactly (|.| < 2^54): one power-of-two factor, two when 54 - e exceeds the normal
+  // exponent range (columns with max < 2^-969); a result below 2^-1022 rounds to 0 either way
+  double f1[8], f2[8];
+  bool live[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int c = c0 + q;
+    live[q] = c < M;
+    const int k = live[q] ? 54 - exps[c] : 0;
+    f1[q] = pow2i(min(k, 1023));
+    f2[q] = k > 1023 ? pow2i(k - 1023) : 1.0;
+  }
+  const bool full = c0 + 8 <= M;
+  for (long long r = blockIdx.y; r < Npad; r += gridDim.y) {
+    double a[8];
+    const double* row = A + r * lda + c0;
+    if (r < N && full && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; q += 2) {
+        const double2 t = __ldcs(reinterpret_cast<const double2*>(row + q));
+        a[q] = t.x;
+        a[q + 1] = t.y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = (r < N && live[q]) ? row[q] : 0.0;
+    }
     uint32_t lo[8], hi[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int c = c0 + q;
-      long long X = 0;
-      if (r < N && c < M) {
-        // A 2^(54 - e) exactly (|.| < 2^54): one power-of-two factor, two when 54 - e exceeds the
-        // normal exponent range (columns with max < 2^-969); a result below 2^-1022 rounds to 0 either way
-        const int k = 54 - exps[c];
-        double v = A[r * lda + c] * pow2i(min(k, 1023));
-        if (k > 1023) v *= pow2i(k - 1023);
-        X = __double2ll_rn(v);
-      }
+      const long long X = __double2ll_rn((a[q] * f1[q]) * f2[q]);
       const unsigned long long V = (static_cast<unsigned long long>(X) + kBias) ^ kBias;
       lo[q] = static_cast<uint32_t>(V);
       hi[q] = static_cast<uint32_t>(V >> 32);
@@ -1003,7 +1020,7 @@ cudaError_t launch_oz_scores(const CUtensorMap* maps, const OzScoresParams& p, c
 }
 
 // Fixed-order reduction of the packed partial tiles: G[i][j] = G[j][i] = (acc ? G[i][j] : 0) +
-// sum_{slot} part[slot][tile(i, j)][i % 128][j % 128] over the lower triangle, slots in increasing
+// sum_{slot} part[slot][tile(i, j)][i % 128][j % 128] over the lower triangle (compensated), slots in increasing
 // order (split-major, group 0 before group 1 within a split).  One CTA per 32 x 32 block, staged in
 // shared memory for the mirrored (transposed) half.
 __global__ void __launch_bounds__(256) oz_finish_kernel(const double* __restrict__ ws, long long wsStride, int slots,
@@ -1024,8 +1041,17 @@ __global__ void __launch_bounds__(256) oz_finish_kernel(const double* __restrict
     if (i < M && j <= i) {
       const int I = i >> 7, J = j >> 7;
       const long long off = static_cast<long long>(I * (I + 1) / 2 + J) * 16384 + (i & 127) * 128 + (j & 127);
-      v = ws[off];
-      for (int sl = 1; sl < slots; ++sl) v = add_rn(v, ws[sl * wsStride + off]);
+      // compensated (TwoSum) fixed-order sum: the error stays ~1 ulp of the result however many split
+      // partials a small Gram is cut into
+      double sum = ws[off], comp = 0.0;
+      for (int sl = 1; sl < slots; ++sl) {
+        const double x = ws[sl * wsStride + off];
+        const double t = add_rn(sum, x);
+        const double bp = sub_rn(t, sum);
+        comp = add_rn(comp, add_rn(sub_rn(sum, sub_rn(t, bp)), sub_rn(x, bp)));
+        sum = t;
+      }
+      v = add_rn(sum, comp);
       if (accumulate) v = add_rn(G[static_cast<long long>(i) * ldg + j], v);
       G[static_cast<long long>(i) * ldg + j] = v;
     }
@@ -1102,9 +1128,10 @@ cudaError_t launch_oz_slice(const double* A, long long lda, long long N, int M, 
   oz_exps_kernel<<<(Mpad + 255) / 256, 256, 0, s>>>(cmax, M, Mpad, exps);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  const long long work = Npad * (Mpad / 8);
-  const unsigned grid = static_cast<unsigned>(std::min<long long>((work + 255) / 256, 148LL * 16));
-  oz_slice_kernel<<<grid, 256, 0, s>>>(A, lda, N, M, exps, S, static_cast<long long>(Mpad) * Npad, Mpad, Npad);
+  const int gx = (Mpad / 8 + 127) / 128;
+  const long long gy = std::min<long long>(Npad, std::max<long long>(1, (148LL * 12 + gx - 1) / gx));
+  oz_slice_kernel<<<dim3(gx, static_cast<unsigned>(gy)), 128, 0, s>>>(A, lda, N, M, exps, S,
+                                                                     static_cast<long long>(Mpad) * Npad, Mpad, Npad);
   return cudaGetLastError();
 }
 
