@@ -374,7 +374,9 @@ def main():
     pred = {"rows": pr, "ms": pms, "TFLOP/s": pflops / (pms * 1e-3) / 1e12,
             "frac_fp64_peak": pflops / (pms * 1e-3) / 1e12 / fp64_peak()[0],
             "alg_flops": pflops, "hbm_bytes": pr * d * 8 + pr * 4,
-            "kernel": "predict_kernel (K6b: fused sigma(XW+b) beta + arg-max labels; H never stored)"}
+            "kernel": ("INT8 path (m > 48): K1i hidden build of row chunks + digit planes + K6i scores with the arg-max "
+                       "epilogue; TFLOP/s are FP64-equivalent" if m > 48 else
+                       "predict_kernel (K6b: fused sigma(XW+b) beta + arg-max labels on DMMA; H never stored)")}
 
     if rank == 0:
         peak, peak_src = fp64_peak()

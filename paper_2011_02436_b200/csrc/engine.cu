@@ -1549,6 +1549,44 @@ bool oz_scores_ready(rbpg_context* ctx, size_t N, size_t M) {
   }
   return r == N;
 }
+// One Gram part's INT8 scores: beta folded with the part's column exponents and split per class, then
+// the hit count (labels = targets), and / or the arg-max labels and the scores of the part's rows.
+void oz_scores_part(rbpg_context* ctx, const rbpg_context::OzPart& pt, size_t L, size_t m, const double* dBeta,
+                    size_t ldb, const int* tlabels, unsigned long long* hits, int* out_labels, double* S, size_t lds) {
+  const size_t K = pt.Mpad;
+  auto* bp = reinterpret_cast<int8_t*>(ctx->buf("ozs.bplanes", 7 * 128 * K));
+  double* cs = ctx->dbuf("ozs.cscale", 128);
+  ctx->run("scores_kernel", [&] {
+    return launch_oz_beta_planes(dBeta, static_cast<long long>(ldb), static_cast<int>(L), static_cast<int>(m), pt.exps,
+                                 static_cast<int>(K), bp, cs, ctx->stream);
+  });
+  auto map = [&](int8_t* base, size_t rows, uint32_t box_rows, uint32_t np) {
+    CUtensorMap mp;
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), 7};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(K) * rows};
+    cuuint32_t box[3] = {32u, box_rows, np};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = ctx->encode(&mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(RBPG_CUDA_ERROR, "cuTensorMapEncodeTiled (scores planes) failed (" + std::to_string(int(r)) + ")");
+    return mp;
+  };
+  CUtensorMap maps[4] = {map(pt.planes, pt.Npad, 128, 4), map(bp, 128, 64, 4), map(pt.planes, pt.Npad, 128, 7),
+                         map(bp, 128, 64, 7)};
+  OzScoresParams p{};
+  p.rows = static_cast<int>(pt.rows);
+  p.m = static_cast<int>(m);
+  p.nP = static_cast<int>((pt.rows + 255) / 256);
+  p.ksteps = static_cast<int>(K / 32);
+  p.cscale = cs;
+  p.labels = tlabels ? tlabels + pt.r0 : nullptr;
+  p.hits = hits;
+  p.out_labels = out_labels ? out_labels + pt.r0 : nullptr;
+  p.S = S ? S + pt.r0 * lds : nullptr;
+  p.lds = static_cast<long long>(lds);
+  ctx->run("scores_kernel", [&] { return launch_oz_scores(maps, p, ctx->stream); });
+}
 void oz_scores_dev(rbpg_context* ctx, size_t N, size_t L, size_t m, const double* dBeta, size_t ldb, const double* dT,
                    size_t ldt, unsigned long long* hits) {
   int* labels = reinterpret_cast<int*>(ctx->buf("ozs.labels", N * sizeof(int)));
@@ -1556,38 +1594,7 @@ void oz_scores_dev(rbpg_context* ctx, size_t N, size_t L, size_t m, const double
     return launch_oz_labels(dT, static_cast<long long>(ldt), static_cast<long long>(N), static_cast<int>(m), labels,
                             ctx->stream);
   });
-  for (const auto& pt : ctx->oz_kept) {
-    const size_t K = pt.Mpad;
-    auto* bp = reinterpret_cast<int8_t*>(ctx->buf("ozs.bplanes", 7 * 128 * K));
-    double* cs = ctx->dbuf("ozs.cscale", 128);
-    ctx->run("scores_kernel", [&] {
-      return launch_oz_beta_planes(dBeta, static_cast<long long>(ldb), static_cast<int>(L), static_cast<int>(m), pt.exps,
-                                   static_cast<int>(K), bp, cs, ctx->stream);
-    });
-    auto map = [&](int8_t* base, size_t rows, uint32_t box_rows, uint32_t np) {
-      CUtensorMap mp;
-      cuuint64_t dims[3] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(rows), 7};
-      cuuint64_t strides[2] = {static_cast<cuuint64_t>(K), static_cast<cuuint64_t>(K) * rows};
-      cuuint32_t box[3] = {32u, box_rows, np};
-      cuuint32_t estr[3] = {1, 1, 1};
-      CUresult r = ctx->encode(&mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, base, dims, strides, box, estr,
-                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) fail(RBPG_CUDA_ERROR, "cuTensorMapEncodeTiled (scores planes) failed (" + std::to_string(int(r)) + ")");
-      return mp;
-    };
-    CUtensorMap maps[4] = {map(pt.planes, pt.Npad, 128, 4), map(bp, 128, 64, 4), map(pt.planes, pt.Npad, 128, 7),
-                           map(bp, 128, 64, 7)};
-    OzScoresParams p{};
-    p.rows = static_cast<int>(pt.rows);
-    p.m = static_cast<int>(m);
-    p.nP = static_cast<int>((pt.rows + 255) / 256);
-    p.ksteps = static_cast<int>(K / 32);
-    p.cscale = cs;
-    p.labels = labels + pt.r0;
-    p.hits = hits;
-    ctx->run("scores_kernel", [&] { return launch_oz_scores(maps, p, ctx->stream); });
-  }
+  for (const auto& pt : ctx->oz_kept) oz_scores_part(ctx, pt, L, m, dBeta, ldb, labels, hits, nullptr, nullptr, 0);
 }
 
 // K6b: fused sigma(X W + b) beta with the arg-max epilogue (m <= 128): optional scores S, labels,
@@ -1598,6 +1605,39 @@ void predict_dev(rbpg_context* ctx, const double* dX, size_t ldx, size_t N, size
   if (N == 0) return;
   const int mp = predict_mp(static_cast<int>(m));
   if (mp == 0) fail(RBPG_INVALID_ARGUMENT, "predict_dev: more than 128 classes");
+  // m > 48: the INT8 path (K1i hidden build of a row chunk with its column scan, digit planes, K6i
+  // scores) -- the fused DMMA kernel below is FP64-bound on its scores product there
+  if (ctx->gram_int8 && m > 48 && d <= kOzHidMaxD && (L + 255) / 256 * 256 <= 16384) {
+    const size_t ldh = even(L);
+    const size_t chunk = std::min<size_t>(N, std::max<size_t>(256, (size_t(8) << 30) / (ldh * 15)));
+    double* dH = ctx->dbuf("pred.H", chunk * ldh);
+    auto* cm = reinterpret_cast<unsigned long long*>(ctx->dbuf("pred.cmax", L));
+    int* tl = nullptr;
+    if (T && hits) {
+      tl = reinterpret_cast<int*>(ctx->buf("pred.tlabels", N * sizeof(int)));
+      ctx->run("scores_kernel", [&] {
+        return launch_oz_labels(T, static_cast<long long>(ldt), static_cast<long long>(N), static_cast<int>(m), tl,
+                                ctx->stream);
+      });
+    }
+    for (size_t r0 = 0; r0 < N; r0 += chunk) {
+      const size_t nr = std::min(chunk, N - r0);
+      ck(cudaMemsetAsync(cm, 0, L * sizeof(unsigned long long), ctx->stream), "zero column maxima");
+      hidden_oz_dev(ctx, dX + r0 * ldx, ldx, nr, d, dW, ldw, db, L, dH, ldh, cm);
+      const int nbI = static_cast<int>((L + 127) / 128), Mpad = (nbI + 1) / 2 * 2 * 128;
+      const long long Npad = static_cast<long long>((nr + 63) / 64 * 64);
+      int* exps = reinterpret_cast<int*>(ctx->dbuf("pred.exps", (Mpad + 1) / 2));
+      auto* planes = reinterpret_cast<int8_t*>(ctx->buf("pred.planes", size_t(7) * Mpad * Npad));
+      ctx->run("oz_slice", [&] {
+        return launch_oz_slice(dH, static_cast<long long>(ldh), static_cast<long long>(nr), static_cast<int>(L), cm, exps,
+                               Mpad, Npad, planes, ctx->stream);
+      });
+      rbpg_context::OzPart pt{0, nr, static_cast<size_t>(Mpad), static_cast<size_t>(Npad), planes, exps};
+      oz_scores_part(ctx, pt, L, m, dBeta, ldb, tl ? tl + r0 : nullptr, hits, labels ? labels + r0 : nullptr,
+                     S ? S + r0 * lds : nullptr, lds);
+    }
+    return;
+  }
   Padded X = pad_device(ctx, "pred.x", dX, ldx, N, d);
   Padded W = pad_device(ctx, "pred.w", dW, ldw, d, L);
   Padded B = pad_device(ctx, "beta.pad", dBeta, ldb, L, m);

@@ -914,9 +914,10 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty);
       ++q;
-      // arg-max over this thread's classes (strict '>' in increasing class order)
+      // arg-max over this thread's classes (strict '>' in increasing class order); scores stored on request
       double best = 0.0;
       int bi = -1;
+      double* srow = (p.S && r < p.rows) ? p.S + static_cast<long long>(r) * p.lds : nullptr;
 #pragma unroll
       for (int i = 0; i < 64; ++i) {
         const int j = half * 64 + i;
@@ -925,6 +926,7 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
           best = sv;
           bi = j;
         }
+        if (srow && j < p.m) srow[j] = sv;
       }
       // the two halves of row rl: half 1 posts, half 0 combines (ties stay with the lower classes)
       named_bar_sync_n(1 + quarter, 64);
@@ -936,7 +938,8 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
       if (half == 0 && r < p.rows) {
         const int b1 = s_idx[rl];
         if (b1 >= 0 && (bi < 0 || s_best[rl] > best)) bi = b1;
-        my_hits += (bi == p.labels[r]) ? 1u : 0u;
+        if (p.labels) my_hits += (bi == p.labels[r]) ? 1u : 0u;
+        if (p.out_labels) p.out_labels[r] = bi;
       }
     }
     if (half == 0) {
@@ -951,7 +954,7 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
   }
-  if (threadIdx.x == 0 && s_hits) atomicAdd(p.hits, static_cast<unsigned long long>(s_hits));
+  if (threadIdx.x == 0 && s_hits && p.hits) atomicAdd(p.hits, static_cast<unsigned long long>(s_hits));
 }
 
 // Digit planes of the folded beta (K-major, [plane][class][column], 128 class rows; rows >= m and

@@ -114,8 +114,11 @@ struct OzScoresParams {
   int nP;              // 256-row pair tiles
   int ksteps;          // plane row length / 32 (the contraction over the columns of [H T])
   const double* cscale;  // [128] 2^(f_j - 60): the class exponents of the folded beta
-  const int* labels;   // target label (arg-max of the T row) of each row of the part
+  const int* labels;   // optional: target label (arg-max of the T row) of each row, for the hit count
   unsigned long long* hits;
+  int* out_labels;     // optional: arg-max class of each row (predict)
+  double* S;           // optional: the scores (rows x m, ld lds)
+  long long lds;
 };
 
 // ---- generic DMMA GEMM: C = alpha * op(A) op(B) + beta * C (row-major)
