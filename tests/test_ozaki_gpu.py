@@ -137,3 +137,22 @@ def test_int8_accuracy_pass_vs_oracle(n, d, L, m):
           f"(oracle {ref['diag']['training_accuracy']})")
     assert diag.training_accuracy == ref["diag"]["training_accuracy"]
     assert diag_d.training_accuracy == ref["diag"]["training_accuracy"]
+
+
+def test_wide_inputs_fall_back_to_dmma_hidden_build():
+    """d > 16384 exceeds the INT8 hidden build's int32 headroom (7 d 2^14 < 2^31): the DMMA hidden kernel
+    builds H and its rows are scanned for the INT8 Gram's column exponents instead; the train still
+    matches the oracle (pivots, rank, labels)."""
+    import oracle
+
+    n, d, L, m = 300, 16400, 40, 3
+    x, t = rb.synth_classification(n, d, m, 91, 92)
+    params = rb.ElmParams(d, L, m, 93)
+    model, diag, order = rb.train(params, x, t, rb.SolverStrategy.rank_based(), return_order=True)
+    ref = oracle.train(d, L, m, 93, x, t, "rank", 0, 0.0)
+    assert diag.rank == ref["diag"]["rank"]
+    assert order == ref["order"]
+    assert diag.training_accuracy == ref["diag"]["training_accuracy"]
+    rel = np.linalg.norm(model.beta - ref["beta"]) / np.linalg.norm(ref["beta"])
+    print(f"d={d}: beta rel {rel:.2e}")
+    assert rel < 1e-6
