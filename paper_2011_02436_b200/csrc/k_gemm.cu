@@ -507,13 +507,15 @@ __global__ void __launch_bounds__(256, 1)
 // TILE 32 (64 threads) for the small late updates: four times the CTAs per DMMA of a 64-wide tile.
 // KS: k-stages resident (4 = the whole rank-64 panel loaded up front; 2 or 1 = the panel streamed
 // through fewer stages, reloaded as they are consumed, so three or four CTAs fit on an SM)
-template <int TILE, int KS = kStages>
-__global__ void __launch_bounds__(2 * TILE, 1)
+// NT: 2 * TILE threads (warps of (TILE / 2) x 32), or 4 * TILE (warps of (TILE / 4) x 32: twice the warps
+// issuing DMMAs per tile -- a warp issues at most one DMMA per ~34 cycles, so the pipe needs several)
+template <int TILE, int KS = kStages, int NT = 2 * TILE>
+__global__ void __launch_bounds__(NT, NT == 4 * TILE ? 3 : 1)
     trail_kernel(const __grid_constant__ CUtensorMap tmP, SyrkParams p) {
-  constexpr int NT = 2 * TILE;      // threads: warps of (TILE / 2) x 32
   constexpr int TP = TILE + 4;      // padded smem rows (TMA box {TILE + 4, 16})
-  constexpr int MT = TILE / 32;     // m16 fragments per warp
   constexpr int WARPS_N = TILE / 32;
+  constexpr int WARPS_M = NT / 32 / WARPS_N;
+  constexpr int MT = TILE / WARPS_M / 16;  // m16 fragments per warp
   constexpr int NG = MT * 2 * 2 * 4;  // G_old entries per thread
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = align1024(smem_raw);
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(2 * TILE, 1)
       if (!diag) tma_load_2d(Bs + s * kBK * TP, &tmP, &full[s], j0, s * kBK);
     }
   }
-  const int wm = (warp / WARPS_N) * (TILE / 2), wn = (warp % WARPS_N) * 32;
+  const int wm = (warp / WARPS_N) * (TILE / WARPS_M), wn = (warp % WARPS_N) * 32;
   const int M = p.M, off = p.off;
   {  // G_old gathers -> gsm
     int sr[MT][2], sc[2][4];
@@ -887,11 +889,13 @@ cudaError_t launch_trail(const CUtensorMap& tmP, const SyrkParams& p, int tile, 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (tile == 64) {
-    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(trail_kernel<64, 1>), trail_smem<64, 1>());
+    // 256 threads (8 warps of 16 x 32) at 3 CTAs per SM: 24 DMMA-issuing warps per SM instead of 16
+    // (C4 L = 8000 trailing 18.1 -> 16.0-16.5 ms, bitwise-identical results)
+    cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(trail_kernel<64, 1, 256>), trail_smem<64, 1>());
     if (e != cudaSuccess) return e;
-    cfg.blockDim = dim3(128);
+    cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = trail_smem<64, 1>();
-    return cudaLaunchKernelEx(&cfg, trail_kernel<64, 1>, tmP, p);
+    return cudaLaunchKernelEx(&cfg, trail_kernel<64, 1, 256>, tmP, p);
   }
   if (tile == 32) {
     cudaError_t e = ensure_attrs(reinterpret_cast<const void*>(trail_kernel<32>), trail_smem<32>());
