@@ -107,6 +107,7 @@ cudaError_t launch_oz_beta_planes(const double*, long long, int, int, const int*
 cudaError_t launch_oz_labels(const double*, long long, long long, int, int*, cudaStream_t);
 cudaError_t launch_oz_scores(const CUtensorMap* maps, const OzScoresParams&, cudaStream_t);
 int oz_pair_order(int nbI, int B, int2* out);
+int oz_pair_items(int nbI);
 cudaError_t launch_oz_finish(const double*, long long, int, int, double*, long long, int, cudaStream_t);
 cudaError_t launch_sum_parts(const double*, long long, int, long long, double*, cudaStream_t);
 }  // namespace rbpg
@@ -547,9 +548,8 @@ long long oz_ksteps_per_split(size_t rows, size_t M, int num_sms) {  // memoised
 }
 long long oz_ksteps_per_split_model(size_t rows, size_t M, int num_sms) {
   const long long ksteps = static_cast<long long>((rows + 63) / 64 * 64 / 32);
-  const int nbI = static_cast<int>((M + 127) / 128), np = (nbI + 1) / 2;
-  long long tiles = 0;
-  for (int P = 0; P < np; ++P) tiles += std::min(nbI, 2 * P + 2);
+  const int nbI = static_cast<int>((M + 127) / 128);
+  const long long tiles = oz_pair_items(nbI);  // CTA-pair items per split and group
   const int pairs = std::max(1, num_sms / 2);
   const long long base = std::max<long long>(1, (ksteps + 511) / 512);
   long long best_per = (ksteps + base - 1) / base;  // uniform splits
@@ -845,6 +845,7 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
 
 
   unsigned long long* trace = nullptr;
+  const bool trace_wide = std::getenv("RBPG_PANEL_TRACE") && std::string(std::getenv("RBPG_PANEL_TRACE")) == "wide";
   if (std::getenv("RBPG_PANEL_TRACE")) {
     trace = static_cast<unsigned long long*>(ctx->buf(tag + ".ptrace", 128));
     ck(cudaMemsetAsync(trace, 0, 128, s), "memset trace");
@@ -902,7 +903,8 @@ FactorResult factor_dev(rbpg_context* ctx, const double* dG, size_t ldg, size_t 
     pp.pivoting = pivoting;
     pp.rows_per_cta = 0;  // chosen by launch_panel
     pp.neligible = static_cast<int>(neligible);
-    pp.trace = trace;
+    // RBPG_PANEL_TRACE=wide: only the 32-wide panels (more than 4096 labels left) are traced
+    pp.trace = (trace && (!trace_wide || panel_width(static_cast<int>(n), static_cast<int>(k)) < 64)) ? trace : nullptr;
     if (tl && tl_n < tl_max) {
       pp.tl = tl;
       pp.tl_slot = tl_n++;

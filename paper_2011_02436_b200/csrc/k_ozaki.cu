@@ -32,6 +32,7 @@
 #include "kernels.cuh"
 
 #include <algorithm>
+#include <vector>
 
 namespace rbpg {
 
@@ -321,7 +322,7 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int (&v)[8]) {
 // TMEM load of the item is done before the caller releases the accumulators; the stores drain after.
 template <int G>
 __device__ __forceinline__ void oz_readout(uint32_t trow, const OzParams& p, int I, int J, int quarter, int lane,
-                                           int col0, const int* ecol, double* tile_out) {
+                                           int col0, const int* ecol, double* tile_out, bool trans) {
   constexpr int kW = OzGramGroup<G>::kW, kW0 = OzGramGroup<G>::kW0;
   const int rl = quarter * 32 + lane, r = I * 128 + rl;
   const bool rok = r < p.M;
@@ -342,11 +343,14 @@ __device__ __forceinline__ void oz_readout(uint32_t trow, const OzParams& p, int
 #pragma unroll
       for (int q = 0; q < 8; ++q) v[q] = fma(v[q], 0x1.0p-8, i51_to_f64(c[q]));
     }
-    if (rok) {
+    if (rok && !trans) {
 #pragma unroll
       for (int q = 0; q < 8; q += 2)
         *reinterpret_cast<double2*>(dst + cb * 8 + q) =
             make_double2(scale2(v[q], er + ecol[cb * 8 + q]), scale2(v[q + 1], er + ecol[cb * 8 + q + 1]));
+    } else if (rok) {  // transposed: the warp's 32 rows are 32 consecutive entries of a stored row
+#pragma unroll
+      for (int q = 0; q < 8; ++q) tile_out[(cb * 8 + q) * 128 + rl] = scale2(v[q], er + ecol[cb * 8 + q]);
     }
   }
 }
@@ -380,6 +384,7 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
 
   struct Item {
     int G, split, I, J, nk;
+    bool valid;  // this CTA's tile is stored (rank 1 of a single-tile item is idle)
     long long kb;
   };
   auto item_of = [&](int it) {
@@ -387,8 +392,10 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
     t.G = it < per ? 1 : 0;
     const int r = it < per ? it : it - per;
     t.split = r / p.nTiles;
-    const int2 pj = p.tiles[r % p.nTiles];
-    t.I = 2 * pj.x + rank;
+    const int2 pj = p.tiles[r % p.nTiles];  // (a0 << 16 | a1, b): oz_pair_order
+    const int a0 = pj.x >> 16, a1 = pj.x & 0xFFFF;
+    t.valid = rank == 0 || a1 != 0xFFFF;
+    t.I = (rank == 0 || !t.valid) ? a0 : a1;
     t.J = pj.y;
     t.kb = static_cast<long long>(t.split) * p.kPerSplit;
     const long long ke = min(p.ksteps, t.kb + p.kPerSplit);
@@ -484,12 +491,19 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
     long long gi = 0;
     for (int it = cl; it < nitems; it += ncl) {
       const Item t = item_of(it);
-      const bool store = t.I < p.nbI && t.J <= t.I;  // the block above the diagonal is not stored
+      const bool store = t.valid;
+      // the accumulator is G[rows I][columns J]; above the diagonal (a leftover computed as its
+      // transpose) it is stored transposed into packed tile (J, I)
+      const bool trans = t.I < t.J;
+      const int PI = trans ? t.J : t.I, PJ = trans ? t.I : t.J;
       double* tile_out = p.ws + static_cast<long long>(t.split * 2 + t.G) * p.wsStride +
-                         static_cast<long long>(store ? t.I * (t.I + 1) / 2 + t.J : 0) * 16384;
+                         static_cast<long long>(store ? PI * (PI + 1) / 2 + PJ : 0) * 16384;
       if (t.nk == 0) {  // empty split: a zero partial
         if (store)
-          for (int c = half * 64; c < half * 64 + 64; ++c) tile_out[(quarter * 32 + lane) * 128 + c] = 0.0;
+          for (int c = half * 64; c < half * 64 + 64; ++c) {
+            const int rl = quarter * 32 + lane;
+            tile_out[trans ? c * 128 + rl : rl * 128 + c] = 0.0;
+          }
         continue;
       }
       // column exponents of this item, staged while the MMAs run (the previous item's read-out by this
@@ -506,8 +520,8 @@ __global__ void __launch_bounds__(kOz2Threads, 1) __cluster_dims__(2, 1, 1)
       long long c2 = (p.dbg && lane == 0) ? clock64() : 0;
       OzParams q = p;
       if (!store) q.M = 0;
-      if (t.G == 0) oz_readout<0>(trow, q, t.I, t.J, quarter, lane, half * 64, ecol - 64 * half, tile_out);
-      else oz_readout<1>(trow, q, t.I, t.J, quarter, lane, half * 64, ecol - 64 * half, tile_out);
+      if (t.G == 0) oz_readout<0>(trow, q, t.I, t.J, quarter, lane, half * 64, ecol - 64 * half, tile_out, trans);
+      else oz_readout<1>(trow, q, t.I, t.J, quarter, lane, half * 64, ecol - 64 * half, tile_out, trans);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty);
@@ -1074,16 +1088,48 @@ cudaError_t launch_oz_finish(const double* ws, long long wsStride, int slots, in
   return cudaGetLastError();
 }
 
-// (pair, J) blocks of the CTA-pair Gram: pair P covers tile rows 2P, 2P + 1 and columns J <= 2P + 1
-// (< nbI), in square blocks of B pairs x 2B columns
+// Items of the CTA-pair Gram: two 128 x 128 tiles that share their B column block (one M = 256 x N = 128
+// MMA stream), packed as x = (a0 << 16) | a1 (rank 0 reads tile rows a0, rank 1 tile rows a1; a1 = 0xFFFF:
+// rank 1 idle), y = b (columns).  Every lower tile (a, c), a >= c, is produced exactly once: column c's
+// tiles (c, c), (c + 1, c), ... pair up top-down; when their count nbI - c is odd, the bottom tile
+// (nbI - 1, c) is left over and computed as its transpose (rows c, columns nbI - 1), so the leftovers of
+// all columns share one B block and pair up too.  (Pairing adjacent tile rows instead computes a tile
+// above the diagonal in every diagonal pair block and a padding tile row when nbI is odd: C5's 65 tile
+// rows took 1122 items, this takes 1073.)  A transposed item's integer accumulators are the transpose
+// of the normal ones (the weight sums include both (i, j) and (j, i)), so the Gram is bitwise the same.
+// Launch order: square blocks of B tile rows x B columns (L2 reuse of both operands), leftovers last.
 int oz_pair_order(int nbI, int B, int2* out) {
-  const int np = (nbI + 1) / 2;
+  struct It {
+    int a0, a1, b;
+  };
+  std::vector<It> its, tail;
+  std::vector<int> left;
+  for (int c = 0; c < nbI; ++c) {
+    int a = c;
+    for (; a + 1 < nbI; a += 2) its.push_back({a, a + 1, c});
+    if (a < nbI) left.push_back(c);  // (nbI - 1, c) left over
+  }
+  for (size_t i = 0; i < left.size(); i += 2)
+    tail.push_back({left[i], i + 1 < left.size() ? left[i + 1] : -1, nbI - 1});
+  std::stable_sort(its.begin(), its.end(), [B](const It& u, const It& v) {
+    if (u.a0 / B != v.a0 / B) return u.a0 / B < v.a0 / B;
+    if (u.b / B != v.b / B) return u.b / B < v.b / B;
+    if (u.a0 != v.a0) return u.a0 < v.a0;
+    return u.b < v.b;
+  });
   int n = 0;
-  for (int bp = 0; bp * B < np; ++bp)
-    for (int bj = 0; bj * 2 * B <= std::min(nbI - 1, 2 * (bp * B + B - 1) + 1); ++bj)
-      for (int P = bp * B; P < std::min(np, bp * B + B); ++P)
-        for (int J = bj * 2 * B; J < std::min({nbI, 2 * P + 2, bj * 2 * B + 2 * B}); ++J) out[n++] = make_int2(P, J);
+  for (const It& t : its) out[n++] = make_int2((t.a0 << 16) | t.a1, t.b);
+  for (const It& t : tail) out[n++] = make_int2((t.a0 << 16) | (t.a1 < 0 ? 0xFFFF : t.a1), t.b);
   return n;
+}
+// number of items oz_pair_order produces
+int oz_pair_items(int nbI) {
+  int n = 0, left = 0;
+  for (int c = 0; c < nbI; ++c) {
+    n += (nbI - c) / 2;
+    left += (nbI - c) & 1;
+  }
+  return n + (left + 1) / 2;
 }
 
 cudaError_t launch_oz_gram2(const CUtensorMap* maps, const OzParams& p, cudaStream_t s) {

@@ -109,3 +109,20 @@ def test_hidden_product_scheme():
     exact = x.astype(np.longdouble) @ w.astype(np.longdouble)
     scale = np.ldexp(1.0, er[:, None] + ec[None, :]) * x.shape[1]
     assert float((np.abs(xw.astype(np.longdouble) - exact) / scale).max()) <= 2.0 ** -52
+
+
+def test_gram_pair_items_cover_lower_tiles(tmp_path):
+    """The INT8 Gram's CTA-pair items (csrc/k_ozaki.cu oz_pair_order): every lower tile exactly once,
+    at most one half-idle item per leftover group, for tile grids up to 160 x 160."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "paper_2011_02436_b200", "csrc", "k_ozaki.cu")).read()
+    body = src[src.index("int oz_pair_order(int nbI"):src.index("cudaError_t launch_oz_gram2")]
+    harness = open(os.path.join(root, "tests", "cpp", "oz_pairing.cpp")).read().replace("// OZ_PAIR_SRC", body)
+    cpp, exe = tmp_path / "oz_pairing.cpp", str(tmp_path / "oz_pairing")
+    cpp.write_text(harness)
+    subprocess.run(["g++", "-std=c++17", "-O2", str(cpp), "-o", exe], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0 and "PASS" in out.stdout, out.stdout
