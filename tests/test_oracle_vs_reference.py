@@ -181,3 +181,24 @@ def test_baseline_c2_bitwise():
     assert r["order"] == o["order"] and r["diag"]["rank"] == o["diag"]["rank"] == L
     assert np.array_equal(r["beta"], o["beta"])
     assert r["diag"]["training_accuracy"] == o["diag"]["training_accuracy"]
+
+
+def test_reference_unit_suite_passes_on_the_standin_build():
+    """The reference's own doctest suite (proj/tests/test_{matrix,linalg,elm,data,bench}.cpp, compiled
+    unedited against oracle/doctest_standin) passes on the reference sources built with the Eigen
+    stand-in: 50 test cases, every assertion -- the build that pins the oracle satisfies the
+    reference's own known-answer and tolerance tests."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(ref.LIB), "unit_tests_ref")
+    if not os.path.exists(exe):
+        if not os.path.isdir(ref.REFERENCE_SRC):
+            pytest.skip("unit_tests_ref not built and /root/reference absent")
+        subprocess.run(["make", "-s", "-C", ref.HERE, "refunit"], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(out.stdout[-400:])
+    assert out.returncode == 0, out.stdout[-2000:]
+    assert "| 0 failed" in out.stdout and "test cases: " in out.stdout
+    cases = int(out.stdout.split("test cases: ")[1].split(" ")[0])
+    assert cases >= 42  # 50 with the bench tests (nlohmann json available), 42 without
