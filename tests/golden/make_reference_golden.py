@@ -62,8 +62,10 @@ def deficient_case(name, n, d, L, dup, m, tol):
 
 cases = [
     train_case("C1", 2000, 16, 200, 2),                 # BASELINE configs[0], 1000 seeded test rows
-    train_case("three_panels", 900, 8, 130, 3, ntest=300),
-    train_case("panel_plus_one", 300, 3, 65, 2, ntest=100),
+    # well-posed shapes (oracle pivot margin >= 1e-8, self-floor ~1e-11): a pivot order decided by
+    # rounding noise could not be held to bit-exactness on any other arithmetic, real Eigen included
+    train_case("three_panels", 900, 24, 130, 3, ntest=300),
+    train_case("panel_plus_one", 600, 16, 65, 2, ntest=100),
     deficient_case("twins_tol1e-6", 1500, 12, 300, 100, 5, 1e-6),
 ]
 out = {"generator": "tests/golden/make_reference_golden.py",

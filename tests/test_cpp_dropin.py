@@ -73,6 +73,22 @@ def test_reference_acceptance_suite_on_device():
     assert "acceptance: all criteria passed" in out.stdout
 
 
+REF_UNIT_BIN = os.path.join(ROOT, "oracle", "_ref", "unit_tests_b200")
+
+
+@pytest.mark.gpu
+def test_reference_unit_suite_on_device():
+    """The reference's own doctest suite (proj/tests/test_{matrix,linalg,elm,data,bench}.cpp), compiled
+    UNEDITED against the drop-in headers and a doctest stand-in (oracle/doctest_standin) by build() into
+    oracle/_ref/, runs on the B200 library: every test case of the reference passes on the drop-in."""
+    if not os.path.exists(REF_UNIT_BIN):
+        pytest.skip("oracle/_ref/unit_tests_b200 not built (needs /root/reference at build time)")
+    out = subprocess.run([REF_UNIT_BIN], capture_output=True, text=True, timeout=900)
+    print(out.stdout[-3000:])
+    assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
+    assert "test cases: 50 | 50 passed | 0 failed" in out.stdout
+
+
 @pytest.mark.gpu
 def test_property_suite_on_device(tmp_path):
     out = subprocess.run([build(tmp_path, os.path.join(ROOT, "tests", "cpp", "verify_suite.cpp"))],
