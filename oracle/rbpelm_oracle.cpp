@@ -8,14 +8,21 @@
 // The product path (paper_2011_02436_b200) never links or calls it.
 //
 // Why a restatement: the reference needs Eigen 3 (proj/CMakeLists.txt:12),
-// which is not installed in this image or on the GPU box, so the reference
-// library cannot be compiled here.  Every function below
-// cites the reference file:line it follows.  Bit-level parity with Eigen's
-// kernels is unpinned (no golden vectors exist in the reference);
-// the oracle is pinned by porting the reference's own known-answer and
-// tolerance tests (tests/test_reference_suite.py, run on this oracle in the CPU
-// suite), and its blocked/threaded loops are pinned bitwise against its own
-// scalar-loop transcription (tests/golden/oracle_digests.json).
+// which is not installed in this image or on the GPU box, so the reference's
+// own build cannot run here.  Every function below cites
+// the reference file:line it follows.
+//
+// Pinning: PINNED AGAINST THE REFERENCE'S OWN CODE.  oracle/_ref/librbpelm_ref.so
+// is proj/src/{matrix,linalg,elm}.cpp compiled unedited against a stand-in for
+// the Eigen subset they use (oracle/eigen_standin; `make reflib`), and
+// tests/test_oracle_vs_reference.py checks this restatement against it bit for
+// bit (C1, C2 at full size, rank-deficient twins, df splits, ties, SPD solves,
+// error messages).  Golden vectors written by that library
+// (tests/golden/reference_golden.json) are checked on CPU and on the B200.
+// The reference's known-answer and tolerance tests are also ported
+// (tests/test_reference_suite.py), and the blocked/threaded loops are pinned
+// bitwise against the scalar-loop transcription (tests/golden/oracle_digests.json).
+// Not pinned: the rounding of real Eigen's blocked kernels (no Eigen build exists).
 //
 // Floating-point contract: compiled with -ffp-contract=off so that every
 // a*b+c is a rounded multiply followed by a rounded add, as in the reference's
