@@ -186,7 +186,9 @@ def sample_text(cfg_name, rows, n_total, L, threads, ph):
            f"hidden build, Gram + H^T T and accuracy pass timed on the first {rows} of {n_total} rows and scaled "
            f"linearly to N_total; pivoted Cholesky + triangular solves timed at full L={L}"
            + (" on the sample Gram + 1e-2 max(diag) I (full rank)" if rows < L else ""))
-    return (f"oracle restatement of train(rank) (reference not buildable: no Eigen), {threads} host threads, "
+    return (f"oracle restatement of train(rank), bitwise equal to the reference's own sources built on an Eigen stand-in "
+            f"(oracle/_ref: scalar, single-threaded, so the faster port is the one timed; real Eigen is absent), "
+            f"{threads} host threads, "
             f"{cfg_name}: {how}; phases {', '.join(f'{k} {v:.2f}s' for k, v in ph.items() if k != 'rank')}")
 
 
