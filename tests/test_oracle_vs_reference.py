@@ -202,3 +202,23 @@ def test_reference_unit_suite_passes_on_the_standin_build():
     assert "| 0 failed" in out.stdout and "test cases: " in out.stdout
     cases = int(out.stdout.split("test cases: ")[1].split(" ")[0])
     assert cases >= 42  # 50 with the bench tests (nlohmann json available), 42 without
+
+
+def test_pseudo_inverse_definition_bitwise():
+    """H+ = P (F F^T)^-1 P^T H^T is not computed by the reference's rank path; the oracle
+    defines it as the full-rank solve (elm.cpp:202-214) with right-hand side H^T.  Composed here from the
+    reference's own rank_revealing_factor / solve_factored_gram / row scatter, it must equal
+    oracle.pseudo_inverse bit for bit, and satisfy the reference's pinv_svd to rounding."""
+    x, _ = oracle.synth_classification(700, 10, 2, 21, 22)
+    w, b = ref.init_hidden(10, 90, 2, 23)
+    h = ref.hidden_matrix(w, b, x)
+    order, rank, _, f, _ = ref.rank_revealing_factor(h)
+    assert rank == 90
+    xs = ref.solve_factored_gram(f, order, rank, np.ascontiguousarray(h.T[order]))
+    hp = np.empty_like(xs)
+    hp[order] = xs  # invert_permutation_rows, linalg.cpp:54-66
+    hp_o, order_o, rank_o = oracle.pseudo_inverse(h)
+    assert order_o == order and rank_o == rank
+    assert np.array_equal(hp, hp_o)
+    ps = ref.pinv_svd(h)
+    assert np.linalg.norm(hp - ps) <= 1e-8 * np.linalg.norm(ps)
