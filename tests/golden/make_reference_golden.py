@@ -30,14 +30,15 @@ def hexes(a):
     return [float(v).hex() for v in np.asarray(a, dtype=np.float64).ravel()]
 
 
-def train_case(name, n, d, L, m, tol=0.0, ntest=1000):
+def train_case(name, n, d, L, m, tol=0.0, ntest=1000, kind="rank", split=0):
     x, t = oracle.synth_classification(n, d, m, SEED_X, SEED_T)
-    r = ref.train(d, L, m, SEED_W, x, t, "rank", 0, tol)
+    r = ref.train(d, L, m, SEED_W, x, t, kind, split, tol)
     xt, _ = oracle.synth_classification(ntest, d, m, SEED_TEST, SEED_T)
     scores = ref.predict(r["w"], r["b"], r["beta"], xt)
     h = ref.hidden_matrix(r["w"], r["b"], x)
     f = ref.rank_revealing_factor(h, tol)
-    return {"name": name, "kind": "train", "n": n, "d": d, "L": L, "m": m, "tol": tol, "ntest": ntest,
+    return {"name": name, "kind": "train", "strategy": kind, "split": split, "n": n, "d": d, "L": L, "m": m, "tol": tol,
+            "ntest": ntest,
             "order": r["order"], "diag": {k: r["diag"][k] for k in DIAG_KEYS},
             "beta_shape": list(r["beta"].shape), "beta_hex": hexes(r["beta"]),
             "train_labels": "".join(str(int(v)) for v in ref.predict(r["w"], r["b"], r["beta"], x).argmax(1)),
@@ -66,6 +67,9 @@ cases = [
     # rounding noise could not be held to bit-exactness on any other arithmetic, real Eigen included
     train_case("three_panels", 900, 24, 130, 3, ntest=300),
     train_case("panel_plus_one", 600, 16, 65, 2, ntest=100),
+    # the DF split and the direct strategy through the same train()
+    train_case("df_split_40", 900, 24, 130, 3, ntest=300, kind="df", split=40),
+    train_case("direct", 900, 24, 130, 3, ntest=300, kind="direct"),
     deficient_case("twins_tol1e-6", 1500, 12, 300, 100, 5, 1e-6),
 ]
 out = {"generator": "tests/golden/make_reference_golden.py",

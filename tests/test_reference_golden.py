@@ -43,8 +43,9 @@ def rel_fro(a, b):
 @pytest.mark.parametrize("c", TRAIN, ids=[c["name"] for c in TRAIN])
 def test_oracle_reproduces_reference_train_vectors(c):
     x, t = oracle.synth_classification(c["n"], c["d"], c["m"], SEEDS["x"], SEEDS["teacher"])
-    o = oracle.train(c["d"], c["L"], c["m"], SEEDS["w"], x, t, "rank", 0, c["tol"])
-    assert o["order"] == c["order"]
+    o = oracle.train(c["d"], c["L"], c["m"], SEEDS["w"], x, t, c["strategy"], c["split"], c["tol"])
+    if c["strategy"] == "rank":
+        assert o["order"] == c["order"]
     assert all(o["diag"][k] == c["diag"][k] for k in FLAGS)
     assert o["diag"]["training_accuracy"] == c["diag"]["training_accuracy"]
     assert np.array_equal(o["beta"], beta_of(c)), "oracle beta is not bitwise the reference's"
@@ -81,10 +82,14 @@ def test_b200_train_matches_reference_vectors(c):
 
     x, t = rb.synth_classification(c["n"], c["d"], c["m"], SEEDS["x"], SEEDS["teacher"])
     params = rb.ElmParams(c["d"], c["L"], c["m"], SEEDS["w"])
-    model, diag, order = rb.train(params, x, t, rb.SolverStrategy.rank_based(c["tol"]), return_order=True)
+    strategy = {"rank": rb.SolverStrategy.rank_based(c["tol"]), "df": rb.SolverStrategy.df_split(c["split"]),
+                "direct": rb.SolverStrategy.direct()}[c["strategy"]]
+    model, diag, order = rb.train(params, x, t, strategy, return_order=True)
     assert digest(model.hidden.weights) == c["sha256"]["w"] and digest(model.hidden.biases) == c["sha256"]["b"]
-    assert order == c["order"], "pivot order differs from the reference's"
+    if c["strategy"] == "rank":
+        assert order == c["order"], "pivot order differs from the reference's"
     assert diag.rank == c["diag"]["rank"] and diag.split_lo == c["diag"]["split_lo"]
+    assert diag.rank_known == bool(c["diag"]["rank_known"]) and diag.used_svd_path == bool(c["diag"]["used_svd_path"])
     assert diag.split_hi == c["diag"]["split_hi"] and not diag.ridge_applied and not diag.fallback_to_direct
     assert diag.training_accuracy == c["diag"]["training_accuracy"]
     err = rel_fro(model.beta, beta_of(c))
