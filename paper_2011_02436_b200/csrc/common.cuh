@@ -144,13 +144,19 @@ __device__ __forceinline__ double ld_volatile_f64(const double* p) {
 // (error 5e-2 -> 2.6e-3 -> 6.5e-6 -> 4e-11 -> ~1e-21 before rounding), the last one giving the
 // correctly rounded quotient in all tested cases.  The DP reciprocal seed (MUFU.RCP64H) is the
 // bottleneck of the sigmoid epilogue on sm_100 (XU pipe ~90% busy), DFMA is not.
+// For x >= 2^1020 (z below about -707: 1/x is subnormal or nearly so) the seed's exponent difference
+// has no room and the iteration returned NaN; such x are scaled by 2^-64 first (exact) and the quotient
+// is scaled back with one rounding onto the subnormal grid.
 __device__ __forceinline__ double recip_ge1(double x) {
-  double y = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(x));
+  const bool big = x >= 0x1p1020;
+  const double xs = big ? x * 0x1p-64 : x;
+  double y = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(xs));
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const double e = fma(-x, y, 1.0);
+    const double e = fma(-xs, y, 1.0);
     y = fma(y, e, y);
   }
+  y = big ? y * 0x1p-64 : y;
   return x <= 1.7976931348623157e308 ? y : (x > 0.0 ? 0.0 : x);  // 1/inf = 0, NaN propagates
 }
 

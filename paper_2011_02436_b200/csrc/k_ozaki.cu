@@ -291,6 +291,35 @@ __device__ __forceinline__ double exp_sig(double t) {
   const double v = (q * pow2i(k1)) * pow2i(k - k1);
   return t > 709.782712893384 ? __longlong_as_double(0x7ff0000000000000LL) : (t < -745.1332191019412 ? 0.0 : v);
 }
+// The epilogue's sigmoid for |z| <= 700 (finite): bit for bit recip_ge1(1.0 + exp_sig(-z)), with the
+// selects that can never fire in that range left out -- e^t neither overflows nor underflows (|k| <= 1010:
+// q 2^k is a normal double, so adding k to q's exponent field equals the two exact power-of-two products),
+// and 1 + e^t is finite.  The caller checks the range with one integer maximum over the high words of its
+// z values and redoes the rare out-of-range block through sigmoid_exact.
+__device__ __forceinline__ double sigmoid_in_range(double z) {
+  const double t = -z;
+  const double kb = fma(t, 0x1.71547652b82fep0, 0x1.8p52);
+  const int k = __double2loint(kb);
+  const double kd = kb - 0x1.8p52;
+  double r = fma(-kd, 0x1.62e42fefa39efp-1, t);
+  r = fma(-kd, 0x1.abc9e3b39803fp-56, r);
+  double q = c_exp_taylor[0];
+#pragma unroll
+  for (int i = 1; i < 14; ++i) q = fma(q, r, c_exp_taylor[i]);
+  const double e = __hiloint2double(__double2hiint(q) + (k << 20), __double2loint(q));
+  const double x = 1.0 + e;
+  double y = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(x));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double d = fma(-x, y, 1.0);
+    y = fma(y, d, y);
+  }
+  return y;
+}
+// every z, including non-finite ones: the reference arithmetic with all its selects (out of line: it runs
+// only for blocks holding |z| > 700, and for the last, partial row block of the matrix)
+__device__ __noinline__ double sigmoid_exact(double z) { return recip_ge1(1.0 + exp_sig(-z)); }
+constexpr int kSigmoidRangeHi = 0x4085E000;  // high word of 700.0
 // mbarrier wait that suspends the thread (up to the hint) instead of spinning: the producer and MMA
 // warps of oz_hidden_kernel share the SM sub-partitions with the epilogue's FP64 math
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t phase) {
@@ -717,13 +746,31 @@ __global__ void __launch_bounds__(kOzHidThreads, 1) __cluster_dims__(2, 1, 1)
         double* dst = p.H + static_cast<long long>(r0) * p.ldh + c;
         const double* frow = s_frow + part * 32;
         double hm = 0.0;  // column maximum of this thread's rows (h >= 0; fmax skips NaN like the scan)
+        bool redo = nr < 32;
+        if (!redo) {  // whole block, no per-row predicates; range checked once for the 32 values
+          int zhi = 0;
+          double* out = dst;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const double z = fma(v[i] * sc, frow[i], bc);
-          const double h = recip_ge1(1.0 + exp_sig(-z));
-          if (i < nr) {
-            dst[static_cast<long long>(i) * p.ldh] = h;
+          for (int i = 0; i < 32; ++i) {
+            const double z = fma(v[i] * sc, frow[i], bc);
+            zhi = max(zhi, __double2hiint(z) & 0x7fffffff);
+            const double h = sigmoid_in_range(z);
+            *out = h;
+            out += p.ldh;
             hm = fmax(hm, h);
+          }
+          redo = zhi > kSigmoidRangeHi;  // some |z| > 700 (or not finite): recompute the block exactly
+        }
+        if (redo) {
+          hm = 0.0;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const double z = fma(v[i] * sc, frow[i], bc);
+            const double h = sigmoid_exact(z);
+            if (i < nr) {
+              dst[static_cast<long long>(i) * p.ldh] = h;
+              hm = fmax(hm, h);
+            }
           }
         }
         // fused column scan of the Gram that follows (oz_colmax_kernel's result for these rows)

@@ -118,6 +118,38 @@ def test_int8_hidden_vs_extended_precision(n, d, L):
     assert np.abs(h - ho).max() < 1e-12
 
 
+@pytest.mark.parametrize("n,d,L", [(1000, 32, 300), (4096, 64, 256), (77, 9, 40)])
+def test_int8_hidden_saturating_and_partial_blocks(n, d, L):
+    """K1i epilogue: blocks whose |z| exceeds 700 leave the in-range sigmoid and are recomputed with the
+    full select chain (overflow to inf -> h = 0 exactly, underflow -> h = 1 exactly), as are the last,
+    partial row blocks; blocks mixing both ranges must still equal the reference formula."""
+    import oracle
+
+    rng = np.random.default_rng(n + L)
+    x = rng.random((n, d))
+    scale = np.where(rng.random(n) < 0.5, 1.0, 180.0)     # half the rows drive |z| into the hundreds / thousands
+    scale[::97] = 4000.0                                  # some far beyond the exp range: exact 0 / 1
+    x *= scale[:, None]
+    hid = rb.init_hidden(rb.ElmParams(d, L, 2, n + L))
+    h = rb.hidden_matrix(hid, x)
+    ho = oracle.hidden_matrix(hid.weights, hid.biases, x)
+    z = x @ hid.weights + hid.biases.reshape(1, -1)
+    assert np.isfinite(h).all() and (np.abs(z) > 745.2).any() and (np.abs(z) < 700).any()
+    assert np.abs(h - ho).max() < 1e-12
+    sat = np.abs(z) > 760
+    assert np.array_equal(h[sat], ho[sat])                # exact 0.0 / 1.0 where the exponential saturates
+    big = np.abs(z) > 40                                  # 1 ulp of e^-z relative to 1: h rounds like the oracle's
+    assert np.abs(h[big] - ho[big]).max() <= 1e-16 * 4
+    sub = (z > -709.7) & (z < -708.5)                     # 1 / (1 + e^-z) is subnormal: was NaN before the
+    if sub.any():                                         # reciprocal scaled such quotients
+        assert np.abs(h[sub] / ho[sub] - 1.0).max() < 1e-10
+    # the fused predict kernel (exp + the same reciprocal on the DMMA path) on the same rows
+    beta = rng.standard_normal((L, 2))
+    model = rb.ElmModel(rb.ElmParams(d, L, 2, n + L), hid, beta)
+    s, so = rb.predict(model, x), oracle.predict(hid.weights, hid.biases, beta, x)
+    assert np.isfinite(s).all() and np.abs(s - so).max() <= 1e-11 * max(1.0, np.abs(so).max())
+
+
 @pytest.mark.parametrize("n,d,L,m", [(7000, 24, 400, 60), (3001, 20, 130, 128), (20000, 40, 700, 100)])
 def test_int8_accuracy_pass_vs_oracle(n, d, L, m):
     """K6i (oz_scores_kernel, m > 48): the training-accuracy pass from the Gram's digit planes gives the
