@@ -160,6 +160,59 @@ __device__ __forceinline__ double recip_ge1(double x) {
   return x <= 1.7976931348623157e308 ? y : (x > 0.0 ? 0.0 : x);  // 1/inf = 0, NaN propagates
 }
 
+// 2^e for a normal exponent (-1022 <= e <= 1023)
+__device__ __forceinline__ double pow2i(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
+// e^t without branches for the sigmoid epilogue (~1 ulp, like exp): t = k ln2 + r with k = rint(t / ln2)
+// read from the bits of the magic-shifted product (no F2I), r by two FMAs (|r| <= ln2 / 2), e^r by its
+// degree-13 Taylor polynomial (truncation < 2^-57; coefficients in constant memory, so every DFMA takes
+// its operand from the constant bank), 2^k as two exact factors; t > 709.78 -> inf and t < -745.14 -> 0
+// by selects.  Branch-free, so the unrolled epilogue interleaves many of them.
+static __constant__ double c_exp_taylor[14] = {1.0 / 6227020800.0, 1.0 / 479001600.0, 1.0 / 39916800.0, 1.0 / 3628800.0,
+                                        1.0 / 362880.0,     1.0 / 40320.0,     1.0 / 5040.0,     1.0 / 720.0,
+                                        1.0 / 120.0,        1.0 / 24.0,        1.0 / 6.0,        0.5,
+                                        1.0,                1.0};
+__device__ __forceinline__ double exp_sig(double t) {
+  const double kb = fma(t, 0x1.71547652b82fep0, 0x1.8p52);
+  const int k = __double2loint(kb);
+  const double kd = kb - 0x1.8p52;
+  double r = fma(-kd, 0x1.62e42fefa39efp-1, t);
+  r = fma(-kd, 0x1.abc9e3b39803fp-56, r);
+  double q = c_exp_taylor[0];
+#pragma unroll
+  for (int i = 1; i < 14; ++i) q = fma(q, r, c_exp_taylor[i]);
+  const int k1 = k >> 1;
+  const double v = (q * pow2i(k1)) * pow2i(k - k1);
+  return t > 709.782712893384 ? __longlong_as_double(0x7ff0000000000000LL) : (t < -745.1332191019412 ? 0.0 : v);
+}
+// The epilogue's sigmoid for |z| <= 700 (finite): bit for bit recip_ge1(1.0 + exp_sig(-z)), with the
+// selects that can never fire in that range left out -- e^t neither overflows nor underflows (|k| <= 1010:
+// q 2^k is a normal double, so adding k to q's exponent field equals the two exact power-of-two products),
+// and 1 + e^t is finite.  The caller checks the range with one integer maximum over the high words of its
+// z values and redoes the rare out-of-range block through sigmoid_exact.
+__device__ __forceinline__ double sigmoid_in_range(double z) {
+  const double t = -z;
+  const double kb = fma(t, 0x1.71547652b82fep0, 0x1.8p52);
+  const int k = __double2loint(kb);
+  const double kd = kb - 0x1.8p52;
+  double r = fma(-kd, 0x1.62e42fefa39efp-1, t);
+  r = fma(-kd, 0x1.abc9e3b39803fp-56, r);
+  double q = c_exp_taylor[0];
+#pragma unroll
+  for (int i = 1; i < 14; ++i) q = fma(q, r, c_exp_taylor[i]);
+  const double e = __hiloint2double(__double2hiint(q) + (k << 20), __double2loint(q));
+  const double x = 1.0 + e;
+  double y = __longlong_as_double(0x7FDE623822FC16E6LL - __double_as_longlong(x));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double d = fma(-x, y, 1.0);
+    y = fma(y, d, y);
+  }
+  return y;
+}
+// every z, including non-finite ones: the reference arithmetic with all its selects (out of line: it runs
+// only for blocks holding |z| > 700, and for the last, partial row block of the matrix)
+static __device__ __noinline__ double sigmoid_exact(double z) { return recip_ge1(1.0 + exp_sig(-z)); }
+constexpr int kSigmoidRangeHi = 0x4085E000;  // high word of 700.0
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }

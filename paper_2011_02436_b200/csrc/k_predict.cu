@@ -133,26 +133,45 @@ __global__ void __launch_bounds__(kGemmThreads, MP <= 48 ? 2 : 1)
     // epilogue 1: h = sigmoid(z + b) into Hs[col][row] (this warp's rows, rows 2g and 2g+1 as one
     // 16-byte store); nodes >= L give 0.  Rows are XOR-swizzled per column group (hsw), which keeps
     // the row pairs together and makes both these stores and GEMM2's fragment loads conflict-free.
+    // The sigmoid is the K1i epilogue's (common.cuh): z in place over the accumulators, one integer
+    // maximum over the high words of the thread's 16 values, then the select-free in-range form --
+    // or, when some |z| > 700 (or is not finite), the out-of-line exact form for all 16.
+    int zhi = 0;
+#pragma unroll
+    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int col = c * kPBN + pp * 16 + 4 * t + q;
+        const double bq = col < p.L ? p.bias[col] : 0.0;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          double& a = acc1[2 * pp + (q & 1)][2 * half + (q >> 1)];
+          a = col < p.L ? add_rn(a, bq) : 0.0;
+          zhi = max(zhi, __double2hiint(a) & 0x7fffffff);
+        }
+      }
+    if (zhi <= kSigmoidRangeHi) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc1[j][e] = sigmoid_in_range(acc1[j][e]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc1[j][e] = sigmoid_exact(acc1[j][e]);
+    }
 #pragma unroll
     for (int pp = 0; pp < 2; ++pp) {
       const int cb = pp * 16 + 4 * t;  // chunk column of acc1[2pp][*] / acc1[2pp+1][*]
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         // acc1[2pp + (q & 1)][2 * half + (q >> 1)] holds (row 2g + half, column cb + q)
-        double h2[2];
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          const int col = c * kPBN + cb + q;
-          const double v = acc1[2 * pp + (q & 1)][2 * half + (q >> 1)];
-          double h = 0.0;
-          if (col < p.L) {
-            const double z = add_rn(v, p.bias[col]);
-            h = recip_ge1(1.0 + exp(-z));
-          }
-          h2[half] = h;
-        }
+        const bool live = c * kPBN + cb + q < p.L;
+        const double h0 = live ? acc1[2 * pp + (q & 1)][q >> 1] : 0.0;
+        const double h1 = live ? acc1[2 * pp + (q & 1)][2 + (q >> 1)] : 0.0;
         const int kc = cb + q;
-        *reinterpret_cast<double2*>(Hs + kc * kPHP + ((wm + 2 * g) ^ hsw(kc))) = make_double2(h2[0], h2[1]);
+        *reinterpret_cast<double2*>(Hs + kc * kPHP + ((wm + 2 * g) ^ hsw(kc))) = make_double2(h0, h1);
       }
     }
     __syncwarp();
